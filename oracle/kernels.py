@@ -144,7 +144,7 @@ def kernel_S(x, y, n, G, nu):
     return (G / (4.0 * PI * (1.0 - nu) * r ** 3))[..., None, None, None] * (t1 + t2 + t3 + t4)
 
 
-def direct_sum(kernel, trg, src, K, G, w=None, f=None, g=None, nrm=None, chunk=256):
+def direct_sum(kernel, trg, src, K, G, w=None, f=None, g=None, nrm=None, chunk=64, schunk=4096):
     """O(N^2) evaluation of PAPER.md Eq. fmm_summation (line 154),
         t_i = sum_j w_j K(x_i, y_j, n_j) s_j,
     for kernel in {U, P, UP, D, S, DS}.  f is the single-layer density (traction-like,
@@ -168,28 +168,26 @@ def direct_sum(kernel, trg, src, K, G, w=None, f=None, g=None, nrm=None, chunk=2
     out = np.zeros((trg.shape[0], 6 if stress else 3))
     for t0 in range(0, trg.shape[0], chunk):
         x = trg[t0:t0 + chunk, None, :]
-        dd = x - src[None, :, :]
-        self_pair = np.all(dd == 0.0, axis=-1)
-        # move coincident sources away so the kernel stays finite; their terms are zeroed
-        ys = np.where(self_pair[..., None], x + 1.0, src[None, :, :])
-        mask = (~self_pair).astype(np.float64)
-        if not stress:
-            acc = np.zeros((x.shape[0], 3))
-            if use_sl:
-                Um = kernel_U(x, ys, G, nu)
-                acc += np.einsum('tsij,sj,ts->ti', Um, fw, mask)
-            if use_dl:
-                Pm = kernel_P(x, ys, nrm[None, :, :], nu)
-                acc += np.einsum('tsij,sj,ts->ti', Pm, gw, mask)
-        else:
-            sig = np.zeros((x.shape[0], 3, 3))
-            if use_sl:
-                Dm = kernel_D(x, ys, nu)
-                sig += np.einsum('tskij,sk,ts->tij', Dm, fw, mask)
-            if use_dl:
-                Sm = kernel_S(x, ys, nrm[None, :, :], G, nu)
-                sig += np.einsum('tskij,sk,ts->tij', Sm, gw, mask)
-            acc = np.stack([sig[:, a, b] for a, b in VOIGT], axis=-1)
+        acc = np.zeros((x.shape[0], 3)) if not stress else np.zeros((x.shape[0], 3, 3))
+        for s0 in range(0, ns, schunk):
+            sl = slice(s0, s0 + schunk)
+            dd = x - src[None, sl, :]
+            self_pair = np.all(dd == 0.0, axis=-1)
+            # move coincident sources away so the kernel stays finite; their terms are zeroed
+            ys = np.where(self_pair[..., None], x + 1.0, src[None, sl, :])
+            mask = (~self_pair).astype(np.float64)
+            if not stress:
+                if use_sl:
+                    acc += np.einsum('tsij,sj,ts->ti', kernel_U(x, ys, G, nu), fw[sl], mask)
+                if use_dl:
+                    acc += np.einsum('tsij,sj,ts->ti', kernel_P(x, ys, nrm[None, sl, :], nu), gw[sl], mask)
+            else:
+                if use_sl:
+                    acc += np.einsum('tskij,sk,ts->tij', kernel_D(x, ys, nu), fw[sl], mask)
+                if use_dl:
+                    acc += np.einsum('tskij,sk,ts->tij', kernel_S(x, ys, nrm[None, sl, :], G, nu), gw[sl], mask)
+        if stress:
+            acc = np.stack([acc[:, a, b] for a, b in VOIGT], axis=-1)
         out[t0:t0 + chunk] = acc
     return out
 
