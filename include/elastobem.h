@@ -1,0 +1,180 @@
+/*
+ * elastobem.h -- C ABI of the B200-native elastostatic BEM / KIFMM hot path.
+ *
+ * What it computes (PAPER.md = arXiv:1612.04082 as extracted, line numbers cited):
+ *   the sums of Eq. fmm_summation (line 154)
+ *       t_i = sum_j w_j K(x_i, y_j, n_j) s_j
+ *   for the four fundamental solutions of Sec. 2.1 -- U (Eq. disp_1, line 94),
+ *   P (Eq. disp_2, line 98), D (Eq. stress_2), S (Eq. stress_3)
+ *   -- by direct summation or by the kernel-independent FMM of Sec. 2.2 (lines
+ *   131-151), and the GMRES solve of the collocation system Eq. num2 (line 175) whose
+ *   matrix-vector products that FMM supplies (lines 181-189).
+ *   Readings of garbled passages (signs/prefactors of P, D, S) are R1-R3 in DESIGN.md.
+ *
+ * Conventions shared by every entry point
+ *   - Points, normals, densities are float32, 3 per item, packed xyzxyz... (AoS).
+ *   - A target is where a value is wanted (the paper's collocation point xi or
+ *     interior point p); a source is an integration point y_j with outward unit
+ *     normal n_j and weight w_j (panel area x quadrature weight).
+ *     r-vector = target - source (reading R1).
+ *   - f_j: single-layer density (traction-like, PAPER.md p_j in Eq. BIE), used by U/D.
+ *     g_j: double-layer density (displacement-like, u_j in Eq. BIE), used by P/S.
+ *   - Displacement outputs are 3 floats per target; stress outputs 6 floats per
+ *     target in Voigt order (xx, yy, zz, xy, yz, xz).
+ *   - Pairs with r == 0 are excluded (the own panel's singular
+ *     contribution is the job of the local pass, not of the sum).
+ *   - Material: bulk modulus K > 0 and shear modulus G > 0 (PAPER.md Eq. elast,
+ *     line 37); the kernels use nu = (3K - 2G) / (2 (3K + G)).
+ *   - Memory: unless stated otherwise, array arguments of one call must be either
+ *     all device pointers (the call is asynchronous on `stream`) or all host pointers
+ *     (the call stages them through device memory and returns after completion).
+ *     The library never takes ownership of caller arrays.
+ *   - stream: a cudaStream_t passed as void* (NULL = legacy default stream).
+ *   - Errors: every int-returning call returns 0 on success and a negative code on
+ *     failure; ebem_last_error() gives a thread-local message.  On failure outputs
+ *     are unspecified.  No call ever falls back to a CPU computation.
+ */
+#ifndef ELASTOBEM_H
+#define ELASTOBEM_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* kernel identifiers */
+enum ebem_kernel {
+    EBEM_U = 0,   /* single layer, displacement out:      sum w U f           */
+    EBEM_P = 1,   /* double layer, displacement out:      sum w P g           */
+    EBEM_UP = 2,  /* both layers, displacement out:       sum w (U f + P g)   */
+    EBEM_D = 3,   /* single layer, stress out:            sum w D f           */
+    EBEM_S = 4,   /* double layer, stress out:            sum w S g           */
+    EBEM_DS = 5   /* both layers, stress out:             sum w (D f + S g)   */
+};
+
+enum ebem_status {
+    EBEM_OK = 0,
+    EBEM_ERR_ARG = -1,      /* invalid argument                          */
+    EBEM_ERR_CUDA = -2,     /* CUDA runtime error (message has details)  */
+    EBEM_ERR_STATE = -3,    /* invalid handle / state                    */
+    EBEM_ERR_NOCONV = -4    /* GMRES did not reach the tolerance          */
+};
+
+/* thread-local description of the last failure ("" if none) */
+const char *ebem_last_error(void);
+
+/*
+ * bem_kernel_direct -- O(N^2) evaluation of Eq. fmm_summation (
+ * "an iterative solution scheme would require O(N^2) operations", line 125).
+ *   kernel   one of enum ebem_kernel
+ *   trg      [ntrg*3]  target points
+ *   src      [nsrc*3]  source points
+ *   nrm      [nsrc*3]  unit normals at the sources (required iff the kernel has a
+ *                      double layer: P, UP, S, DS; else may be NULL)
+ *   w        [nsrc]    weights (NULL = all 1)
+ *   f        [nsrc*3]  single-layer density (required iff U, UP, D, DS)
+ *   g        [nsrc*3]  double-layer density (required iff P, UP, S, DS)
+ *   out      [ntrg*3] (U, P, UP) or [ntrg*6] (D, S, DS), overwritten
+ * fp32 arithmetic (FFMA + rsqrt), one pass over all pairs.
+ */
+int bem_kernel_direct(int kernel, const float *trg, int64_t ntrg, const float *src,
+                      const float *nrm, const float *w, const float *f, const float *g,
+                      int64_t nsrc, double K, double G, float *out, void *stream);
+
+/* opaque FMM tree + plan: geometry, octree, interaction lists, translation operators */
+typedef struct ebem_tree ebem_tree;
+
+/*
+ * fmm_build_tree -- build the octree of PAPER.md Sec. 2.2 ("Generation of an octree
+ * partitioning of the domain into boxes", line 135) on the device: Morton codes of
+ * sources U targets, radix sort, level-by-level adaptive refinement (a box splits iff
+ * it holds more than max_pts sources or more than max_pts targets; reading R5),
+ * the U/V/W/X interaction lists, and the KIFMM translation operators for multipole
+ * order p (surface grid of p points per cube edge, 6(p-1)^2+2 points; reading R6).
+ *   src/nrm/w [nsrc*3]/[nsrc*3]/[nsrc]  sources, normals (NULL allowed if only
+ *             single-layer kernels will be used), weights (NULL = 1)
+ *   trg       [ntrg*3] targets (may alias src)
+ *   max_pts   leaf capacity (>= 1), p in [3, 12], K, G material
+ *   *tree     receives the handle (free with fmm_tree_free)
+ * The tree copies what it needs; caller arrays may be released afterwards.
+ * Synchronises `stream` (output sizes are data dependent).
+ */
+int fmm_build_tree(const float *src, const float *nrm, const float *w, int64_t nsrc,
+                   const float *trg, int64_t ntrg, int max_pts, int p, double K, double G,
+                   ebem_tree **tree, void *stream);
+
+/*
+ * fmm_matvec -- KIFMM evaluation of Eq. fmm_summation with displacement output
+ * (kernel U, P or UP): upward pass (S2M, M2M), downward pass (M2L, S2L, L2L),
+ * leaf evaluation (L2T, M2T) and near field (P2P over the U list); PAPER.md
+ * lines 131-151.  f/g [nsrc*3] in the caller's source order (NULL where unused),
+ * out [ntrg*3] in the caller's target order, overwritten.
+ * Device pointers: asynchronous, no allocation, capturable in a CUDA graph.
+ */
+int fmm_matvec(ebem_tree *tree, int kernel, const float *f, const float *g, float *out,
+               void *stream);
+
+/*
+ * fmm_eval_stress -- the same FMM with stress output (kernel D, S or DS): PAPER.md
+ * Eq. stress_1 (line 104) evaluated "via fast summation of the kernels" (line 194).
+ * out [ntrg*6], Voigt order.  Returns sum w (D f + S g); the caller applies the signs
+ * of Eq. stress_1 (sigma = sum D t - sum S u).
+ */
+int fmm_eval_stress(ebem_tree *tree, int kernel, const float *f, const float *g, float *out,
+                    void *stream);
+
+int fmm_tree_free(ebem_tree *tree);
+
+typedef struct ebem_tree_info {
+    int64_t nsrc, ntrg, nboxes, nleaves;
+    int32_t nlevels, p, max_pts, n_equiv;   /* n_equiv = 6(p-1)^2+2 surface points */
+    int64_t n_u, n_v, n_w, n_x;             /* total entries of each interaction list */
+    double origin[3], side;                 /* root cube */
+    int64_t device_bytes;                   /* device memory held by the handle */
+} ebem_tree_info;
+
+int fmm_tree_info(const ebem_tree *tree, ebem_tree_info *info);
+
+/*
+ * fmm_tree_export -- copy one tree array to HOST memory (parity tests).
+ *   what: 0 point Morton keys in sorted order   int64[nsrc+ntrg]
+ *         1 sorted position -> original point index (sources 0..nsrc-1, then
+ *           targets nsrc..)                      int32[nsrc+ntrg]
+ *         2 box level                            int32[nboxes]
+ *         3 box anchor (ix,iy,iz)                int32[nboxes*3]
+ *         4 box parent (-1 root)                 int32[nboxes]
+ *         5 box point range [begin,end)          int32[nboxes*2]
+ *         6..9 list U,V,W,X offsets (CSR)        int32[nboxes+1]
+ *         10..13 list U,V,W,X entries            int32[n_list]
+ *   buf/cap: destination and its capacity in bytes.  Returns bytes written (>= 0)
+ *   or a negative error.
+ */
+int64_t fmm_tree_export(const ebem_tree *tree, int what, void *buf, int64_t cap);
+
+/*
+ * bem_gmres_solve -- restarted GMRES (Saad) with device-side
+ * Arnoldi for the collocation system A x = b of the mixed BVP (Eqs. num, num2),
+ * whose operator is applied matrix-free by the FMM above (lines 184-189).
+ *   tree     built on collocation points = sources (panel centroids)
+ *   bc_type  [n] per panel: 0 = displacement prescribed (Dirichlet), 1 = traction
+ *            prescribed (Neumann)
+ *   self_U   [n*9] row-major 3x3 singular self-integral of U over the panel at its
+ *            centroid ("evaluated analytically"); NULL = 0
+ *   self_P   [n*9] the panel's own principal-value term of (1/2 I + P) (the jump
+ *            1/2 I included); NULL = 1/2 I
+ *   bc_val   [n*3] prescribed value (displacement or traction) per panel
+ *   x        [n*3] in: initial guess (device) / out: unknown per panel (traction on
+ *            Dirichlet panels, displacement on Neumann panels)
+ *   restart, max_iter, tol (relative residual)
+ *   iters_out, resid_out: iterations done and final relative residual (host)
+ */
+int bem_gmres_solve(ebem_tree *tree, const int32_t *bc_type, const float *self_U,
+                    const float *self_P, const float *bc_val, float *x, int restart,
+                    int max_iter, double tol, int32_t *iters_out, double *resid_out,
+                    void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ELASTOBEM_H */

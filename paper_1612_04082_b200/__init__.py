@@ -1,0 +1,216 @@
+"""B200-native elastostatic BEM / KIFMM hot path (arXiv:1612.04082), Python binding.
+
+Thin ctypes marshalling over the C ABI of ``lib/libelastobem.so`` (declared in
+``include/elastobem.h``): the same entry points, the same argument order.  Every
+computation runs in the CUDA library; there is no Python or CPU fallback -- importing
+this package fails if the library has not been built (``__graft_entry__.build()``).
+
+Arrays may be torch CUDA tensors (the call is asynchronous on the current torch stream)
+or host arrays (numpy / CPU tensors; the library stages them and returns when done).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "lib", "libelastobem.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"{LIB_PATH} not built; run `python -c 'import __graft_entry__ as g; g.build()'`")
+
+_lib = ctypes.CDLL(LIB_PATH)
+
+KERNEL_U, KERNEL_P, KERNEL_UP, KERNEL_D, KERNEL_S, KERNEL_DS = range(6)
+_VP = ctypes.c_void_p
+_I64 = ctypes.c_int64
+
+_lib.ebem_last_error.restype = ctypes.c_char_p
+_lib.bem_kernel_direct.argtypes = [ctypes.c_int, _VP, _I64, _VP, _VP, _VP, _VP, _VP, _I64,
+                                   ctypes.c_double, ctypes.c_double, _VP, _VP]
+_lib.fmm_build_tree.argtypes = [_VP, _VP, _VP, _I64, _VP, _I64, ctypes.c_int, ctypes.c_int,
+                                ctypes.c_double, ctypes.c_double, ctypes.POINTER(_VP), _VP]
+_lib.fmm_matvec.argtypes = [_VP, ctypes.c_int, _VP, _VP, _VP, _VP]
+_lib.fmm_eval_stress.argtypes = [_VP, ctypes.c_int, _VP, _VP, _VP, _VP]
+_lib.fmm_tree_free.argtypes = [_VP]
+_lib.fmm_tree_export.argtypes = [_VP, ctypes.c_int, _VP, _I64]
+_lib.fmm_tree_export.restype = _I64
+_lib.bem_gmres_solve.argtypes = [_VP, _VP, _VP, _VP, _VP, _VP, ctypes.c_int, ctypes.c_int,
+                                 ctypes.c_double, ctypes.POINTER(ctypes.c_int32),
+                                 ctypes.POINTER(ctypes.c_double), _VP]
+
+
+class TreeInfo(ctypes.Structure):
+    _fields_ = [("nsrc", _I64), ("ntrg", _I64), ("nboxes", _I64), ("nleaves", _I64),
+                ("nlevels", ctypes.c_int32), ("p", ctypes.c_int32), ("max_pts", ctypes.c_int32),
+                ("n_equiv", ctypes.c_int32), ("n_u", _I64), ("n_v", _I64), ("n_w", _I64),
+                ("n_x", _I64), ("origin", ctypes.c_double * 3), ("side", ctypes.c_double),
+                ("device_bytes", _I64)]
+
+
+_lib.fmm_tree_info.argtypes = [_VP, ctypes.POINTER(TreeInfo)]
+
+
+class EbemError(RuntimeError):
+    pass
+
+
+def _check(rc):
+    if rc != 0:
+        raise EbemError(f"elastobem error {rc}: {_lib.ebem_last_error().decode()}")
+
+
+def _is_cuda(a):
+    return a is not None and hasattr(a, "is_cuda") and a.is_cuda
+
+
+def _ptr(a, keep):
+    """device or host pointer of a float32/int32 contiguous array (None -> NULL)."""
+    if a is None:
+        return None
+    if hasattr(a, "data_ptr"):                      # torch tensor
+        if not a.is_contiguous():
+            a = a.contiguous()
+        keep.append(a)
+        return a.data_ptr()
+    arr = np.ascontiguousarray(a)
+    keep.append(arr)
+    return arr.ctypes.data
+
+
+def _stream(*arrs):
+    if any(_is_cuda(a) for a in arrs):
+        import torch
+        return torch.cuda.current_stream().cuda_stream
+    return None
+
+
+def _f32(a):
+    if a is None or hasattr(a, "data_ptr"):
+        if a is not None:
+            import torch
+            assert a.dtype == torch.float32, "float32 expected"
+        return a
+    return np.ascontiguousarray(a, dtype=np.float32)
+
+
+def _out_like(ref, shape):
+    if _is_cuda(ref):
+        import torch
+        return torch.empty(shape, dtype=torch.float32, device=ref.device)
+    return np.empty(shape, dtype=np.float32)
+
+
+def bem_kernel_direct(kernel, trg, src, nrm=None, w=None, f=None, g=None, K=1.0, G=0.5, out=None):
+    """O(N^2) sum of Eq. fmm_summation on the GPU; see include/elastobem.h."""
+    trg, src, nrm, w, f, g = map(_f32, (trg, src, nrm, w, f, g))
+    ntrg = int(trg.shape[0]) if trg.ndim == 2 else int(trg.shape[0]) // 3
+    nsrc = int(src.shape[0]) if src.ndim == 2 else int(src.shape[0]) // 3
+    nc = 6 if kernel >= KERNEL_D else 3
+    if out is None:
+        out = _out_like(trg, (ntrg, nc))
+    keep = []
+    _check(_lib.bem_kernel_direct(kernel, _ptr(trg, keep), ntrg, _ptr(src, keep), _ptr(nrm, keep),
+                                  _ptr(w, keep), _ptr(f, keep), _ptr(g, keep), nsrc, float(K),
+                                  float(G), _ptr(out, keep), _stream(trg, out)))
+    return out
+
+
+class FmmTree:
+    """owning wrapper of an ebem_tree* (fmm_build_tree / fmm_tree_free)."""
+
+    def __init__(self, handle, nsrc, ntrg, device):
+        self.handle = handle
+        self.nsrc, self.ntrg, self.device = nsrc, ntrg, device
+
+    def __del__(self):
+        if getattr(self, "handle", None):
+            _lib.fmm_tree_free(self.handle)
+            self.handle = None
+
+    def info(self):
+        return fmm_tree_info(self)
+
+
+def fmm_build_tree(src, nrm=None, w=None, trg=None, max_pts=64, p=6, K=1.0, G=0.5):
+    trg = src if trg is None else trg
+    src, nrm, w, trg = map(_f32, (src, nrm, w, trg))
+    nsrc = int(src.shape[0])
+    ntrg = int(trg.shape[0])
+    h = _VP()
+    keep = []
+    _check(_lib.fmm_build_tree(_ptr(src, keep), _ptr(nrm, keep), _ptr(w, keep), nsrc, _ptr(trg, keep),
+                               ntrg, int(max_pts), int(p), float(K), float(G), ctypes.byref(h),
+                               _stream(src, trg)))
+    return FmmTree(h.value, nsrc, ntrg, src.device if _is_cuda(src) else None)
+
+
+def _fmm_eval(fn, tree, kernel, f, g, out, nc):
+    f, g = _f32(f), _f32(g)
+    ref = f if f is not None else g
+    if out is None:
+        out = _out_like(ref, (tree.ntrg, nc))
+    keep = []
+    _check(fn(tree.handle, kernel, _ptr(f, keep), _ptr(g, keep), _ptr(out, keep), _stream(f, g, out)))
+    return out
+
+
+def fmm_matvec(tree, kernel, f=None, g=None, out=None):
+    """KIFMM sum with displacement output (U, P, UP); see include/elastobem.h."""
+    return _fmm_eval(_lib.fmm_matvec, tree, kernel, f, g, out, 3)
+
+
+def fmm_eval_stress(tree, kernel, f=None, g=None, out=None):
+    """KIFMM sum with stress output (D, S, DS), Voigt order; see include/elastobem.h."""
+    return _fmm_eval(_lib.fmm_eval_stress, tree, kernel, f, g, out, 6)
+
+
+def fmm_tree_info(tree):
+    info = TreeInfo()
+    _check(_lib.fmm_tree_info(tree.handle, ctypes.byref(info)))
+    d = {k: getattr(info, k) for k, _ in TreeInfo._fields_}
+    d["origin"] = tuple(info.origin)
+    return d
+
+
+_EXPORT = {"keys": (0, np.int64, 1), "perm": (1, np.int32, 1), "level": (2, np.int32, 1),
+           "anchor": (3, np.int32, 3), "parent": (4, np.int32, 1), "range": (5, np.int32, 2),
+           "U_off": (6, np.int32, 1), "V_off": (7, np.int32, 1), "W_off": (8, np.int32, 1),
+           "X_off": (9, np.int32, 1), "U": (10, np.int32, 1), "V": (11, np.int32, 1),
+           "W": (12, np.int32, 1), "X": (13, np.int32, 1)}
+
+
+def fmm_tree_export(tree, what):
+    code, dt, width = _EXPORT[what]
+    info = fmm_tree_info(tree)
+    n = {0: info["nsrc"] + info["ntrg"], 1: info["nsrc"] + info["ntrg"]}.get(code)
+    if n is None:
+        if 6 <= code <= 9:
+            n = info["nboxes"] + 1
+        elif code >= 10:
+            n = info[["n_u", "n_v", "n_w", "n_x"][code - 10]]
+        else:
+            n = info["nboxes"]
+    buf = np.zeros(max(n, 1) * width, dtype=dt)
+    got = _lib.fmm_tree_export(tree.handle, code, buf.ctypes.data, buf.nbytes)
+    if got < 0:
+        _check(got)
+    buf = buf[: n * width]
+    return buf.reshape(-1, width) if width > 1 else buf
+
+
+def bem_gmres_solve(tree, bc_type, self_U, self_P, bc_val, x, restart=50, max_iter=1000, tol=1e-6):
+    keep = []
+    it = ctypes.c_int32(0)
+    res = ctypes.c_double(0)
+    _check(_lib.bem_gmres_solve(tree.handle, _ptr(bc_type, keep), _ptr(self_U, keep), _ptr(self_P, keep),
+                                _ptr(bc_val, keep), _ptr(x, keep), int(restart), int(max_iter), float(tol),
+                                ctypes.byref(it), ctypes.byref(res), _stream(x)))
+    return x, int(it.value), float(res.value)
+
+
+__all__ = ["bem_kernel_direct", "fmm_build_tree", "fmm_matvec", "fmm_eval_stress", "fmm_tree_info",
+           "fmm_tree_export", "bem_gmres_solve", "FmmTree", "EbemError", "LIB_PATH",
+           "KERNEL_U", "KERNEL_P", "KERNEL_UP", "KERNEL_D", "KERNEL_S", "KERNEL_DS"]

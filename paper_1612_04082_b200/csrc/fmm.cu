@@ -1,0 +1,439 @@
+// KIFMM evaluation (Sec. 2.2) on the tree built by tree.cu:
+//   upward   : S2M (sources -> upward check potential, fp32 pair loop) -> z = Q_u1^T q
+//              M2M (z_P += M2M_c z_C, level by level, fine to coarse)
+//   downward : S2L (X-list sources -> downward check potential) -> w += Q_d1^T q
+//              M2L (w_B += M2L_o z_A, all levels in one launch, grouped by translation o)
+//              L2L (w_C += L2L_c w_P, coarse to fine)
+//   leaves   : phi_d = r R_d^-1 w, phi_u = r R_u^-1 z in fp64; one kernel per target leaf
+//              does L2T + M2T in fp64 and the U-list near field (P2P) in fp32.
+#include <algorithm>
+#include <cstring>
+
+#include "fmm.cuh"
+#include "p2p.cuh"
+
+namespace ebem {
+
+struct BoxGeo {
+    double ox, oy, oz, side;
+    __device__ __forceinline__ void center(const int* anchor, const int* level, int b, double& cx, double& cy,
+                                           double& cz, double& r) const {
+        const double h = side / (double)(1 << level[b]);
+        cx = ox + (anchor[3 * b] + 0.5) * h;
+        cy = oy + (anchor[3 * b + 1] + 0.5) * h;
+        cz = oz + (anchor[3 * b + 2] + 0.5) * h;
+        r = 0.5 * h;
+    }
+};
+
+// ------------------------------------------------------------------ check potentials
+// Entry i: target = check surface of box tbox[i] (radius factor rad), sources = the
+// sources of boxes sidx[soff[i] .. soff[i+1]) (or of tbox[i] itself when soff is null).
+// Output Q[i][3 nc] (fp32).  PAPER.md line 147: the approximation sum_i phi_i K(x_i, y)
+// is fitted to the sources' field on a check surface.
+constexpr int CP_T = 128, CP_TILE = 64;
+
+template <bool SL, bool DL>
+__global__ void __launch_bounds__(CP_T)
+check_potential_kernel(const int* __restrict__ tbox, const int* __restrict__ soff, const int* __restrict__ sidx,
+                       const int* __restrict__ sbeg, const int* __restrict__ send, const int* __restrict__ anchor,
+                       const int* __restrict__ level, BoxGeo geo, double rad, const float* __restrict__ sc, int nc,
+                       const float4* __restrict__ rec, KConst kc, float* __restrict__ Q) {
+    extern __shared__ float smem[];
+    float* acc = smem;                                                  // [3 nc]
+    float4* srec = reinterpret_cast<float4*>(smem + ((3 * nc + 3) & ~3));   // [CP_TILE * 4]
+    const int i = blockIdx.x;
+    const int b = tbox[i];
+    double cx, cy, cz, r;
+    geo.center(anchor, level, b, cx, cy, cz, r);
+    const float R = (float)(rad * r);
+    for (int k = threadIdx.x; k < 3 * nc; k += CP_T) acc[k] = 0.f;
+    const int e0 = soff ? soff[i] : 0, e1 = soff ? soff[i + 1] : 1;
+    for (int e = e0; e < e1; ++e) {
+        const int a = soff ? sidx[e] : b;
+        for (int s0 = sbeg[a]; s0 < send[a]; s0 += CP_TILE) {
+            const int cnt = min(CP_TILE, send[a] - s0);
+            __syncthreads();
+            for (int q = threadIdx.x; q < cnt * REC_DISP; q += CP_T) srec[q] = rec[(int64_t)s0 * REC_DISP + q];
+            __syncthreads();
+            for (int k = threadIdx.x; k < nc; k += CP_T) {
+                float u[3] = {0.f, 0.f, 0.f};
+                float x = (float)cx + R * sc[3 * k], y = (float)cy + R * sc[3 * k + 1], z = (float)cz + R * sc[3 * k + 2];
+                pair_loop<SL, DL, false>(srec, cnt, x, y, z, kc, u);
+                acc[3 * k] += u[0];
+                acc[3 * k + 1] += u[1];
+                acc[3 * k + 2] += u[2];
+            }
+        }
+    }
+    __syncthreads();
+    for (int k = threadIdx.x; k < 3 * nc; k += CP_T) Q[(int64_t)i * 3 * nc + k] = acc[k];
+}
+
+// ------------------------------------------------------------------ leaf evaluation
+// One CTA per target leaf: L2T (own downward equivalent density) and M2T (W list) in
+// fp64 from phi, near field over the U list in fp32, result scattered to caller order.
+constexpr int EV_T = 64, EV_TILE = 64;
+
+template <bool SL, bool DL, bool STRESS>
+__global__ void __launch_bounds__(EV_T)
+leaf_eval_kernel(const int* __restrict__ eval_box, const int* __restrict__ l2t_slot,
+                 const double* __restrict__ PHID, const double* __restrict__ PHIU, const int* __restrict__ phiu_slot,
+                 const int* __restrict__ woff, const int* __restrict__ widx, const int* __restrict__ uoff,
+                 const int* __restrict__ uidx, const int* __restrict__ sbeg, const int* __restrict__ send,
+                 const int* __restrict__ tbeg, const int* __restrict__ tend, const int* __restrict__ anchor,
+                 const int* __restrict__ level, BoxGeo geo, const double* __restrict__ se, int ne,
+                 const float* __restrict__ trg, const int* __restrict__ trg_perm, const float4* __restrict__ rec,
+                 KConst kc, double cfar, float* __restrict__ out) {
+    constexpr int NC = STRESS ? 6 : 3;
+    constexpr int R = STRESS ? REC_STRESS : REC_DISP;
+    extern __shared__ double dsm[];
+    double* ey = dsm;                   // [3 ne] equivalent points
+    double* ephi = dsm + 3 * ne;        // [3 ne] prepared equivalent densities
+    float4* srec = reinterpret_cast<float4*>(dsm + 6 * ne);   // [EV_TILE * R]
+    const int b = eval_box[blockIdx.x];
+    const int t_beg = tbeg[b], t_end = tend[b];
+    for (int t0 = t_beg; t0 < t_end; t0 += EV_T) {
+        const int t = t0 + threadIdx.x;
+        const bool act = t < t_end;
+        const int tc = act ? t : t_beg;
+        const float x = trg[3 * tc], y = trg[3 * tc + 1], z = trg[3 * tc + 2];
+        double acc64[NC];
+        float acc32[NC];
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+            acc64[c] = 0.0;
+            acc32[c] = 0.f;
+        }
+        // far field: own local expansion (L2T) then the W list (M2T)
+        const int nfar = (l2t_slot[blockIdx.x] >= 0 ? 1 : 0) + (woff[b + 1] - woff[b]);
+        for (int e = 0; e < nfar; ++e) {
+            const bool own = (l2t_slot[blockIdx.x] >= 0) && e == 0;
+            const int a = own ? b : widx[woff[b] + e - (l2t_slot[blockIdx.x] >= 0 ? 1 : 0)];
+            const double* phi = own ? PHID + (int64_t)l2t_slot[blockIdx.x] * 3 * ne
+                                    : (phiu_slot[a] >= 0 ? PHIU + (int64_t)phiu_slot[a] * 3 * ne : nullptr);
+            if (!phi) continue;   // box without sources: zero multipole
+            double cx, cy, cz, r;
+            geo.center(anchor, level, a, cx, cy, cz, r);
+            const double Rr = (own ? RAD_DE : RAD_UE) * r;
+            __syncthreads();
+            for (int k = threadIdx.x; k < ne; k += EV_T) {
+                ey[3 * k] = cx + Rr * se[3 * k];
+                ey[3 * k + 1] = cy + Rr * se[3 * k + 1];
+                ey[3 * k + 2] = cz + Rr * se[3 * k + 2];
+                ephi[3 * k] = cfar * phi[3 * k];
+                ephi[3 * k + 1] = cfar * phi[3 * k + 1];
+                ephi[3 * k + 2] = cfar * phi[3 * k + 2];
+            }
+            __syncthreads();
+            const double xd = x, yd = y, zd = z;
+            for (int k = 0; k < ne; ++k) {
+                double dx = xd - ey[3 * k], dy = yd - ey[3 * k + 1], dz = zd - ey[3 * k + 2];
+                double ri = safe_rinv(dx * dx + dy * dy + dz * dz);
+                if (!STRESS)
+                    acc_U<double>(dx, dy, dz, ri, ephi[3 * k], ephi[3 * k + 1], ephi[3 * k + 2], kc.a1d, acc64);
+                else
+                    acc_D<double>(dx, dy, dz, ri, ephi[3 * k], ephi[3 * k + 1], ephi[3 * k + 2], kc.ad, acc64);
+            }
+        }
+        // near field over the U list
+        for (int e = uoff[b]; e < uoff[b + 1]; ++e) {
+            const int a = uidx[e];
+            for (int s0 = sbeg[a]; s0 < send[a]; s0 += EV_TILE) {
+                const int cnt = min(EV_TILE, send[a] - s0);
+                __syncthreads();
+                for (int q = threadIdx.x; q < cnt * R; q += EV_T) srec[q] = rec[(int64_t)s0 * R + q];
+                __syncthreads();
+                pair_loop<SL, DL, STRESS>(srec, cnt, x, y, z, kc, acc32);
+            }
+        }
+        if (act) {
+            float* o = out + (int64_t)trg_perm[t] * NC;
+#pragma unroll
+            for (int c = 0; c < NC; ++c) o[c] = (float)(acc64[c] + (double)acc32[c]);
+        }
+    }
+}
+
+// ------------------------------------------------------------------ schedule (host)
+void schedule_tree(Tree& t, cudaStream_t s) {
+    const Plan& P = *t.plan;
+    const int nb = t.nboxes;
+    auto dl = [&](const DBuf<int>& d, size_t n) {
+        std::vector<int> h(n);
+        if (n) d2h(h.data(), d.p, n, s);
+        return h;
+    };
+    std::vector<int> level = dl(t.level, nb), parent = dl(t.parent, nb), child = dl(t.child, 8 * (size_t)nb),
+                     leaf = dl(t.is_leaf, nb), nsub = dl(t.nsrc_sub, nb), tsub = dl(t.ntrg_sub, nb),
+                     anchor = dl(t.anchor, 3 * (size_t)nb);
+    std::vector<int> off[4], idx[4];
+    for (int k = 0; k < 4; ++k) {
+        off[k] = dl(t.lst_off[k], nb + 1);
+        idx[k] = dl(t.lst_idx[k], t.lst_n[k]);
+    }
+    EB_CUDA(cudaStreamSynchronize(s));
+    t.nleaves = 0;
+    for (int b = 0; b < nb; ++b) t.nleaves += leaf[b];
+
+    std::vector<int> up(nb, -1), dn(nb, -1);
+    t.n_up = t.n_dn = 0;
+    for (int b = 0; b < nb; ++b) {
+        if (level[b] >= 2 && nsub[b] > 0) up[b] = t.n_up++;
+        if (level[b] >= 2 && tsub[b] > 0) dn[b] = t.n_dn++;
+    }
+    t.up_slot.alloc(nb);
+    t.dn_slot.alloc(nb);
+    h2d(t.up_slot.p, up.data(), nb, s);
+    h2d(t.dn_slot.p, dn.data(), nb, s);
+
+    // S2M on leaves carrying z; check potential rows are s2m indices
+    std::vector<int> s2m;
+    std::vector<int> op1;
+    std::vector<int2> pr;
+    for (int b = 0; b < nb; ++b)
+        if (leaf[b] && up[b] >= 0) {
+            pr.push_back(make_int2(up[b], (int)s2m.size()));
+            s2m.push_back(b);
+        }
+    t.n_s2m = (int)s2m.size();
+    t.s2m_box.alloc(std::max<size_t>(s2m.size(), 1));
+    h2d(t.s2m_box.p, s2m.data(), s2m.size(), s);
+    op1.assign(pr.size(), 0);
+    build_op_pairs(t.q2z_up, 1, op1, pr, s);
+
+    // M2M per parent level
+    t.m2m.clear();
+    t.m2m.resize(t.nlevels);
+    for (int l = 2; l < t.nlevels; ++l) {
+        std::vector<int> op;
+        std::vector<int2> p2;
+        for (int b = t.level_start[l]; b < t.level_start[l + 1]; ++b) {
+            if (leaf[b] || up[b] < 0) continue;
+            for (int c = 0; c < 8; ++c) {
+                int ch = child[8 * b + c];
+                if (ch >= 0 && up[ch] >= 0) {
+                    op.push_back(c);
+                    p2.push_back(make_int2(up[b], up[ch]));
+                }
+            }
+        }
+        build_op_pairs(t.m2m[l], 8, op, p2, s);
+    }
+
+    // S2L: boxes with X-list leaves that hold sources
+    std::vector<int> s2l, xoff(1, 0), xidx;
+    pr.clear();
+    for (int b = 0; b < nb; ++b) {
+        if (dn[b] < 0) continue;
+        int cnt = 0;
+        for (int e = off[3][b]; e < off[3][b + 1]; ++e)
+            if (nsub[idx[3][e]] > 0) {
+                xidx.push_back(idx[3][e]);
+                ++cnt;
+            }
+        if (cnt) {
+            pr.push_back(make_int2(dn[b], (int)s2l.size()));
+            s2l.push_back(b);
+            xoff.push_back((int)xidx.size());
+        }
+    }
+    t.n_s2l = (int)s2l.size();
+    t.s2l_box.alloc(std::max<size_t>(s2l.size(), 1));
+    h2d(t.s2l_box.p, s2l.data(), s2l.size(), s);
+    t.x_src_off.alloc(xoff.size());
+    h2d(t.x_src_off.p, xoff.data(), xoff.size(), s);
+    t.x_src_idx.alloc(std::max<size_t>(xidx.size(), 1));
+    h2d(t.x_src_idx.p, xidx.data(), xidx.size(), s);
+    op1.assign(pr.size(), 0);
+    build_op_pairs(t.q2z_dn, 1, op1, pr, s);
+
+    // M2L, all levels, grouped by translation vector
+    {
+        std::vector<int> op;
+        std::vector<int2> p2;
+        for (int b = 0; b < nb; ++b) {
+            if (dn[b] < 0) continue;
+            for (int e = off[1][b]; e < off[1][b + 1]; ++e) {
+                int a = idx[1][e];
+                if (up[a] < 0) continue;
+                int ox = anchor[3 * a] - anchor[3 * b], oy = anchor[3 * a + 1] - anchor[3 * b + 1],
+                    oz = anchor[3 * a + 2] - anchor[3 * b + 2];
+                int o = P.off_index[(ox + 3) * 49 + (oy + 3) * 7 + (oz + 3)];
+                EB_REQUIRE(o >= 0, "internal: V-list offset outside the 7^3 stencil");
+                op.push_back(o);
+                p2.push_back(make_int2(dn[b], up[a]));
+            }
+        }
+        build_op_pairs(t.m2l, NV_OFFSETS, op, p2, s);
+    }
+
+    // L2L per child level
+    t.l2l.clear();
+    t.l2l.resize(t.nlevels);
+    for (int l = 3; l < t.nlevels; ++l) {
+        std::vector<int> op;
+        std::vector<int2> p2;
+        for (int b = t.level_start[l]; b < t.level_start[l + 1]; ++b) {
+            if (dn[b] < 0) continue;
+            int par = parent[b];
+            if (dn[par] < 0) continue;
+            int oc = ((anchor[3 * b] & 1) << 2) | ((anchor[3 * b + 1] & 1) << 1) | (anchor[3 * b + 2] & 1);
+            op.push_back(oc);
+            p2.push_back(make_int2(dn[b], dn[par]));
+        }
+        build_op_pairs(t.l2l[l], 8, op, p2, s);
+    }
+
+    // leaf evaluation
+    std::vector<int> ev, l2t, phid_box, phiu_box, phiu(nb, -1);
+    std::vector<double> phid_scale, phiu_scale;
+    std::vector<int2> prd, pru;
+    auto half = [&](int b) { return t.side / (double)(1 << level[b]) * 0.5; };
+    for (int b = 0; b < nb; ++b) {
+        if (!leaf[b] || tsub[b] == 0) continue;
+        ev.push_back(b);
+        if (dn[b] >= 0) {
+            l2t.push_back((int)phid_box.size());
+            prd.push_back(make_int2((int)phid_box.size(), dn[b]));
+            phid_scale.push_back(half(b));
+            phid_box.push_back(b);
+        } else {
+            l2t.push_back(-1);
+        }
+        for (int e = off[2][b]; e < off[2][b + 1]; ++e) {
+            int a = idx[2][e];
+            if (up[a] >= 0 && phiu[a] < 0) {
+                phiu[a] = (int)phiu_box.size();
+                pru.push_back(make_int2(phiu[a], up[a]));
+                phiu_scale.push_back(half(a));
+                phiu_box.push_back(a);
+            }
+        }
+    }
+    t.n_eval = (int)ev.size();
+    t.n_phid = (int)phid_box.size();
+    t.n_phiu = (int)phiu_box.size();
+    t.eval_box.alloc(std::max<size_t>(ev.size(), 1));
+    h2d(t.eval_box.p, ev.data(), ev.size(), s);
+    t.eval_l2t_slot.alloc(std::max<size_t>(l2t.size(), 1));
+    h2d(t.eval_l2t_slot.p, l2t.data(), l2t.size(), s);
+    t.phiu_slot.alloc(nb);
+    h2d(t.phiu_slot.p, phiu.data(), nb, s);
+    t.phid_scale.alloc(std::max<size_t>(phid_scale.size(), 1));
+    h2d(t.phid_scale.p, phid_scale.data(), phid_scale.size(), s);
+    t.phiu_scale.alloc(std::max<size_t>(phiu_scale.size(), 1));
+    h2d(t.phiu_scale.p, phiu_scale.data(), phiu_scale.size(), s);
+    op1.assign(prd.size(), 0);
+    build_op_pairs(t.phid_pairs, 1, op1, prd, s);
+    op1.assign(pru.size(), 0);
+    build_op_pairs(t.phiu_pairs, 1, op1, pru, s);
+
+    // workspace
+    const int me = P.me, mc = P.mc;
+    t.rec_disp.alloc(std::max<int64_t>(t.nsrc * REC_DISP, 1));
+    t.rec_stress.alloc(std::max<int64_t>(t.nsrc * REC_STRESS, 1));
+    t.Q.alloc((size_t)std::max(1, std::max(t.n_s2m, t.n_s2l)) * mc);
+    t.Z.alloc((size_t)std::max(1, t.n_up) * me);
+    t.W.alloc((size_t)std::max(1, t.n_dn) * me);
+    t.PHID.alloc((size_t)std::max(1, t.n_phid) * me);
+    t.PHIU.alloc((size_t)std::max(1, t.n_phiu) * me);
+    EB_CUDA(cudaStreamSynchronize(s));
+
+    int64_t bytes = 0;
+    bytes += t.keys.bytes() + t.perm.bytes() + t.src_perm.bytes() + t.trg_perm.bytes() + t.src_xyz.bytes() +
+             t.src_nrm.bytes() + t.src_w.bytes() + t.trg_xyz.bytes();
+    bytes += (int64_t)nb * 4 * 40;
+    for (int k = 0; k < 4; ++k) bytes += t.lst_off[k].bytes() + t.lst_idx[k].bytes();
+    bytes += t.rec_disp.bytes() + t.rec_stress.bytes() + t.Q.bytes() + t.Z.bytes() + t.W.bytes() + t.PHID.bytes() +
+             t.PHIU.bytes();
+    bytes += t.m2l.pairs.bytes();
+    t.device_bytes = bytes;
+}
+
+// ------------------------------------------------------------------ evaluation
+template <bool SL, bool DL>
+static void launch_check(const Tree& t, const int* tbox, int n, const int* soff, const int* sidx, double rad,
+                         cudaStream_t s) {
+    if (n == 0) return;
+    const Plan& P = *t.plan;
+    BoxGeo geo{t.origin[0], t.origin[1], t.origin[2], t.side};
+    size_t sm = sizeof(float) * ((3 * P.nc + 3) & ~3) + sizeof(float4) * CP_TILE * REC_DISP;
+    KConst kc = make_kconst(t.mat);
+    check_potential_kernel<SL, DL><<<n, CP_T, sm, s>>>(tbox, soff, sidx, t.sbeg.p, t.send.p, t.anchor.p, t.level.p,
+                                                       geo, rad, P.s_c.p, P.nc, t.rec_disp.p, kc, t.Q.p);
+    EB_CHECK_LAUNCH();
+}
+
+template <bool SL, bool DL, bool STRESS>
+static void launch_eval(const Tree& t, float* out, cudaStream_t s) {
+    if (t.n_eval == 0) return;
+    const Plan& P = *t.plan;
+    BoxGeo geo{t.origin[0], t.origin[1], t.origin[2], t.side};
+    constexpr int R = STRESS ? REC_STRESS : REC_DISP;
+    size_t sm = sizeof(double) * 6 * P.ne + sizeof(float4) * EV_TILE * R;
+    KConst kc = make_kconst(t.mat);
+    const double cfar = STRESS ? t.mat.cD : t.mat.cU;
+    auto kfn = leaf_eval_kernel<SL, DL, STRESS>;
+    if (sm > 48 * 1024) EB_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    kfn<<<t.n_eval, EV_T, sm, s>>>(t.eval_box.p, t.eval_l2t_slot.p, t.PHID.p, t.PHIU.p, t.phiu_slot.p,
+                                   t.lst_off[2].p, t.lst_idx[2].p, t.lst_off[0].p, t.lst_idx[0].p, t.sbeg.p,
+                                   t.send.p, t.tbeg.p, t.tend.p, t.anchor.p, t.level.p, geo, P.s_e64.p, P.ne,
+                                   t.trg_xyz.p, t.trg_perm.p, STRESS ? t.rec_stress.p : t.rec_disp.p, kc, cfar, out);
+    EB_CHECK_LAUNCH();
+}
+
+void fmm_evaluate(Tree& t, int kernel, const float* f, const float* g, float* out, cudaStream_t s) {
+    const Plan& P = *t.plan;
+    const int me = P.me, mc = P.mc;
+    const bool stress = kernel_stress(kernel);
+    const bool sl = kernel_sl(kernel), dl = kernel_dl(kernel);
+    const int src_kernel = stress ? kernel - 3 : kernel;    // D->U, S->P, DS->UP
+    EB_REQUIRE(!dl || t.has_normals, "double-layer kernel needs normals at fmm_build_tree");
+    if (t.ntrg == 0) return;
+
+    // prepared sources in tree order (geometry sorted, densities via src_perm)
+    prepare_sources(src_kernel, t.mat, t.src_xyz.p, t.src_nrm.p, t.src_w.p, nullptr, f, g, t.src_perm.p, t.nsrc,
+                    t.rec_disp.p, s);
+    if (stress)
+        prepare_sources(kernel, t.mat, t.src_xyz.p, t.src_nrm.p, t.src_w.p, nullptr, f, g, t.src_perm.p, t.nsrc,
+                        t.rec_stress.p, s);
+    t.Z.zero(s);
+    t.W.zero(s);
+
+    // upward pass
+    if (sl && dl) launch_check<true, true>(t, t.s2m_box.p, t.n_s2m, nullptr, nullptr, RAD_UC, s);
+    else if (sl) launch_check<true, false>(t, t.s2m_box.p, t.n_s2m, nullptr, nullptr, RAD_UC, s);
+    else launch_check<false, true>(t, t.s2m_box.p, t.n_s2m, nullptr, nullptr, RAD_UC, s);
+    gemm_pairs_f32(t.q2z_up, P.Qu1T.p, me, mc, t.Q.p, mc, t.Z.p, me, s);
+    for (int l = t.nlevels - 1; l >= 2; --l) gemm_pairs_f32(t.m2m[l], P.M2M.p, me, me, t.Z.p, me, t.Z.p, me, s);
+
+    // downward pass
+    if (t.n_s2l) {
+        if (sl && dl) launch_check<true, true>(t, t.s2l_box.p, t.n_s2l, t.x_src_off.p, t.x_src_idx.p, RAD_DC, s);
+        else if (sl) launch_check<true, false>(t, t.s2l_box.p, t.n_s2l, t.x_src_off.p, t.x_src_idx.p, RAD_DC, s);
+        else launch_check<false, true>(t, t.s2l_box.p, t.n_s2l, t.x_src_off.p, t.x_src_idx.p, RAD_DC, s);
+        gemm_pairs_f32(t.q2z_dn, P.Qd1T.p, me, mc, t.Q.p, mc, t.W.p, me, s);
+    }
+    gemm_pairs_f32(t.m2l, P.M2L.p, me, me, t.Z.p, me, t.W.p, me, s);
+    for (int l = 3; l < t.nlevels; ++l) gemm_pairs_f32(t.l2l[l], P.L2L.p, me, me, t.W.p, me, t.W.p, me, s);
+
+    // equivalent densities (fp64) and leaf evaluation
+    gemm_pairs_f64(t.phid_pairs, P.Rdinv.p, me, me, t.W.p, me, t.phid_scale.p, t.PHID.p, me, s);
+    gemm_pairs_f64(t.phiu_pairs, P.Ruinv.p, me, me, t.Z.p, me, t.phiu_scale.p, t.PHIU.p, me, s);
+    switch (kernel) {
+        case K_U: launch_eval<true, false, false>(t, out, s); break;
+        case K_P: launch_eval<false, true, false>(t, out, s); break;
+        case K_UP: launch_eval<true, true, false>(t, out, s); break;
+        case K_D: launch_eval<true, false, true>(t, out, s); break;
+        case K_S: launch_eval<false, true, true>(t, out, s); break;
+        case K_DS: launch_eval<true, true, true>(t, out, s); break;
+    }
+}
+
+int gmres_solve(Tree&, const int32_t*, const float*, const float*, const float*, float*, int, int, double, int32_t*,
+                double*, cudaStream_t) {
+    throw Error("bem_gmres_solve: not available in this build");
+}
+
+}  // namespace ebem

@@ -1,0 +1,147 @@
+// Tree, plan and pass declarations of the B200 KIFMM (Sec. 2.2).
+//
+// Representation ("well-conditioned KIFMM state"): the paper's
+// equivalent densities phi (line 147) are never stored in fp32.  Each box keeps the
+// rotated check potential
+//     z_B = Q_u1^T q_u(B)   (upward)      w_B = Q_d1^T q_d(B)   (downward)
+// where [K_uc<-ue ; a I] = Q_u R_u is the QR factorisation of the Tikhonov-augmented
+// check-to-equivalent kernel matrix at unit scale (Q_u1 = its first 3 n_c rows), so
+// phi = r R_u^-1 z.  The M2M / M2L / L2L operators of line 149 become composites
+//     M2M_c = Q_u1^T (1/2 K(uc_P, ue_C)) R_u^-1,  M2L_o = Q_d1^T K(dc_B, ue_A) R_u^-1,
+//     L2L_c = Q_d1^T K(dc_C, de_P) R_d^-1
+// computed once in fp64 and applied in fp32: they map well-scaled vectors to
+// well-scaled vectors (|z| <= |q|), so fp32 rounding is not amplified by the
+// ill-conditioned solve.  phi is only formed (in fp64) for the leaf evaluations
+// L2T and M2T.
+#pragma once
+#include <map>
+#include <memory>
+#include <mutex>
+
+#include "../../include/elastobem.h"
+#include "common.cuh"
+
+namespace ebem {
+
+constexpr int MAXLEVEL = 20;
+constexpr double RAD_UE = 1.05, RAD_UC = 2.95, RAD_DE = 2.95, RAD_DC = 1.05;
+constexpr int NV_OFFSETS = 316;        // 7^3 - 3^3 M2L translation vectors
+
+// ------------------------------------------------------------------ plan (operators)
+struct Plan {
+    int p = 0, pc = 0;          // equivalent / check surface points per edge (pc = p + 1)
+    int ne = 0, nc = 0;         // surface point counts
+    int me = 0, mc = 0;         // 3 ne, 3 nc (vector lengths)
+    double rcond = 0;
+    Material mat{};
+    DBuf<float> s_e, s_c;       // unit surface grids [ne*3], [nc*3] (fp32 copies)
+    DBuf<double> s_e64, s_c64;
+    DBuf<float> Qu1T, Qd1T;     // [me x mc] row-major: z = Qu1T q
+    DBuf<double> Ruinv, Rdinv;  // [me x me] row-major upper triangular: phi = r Rinv z
+    DBuf<float> M2M, L2L;       // [8][me x me]
+    DBuf<float> M2L;            // [316][me x me]
+    int off_index[343];         // (ox+3)*49+(oy+3)*7+(oz+3) -> 0..315 or -1
+};
+
+std::shared_ptr<Plan> get_plan(int p, const Material& m, cudaStream_t s);
+
+// ------------------------------------------------------------------ pair lists
+// Work grouped by operator: pairs (target row, source row) sorted by op.
+struct OpPairs {
+    int nops = 0;
+    int64_t npairs = 0;
+    DBuf<int> op_ptr;            // [nops+1]
+    DBuf<int2> pairs;            // [npairs] (target row, source row)
+    std::vector<int> op_ptr_h;   // host copy (launch sizing)
+    int max_per_op = 0;
+};
+
+// ------------------------------------------------------------------ tree
+struct Tree {
+    int64_t nsrc = 0, ntrg = 0, npts = 0;
+    int max_pts = 0, p = 0;
+    Material mat{};
+    bool has_normals = false, has_weights = false;
+    double origin[3] = {0, 0, 0}, side = 1;
+    int nlevels = 0, nboxes = 0, nleaves = 0;
+    std::vector<int> level_start;       // host [nlevels+1]
+
+    // points, sorted by Morton key (stable: sources first, then targets)
+    DBuf<long long> keys;               // [npts]
+    DBuf<int> perm;                     // sorted pos -> original point index
+    DBuf<int> src_perm, trg_perm;       // sorted source/target pos -> original index
+    DBuf<float> src_xyz, src_nrm, src_w, trg_xyz;   // sorted copies
+
+    // boxes (level then Morton order)
+    DBuf<int> level, anchor, parent, child, pbeg, pend;
+    DBuf<int> sbeg, send, tbeg, tend;   // ranges in the sorted source / target arrays
+    DBuf<int> nsrc_sub, ntrg_sub;       // sources / targets in the subtree (= in range)
+    DBuf<long long> bkey;               // Morton key of the box at its level
+    DBuf<int> is_leaf;
+    DBuf<int> colleague;                // [nboxes*27] same-level neighbours (-1 absent)
+    DBuf<int> lst_off[4], lst_idx[4];   // U, V, W, X lists (CSR, ascending ids)
+    int64_t lst_n[4] = {0, 0, 0, 0};
+
+    // execution plan
+    std::shared_ptr<Plan> plan;
+    int n_up = 0;                        // boxes carrying z (level >= 2, sources in subtree)
+    DBuf<int> up_slot;                   // box -> row in Z (-1 none)
+    int n_dn = 0;                        // boxes carrying w (level >= 2, targets in subtree)
+    DBuf<int> dn_slot;                   // box -> row in W (-1 none)
+    // S2M: leaves with sources (rows of Z); S2L: boxes with X lists (rows of W)
+    int n_s2m = 0, n_s2l = 0;
+    DBuf<int> s2m_box, s2l_box;
+    DBuf<int> x_src_off, x_src_idx;       // S2L: per s2l box, the X-list leaves (source boxes)
+    OpPairs q2z_up, q2z_dn;              // check potential -> z / w (single op)
+    std::vector<OpPairs> m2m;            // per level (parents at that level), 8 ops
+    OpPairs m2l;                         // all levels, 316 ops
+    std::vector<OpPairs> l2l;            // per level (children at that level), 8 ops
+    // leaf evaluation
+    int n_eval = 0;                      // leaves with targets
+    DBuf<int> eval_box;                  // [n_eval]
+    DBuf<int> eval_l2t_slot;             // row in PHI_D (-1 if leaf level < 2)
+    int n_phid = 0;                      // leaves with L2T
+    DBuf<int> phid_box;                  // [n_phid] (box ids) for the fp64 phi reconstruction
+    int n_phiu = 0;                      // boxes appearing in some W list (with sources)
+    DBuf<int> phiu_box, phiu_slot;       // [n_phiu] box ids; box -> row in PHI_U (-1)
+    OpPairs phid_pairs, phiu_pairs;      // single-op pairs for the fp64 reconstruction GEMM
+    DBuf<double> phid_scale, phiu_scale; // half-width r of the box of each PHI row
+
+    // workspace (allocated at build time; evaluation allocates nothing)
+    DBuf<float4> rec_disp, rec_stress;   // prepared sources, tree order
+    DBuf<float> Q;                       // check potentials [max(n_s2m, n_s2l) x mc]
+    DBuf<float> Z, W;                    // [n_up x me], [n_dn x me]
+    DBuf<double> PHID, PHIU;             // [n_phid x me], [n_phiu x me]
+    DBuf<float> out_sorted;              // [ntrg x 6]
+    int64_t device_bytes = 0;
+};
+
+Tree* build_tree(const float* src, const float* nrm, const float* w, int64_t nsrc, const float* trg,
+                 int64_t ntrg, int max_pts, int p, const Material& m, cudaStream_t s);
+void fmm_evaluate(Tree& t, int kernel, const float* f, const float* g, float* out, cudaStream_t s);
+void tree_info(const Tree& t, ebem_tree_info* info);
+int64_t tree_export(const Tree& t, int what, void* buf, int64_t cap);
+int gmres_solve(Tree& t, const int32_t* bc_type, const float* self_U, const float* self_P,
+                const float* bc_val, float* x, int restart, int max_iter, double tol,
+                int32_t* iters_out, double* resid_out, cudaStream_t s);
+
+// ------------------------------------------------------------------ primitives (linalg.cu)
+// exclusive scan of n ints (out may alias in); returns the total on the host (syncs)
+int64_t exclusive_scan_i32(const int* in, int* out, int64_t n, cudaStream_t s);
+// stable LSD radix sort of (key, value) pairs on the low `bits` bits of the keys
+void radix_sort_pairs(long long* keys, int* vals, int64_t n, int bits, cudaStream_t s);
+// C[b] = alpha * A[b] * B[b] (+ beta C[b]); row-major; fp64; batch strides in elements
+void gemm_f64(int m, int n, int k, double alpha, const double* A, int64_t sA, int lda,
+              const double* B, int64_t sB, int ldb, double beta, double* C, int64_t sC, int ldc,
+              int batch, cudaStream_t s);
+// pairs GEMM: Y[t] += Mat[op] * X[src] for every pair (t, src) of every op; Mat row-major
+// [M x K]; X rows of length ldx >= K; Y rows of length ldy >= M.  fp32.
+void gemm_pairs_f32(const OpPairs& P, const float* mats, int M, int K, const float* X, int ldx,
+                    float* Y, int ldy, cudaStream_t s);
+// fp64 variant with per-pair scale (r of the box, looked up from scale[t])
+void gemm_pairs_f64(const OpPairs& P, const double* mat, int M, int K, const float* X, int ldx,
+                    const double* scale, double* Y, int ldy, cudaStream_t s);
+void build_op_pairs(OpPairs& P, int nops, const std::vector<int>& op, const std::vector<int2>& pr,
+                    cudaStream_t s);
+
+}  // namespace ebem

@@ -1,0 +1,84 @@
+// Prepared source records and the shared-memory tiled pair loops used by the direct
+// sum (bem_kernel_direct) and by every point-to-point-like FMM pass (near field, S2M,
+// S2L).  PAPER.md Eq. fmm_summation: t_i = sum_j K(x_i, y_j, n_j) s_j.
+#pragma once
+#include "common.cuh"
+#include "elastic.cuh"
+
+namespace ebem {
+
+enum KernelId { K_U = 0, K_P = 1, K_UP = 2, K_D = 3, K_S = 4, K_DS = 5 };
+
+inline bool kernel_sl(int k) { return k == K_U || k == K_UP || k == K_D || k == K_DS; }
+inline bool kernel_dl(int k) { return k == K_P || k == K_UP || k == K_S || k == K_DS; }
+inline bool kernel_stress(int k) { return k >= K_D; }
+inline int kernel_ncomp(int k) { return kernel_stress(k) ? 6 : 3; }
+
+// Per-source record, 4 float4 (displacement family) or 6 float4 (stress family):
+//   disp   : [y.xyz, q=a (n.g)] [f = cU w f, 0] [g = cP w g, 0] [n, 0]
+//   stress : [y.xyz, ng = n.g]  [f = cD w f, 0] [g = cS w g, 0] [n, 0]
+//            [NG_xx, NG_yy, NG_zz, NG_xy] [NG_yz, NG_xz, 0, 0],  NG = a (n g^T + g n^T)
+constexpr int REC_DISP = 4;
+constexpr int REC_STRESS = 6;
+
+struct KConst {
+    float a1, a, nu, b4;
+    double a1d, ad, nud, b4d;
+};
+
+inline KConst make_kconst(const Material& m) {
+    KConst k;
+    k.a1 = (float)m.a1; k.a = (float)m.a; k.nu = (float)m.nu; k.b4 = (float)m.b4;
+    k.a1d = m.a1; k.ad = m.a; k.nud = m.nu; k.b4d = m.b4;
+    return k;
+}
+
+// Build prepared records.  Record i takes its geometry (y, nrm, w) from index
+// gperm[i] and its densities (f, g) from index dperm[i] (null perm = identity), so the
+// FMM can combine tree-ordered geometry with caller-ordered densities.  w/f/g/nrm may
+// be null where the kernel does not use them (w null = 1).
+void prepare_sources(int kernel, const Material& m, const float* y, const float* nrm,
+                     const float* w, const int* gperm, const float* f, const float* g,
+                     const int* dperm, int64_t n, float4* rec, cudaStream_t s);
+
+// ------------------------------------------------------------------ pair loop
+// Accumulate the interactions of `cnt` prepared sources staged in shared memory
+// (srec, stride R float4) into one target's accumulator acc[3 or 6].
+template <bool SL, bool DL, bool STRESS>
+__device__ __forceinline__ void pair_loop(const float4* __restrict__ srec, int cnt, float x, float y,
+                                          float z, const KConst& kc, float* acc) {
+    constexpr int R = STRESS ? REC_STRESS : REC_DISP;
+#pragma unroll 4
+    for (int j = 0; j < cnt; ++j) {
+        const float4 p = srec[j * R + 0];
+        float dx = x - p.x, dy = y - p.y, dz = z - p.z;
+        float r2 = dx * dx + dy * dy + dz * dz;
+        float ri = safe_rinv(r2);
+        if (!STRESS) {
+            if (SL) {
+                const float4 f = srec[j * R + 1];
+                acc_U(dx, dy, dz, ri, f.x, f.y, f.z, kc.a1, acc);
+            }
+            if (DL) {
+                const float4 g = srec[j * R + 2];
+                const float4 n = srec[j * R + 3];
+                acc_P(dx, dy, dz, ri, g.x, g.y, g.z, n.x, n.y, n.z, p.w, kc.a, acc);
+            }
+        } else {
+            if (SL) {
+                const float4 f = srec[j * R + 1];
+                acc_D(dx, dy, dz, ri, f.x, f.y, f.z, kc.a, acc);
+            }
+            if (DL) {
+                const float4 g = srec[j * R + 2];
+                const float4 n = srec[j * R + 3];
+                const float4 t0 = srec[j * R + 4];
+                const float4 t1 = srec[j * R + 5];
+                const float NG[6] = {t0.x, t0.y, t0.z, t0.w, t1.x, t1.y};
+                acc_S(dx, dy, dz, ri, g.x, g.y, g.z, n.x, n.y, n.z, p.w, NG, kc.a, kc.nu, kc.b4, acc);
+            }
+        }
+    }
+}
+
+}  // namespace ebem

@@ -1,0 +1,313 @@
+// KIFMM operator precomputation (fp64, on the device): "The M2M, L2L
+// and M2L operators needed in the algorithm, in the case of KIFMM are represented by
+// matrices mapping density values on different equivalent surfaces to each other, and
+// are computed automatically for each needed kernel."
+//
+// Reading R6: cube surfaces with p points per edge (equivalent) and p+1
+// (check); radii 1.05 / 2.95; Tikhonov-regularised check->equivalent solve with
+// a = rcond * s_max(K), rcond = max(1e-9, 10^-(p+1)).  The solve is factored as
+// [K; a I] = Q R (classical Gram-Schmidt with one full re-orthogonalisation, fp64), so
+// the Tikhonov pseudo-inverse is R^-1 Q_1^T (Q_1 = first 3 n_c rows of Q).
+#include <cmath>
+
+#include "elastic.cuh"
+#include "fmm.cuh"
+
+namespace ebem {
+
+static std::vector<double> surface_grid(int p) {
+    std::vector<double> out;
+    for (int i = 0; i < p; ++i)
+        for (int j = 0; j < p; ++j)
+            for (int k = 0; k < p; ++k)
+                if (i == 0 || i == p - 1 || j == 0 || j == p - 1 || k == 0 || k == p - 1) {
+                    double t[3] = {-1.0 + 2.0 * i / (p - 1), -1.0 + 2.0 * j / (p - 1), -1.0 + 2.0 * k / (p - 1)};
+                    out.insert(out.end(), t, t + 3);
+                }
+    return out;
+}
+
+// K[b] (3nx x 3ny, row-major, ld = ldk) with X_i = xo[b] + xs sx_i, Y_j = yo[b] + ys sy_j,
+// U kernel (PAPER.md Eq. disp_1), times scale.
+__global__ void kmat_kernel(const double* __restrict__ sx, int nx, double xs, const double* __restrict__ sy,
+                            int ny, double ys, const double* __restrict__ xo, const double* __restrict__ yo,
+                            double cU, double a1, double scale, double* __restrict__ K, int64_t strideK) {
+    const int b = blockIdx.y;
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= (int64_t)nx * ny) return;
+    const int i = (int)(e / ny), j = (int)(e % ny);
+    double dx = xo[3 * b] + xs * sx[3 * i] - (yo[3 * b] + ys * sy[3 * j]);
+    double dy = xo[3 * b + 1] + xs * sx[3 * i + 1] - (yo[3 * b + 1] + ys * sy[3 * j + 1]);
+    double dz = xo[3 * b + 2] + xs * sx[3 * i + 2] - (yo[3 * b + 2] + ys * sy[3 * j + 2]);
+    double r = sqrt(dx * dx + dy * dy + dz * dz);
+    double d[3] = {dx / r, dy / r, dz / r};
+    double c = scale * cU / r;
+    double* Kb = K + b * strideK;
+    const int ld = 3 * ny;
+    for (int a = 0; a < 3; ++a)
+        for (int q = 0; q < 3; ++q)
+            Kb[(int64_t)(3 * i + a) * ld + 3 * j + q] = c * ((a == q ? a1 : 0.0) + d[a] * d[q]);
+}
+
+static void kmat(const Plan& P, const DBuf<double>& sx, int nx, double xs, const DBuf<double>& sy, int ny,
+                 double ys, const std::vector<double>& xo, const std::vector<double>& yo, double scale,
+                 double* K, int batch, cudaStream_t s) {
+    DBuf<double> dxo(3 * batch), dyo(3 * batch);
+    h2d(dxo.p, xo.data(), 3 * batch, s);
+    h2d(dyo.p, yo.data(), 3 * batch, s);
+    dim3 grid(ceil_div((int64_t)nx * ny, 256), batch);
+    kmat_kernel<<<grid, 256, 0, s>>>(sx.p, nx, xs, sy.p, ny, ys, dxo.p, dyo.p, P.mat.cU, P.mat.a1, scale, K,
+                                     (int64_t)9 * nx * ny);
+    EB_CHECK_LAUNCH();
+    EB_CUDA(cudaStreamSynchronize(s));
+}
+
+// ------------------------------------------------------------------ CGS2 QR
+__global__ void cgs_dots(const double* __restrict__ Q, int m, const double* __restrict__ v, double* __restrict__ r) {
+    const int k = blockIdx.x;
+    __shared__ double sh[256];
+    double s = 0.0;
+    for (int i = threadIdx.x; i < m; i += 256) s += Q[(int64_t)k * m + i] * v[i];
+    sh[threadIdx.x] = s;
+    __syncthreads();
+    for (int o = 128; o > 0; o >>= 1) {
+        if (threadIdx.x < o) sh[threadIdx.x] += sh[threadIdx.x + o];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) r[k] = sh[0];
+}
+
+__global__ void cgs_update(const double* __restrict__ Q, int m, int j, const double* __restrict__ r,
+                           double* __restrict__ v, double* __restrict__ Rcol) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < m) {
+        double s = 0.0;
+        for (int k = 0; k < j; ++k) s += Q[(int64_t)k * m + i] * r[k];
+        v[i] -= s;
+    }
+    if (i < j) Rcol[i] += r[i];
+}
+
+__global__ void cgs_finish(double* __restrict__ Q, int m, int j, const double* __restrict__ v,
+                           double* __restrict__ Rjj) {
+    __shared__ double sh[256];
+    double s = 0.0;
+    for (int i = threadIdx.x; i < m; i += 256) s += v[i] * v[i];
+    sh[threadIdx.x] = s;
+    __syncthreads();
+    for (int o = 128; o > 0; o >>= 1) {
+        if (threadIdx.x < o) sh[threadIdx.x] += sh[threadIdx.x + o];
+        __syncthreads();
+    }
+    const double nrm = sqrt(sh[0]);
+    for (int i = threadIdx.x; i < m; i += 256) Q[(int64_t)j * m + i] = v[i] / nrm;
+    if (threadIdx.x == 0) *Rjj = nrm;
+}
+
+// A (m x n) column-major in Q on entry; on exit Q has orthonormal columns and R (n x n,
+// column-major, upper) satisfies A = Q R.
+static void cgs2_qr(double* Q, int m, int n, double* R, cudaStream_t s) {
+    DBuf<double> v(m), r(n);
+    EB_CUDA(cudaMemsetAsync(R, 0, sizeof(double) * n * n, s));
+    for (int j = 0; j < n; ++j) {
+        d2d(v.p, Q + (int64_t)j * m, m, s);
+        for (int pass = 0; pass < 2 && j > 0; ++pass) {
+            cgs_dots<<<j, 256, 0, s>>>(Q, m, v.p, r.p);
+            cgs_update<<<ceil_div(std::max(m, j), 256), 256, 0, s>>>(Q, m, j, r.p, v.p, R + (int64_t)j * n);
+        }
+        cgs_finish<<<1, 256, 0, s>>>(Q, m, j, v.p, R + (int64_t)j * n + j);
+    }
+    EB_CHECK_LAUNCH();
+}
+
+// X = R^-1 (both n x n; R column-major upper, X row-major upper), row i from the bottom:
+// X[i, :] = (e_i - sum_{k>i} R[i,k] X[k, :]) / R[i,i]
+__global__ void trinv_row(const double* __restrict__ R, int n, int i, double* __restrict__ X) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= n) return;
+    double s = (i == j) ? 1.0 : 0.0;
+    for (int k = i + 1; k <= j; ++k) s -= R[(int64_t)k * n + i] * X[(int64_t)k * n + j];
+    X[(int64_t)i * n + j] = (j < i) ? 0.0 : s / R[(int64_t)i * n + i];
+}
+
+__global__ void power_step(const double* __restrict__ K, int m, int n, const double* __restrict__ v,
+                           double* __restrict__ t) {
+    // t = K v  (K row-major m x n)
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= m) return;
+    double s = 0.0;
+    for (int j = 0; j < n; ++j) s += K[(int64_t)i * n + j] * v[j];
+    t[i] = s;
+}
+__global__ void power_stepT(const double* __restrict__ K, int m, int n, const double* __restrict__ t,
+                            double* __restrict__ v) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= n) return;
+    double s = 0.0;
+    for (int i = 0; i < m; ++i) s += K[(int64_t)i * n + j] * t[i];
+    v[j] = s;
+}
+
+// largest singular value of K (row-major m x n) by 60 power iterations on K^T K
+static double sigma_max(const double* K, int m, int n, cudaStream_t s) {
+    DBuf<double> v(n), t(m);
+    std::vector<double> hv(n, 1.0 / std::sqrt((double)n));
+    h2d(v.p, hv.data(), n, s);
+    double sig = 0;
+    for (int it = 0; it < 60; ++it) {
+        power_step<<<ceil_div(m, 256), 256, 0, s>>>(K, m, n, v.p, t.p);
+        power_stepT<<<ceil_div(n, 256), 256, 0, s>>>(K, m, n, t.p, v.p);
+        d2h(hv.data(), v.p, n, s);
+        EB_CUDA(cudaStreamSynchronize(s));
+        double nn = 0;
+        for (double x : hv) nn += x * x;
+        nn = std::sqrt(nn);
+        sig = std::sqrt(nn);
+        for (double& x : hv) x /= nn;
+        h2d(v.p, hv.data(), n, s);
+    }
+    EB_CHECK_LAUNCH();
+    return sig;
+}
+
+__global__ void build_aug(const double* __restrict__ K, int mc, int me, double alpha, double* __restrict__ A) {
+    // A column-major (mc+me) x me = [K; alpha I]
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int m = mc + me;
+    if (e >= (int64_t)m * me) return;
+    const int col = (int)(e / m), row = (int)(e % m);
+    A[e] = row < mc ? K[(int64_t)row * me + col] : (row - mc == col ? alpha : 0.0);
+}
+
+__global__ void extract_q1t(const double* __restrict__ Q, int m, int mc, int me, double* __restrict__ Q1T) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= (int64_t)me * mc) return;
+    const int i = (int)(e / mc), k = (int)(e % mc);
+    Q1T[e] = Q[(int64_t)i * m + k];
+}
+
+__global__ void cast_f32(const double* __restrict__ a, float* __restrict__ b, int64_t n) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) b[i] = (float)a[i];
+}
+
+static void to_f32(const double* a, float* b, int64_t n, cudaStream_t s) {
+    cast_f32<<<ceil_div(n, 256), 256, 0, s>>>(a, b, n);
+    EB_CHECK_LAUNCH();
+}
+
+// Factor one check->equivalent solve: returns Q1T (me x mc, fp64) and Rinv (me x me).
+static void factor_solve(const Plan& P, const DBuf<double>& sc, double rc, const DBuf<double>& se,
+                         double re, DBuf<double>& Q1T, DBuf<double>& Rinv, cudaStream_t s) {
+    const int mc = P.mc, me = P.me, m = mc + me;
+    DBuf<double> K((size_t)mc * me);
+    std::vector<double> zero(3, 0.0);
+    kmat(P, sc, P.nc, rc, se, P.ne, re, zero, zero, 1.0, K.p, 1, s);
+    const double alpha = P.rcond * sigma_max(K.p, mc, me, s);
+    DBuf<double> Q((size_t)m * me), R((size_t)me * me);
+    build_aug<<<ceil_div((int64_t)m * me, 256), 256, 0, s>>>(K.p, mc, me, alpha, Q.p);
+    EB_CHECK_LAUNCH();
+    cgs2_qr(Q.p, m, me, R.p, s);
+    Rinv.alloc((size_t)me * me);
+    for (int i = me - 1; i >= 0; --i) trinv_row<<<ceil_div(me, 256), 256, 0, s>>>(R.p, me, i, Rinv.p);
+    EB_CHECK_LAUNCH();
+    Q1T.alloc((size_t)me * mc);
+    extract_q1t<<<ceil_div((int64_t)me * mc, 256), 256, 0, s>>>(Q.p, m, mc, me, Q1T.p);
+    EB_CHECK_LAUNCH();
+    EB_CUDA(cudaStreamSynchronize(s));
+}
+
+// composites C[b] = Q1T * (Kb * Rinv) for a batch of kernel matrices Kb (mc x me)
+static void composites(const Plan& P, const DBuf<double>& Q1T, const DBuf<double>& Rinv, const DBuf<double>& sx,
+                       double xs, const DBuf<double>& sy, double ys, const std::vector<double>& xo,
+                       const std::vector<double>& yo, double scale, float* out, cudaStream_t s) {
+    const int mc = P.mc, me = P.me;
+    const int nb = (int)xo.size() / 3;
+    const int chunk = 16;
+    DBuf<double> K((size_t)chunk * mc * me), T((size_t)chunk * mc * me), C((size_t)chunk * me * me);
+    for (int b0 = 0; b0 < nb; b0 += chunk) {
+        const int nbc = std::min(chunk, nb - b0);
+        std::vector<double> xoc(xo.begin() + 3 * b0, xo.begin() + 3 * (b0 + nbc));
+        std::vector<double> yoc(yo.begin() + 3 * b0, yo.begin() + 3 * (b0 + nbc));
+        kmat(P, sx, P.nc, xs, sy, P.ne, ys, xoc, yoc, scale, K.p, nbc, s);
+        gemm_f64(mc, me, me, 1.0, K.p, (int64_t)mc * me, me, Rinv.p, 0, me, 0.0, T.p, (int64_t)mc * me, me, nbc, s);
+        gemm_f64(me, me, mc, 1.0, Q1T.p, 0, mc, T.p, (int64_t)mc * me, me, 0.0, C.p, (int64_t)me * me, me, nbc, s);
+        to_f32(C.p, out + (int64_t)b0 * me * me, (int64_t)nbc * me * me, s);
+    }
+    EB_CUDA(cudaStreamSynchronize(s));
+}
+
+static std::shared_ptr<Plan> make_plan(int p, const Material& m, cudaStream_t s) {
+    auto P = std::make_shared<Plan>();
+    P->p = p;
+    P->pc = p + 1;
+    P->mat = m;
+    P->rcond = std::max(1e-9, std::pow(10.0, -(p + 1)));
+    std::vector<double> se = surface_grid(p), sc = surface_grid(P->pc);
+    P->ne = (int)se.size() / 3;
+    P->nc = (int)sc.size() / 3;
+    P->me = 3 * P->ne;
+    P->mc = 3 * P->nc;
+    P->s_e64.alloc(se.size());
+    P->s_c64.alloc(sc.size());
+    h2d(P->s_e64.p, se.data(), se.size(), s);
+    h2d(P->s_c64.p, sc.data(), sc.size(), s);
+    std::vector<float> sef(se.begin(), se.end()), scf(sc.begin(), sc.end());
+    P->s_e.alloc(sef.size());
+    P->s_c.alloc(scf.size());
+    h2d(P->s_e.p, sef.data(), sef.size(), s);
+    h2d(P->s_c.p, scf.data(), scf.size(), s);
+
+    DBuf<double> Qu1T, Qd1T;
+    factor_solve(*P, P->s_c64, RAD_UC, P->s_e64, RAD_UE, Qu1T, P->Ruinv, s);
+    factor_solve(*P, P->s_c64, RAD_DC, P->s_e64, RAD_DE, Qd1T, P->Rdinv, s);
+    P->Qu1T.alloc((size_t)P->me * P->mc);
+    P->Qd1T.alloc((size_t)P->me * P->mc);
+    to_f32(Qu1T.p, P->Qu1T.p, (int64_t)P->me * P->mc, s);
+    to_f32(Qd1T.p, P->Qd1T.p, (int64_t)P->me * P->mc, s);
+
+    // M2M_c = Q_u1^T (1/2 K(uc_P, ue_C)) R_u^-1 (parent half-width 1; child centre o_c)
+    // L2L_c = Q_d1^T K(dc_C, de_P) R_d^-1
+    std::vector<double> oc, zero8(24, 0.0);
+    for (int c = 0; c < 8; ++c) {
+        oc.push_back(((c >> 2) & 1) - 0.5);
+        oc.push_back(((c >> 1) & 1) - 0.5);
+        oc.push_back((c & 1) - 0.5);
+    }
+    P->M2M.alloc((size_t)8 * P->me * P->me);
+    P->L2L.alloc((size_t)8 * P->me * P->me);
+    composites(*P, Qu1T, P->Ruinv, P->s_c64, RAD_UC, P->s_e64, 0.5 * RAD_UE, zero8, oc, 0.5, P->M2M.p, s);
+    composites(*P, Qd1T, P->Rdinv, P->s_c64, 0.5 * RAD_DC, P->s_e64, RAD_DE, oc, zero8, 1.0, P->L2L.p, s);
+
+    // M2L_o = Q_d1^T K(dc_B, ue_A) R_u^-1, target box B at the origin, source box A at 2o
+    std::vector<double> xo, yo;
+    int idx = 0;
+    for (int i = 0; i < 343; ++i) P->off_index[i] = -1;
+    for (int ox = -3; ox <= 3; ++ox)
+        for (int oy = -3; oy <= 3; ++oy)
+            for (int oz = -3; oz <= 3; ++oz) {
+                if (std::max(std::abs(ox), std::max(std::abs(oy), std::abs(oz))) < 2) continue;
+                P->off_index[(ox + 3) * 49 + (oy + 3) * 7 + (oz + 3)] = idx++;
+                xo.insert(xo.end(), {0.0, 0.0, 0.0});
+                yo.insert(yo.end(), {2.0 * ox, 2.0 * oy, 2.0 * oz});
+            }
+    P->M2L.alloc((size_t)NV_OFFSETS * P->me * P->me);
+    composites(*P, Qd1T, P->Ruinv, P->s_c64, RAD_DC, P->s_e64, RAD_UE, xo, yo, 1.0, P->M2L.p, s);
+    return P;
+}
+
+std::shared_ptr<Plan> get_plan(int p, const Material& m, cudaStream_t s) {
+    static std::mutex mu;
+    static std::map<std::tuple<int, int, double, double>, std::shared_ptr<Plan>> cache;
+    int dev = 0;
+    EB_CUDA(cudaGetDevice(&dev));
+    auto key = std::make_tuple(dev, p, m.K, m.G);
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cache.find(key);
+    if (it != cache.end()) return it->second;
+    auto P = make_plan(p, m, s);
+    cache[key] = P;
+    return P;
+}
+
+}  // namespace ebem

@@ -1,0 +1,98 @@
+"""Parity of the GPU octree (bit-exact vs oracle.tree) and of the KIFMM (vs the fp64
+direct sum and vs the fp64 reference tree code oracle.kifmm)."""
+import numpy as np
+import pytest
+
+from oracle import cdirect
+from oracle import kernels as KN
+from oracle import kifmm as OF
+from oracle import tree as OT
+from workloads import geometry as geo
+from tests.gpu_util import csr_lists, need_gpu, to_dev, torch
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def eb():
+    need_gpu()
+    import paper_1612_04082_b200 as eb
+    return eb
+
+
+def _compare_tree(eb, tree, src, trg, max_pts):
+    ot = OT.build_tree(src, trg, max_pts)
+    assert np.array_equal(eb.fmm_tree_export(tree, "keys"), ot.keys)
+    assert np.array_equal(eb.fmm_tree_export(tree, "perm"), ot.perm)
+    assert np.array_equal(eb.fmm_tree_export(tree, "level"), ot.level)
+    assert np.array_equal(eb.fmm_tree_export(tree, "anchor"), ot.anchor)
+    assert np.array_equal(eb.fmm_tree_export(tree, "parent"), ot.parent)
+    rng_ = eb.fmm_tree_export(tree, "range")
+    assert np.array_equal(rng_[:, 0], ot.begin) and np.array_equal(rng_[:, 1], ot.end)
+    ol = OT.build_lists(ot)
+    for k in "UVWX":
+        got = csr_lists(eb.fmm_tree_export(tree, k + "_off"), eb.fmm_tree_export(tree, k))
+        assert got == ol[k], k
+    return ot
+
+
+@pytest.mark.parametrize("case", ["sphere", "beam", "split", "cluster"])
+def test_tree_and_lists_bit_exact(eb, case):
+    rng = np.random.default_rng(1)
+    if case == "sphere":
+        src = geo.sphere_points(3000, seed=2); trg = src; s = 20
+    elif case == "beam":
+        src = geo.config2(n=20000)["src"]; trg = src; s = 64
+    elif case == "split":
+        src = geo.sphere_points(2000, seed=5); trg = (rng.uniform(-0.5, 0.5, (1500, 3))).astype(np.float32); s = 16
+    else:
+        src = np.concatenate([rng.normal(0.3, 1e-4, (500, 3)), rng.uniform(0, 1, (500, 3))]).astype(np.float32)
+        trg = src; s = 8
+    tree = eb.fmm_build_tree(torch.from_numpy(src).cuda(), trg=torch.from_numpy(trg).cuda(), max_pts=s, p=4)
+    _compare_tree(eb, tree, src, trg, s)
+
+
+@pytest.fixture(scope="module")
+def beam20k():
+    d = geo.config2(n=20000, seed=4)
+    ref = cdirect.direct_sum(KN.KERNEL_UP, d["src"], d["src"], d["K"], d["G"], w=d["w"], f=d["f"], g=d["g"],
+                             nrm=d["nrm"])
+    return d, ref
+
+
+def test_fmm_matvec_converges_in_p(eb, beam20k):
+    d, ref = beam20k
+    t = to_dev(d)
+    errs = {}
+    for p in (4, 6, 8, 10):
+        tree = eb.fmm_build_tree(t["src"], t["nrm"], t["w"], max_pts=64, p=p, K=d["K"], G=d["G"])
+        out = eb.fmm_matvec(tree, eb.KERNEL_UP, t["f"], t["g"])
+        errs[p] = KN.rel_l2(out.cpu().numpy().astype(np.float64), ref)
+    print("fmm rel-L2 by p:", errs)
+    assert errs[4] > errs[6] > errs[8] > errs[10]
+    assert errs[6] <= 1e-4
+    assert errs[10] <= 1e-6
+
+
+def test_fmm_matches_reference_tree_code(eb):
+    """same algorithm, same p: GPU (fp32 translations) vs oracle.kifmm (fp64)."""
+    d = geo.config2(n=2500, seed=6)
+    t = to_dev(d)
+    tree = eb.fmm_build_tree(t["src"], t["nrm"], t["w"], max_pts=32, p=6, K=d["K"], G=d["G"])
+    out = eb.fmm_matvec(tree, eb.KERNEL_UP, t["f"], t["g"]).cpu().numpy().astype(np.float64)
+    fm = OF.KIFMM(d["src"], d["src"], d["K"], d["G"], p=6, max_pts=32, nrm=d["nrm"])
+    ref = fm.evaluate(KN.KERNEL_UP, w=d["w"], f=d["f"], g=d["g"])
+    assert KN.rel_l2(out, ref) <= 1e-5
+
+
+@pytest.mark.parametrize("kern", [0, 1, 3, 4, 5])
+def test_fmm_kernels_and_separate_targets(eb, kern):
+    d = geo.config3(n_src=30000, grid=(40, 10, 20), seed=8)
+    t = to_dev(d)
+    tree = eb.fmm_build_tree(t["src"], t["nrm"], t["w"], trg=t["trg"], max_pts=64, p=8, K=d["K"], G=d["G"])
+    fn = eb.fmm_eval_stress if kern >= 3 else eb.fmm_matvec
+    out = fn(tree, kern, t["f"], t["g"]).cpu().numpy().astype(np.float64)
+    ref = cdirect.direct_sum(kern, d["trg"], d["src"], d["K"], d["G"], w=d["w"], f=d["f"], g=d["g"], nrm=d["nrm"])
+    err = KN.rel_l2(out, ref)
+    print("kernel", kern, "rel-L2", err)
+    assert err <= 1e-5
