@@ -1,0 +1,334 @@
+#!/usr/bin/env python3
+"""Benchmark of the B200 KIFMM elastic matvec (the hot path of arXiv:1612.04082, Sec. 2.2).
+
+One step = one fmm_matvec (single + double layer, kernel UP) over the 1M-point beam
+surface (BASELINE.json configs[2] recipe scaled to N = 1,000,000; p = 6; 64 points per
+leaf) with the tree already built -- "Single FMM pass (without tree construction)",
+PAPER.md line 251 -- i.e. the operator applied at every GMRES iteration.
+
+Output: one JSON line (rank 0).  Extra objects: `phases` (native per-phase device
+time and roofline fraction), `p2p` (direct all-pairs double-layer kernel on configs[1],
+Ginteractions/s and fraction of FP32 peak), `roofline` (dominant phase), `cpu_baseline`
+(the fp64 oracle direct sum timed on the host cores on a bounded target sample; the
+same sample gives the GPU result's relative L2 error `rel_l2`), `e2e` (host buffers,
+copies inside the timed region), `clocks`.
+
+`--impl reference` times the oracle (fp64 C direct sum, the plain definition of
+Eq. fmm_summation) on the host cores on bounded target samples of the same workload.
+Multi-GPU (torchrun): replicas only -- every rank runs the same independent matvec
+(DESIGN.md Sec. 8(e)); the timed region is barrier-bracketed and the max over ranks
+is reported.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
+METRIC = "elastic P2P Ginteractions/s (% FP32 peak); FMM matvec ms at N=1M, rel-L2 err"
+WORKLOAD = "beam4x1x1_surface_N1M_graded_UP_kifmm_p6_leaf64"
+
+
+def peaks():
+    try:
+        d = json.load(open(PEAKS_FILE))
+        src = "measured"
+    except Exception:
+        d = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "sm_max_mhz": 1965.0}
+        src = "fallback"
+    clk = d.get("sm_max_mhz", 1965.0) * 1e6
+    # FP32: 148 SMs x 128 FFMA lanes x 2 flops x max SM clock; FP64: 64 lanes (B200 guide)
+    return dict(src=src, hbm_gbs=d["hbm_gbs"], fp32_tflops=148 * 128 * 2 * clk / 1e12,
+                fp64_tflops=148 * 64 * 2 * clk / 1e12, tf32_tflops=d["bf16_tflops"] / 2,
+                bf16_tflops=d["bf16_tflops"])
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+
+    def __init__(self, index=0):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = float(f[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, f[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def workload(n):
+    from workloads import geometry as geo
+    return geo.config2(n=n)
+
+
+def oracle_sample(d, sample_idx):
+    """fp64 oracle (C direct sum) at the sampled targets; returns (values, seconds, threads)."""
+    from oracle import cdirect
+    from oracle import kernels as KN
+    t0 = time.perf_counter()
+    ref = cdirect.direct_sum(KN.KERNEL_UP, d["trg"][sample_idx], d["src"], d["K"], d["G"], w=d["w"], f=d["f"],
+                             g=d["g"], nrm=d["nrm"])
+    return ref, time.perf_counter() - t0, int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
+
+
+def run_reference(args):
+    """--impl reference: the oracle timed on the host cores, bounded samples per step."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    d = workload(args.n)
+    n = d["trg"].shape[0]
+    rng = np.random.default_rng(123)
+    per_step = args.ref_sample
+    times = []
+    for k in range(args.warmup + args.steps):
+        idx = np.sort(rng.choice(n, per_step, replace=False))
+        _, sec, cores = oracle_sample(d, idx)
+        if k >= args.warmup:
+            times.append(sec * n / per_step)
+    ms = 1e3 * float(np.mean(times))
+    line = {"impl": "reference", "metric": METRIC, "value": ms, "unit": "ms", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": WORKLOAD, "n_points": n, "kernel": "UP", "method": "oracle direct sum (fp64 C)"},
+            "cpu_baseline": {"value": ms, "unit": "ms", "cores": cores, "kind": "oracle",
+                             "sample": f"{per_step} random targets x all {n} sources per step, "
+                                       f"extrapolated to all {n} targets"},
+            "e2e": {"value": ms, "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def p2p_bench(eb, torch, pk, reps=5):
+    """configs[1]: direct double-layer traction kernel on the 24,576-triangle cube, all pairs."""
+    from workloads import geometry as geo
+    d = geo.config1()
+    t = {k: torch.from_numpy(v).cuda() for k, v in d.items() if isinstance(v, np.ndarray)}
+    n = d["src"].shape[0]
+    out = torch.empty((n, 3), device="cuda")
+    for _ in range(3):
+        eb.bem_kernel_direct(eb.KERNEL_P, t["src"], t["src"], nrm=t["nrm"], w=t["w"], g=t["g"], K=d["K"], G=d["G"],
+                             out=out)
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(reps):
+        eb.bem_kernel_direct(eb.KERNEL_P, t["src"], t["src"], nrm=t["nrm"], w=t["w"], g=t["g"], K=d["K"], G=d["G"],
+                             out=out)
+    e.record()
+    torch.cuda.synchronize()
+    ms = s.elapsed_time(e) / reps
+    inter = float(n) * (n - 1)
+    flops = inter * 44.0          # P kernel, elastic.cuh acc_P + pair setup
+    tf = flops / (ms * 1e-3) / 1e12
+    return {"config": "configs[1] cube 24576 triangles, kernel P, all pairs", "ms": ms,
+            "ginteractions_per_s": inter / (ms * 1e-3) / 1e9, "tflops": tf,
+            "frac_fp32_peak": tf / pk["fp32_tflops"], "flops_per_interaction": 44}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n", type=int, default=1_000_000)
+    ap.add_argument("--p", type=int, default=6)
+    ap.add_argument("--max-pts", type=int, default=64)
+    ap.add_argument("--ref-sample", type=int, default=64)
+    ap.add_argument("--cpu-sample", type=int, default=3072)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-p2p", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import paper_1612_04082_b200 as eb
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    pk = peaks()
+
+    d = workload(args.n)
+    n = d["src"].shape[0]
+    t = {k: torch.from_numpy(v).cuda() for k, v in d.items() if isinstance(v, np.ndarray)}
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    tree = eb.fmm_build_tree(t["src"], t["nrm"], t["w"], max_pts=args.max_pts, p=args.p, K=d["K"], G=d["G"])
+    torch.cuda.synchronize()
+    build_s = time.perf_counter() - t0      # includes the one-time operator precompute
+    t0 = time.perf_counter()
+    tree2 = eb.fmm_build_tree(t["src"], t["nrm"], t["w"], max_pts=args.max_pts, p=args.p, K=d["K"], G=d["G"])
+    torch.cuda.synchronize()
+    rebuild_s = time.perf_counter() - t0    # tree + lists + schedule only (operators cached)
+    del tree2
+    info = eb.fmm_tree_info(tree)
+    out = torch.empty((n, 3), device="cuda")
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")   # 256 MB > 126 MB L2
+
+    for _ in range(max(args.warmup, 3)):
+        eb.fmm_matvec(tree, eb.KERNEL_UP, t["f"], t["g"], out=out)
+    torch.cuda.synchronize()
+
+    # ---- timed region: K steps, L2 flushed between steps (flush outside the events)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    launches0 = eb.ebem_launch_count()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for k in range(args.steps):
+            flush.fill_(float(k))
+            ev[k][0].record()
+            eb.fmm_matvec(tree, eb.KERNEL_UP, t["f"], t["g"], out=out)
+            ev[k][1].record()
+        torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    launches = (eb.ebem_launch_count() - launches0) // args.steps
+    ms_steps = [a.elapsed_time(b) for a, b in ev]
+    ms = float(np.mean(ms_steps))
+    if dist:
+        tt = torch.tensor([ms], device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+
+    # ---- per-phase device times (native profiler, one more L2-flushed step)
+    eb.fmm_set_profiling(tree, True)
+    flush.fill_(1.0)
+    eb.fmm_matvec(tree, eb.KERNEL_UP, t["f"], t["g"], out=out)
+    phases = eb.fmm_phase_stats(tree, eb.KERNEL_UP)
+    eb.fmm_set_profiling(tree, False)
+    ph_out = []
+    for ph in phases:
+        f64, f32 = ph["flops_fp64"], ph["flops"] - ph["flops_fp64"]
+        tmin = f32 / (pk["fp32_tflops"] * 1e12) + f64 / (pk["fp64_tflops"] * 1e12)   # ALU lower bound (s)
+        tmem = ph["bytes"] / (pk["hbm_gbs"] * 1e9)
+        sec = ph["ms"] * 1e-3
+        bound = "alu" if tmin >= tmem else "hbm"
+        frac = (max(tmin, tmem) / sec) if sec > 0 else None
+        ph_out.append({"name": ph["name"], "ms": ph["ms"], "launches": ph["launches"], "bound": bound,
+                       "gflop": ph["flops"] / 1e9, "gflop_fp64": f64 / 1e9, "interactions": ph["interactions"],
+                       "mbytes": ph["bytes"] / 1e6, "frac": frac})
+    dom = max(ph_out, key=lambda x: x["ms"])
+    dph = next(p for p in phases if p["name"] == dom["name"])
+    sec = dom["ms"] * 1e-3
+    if dom["bound"] == "alu":
+        f64, f32 = dph["flops_fp64"], dph["flops"] - dph["flops_fp64"]
+        peak = dph["flops"] / (f32 / pk["fp32_tflops"] + f64 / pk["fp64_tflops"]) if dph["flops"] else pk["fp32_tflops"]
+        roof = {"bound": "alu", "phase": dom["name"], "achieved": dph["flops"] / sec / 1e12, "peak": peak,
+                "unit": "TFLOP/s", "frac": dph["flops"] / sec / 1e12 / peak, "traffic": None,
+                "peak_source": f"derived: 148 SM x 128 FP32 (64 FP64) lanes x 2 x {pk['fp32_tflops']/148/256*1e6:.0f} MHz"}
+    else:
+        roof = {"bound": "hbm", "phase": dom["name"], "achieved": dph["bytes"] / sec / 1e9, "peak": pk["hbm_gbs"],
+                "unit": "GB/s", "frac": dph["bytes"] / sec / 1e9 / pk["hbm_gbs"], "traffic": None,
+                "peak_source": pk["src"]}
+
+    # ---- e2e through the C ABI with host buffers (pinned), copies inside the timed region
+    fh = torch.from_numpy(d["f"]).pin_memory().numpy()
+    gh = torch.from_numpy(d["g"]).pin_memory().numpy()
+    oh = torch.empty((n, 3), dtype=torch.float32).pin_memory().numpy()
+    eb.fmm_matvec(tree, eb.KERNEL_UP, fh, gh, out=oh)
+    e2e = []
+    for k in range(max(2, args.steps // 2)):
+        flush.fill_(float(k))
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        eb.fmm_matvec(tree, eb.KERNEL_UP, fh, gh, out=oh)
+        b.record()
+        torch.cuda.synchronize()
+        e2e.append(a.elapsed_time(b))
+
+    p2p = None if args.no_p2p else p2p_bench(eb, torch, pk)
+
+    # ---- CPU oracle on a bounded target sample (rank 0, N = 1 only) + accuracy on it
+    cpu = None
+    rel = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        rng = np.random.default_rng(7)
+        idx = np.sort(rng.choice(n, args.cpu_sample, replace=False))
+        ref, sec, cores = oracle_sample(d, idx)
+        got = out.cpu().numpy().astype(np.float64)[idx]
+        rel = float(np.linalg.norm(got - ref) / np.linalg.norm(ref))
+        cpu = {"value": 1e3 * sec * n / args.cpu_sample, "unit": "ms", "cores": cores, "kind": "oracle",
+               "sample": f"{args.cpu_sample} random targets x all {n} sources (fp64 C direct sum), "
+                         f"{sec:.1f} s, extrapolated to all {n} targets"}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": ms, "unit": "ms", "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False, "scaling": "weak",
+                "vs_baseline": None, "dtype": "f32 (fp64 plan, fp64 L2T/M2T)", "data": "synthetic",
+                "config": {"workload": WORKLOAD, "n_points": n, "p": args.p, "max_pts": args.max_pts,
+                           "kernel": "UP", "l2": "flushed between steps (256 MB write)",
+                           "nboxes": info["nboxes"], "nlevels": info["nlevels"], "n_v": info["n_v"],
+                           "parallelism": "replicas" if world > 1 else "single"},
+                "points_per_s": n / (ms * 1e-3), "rel_l2": rel, "tree_build_s": rebuild_s,
+                "first_build_s_incl_operators": build_s, "gpu_launches": int(launches),
+                "roofline": roof, "phases": ph_out, "p2p": p2p, "cpu_baseline": cpu,
+                "e2e": {"value": float(np.mean(e2e)), "unit": "ms", "h2d_bytes_per_step": int(fh.nbytes + gh.nbytes),
+                        "d2h_bytes_per_step": int(oh.nbytes)},
+                "clocks": clk.summary(), "peaks": pk}
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

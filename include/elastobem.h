@@ -126,6 +126,34 @@ int fmm_eval_stress(ebem_tree *tree, int kernel, const float *f, const float *g,
 
 int fmm_tree_free(ebem_tree *tree);
 
+/*
+ * Native phase profiler.  fmm_set_profiling(tree, 1) makes every later evaluation
+ * record CUDA events on its stream between the phases below; fmm_phase_stats fills
+ * up to `cap` entries (returns the number of phases) with, per phase and for the
+ * given kernel id: kernel launches per evaluation, ALGORITHMIC work per evaluation
+ * (flops: pair interactions x flops per interaction of the kernel as written in
+ * elastic.cuh, or 2 M K per GEMM column; bytes: operands read once + results
+ * written once), its arithmetic precision and the device time of the last profiled
+ * evaluation (ms, -1 if none; synchronises on that evaluation's last event).
+ * Phases: prep, S2M, Q2Z_up, M2M, S2L, Q2Z_dn, M2L, L2L, PHI, EVAL.
+ */
+typedef struct ebem_phase_stat {
+    char name[16];
+    int32_t launches;
+    int32_t fp64;          /* 1 if the phase computes (partly) in fp64 */
+    double flops;          /* algorithmic floating-point operations per evaluation */
+    double flops_fp64;     /* the part of `flops` computed in fp64 */
+    double interactions;   /* kernel pair evaluations per evaluation (0 for GEMM phases) */
+    double bytes;          /* algorithmic DRAM bytes per evaluation */
+    double ms;             /* device time of the last profiled evaluation */
+} ebem_phase_stat;
+
+int fmm_set_profiling(ebem_tree *tree, int on);
+int fmm_phase_stats(ebem_tree *tree, int kernel, ebem_phase_stat *out, int cap);
+
+/* number of CUDA kernel launches issued by this library since it was loaded */
+int64_t ebem_launch_count(void);
+
 typedef struct ebem_tree_info {
     int64_t nsrc, ntrg, nboxes, nleaves;
     int32_t nlevels, p, max_pts, n_equiv;   /* n_equiv = 6(p-1)^2+2 surface points */

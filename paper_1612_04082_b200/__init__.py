@@ -53,6 +53,18 @@ class TreeInfo(ctypes.Structure):
 _lib.fmm_tree_info.argtypes = [_VP, ctypes.POINTER(TreeInfo)]
 
 
+class PhaseStat(ctypes.Structure):
+    _fields_ = [("name", ctypes.c_char * 16), ("launches", ctypes.c_int32), ("fp64", ctypes.c_int32),
+                ("flops", ctypes.c_double), ("flops_fp64", ctypes.c_double),
+                ("interactions", ctypes.c_double), ("bytes", ctypes.c_double),
+                ("ms", ctypes.c_double)]
+
+
+_lib.fmm_set_profiling.argtypes = [_VP, ctypes.c_int]
+_lib.fmm_phase_stats.argtypes = [_VP, ctypes.c_int, ctypes.POINTER(PhaseStat), ctypes.c_int]
+_lib.ebem_launch_count.restype = _I64
+
+
 class EbemError(RuntimeError):
     pass
 
@@ -201,6 +213,27 @@ def fmm_tree_export(tree, what):
     return buf.reshape(-1, width) if width > 1 else buf
 
 
+def fmm_set_profiling(tree, on=True):
+    """record CUDA events between the KIFMM phases of every later evaluation (native profiler)."""
+    _check(_lib.fmm_set_profiling(tree.handle, 1 if on else 0))
+
+
+def fmm_phase_stats(tree, kernel):
+    """per-phase launches, algorithmic flops/bytes/interactions and last profiled device ms."""
+    arr = (PhaseStat * 16)()
+    n = _lib.fmm_phase_stats(tree.handle, kernel, arr, 16)
+    if n < 0:
+        _check(n)
+    return [dict(name=a.name.decode(), launches=a.launches, fp64=bool(a.fp64), flops=a.flops,
+                 flops_fp64=a.flops_fp64,
+                 interactions=a.interactions, bytes=a.bytes, ms=a.ms) for a in arr[:n]]
+
+
+def ebem_launch_count():
+    """CUDA kernel launches issued by the library since it was loaded."""
+    return int(_lib.ebem_launch_count())
+
+
 def bem_gmres_solve(tree, bc_type, self_U, self_P, bc_val, x, restart=50, max_iter=1000, tol=1e-6):
     keep = []
     it = ctypes.c_int32(0)
@@ -212,5 +245,6 @@ def bem_gmres_solve(tree, bc_type, self_U, self_P, bc_val, x, restart=50, max_it
 
 
 __all__ = ["bem_kernel_direct", "fmm_build_tree", "fmm_matvec", "fmm_eval_stress", "fmm_tree_info",
-           "fmm_tree_export", "bem_gmres_solve", "FmmTree", "EbemError", "LIB_PATH",
+           "fmm_tree_export", "bem_gmres_solve", "fmm_set_profiling", "fmm_phase_stats",
+           "ebem_launch_count", "FmmTree", "EbemError", "LIB_PATH",
            "KERNEL_U", "KERNEL_P", "KERNEL_UP", "KERNEL_D", "KERNEL_S", "KERNEL_DS"]

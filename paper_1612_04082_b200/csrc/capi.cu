@@ -11,6 +11,10 @@ namespace ebem {
 static thread_local std::string g_last_error;
 void set_last_error(const std::string& s) { g_last_error = s; }
 
+static std::atomic<int64_t> g_launches{0};
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+int64_t launch_count() { return g_launches.load(std::memory_order_relaxed); }
+
 bool is_device_ptr(const void* p) {
     if (!p) return false;
     cudaPointerAttributes a;
@@ -197,6 +201,24 @@ extern "C" int fmm_tree_free(ebem_tree* tree) {
     EB_API_BEGIN
     delete reinterpret_cast<Tree*>(tree);
     return EBEM_OK;
+    EB_API_END
+}
+
+extern "C" int64_t ebem_launch_count(void) { return launch_count(); }
+
+extern "C" int fmm_set_profiling(ebem_tree* tree, int on) {
+    EB_API_BEGIN
+    EB_REQUIRE(tree, "NULL tree");
+    reinterpret_cast<Tree*>(tree)->profile = on != 0;
+    return EBEM_OK;
+    EB_API_END
+}
+
+extern "C" int fmm_phase_stats(ebem_tree* tree, int kernel, ebem_phase_stat* out, int cap) {
+    EB_API_BEGIN
+    EB_REQUIRE(tree && out && cap >= 0, "bad argument");
+    EB_REQUIRE(kernel >= K_U && kernel <= K_DS, "unknown kernel id");
+    return phase_stats(*reinterpret_cast<Tree*>(tree), kernel, out, cap);
     EB_API_END
 }
 

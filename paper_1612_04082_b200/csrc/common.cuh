@@ -1,6 +1,8 @@
 // Shared host/device plumbing for the elastostatic BEM/KIFMM library (sm_100a).
 #pragma once
 #include <cuda_runtime.h>
+
+#include <atomic>
 #include <cstdint>
 #include <cstdio>
 #include <stdexcept>
@@ -24,7 +26,14 @@ void set_last_error(const std::string& s);
                                 + __FILE__ + ":" + std::to_string(__LINE__));               \
     } while (0)
 
-#define EB_CHECK_LAUNCH() EB_CUDA(cudaGetLastError())
+// every kernel launch of the library is followed by EB_CHECK_LAUNCH(), which also counts it
+// (ebem_launch_count(): the bench's evidence of how many of our kernels ran)
+void count_launch();
+#define EB_CHECK_LAUNCH()          \
+    do {                           \
+        ::ebem::count_launch();    \
+        EB_CUDA(cudaGetLastError()); \
+    } while (0)
 
 #define EB_REQUIRE(cond, msg)                                  \
     do {                                                       \

@@ -14,6 +14,8 @@
 
 namespace ebem {
 
+int64_t launch_count();
+
 struct BoxGeo {
     double ox, oy, oz, side;
     __device__ __forceinline__ void center(const int* anchor, const int* level, int b, double& cx, double& cy,
@@ -311,6 +313,30 @@ void schedule_tree(Tree& t, cudaStream_t s) {
             }
         }
     }
+    // algorithmic work counts for the phase profiler
+    {
+        const double nc = P.nc, ne = P.ne;
+        t.w_s2m_inter = t.w_s2m_src = t.w_s2l_inter = t.w_s2l_src = 0;
+        t.w_p2p_inter = t.w_p2p_src = t.w_l2t_inter = t.w_m2t_inter = 0;
+        for (int b : s2m) { t.w_s2m_src += nsub[b]; t.w_s2m_inter += nsub[b] * nc; }
+        for (size_t i = 0; i + 1 < xoff.size(); ++i)
+            for (int e = xoff[i]; e < xoff[i + 1]; ++e) { t.w_s2l_src += nsub[xidx[e]]; t.w_s2l_inter += nsub[xidx[e]] * nc; }
+        for (size_t i = 0; i < ev.size(); ++i) {
+            const int b = ev[i];
+            double ns = 0;
+            for (int e = off[0][b]; e < off[0][b + 1]; ++e) ns += nsub[idx[0][e]];
+            t.w_p2p_src += ns;
+            t.w_p2p_inter += ns * tsub[b];
+            if (l2t[i] >= 0) t.w_l2t_inter += ne * tsub[b];
+            for (int e = off[2][b]; e < off[2][b + 1]; ++e)
+                if (phiu[idx[2][e]] >= 0) t.w_m2t_inter += ne * tsub[b];
+        }
+        t.w_m2m_pairs = t.w_l2l_pairs = 0;
+        for (auto& x : t.m2m) t.w_m2m_pairs += x.npairs;
+        for (auto& x : t.l2l) t.w_l2l_pairs += x.npairs;
+        t.w_m2l_ops = 0;
+        for (int o = 0; o < t.m2l.nops; ++o) t.w_m2l_ops += t.m2l.op_ptr_h[o + 1] > t.m2l.op_ptr_h[o];
+    }
     t.n_eval = (int)ev.size();
     t.n_phid = (int)phid_box.size();
     t.n_phiu = (int)phiu_box.size();
@@ -391,6 +417,17 @@ void fmm_evaluate(Tree& t, int kernel, const float* f, const float* g, float* ou
     const int src_kernel = stress ? kernel - 3 : kernel;    // D->U, S->P, DS->UP
     EB_REQUIRE(!dl || t.has_normals, "double-layer kernel needs normals at fmm_build_tree");
     if (t.ntrg == 0) return;
+    int phase = 0;
+    int64_t l0 = 0;
+    auto mark = [&](int ph) {   // phase boundary: event + launch count of the finished phase
+        const int64_t l = launch_count();
+        if (ph > 0) t.phase_launches[ph - 1] = (int)(l - l0);
+        l0 = l;
+        if (t.profile) EB_CUDA(cudaEventRecord(t.ev[ph], s));
+    };
+    if (t.profile && !t.ev[0])
+        for (auto& e : t.ev) EB_CUDA(cudaEventCreate(&e));
+    mark(phase++);
 
     // prepared sources in tree order (geometry sorted, densities via src_perm)
     prepare_sources(src_kernel, t.mat, t.src_xyz.p, t.src_nrm.p, t.src_w.p, nullptr, f, g, t.src_perm.p, t.nsrc,
@@ -400,27 +437,36 @@ void fmm_evaluate(Tree& t, int kernel, const float* f, const float* g, float* ou
                         t.rec_stress.p, s);
     t.Z.zero(s);
     t.W.zero(s);
+    mark(phase++);
 
     // upward pass
     if (sl && dl) launch_check<true, true>(t, t.s2m_box.p, t.n_s2m, nullptr, nullptr, RAD_UC, s);
     else if (sl) launch_check<true, false>(t, t.s2m_box.p, t.n_s2m, nullptr, nullptr, RAD_UC, s);
     else launch_check<false, true>(t, t.s2m_box.p, t.n_s2m, nullptr, nullptr, RAD_UC, s);
+    mark(phase++);
     gemm_pairs_f32(t.q2z_up, P.Qu1T.p, me, mc, t.Q.p, mc, t.Z.p, me, s);
+    mark(phase++);
     for (int l = t.nlevels - 1; l >= 2; --l) gemm_pairs_f32(t.m2m[l], P.M2M.p, me, me, t.Z.p, me, t.Z.p, me, s);
+    mark(phase++);
 
     // downward pass
     if (t.n_s2l) {
         if (sl && dl) launch_check<true, true>(t, t.s2l_box.p, t.n_s2l, t.x_src_off.p, t.x_src_idx.p, RAD_DC, s);
         else if (sl) launch_check<true, false>(t, t.s2l_box.p, t.n_s2l, t.x_src_off.p, t.x_src_idx.p, RAD_DC, s);
         else launch_check<false, true>(t, t.s2l_box.p, t.n_s2l, t.x_src_off.p, t.x_src_idx.p, RAD_DC, s);
-        gemm_pairs_f32(t.q2z_dn, P.Qd1T.p, me, mc, t.Q.p, mc, t.W.p, me, s);
     }
+    mark(phase++);
+    if (t.n_s2l) gemm_pairs_f32(t.q2z_dn, P.Qd1T.p, me, mc, t.Q.p, mc, t.W.p, me, s);
+    mark(phase++);
     gemm_pairs_f32(t.m2l, P.M2L.p, me, me, t.Z.p, me, t.W.p, me, s);
+    mark(phase++);
     for (int l = 3; l < t.nlevels; ++l) gemm_pairs_f32(t.l2l[l], P.L2L.p, me, me, t.W.p, me, t.W.p, me, s);
+    mark(phase++);
 
     // equivalent densities (fp64) and leaf evaluation
     gemm_pairs_f64(t.phid_pairs, P.Rdinv.p, me, me, t.W.p, me, t.phid_scale.p, t.PHID.p, me, s);
     gemm_pairs_f64(t.phiu_pairs, P.Ruinv.p, me, me, t.Z.p, me, t.phiu_scale.p, t.PHIU.p, me, s);
+    mark(phase++);
     switch (kernel) {
         case K_U: launch_eval<true, false, false>(t, out, s); break;
         case K_P: launch_eval<false, true, false>(t, out, s); break;
@@ -429,6 +475,75 @@ void fmm_evaluate(Tree& t, int kernel, const float* f, const float* g, float* ou
         case K_S: launch_eval<false, true, true>(t, out, s); break;
         case K_DS: launch_eval<true, true, true>(t, out, s); break;
     }
+    mark(phase++);
+    t.ev_valid = t.profile;
+}
+
+// flops per pair interaction of the fp32 pair loop, counted from elastic.cuh as written
+// (FFMA = 2, FADD/FMUL = 1; rsqrt not counted): d and r^2 8, then U 18, P 36, D 54, S 89.
+static double flops_per_pair(int kernel) {
+    switch (kernel) {
+        case K_U: return 26;
+        case K_P: return 44;
+        case K_UP: return 62;
+        case K_D: return 62;
+        case K_S: return 97;
+        default: return 151;
+    }
+}
+
+int phase_stats(Tree& t, int kernel, ebem_phase_stat* out, int cap) {
+    static const char* names[Tree::NPHASE] = {"prep", "S2M", "Q2Z_up", "M2M", "S2L", "Q2Z_dn", "M2L", "L2L", "PHI", "EVAL"};
+    const Plan& P = *t.plan;
+    const double me = P.me, mc = P.mc, ne = P.ne;
+    const bool stress = kernel_stress(kernel);
+    const int srck = stress ? kernel - 3 : kernel;
+    const double rec_b = 16.0 * REC_DISP, rec_sb = 16.0 * REC_STRESS;
+    ebem_phase_stat st[Tree::NPHASE];
+    std::memset(st, 0, sizeof(st));
+    for (int i = 0; i < Tree::NPHASE; ++i) {
+        std::strncpy(st[i].name, names[i], 15);
+        st[i].launches = t.phase_launches[i];
+        st[i].ms = -1;
+    }
+    // prep: densities + sorted geometry in, prepared records out
+    st[0].bytes = t.nsrc * (4.0 * (3 + 3 + 3 + 3 + 1 + 1) + rec_b + (stress ? rec_sb : 0));
+    st[1].interactions = t.w_s2m_inter;
+    st[1].flops = t.w_s2m_inter * flops_per_pair(srck);
+    st[1].bytes = t.w_s2m_src * rec_b + 4.0 * mc * t.n_s2m;
+    st[2].flops = 2.0 * me * mc * t.n_s2m;
+    st[2].bytes = 4.0 * me * mc + 4.0 * (mc + me) * t.n_s2m;
+    st[3].flops = 2.0 * me * me * t.w_m2m_pairs;
+    st[3].bytes = 4.0 * 8 * me * me + 4.0 * 2 * me * t.w_m2m_pairs;
+    st[4].interactions = t.w_s2l_inter;
+    st[4].flops = t.w_s2l_inter * flops_per_pair(srck);
+    st[4].bytes = t.w_s2l_src * rec_b + 4.0 * mc * t.n_s2l;
+    st[5].flops = 2.0 * me * mc * t.n_s2l;
+    st[5].bytes = t.n_s2l ? 4.0 * me * mc + 4.0 * (mc + me) * t.n_s2l : 0;
+    st[6].flops = 2.0 * me * me * t.m2l.npairs;
+    st[6].bytes = 4.0 * me * me * t.w_m2l_ops + 4.0 * me * (t.n_up + t.n_dn);
+    st[7].flops = 2.0 * me * me * t.w_l2l_pairs;
+    st[7].bytes = 4.0 * 8 * me * me + 4.0 * 2 * me * t.w_l2l_pairs;
+    st[8].fp64 = 1;
+    st[8].flops = st[8].flops_fp64 = 2.0 * me * me * (t.n_phid + t.n_phiu);
+    st[8].bytes = 2 * 8.0 * me * me + (4.0 + 8.0) * me * (t.n_phid + t.n_phiu);
+    st[9].interactions = t.w_p2p_inter + t.w_l2t_inter + t.w_m2t_inter;
+    st[9].fp64 = 1;
+    st[9].flops_fp64 = (t.w_l2t_inter + t.w_m2t_inter) * flops_per_pair(stress ? K_D : K_U);
+    st[9].flops = t.w_p2p_inter * flops_per_pair(kernel) + st[9].flops_fp64;
+    st[9].bytes = t.w_p2p_src * (stress ? rec_sb : rec_b) + t.ntrg * (12.0 + 4.0 * (stress ? 6 : 3)) +
+                  8.0 * me * (t.n_phid + t.n_phiu);
+    if (t.ev_valid) {
+        EB_CUDA(cudaEventSynchronize(t.ev[Tree::NPHASE]));
+        for (int i = 0; i < Tree::NPHASE; ++i) {
+            float ms = 0;
+            EB_CUDA(cudaEventElapsedTime(&ms, t.ev[i], t.ev[i + 1]));
+            st[i].ms = ms;
+        }
+    }
+    const int n = std::min(cap, (int)Tree::NPHASE);
+    std::memcpy(out, st, sizeof(ebem_phase_stat) * n);
+    return Tree::NPHASE;
 }
 
 int gmres_solve(Tree&, const int32_t*, const float*, const float*, const float*, float*, int, int, double, int32_t*,

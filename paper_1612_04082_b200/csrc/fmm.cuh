@@ -107,6 +107,22 @@ struct Tree {
     OpPairs phid_pairs, phiu_pairs;      // single-op pairs for the fp64 reconstruction GEMM
     DBuf<double> phid_scale, phiu_scale; // half-width r of the box of each PHI row
 
+    // profiling (fmm_set_profiling / fmm_phase_stats)
+    static constexpr int NPHASE = 10;
+    bool profile = false;
+    cudaEvent_t ev[NPHASE + 1] = {};
+    bool ev_valid = false;
+    int phase_launches[NPHASE] = {};
+    // algorithmic work counts (schedule time)
+    double w_s2m_inter = 0, w_s2l_inter = 0, w_p2p_inter = 0, w_l2t_inter = 0, w_m2t_inter = 0;
+    double w_s2m_src = 0, w_s2l_src = 0, w_p2p_src = 0;
+    int64_t w_m2m_pairs = 0, w_l2l_pairs = 0;
+    int w_m2l_ops = 0;
+    ~Tree() {
+        for (auto& e : ev)
+            if (e) cudaEventDestroy(e);
+    }
+
     // workspace (allocated at build time; evaluation allocates nothing)
     DBuf<float4> rec_disp, rec_stress;   // prepared sources, tree order
     DBuf<float> Q;                       // check potentials [max(n_s2m, n_s2l) x mc]
@@ -121,6 +137,7 @@ Tree* build_tree(const float* src, const float* nrm, const float* w, int64_t nsr
 void fmm_evaluate(Tree& t, int kernel, const float* f, const float* g, float* out, cudaStream_t s);
 void tree_info(const Tree& t, ebem_tree_info* info);
 int64_t tree_export(const Tree& t, int what, void* buf, int64_t cap);
+int phase_stats(Tree& t, int kernel, ebem_phase_stat* out, int cap);
 int gmres_solve(Tree& t, const int32_t* bc_type, const float* self_U, const float* self_P,
                 const float* bc_val, float* x, int restart, int max_iter, double tol,
                 int32_t* iters_out, double* resid_out, cudaStream_t s);
