@@ -138,9 +138,13 @@ class FmmTree:
         self.nsrc, self.ntrg, self.device = nsrc, ntrg, device
 
     def __del__(self):
-        if getattr(self, "handle", None):
-            _lib.fmm_tree_free(self.handle)
-            self.handle = None
+        h = getattr(self, "handle", None)
+        self.handle = None
+        if h and _lib is not None:
+            try:
+                _lib.fmm_tree_free(h)
+            except Exception:       # interpreter teardown
+                pass
 
     def info(self):
         return fmm_tree_info(self)
