@@ -7,6 +7,7 @@
 //   leaves   : phi_d = r R_d^-1 w, phi_u = r R_u^-1 z in fp64; one kernel per target leaf
 //              does L2T + M2T in fp64 and the U-list near field (P2P) in fp32.
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 
 #include "fmm.cuh"
@@ -40,7 +41,7 @@ __global__ void __launch_bounds__(CP_T)
 check_potential_kernel(const int* __restrict__ tbox, const int* __restrict__ soff, const int* __restrict__ sidx,
                        const int* __restrict__ sbeg, const int* __restrict__ send, const int* __restrict__ anchor,
                        const int* __restrict__ level, BoxGeo geo, double rad, const float* __restrict__ sc, int nc,
-                       const float4* __restrict__ rec, KConst kc, float* __restrict__ Q) {
+                       const float4* __restrict__ rec, KConst kc, float* __restrict__ Q, int ldq) {
     extern __shared__ float smem[];
     float* acc = smem;                                                  // [3 nc]
     float4* srec = reinterpret_cast<float4*>(smem + ((3 * nc + 3) & ~3));   // [CP_TILE * 4]
@@ -69,7 +70,7 @@ check_potential_kernel(const int* __restrict__ tbox, const int* __restrict__ sof
         }
     }
     __syncthreads();
-    for (int k = threadIdx.x; k < 3 * nc; k += CP_T) Q[(int64_t)i * 3 * nc + k] = acc[k];
+    for (int k = threadIdx.x; k < 3 * nc; k += CP_T) Q[(int64_t)i * ldq + k] = acc[k];
 }
 
 // ------------------------------------------------------------------ leaf evaluation
@@ -183,6 +184,16 @@ void schedule_tree(Tree& t, cudaStream_t s) {
     for (int b = 0; b < nb; ++b) {
         if (level[b] >= 2 && nsub[b] > 0) up[b] = t.n_up++;
         if (level[b] >= 2 && tsub[b] > 0) dn[b] = t.n_dn++;
+    }
+    t.up_lstart.assign(t.nlevels + 1, 0);
+    t.dn_lstart.assign(t.nlevels + 1, 0);
+    for (int b = 0; b < nb; ++b) {
+        if (up[b] >= 0) t.up_lstart[level[b] + 1] = up[b] + 1;
+        if (dn[b] >= 0) t.dn_lstart[level[b] + 1] = dn[b] + 1;
+    }
+    for (int l = 1; l <= t.nlevels; ++l) {
+        t.up_lstart[l] = std::max(t.up_lstart[l], t.up_lstart[l - 1]);
+        t.dn_lstart[l] = std::max(t.dn_lstart[l], t.dn_lstart[l - 1]);
     }
     t.up_slot.alloc(nb);
     t.dn_slot.alloc(nb);
@@ -359,9 +370,29 @@ void schedule_tree(Tree& t, cudaStream_t s) {
     const int me = P.me, mc = P.mc;
     t.rec_disp.alloc(std::max<int64_t>(t.nsrc * REC_DISP, 1));
     t.rec_stress.alloc(std::max<int64_t>(t.nsrc * REC_STRESS, 1));
-    t.Q.alloc((size_t)std::max(1, std::max(t.n_s2m, t.n_s2l)) * mc);
-    t.Z.alloc((size_t)std::max(1, t.n_up) * me);
-    t.W.alloc((size_t)std::max(1, t.n_dn) * me);
+    const int lde = P.lde, ldc = P.ldc;
+    const int64_t nq = std::max(1, std::max(t.n_s2m, t.n_s2l));
+    t.Q.alloc((size_t)nq * ldc);
+    t.Z.alloc((size_t)std::max(1, t.n_up) * lde);
+    t.W.alloc((size_t)std::max(1, t.n_dn) * lde);
+    if (const char* e = std::getenv("EBEM_SIMT")) t.use_tc = std::atoi(e) == 0;
+    if (t.use_tc) {
+        t.Qb.alloc(t.Q.n); t.Qs.alloc(t.Q.n);
+        t.Zb.alloc(t.Z.n); t.Zs.alloc(t.Z.n);
+        t.Wb.alloc(t.W.n); t.Ws.alloc(t.W.n);
+        for (DBuf<float>* b : {&t.Qb, &t.Qs, &t.Zb, &t.Zs, &t.Wb, &t.Ws}) b->zero(s);
+        tc_make_map_b(&t.mQb, t.Qb.p, nq, mc, ldc);
+        tc_make_map_b(&t.mQs, t.Qs.p, nq, mc, ldc);
+        tc_make_map_b(&t.mZb, t.Zb.p, std::max(1, t.n_up), me, lde);
+        tc_make_map_b(&t.mZs, t.Zs.p, std::max(1, t.n_up), me, lde);
+        tc_make_map_b(&t.mWb, t.Wb.p, std::max(1, t.n_dn), me, lde);
+        tc_make_map_b(&t.mWs, t.Ws.p, std::max(1, t.n_dn), me, lde);
+        tc_build_tiles(t.q2z_up, me);
+        tc_build_tiles(t.q2z_dn, me);
+        tc_build_tiles(t.m2l, me);
+        for (auto& x : t.m2m) tc_build_tiles(x, me);
+        for (auto& x : t.l2l) tc_build_tiles(x, me);
+    }
     t.PHID.alloc((size_t)std::max(1, t.n_phid) * me);
     t.PHIU.alloc((size_t)std::max(1, t.n_phiu) * me);
     EB_CUDA(cudaStreamSynchronize(s));
@@ -387,7 +418,7 @@ static void launch_check(const Tree& t, const int* tbox, int n, const int* soff,
     size_t sm = sizeof(float) * ((3 * P.nc + 3) & ~3) + sizeof(float4) * CP_TILE * REC_DISP;
     KConst kc = make_kconst(t.mat);
     check_potential_kernel<SL, DL><<<n, CP_T, sm, s>>>(tbox, soff, sidx, t.sbeg.p, t.send.p, t.anchor.p, t.level.p,
-                                                       geo, rad, P.s_c.p, P.nc, t.rec_disp.p, kc, t.Q.p);
+                                                       geo, rad, P.s_c.p, P.nc, t.rec_disp.p, kc, t.Q.p, P.ldc);
     EB_CHECK_LAUNCH();
 }
 
@@ -444,9 +475,25 @@ void fmm_evaluate(Tree& t, int kernel, const float* f, const float* g, float* ou
     else if (sl) launch_check<true, false>(t, t.s2m_box.p, t.n_s2m, nullptr, nullptr, RAD_UC, s);
     else launch_check<false, true>(t, t.s2m_box.p, t.n_s2m, nullptr, nullptr, RAD_UC, s);
     mark(phase++);
-    gemm_pairs_f32(t.q2z_up, P.Qu1T.p, me, mc, t.Q.p, mc, t.Z.p, me, s);
+    const int lde = P.lde, ldc = P.ldc;
+    auto zrows = [&](int l) { return (int64_t)t.up_lstart[l + 1] - t.up_lstart[l]; };
+    auto wrows = [&](int l) { return (int64_t)t.dn_lstart[l + 1] - t.dn_lstart[l]; };
+    if (t.use_tc) {
+        tc_split_rows(t.Q.p, ldc, 0, t.n_s2m, mc, t.Qb.p, t.Qs.p, s);
+        tc_pairs_gemm(t.q2z_up, P.mQu1T_b, P.mQu1T_s, t.mQb, t.mQs, me, mc, t.Z.p, lde, s);
+    } else {
+        gemm_pairs_f32(t.q2z_up, P.Qu1T.p, me, mc, ldc, t.Q.p, ldc, t.Z.p, lde, s);
+    }
     mark(phase++);
-    for (int l = t.nlevels - 1; l >= 2; --l) gemm_pairs_f32(t.m2m[l], P.M2M.p, me, me, t.Z.p, me, t.Z.p, me, s);
+    for (int l = t.nlevels - 2; l >= 2; --l) {
+        if (t.use_tc) {
+            tc_split_rows(t.Z.p, lde, t.up_lstart[l + 1], zrows(l + 1), me, t.Zb.p, t.Zs.p, s);
+            tc_pairs_gemm(t.m2m[l], P.mM2M_b, P.mM2M_s, t.mZb, t.mZs, me, me, t.Z.p, lde, s);
+        } else {
+            gemm_pairs_f32(t.m2m[l], P.M2M.p, me, me, lde, t.Z.p, lde, t.Z.p, lde, s);
+        }
+    }
+    if (t.use_tc && t.nlevels > 2) tc_split_rows(t.Z.p, lde, t.up_lstart[2], zrows(2), me, t.Zb.p, t.Zs.p, s);
     mark(phase++);
 
     // downward pass
@@ -456,16 +503,31 @@ void fmm_evaluate(Tree& t, int kernel, const float* f, const float* g, float* ou
         else launch_check<false, true>(t, t.s2l_box.p, t.n_s2l, t.x_src_off.p, t.x_src_idx.p, RAD_DC, s);
     }
     mark(phase++);
-    if (t.n_s2l) gemm_pairs_f32(t.q2z_dn, P.Qd1T.p, me, mc, t.Q.p, mc, t.W.p, me, s);
+    if (t.n_s2l) {
+        if (t.use_tc) {
+            tc_split_rows(t.Q.p, ldc, 0, t.n_s2l, mc, t.Qb.p, t.Qs.p, s);
+            tc_pairs_gemm(t.q2z_dn, P.mQd1T_b, P.mQd1T_s, t.mQb, t.mQs, me, mc, t.W.p, lde, s);
+        } else {
+            gemm_pairs_f32(t.q2z_dn, P.Qd1T.p, me, mc, ldc, t.Q.p, ldc, t.W.p, lde, s);
+        }
+    }
     mark(phase++);
-    gemm_pairs_f32(t.m2l, P.M2L.p, me, me, t.Z.p, me, t.W.p, me, s);
+    if (t.use_tc) tc_pairs_gemm(t.m2l, P.mM2L_b, P.mM2L_s, t.mZb, t.mZs, me, me, t.W.p, lde, s);
+    else gemm_pairs_f32(t.m2l, P.M2L.p, me, me, lde, t.Z.p, lde, t.W.p, lde, s);
     mark(phase++);
-    for (int l = 3; l < t.nlevels; ++l) gemm_pairs_f32(t.l2l[l], P.L2L.p, me, me, t.W.p, me, t.W.p, me, s);
+    for (int l = 3; l < t.nlevels; ++l) {
+        if (t.use_tc) {
+            tc_split_rows(t.W.p, lde, t.dn_lstart[l - 1], wrows(l - 1), me, t.Wb.p, t.Ws.p, s);
+            tc_pairs_gemm(t.l2l[l], P.mL2L_b, P.mL2L_s, t.mWb, t.mWs, me, me, t.W.p, lde, s);
+        } else {
+            gemm_pairs_f32(t.l2l[l], P.L2L.p, me, me, lde, t.W.p, lde, t.W.p, lde, s);
+        }
+    }
     mark(phase++);
 
     // equivalent densities (fp64) and leaf evaluation
-    gemm_pairs_f64(t.phid_pairs, P.Rdinv.p, me, me, t.W.p, me, t.phid_scale.p, t.PHID.p, me, s);
-    gemm_pairs_f64(t.phiu_pairs, P.Ruinv.p, me, me, t.Z.p, me, t.phiu_scale.p, t.PHIU.p, me, s);
+    gemm_pairs_f64(t.phid_pairs, P.Rdinv.p, me, me, t.W.p, lde, t.phid_scale.p, t.PHID.p, me, s);
+    gemm_pairs_f64(t.phiu_pairs, P.Ruinv.p, me, me, t.Z.p, lde, t.phiu_scale.p, t.PHIU.p, me, s);
     mark(phase++);
     switch (kernel) {
         case K_U: launch_eval<true, false, false>(t, out, s); break;

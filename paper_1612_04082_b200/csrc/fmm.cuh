@@ -14,6 +14,8 @@
 // ill-conditioned solve.  phi is only formed (in fp64) for the leaf evaluations
 // L2T and M2T.
 #pragma once
+#include <cuda.h>
+
 #include <map>
 #include <memory>
 #include <mutex>
@@ -32,14 +34,18 @@ struct Plan {
     int p = 0, pc = 0;          // equivalent / check surface points per edge (pc = p + 1)
     int ne = 0, nc = 0;         // surface point counts
     int me = 0, mc = 0;         // 3 ne, 3 nc (vector lengths)
+    int lde = 0, ldc = 0;       // row strides (me, mc rounded up to a multiple of 4: 16-B TMA rows)
     double rcond = 0;
     Material mat{};
     DBuf<float> s_e, s_c;       // unit surface grids [ne*3], [nc*3] (fp32 copies)
     DBuf<double> s_e64, s_c64;
-    DBuf<float> Qu1T, Qd1T;     // [me x mc] row-major: z = Qu1T q
+    DBuf<float> Qu1T, Qd1T;     // [me x ldc] row-major: z = Qu1T q
     DBuf<double> Ruinv, Rdinv;  // [me x me] row-major upper triangular: phi = r Rinv z
-    DBuf<float> M2M, L2L;       // [8][me x me]
-    DBuf<float> M2L;            // [316][me x me]
+    DBuf<float> M2M, L2L;       // [8][me x lde]
+    DBuf<float> M2L;            // [316][me x lde]
+    // exact-TF32 head / remainder splits of the operators (3xTF32 tensor-core path)
+    DBuf<float> Qu1T_b, Qu1T_s, Qd1T_b, Qd1T_s, M2M_b, M2M_s, L2L_b, L2L_s, M2L_b, M2L_s;
+    CUtensorMap mQu1T_b, mQu1T_s, mQd1T_b, mQd1T_s, mM2M_b, mM2M_s, mL2L_b, mL2L_s, mM2L_b, mM2L_s;
     int off_index[343];         // (ox+3)*49+(oy+3)*7+(oz+3) -> 0..315 or -1
 };
 
@@ -54,6 +60,8 @@ struct OpPairs {
     DBuf<int2> pairs;            // [npairs] (target row, source row)
     std::vector<int> op_ptr_h;   // host copy (launch sizing)
     int max_per_op = 0;
+    int ntiles = 0;              // tensor-core tiles (op, first pair, #pairs, row block)
+    DBuf<int> tiles;
 };
 
 // ------------------------------------------------------------------ tree
@@ -106,6 +114,8 @@ struct Tree {
     DBuf<int> phiu_box, phiu_slot;       // [n_phiu] box ids; box -> row in PHI_U (-1)
     OpPairs phid_pairs, phiu_pairs;      // single-op pairs for the fp64 reconstruction GEMM
     DBuf<double> phid_scale, phiu_scale; // half-width r of the box of each PHI row
+    std::vector<int> up_lstart, dn_lstart;  // per level: first Z / W row (rows are level-major)
+    bool use_tc = true;                  // tcgen05 3xTF32 translations (else SIMT fp32)
 
     // profiling (fmm_set_profiling / fmm_phase_stats)
     static constexpr int NPHASE = 10;
@@ -126,7 +136,9 @@ struct Tree {
     // workspace (allocated at build time; evaluation allocates nothing)
     DBuf<float4> rec_disp, rec_stress;   // prepared sources, tree order
     DBuf<float> Q;                       // check potentials [max(n_s2m, n_s2l) x mc]
-    DBuf<float> Z, W;                    // [n_up x me], [n_dn x me]
+    DBuf<float> Z, W;                    // [n_up x lde], [n_dn x lde]
+    DBuf<float> Qb, Qs, Zb, Zs, Wb, Ws;  // TF32 head / remainder copies (B operands)
+    CUtensorMap mQb, mQs, mZb, mZs, mWb, mWs;
     DBuf<double> PHID, PHIU;             // [n_phid x me], [n_phiu x me]
     DBuf<float> out_sorted;              // [ntrg x 6]
     int64_t device_bytes = 0;
@@ -153,8 +165,16 @@ void gemm_f64(int m, int n, int k, double alpha, const double* A, int64_t sA, in
               int batch, cudaStream_t s);
 // pairs GEMM: Y[t] += Mat[op] * X[src] for every pair (t, src) of every op; Mat row-major
 // [M x K]; X rows of length ldx >= K; Y rows of length ldy >= M.  fp32.
-void gemm_pairs_f32(const OpPairs& P, const float* mats, int M, int K, const float* X, int ldx,
+void gemm_pairs_f32(const OpPairs& P, const float* mats, int M, int K, int ldm, const float* X, int ldx,
                     float* Y, int ldy, cudaStream_t s);
+// tensor-core path (tc_gemm.cu)
+void tc_make_map_a(CUtensorMap* m, const float* base, int nops, int M, int K, int ld);
+void tc_make_map_b(CUtensorMap* m, const float* base, int64_t rows, int K, int ld);
+void tc_split_rows(const float* X, int ld, int64_t row0, int64_t nrows, int K, float* Xb, float* Xs,
+                   cudaStream_t s);
+void tc_build_tiles(OpPairs& P, int M);
+void tc_pairs_gemm(const OpPairs& P, const CUtensorMap& Ab, const CUtensorMap& As, const CUtensorMap& Bb,
+                   const CUtensorMap& Bs, int M, int K, float* Y, int ldy, cudaStream_t s);
 // fp64 variant with per-pair scale (r of the box, looked up from scale[t])
 void gemm_pairs_f64(const OpPairs& P, const double* mat, int M, int K, const float* X, int ldx,
                     const double* scale, double* Y, int ldy, cudaStream_t s);

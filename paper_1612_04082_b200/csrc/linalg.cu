@@ -270,7 +270,7 @@ constexpr int PG_M = 64, PG_N = 64, PG_K = 16;
 // target land on the same rows).
 __global__ void __launch_bounds__(256)
 gemm_pairs_f32_kernel(const int* __restrict__ op_ptr, const int2* __restrict__ pairs, int nops,
-                      const float* __restrict__ mats, int M, int K, const float* __restrict__ X,
+                      const float* __restrict__ mats, int M, int K, int ldm, const float* __restrict__ X,
                       int ldx, float* __restrict__ Y, int ldy) {
     const int op = blockIdx.z;
     const int p0 = op_ptr[op] + blockIdx.y * PG_N;
@@ -278,7 +278,7 @@ gemm_pairs_f32_kernel(const int* __restrict__ op_ptr, const int2* __restrict__ p
     if (p0 >= p1) return;
     const int np = min(PG_N, p1 - p0);
     const int m0 = blockIdx.x * PG_M;
-    const float* Mt = mats + (int64_t)op * M * K;
+    const float* Mt = mats + (int64_t)op * M * ldm;
     __shared__ float As[PG_K][PG_M + 4];
     __shared__ float Bs[PG_K][PG_N + 4];
     __shared__ int2 pr[PG_N];
@@ -290,7 +290,7 @@ gemm_pairs_f32_kernel(const int* __restrict__ op_ptr, const int2* __restrict__ p
         for (int e = threadIdx.x; e < PG_K * PG_M; e += 256) {
             int r = e / PG_K, c = e % PG_K;
             int gm = m0 + r, gk = k0 + c;
-            As[c][r] = (gm < M && gk < K) ? Mt[(int64_t)gm * K + gk] : 0.f;
+            As[c][r] = (gm < M && gk < K) ? Mt[(int64_t)gm * ldm + gk] : 0.f;
             int j = e / PG_K;                      // pair j, k offset c
             int src = pr[j].y;
             Bs[c][j] = (src >= 0 && gk < K) ? X[(int64_t)src * ldx + gk] : 0.f;
@@ -323,11 +323,11 @@ gemm_pairs_f32_kernel(const int* __restrict__ op_ptr, const int2* __restrict__ p
     }
 }
 
-void gemm_pairs_f32(const OpPairs& P, const float* mats, int M, int K, const float* X, int ldx,
+void gemm_pairs_f32(const OpPairs& P, const float* mats, int M, int K, int ldm, const float* X, int ldx,
                     float* Y, int ldy, cudaStream_t s) {
     if (P.npairs == 0) return;
     dim3 grid(ceil_div(M, PG_M), ceil_div(P.max_per_op, PG_N), P.nops);
-    gemm_pairs_f32_kernel<<<grid, 256, 0, s>>>(P.op_ptr.p, P.pairs.p, P.nops, mats, M, K, X, ldx, Y, ldy);
+    gemm_pairs_f32_kernel<<<grid, 256, 0, s>>>(P.op_ptr.p, P.pairs.p, P.nops, mats, M, K, ldm, X, ldx, Y, ldy);
     EB_CHECK_LAUNCH();
 }
 

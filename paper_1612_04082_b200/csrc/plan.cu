@@ -186,13 +186,17 @@ __global__ void extract_q1t(const double* __restrict__ Q, int m, int mc, int me,
     Q1T[e] = Q[(int64_t)i * m + k];
 }
 
-__global__ void cast_f32(const double* __restrict__ a, float* __restrict__ b, int64_t n) {
+// fp64 [rows x cols] (dense) -> fp32 [rows x ldb]
+__global__ void cast_f32(const double* __restrict__ a, float* __restrict__ b, int64_t rows, int cols, int ldb) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) b[i] = (float)a[i];
+    if (i >= rows * cols) return;
+    const int64_t r = i / cols;
+    const int c = (int)(i % cols);
+    b[r * ldb + c] = (float)a[i];
 }
 
-static void to_f32(const double* a, float* b, int64_t n, cudaStream_t s) {
-    cast_f32<<<ceil_div(n, 256), 256, 0, s>>>(a, b, n);
+static void to_f32(const double* a, float* b, int64_t rows, int cols, int ldb, cudaStream_t s) {
+    cast_f32<<<ceil_div(rows * cols, 256), 256, 0, s>>>(a, b, rows, cols, ldb);
     EB_CHECK_LAUNCH();
 }
 
@@ -232,7 +236,7 @@ static void composites(const Plan& P, const DBuf<double>& Q1T, const DBuf<double
         kmat(P, sx, P.nc, xs, sy, P.ne, ys, xoc, yoc, scale, K.p, nbc, s);
         gemm_f64(mc, me, me, 1.0, K.p, (int64_t)mc * me, me, Rinv.p, 0, me, 0.0, T.p, (int64_t)mc * me, me, nbc, s);
         gemm_f64(me, me, mc, 1.0, Q1T.p, 0, mc, T.p, (int64_t)mc * me, me, 0.0, C.p, (int64_t)me * me, me, nbc, s);
-        to_f32(C.p, out + (int64_t)b0 * me * me, (int64_t)nbc * me * me, s);
+        to_f32(C.p, out + (int64_t)b0 * me * P.lde, (int64_t)nbc * me, me, P.lde, s);
     }
     EB_CUDA(cudaStreamSynchronize(s));
 }
@@ -248,6 +252,8 @@ static std::shared_ptr<Plan> make_plan(int p, const Material& m, cudaStream_t s)
     P->nc = (int)sc.size() / 3;
     P->me = 3 * P->ne;
     P->mc = 3 * P->nc;
+    P->lde = (P->me + 3) & ~3;
+    P->ldc = (P->mc + 3) & ~3;
     P->s_e64.alloc(se.size());
     P->s_c64.alloc(sc.size());
     h2d(P->s_e64.p, se.data(), se.size(), s);
@@ -261,10 +267,12 @@ static std::shared_ptr<Plan> make_plan(int p, const Material& m, cudaStream_t s)
     DBuf<double> Qu1T, Qd1T;
     factor_solve(*P, P->s_c64, RAD_UC, P->s_e64, RAD_UE, Qu1T, P->Ruinv, s);
     factor_solve(*P, P->s_c64, RAD_DC, P->s_e64, RAD_DE, Qd1T, P->Rdinv, s);
-    P->Qu1T.alloc((size_t)P->me * P->mc);
-    P->Qd1T.alloc((size_t)P->me * P->mc);
-    to_f32(Qu1T.p, P->Qu1T.p, (int64_t)P->me * P->mc, s);
-    to_f32(Qd1T.p, P->Qd1T.p, (int64_t)P->me * P->mc, s);
+    P->Qu1T.alloc((size_t)P->me * P->ldc);
+    P->Qd1T.alloc((size_t)P->me * P->ldc);
+    P->Qu1T.zero(s);
+    P->Qd1T.zero(s);
+    to_f32(Qu1T.p, P->Qu1T.p, P->me, P->mc, P->ldc, s);
+    to_f32(Qd1T.p, P->Qd1T.p, P->me, P->mc, P->ldc, s);
 
     // M2M_c = Q_u1^T (1/2 K(uc_P, ue_C)) R_u^-1 (parent half-width 1; child centre o_c)
     // L2L_c = Q_d1^T K(dc_C, de_P) R_d^-1
@@ -274,8 +282,10 @@ static std::shared_ptr<Plan> make_plan(int p, const Material& m, cudaStream_t s)
         oc.push_back(((c >> 1) & 1) - 0.5);
         oc.push_back((c & 1) - 0.5);
     }
-    P->M2M.alloc((size_t)8 * P->me * P->me);
-    P->L2L.alloc((size_t)8 * P->me * P->me);
+    P->M2M.alloc((size_t)8 * P->me * P->lde);
+    P->L2L.alloc((size_t)8 * P->me * P->lde);
+    P->M2M.zero(s);
+    P->L2L.zero(s);
     composites(*P, Qu1T, P->Ruinv, P->s_c64, RAD_UC, P->s_e64, 0.5 * RAD_UE, zero8, oc, 0.5, P->M2M.p, s);
     composites(*P, Qd1T, P->Rdinv, P->s_c64, 0.5 * RAD_DC, P->s_e64, RAD_DE, oc, zero8, 1.0, P->L2L.p, s);
 
@@ -291,8 +301,27 @@ static std::shared_ptr<Plan> make_plan(int p, const Material& m, cudaStream_t s)
                 xo.insert(xo.end(), {0.0, 0.0, 0.0});
                 yo.insert(yo.end(), {2.0 * ox, 2.0 * oy, 2.0 * oz});
             }
-    P->M2L.alloc((size_t)NV_OFFSETS * P->me * P->me);
+    P->M2L.alloc((size_t)NV_OFFSETS * P->me * P->lde);
+    P->M2L.zero(s);
     composites(*P, Qd1T, P->Ruinv, P->s_c64, RAD_DC, P->s_e64, RAD_UE, xo, yo, 1.0, P->M2L.p, s);
+
+    // exact-TF32 head / remainder splits and TMA maps for the tensor-core path
+    auto split = [&](const DBuf<float>& X, int nops, int K, int ld, DBuf<float>& Xb, DBuf<float>& Xs, CUtensorMap* mb,
+                     CUtensorMap* ms) {
+        Xb.alloc(X.n);
+        Xs.alloc(X.n);
+        Xb.zero(s);
+        Xs.zero(s);
+        tc_split_rows(X.p, ld, 0, (int64_t)nops * P->me, K, Xb.p, Xs.p, s);
+        tc_make_map_a(mb, Xb.p, nops, P->me, K, ld);
+        tc_make_map_a(ms, Xs.p, nops, P->me, K, ld);
+    };
+    split(P->Qu1T, 1, P->mc, P->ldc, P->Qu1T_b, P->Qu1T_s, &P->mQu1T_b, &P->mQu1T_s);
+    split(P->Qd1T, 1, P->mc, P->ldc, P->Qd1T_b, P->Qd1T_s, &P->mQd1T_b, &P->mQd1T_s);
+    split(P->M2M, 8, P->me, P->lde, P->M2M_b, P->M2M_s, &P->mM2M_b, &P->mM2M_s);
+    split(P->L2L, 8, P->me, P->lde, P->L2L_b, P->L2L_s, &P->mL2L_b, &P->mL2L_s);
+    split(P->M2L, NV_OFFSETS, P->me, P->lde, P->M2L_b, P->M2L_s, &P->mM2L_b, &P->mM2L_s);
+    EB_CUDA(cudaStreamSynchronize(s));
     return P;
 }
 

@@ -1,0 +1,371 @@
+// Tensor-core (tcgen05, sm_100a) operator-grouped pairs GEMM, 3xTF32:
+//     Y[t] += Mat[op] X[s]      for every pair (t, s) of every operator op
+// used for the KIFMM translations ("M2M, L2L and M2L operators ...
+// represented by matrices"): Q2Z, M2M, M2L, L2L.  Pairs are grouped by operator (for
+// M2L: by translation vector), so a CTA tile is one operator's 128-row slice times 128
+// pairs: a dense [128 x K] x [K x 128] contraction with the B operand gathered row by
+// row (TMA tile::gather4) from the state array.
+//
+// Precision: A = A_b + A_s and B = B_b + B_s with A_b = rna_tf32(A), A_s = rna_tf32(A - A_b)
+// (same for B); D += A_b B_b + A_b B_s + A_s B_b in fp32 TMEM accumulators: unbiased
+// error ~3 * 2^-22 relative per product, the fp32 level.
+//
+// CTA = 8 warps.  warp 0: TMA producer (A_b, A_s 3-D tile loads; B_b, B_s gather4),
+// warp 1 lane 0: tcgen05.mma issuer, warp 2: TMEM allocator, warps 4-7: drain TMEM partial
+// sums into fp32 registers, then fp32 atomics into Y (coalesced along rows).
+// 3-stage smem ring of 4 x 16 KB (SWIZZLE_128B, K-major), mbarrier full/empty pipeline.
+#include <cuda.h>
+
+#include <algorithm>
+
+#include "fmm.cuh"
+
+namespace ebem {
+
+namespace tc {
+
+constexpr int BM = 128, BN = 128, BK = 32;     // tile: 128 rows x 128 pairs x 32 K (128 B)
+constexpr int STAGES = 3;
+constexpr int OPND_BYTES = BM * BK * 4;        // 16 KB per operand tile (BM == BN)
+constexpr int STAGE_BYTES = 4 * OPND_BYTES;    // Ab, As, Bb, Bs
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/ + BN * 4;
+constexpr int THREADS = 256;
+constexpr int TMEM_COLS = 4 * BN;              // 3 accumulators used (power-of-2 allocation)
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+    uint32_t done;
+    do {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done)
+            : "r"(bar), "r"(parity)
+            : "memory");
+    } while (!done);
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map, int c0, int c1, int c2,
+                                            uint32_t bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cta.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
+        ::"r"(dst), "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(bar)
+        : "memory");
+}
+__device__ __forceinline__ void tma_gather4(uint32_t dst, const CUtensorMap* map, int col, int r0, int r1, int r2,
+                                            int r3, uint32_t bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cta.global.tile::gather4.mbarrier::complete_tx::bytes "
+        "[%0], [%1, {%2, %3, %4, %5, %6}], [%7];"
+        ::"r"(dst), "l"(map), "r"(col), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(bar)
+        : "memory");
+}
+
+// K-major SWIZZLE_128B UMMA shared-memory descriptor (rows of 128 B, 8-row atoms 1024 B apart)
+__device__ __forceinline__ uint64_t smem_desc(uint32_t addr) {
+    uint64_t d = 0;
+    d |= (uint64_t)((addr >> 4) & 0x3FFF);          // start address
+    d |= (uint64_t)1 << 16;                         // LBO (unused for swizzled K-major)
+    d |= (uint64_t)(1024 >> 4) << 32;               // SBO: 8 rows x 128 B
+    d |= (uint64_t)1 << 46;                         // descriptor version (sm_100)
+    d |= (uint64_t)2 << 61;                         // SWIZZLE_128B
+    return d;
+}
+
+__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}"
+        ::"r"(tmem_d), "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void mma_commit(uint32_t bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
+}
+
+struct Tile {
+    int op, p0, np, m0;
+};
+
+// The tensor core's fp32 accumulation is not round-to-nearest: chaining all K/8 MMAs
+// into one accumulator costs ~(chain length) x 2^-24 of bias (measured: FMM p=10 error
+// 8e-6 with one chain vs 5.5e-7 with SIMT fp32).  The main products therefore go to two
+// ping-pong TMEM accumulators that restart every GROUP K-chunks; epilogue warps drain
+// each finished group into fp32 registers (round-to-nearest adds) while the MMA warp
+// fills the other buffer.  The small correction products (A_b B_s + A_s B_b, ~2^-11 of
+// the main) accumulate in a third buffer over the whole K.
+constexpr int GROUP = 2;
+constexpr int EPI_WARP0 = 4;                   // warps 4..7: epilogue / drain (TMEM lanes 0..127)
+
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t* v) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+          "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]),
+          "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]),
+          "=r"(v[30]), "=r"(v[31])
+        : "r"(taddr));
+}
+
+// add the 128 columns of TMEM buffer `col` (this warp's 32 lanes) into acc[128]
+__device__ __forceinline__ void drain_add(uint32_t tmem, int wq, int col, float* acc) {
+#pragma unroll
+    for (int c0 = 0; c0 < BN; c0 += 32) {
+        uint32_t v[32];
+        tmem_ld32(tmem + ((uint32_t)(32 * wq) << 16) + (uint32_t)(col + c0), v);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+        for (int j = 0; j < 32; ++j) acc[c0 + j] += __uint_as_float(v[j]);
+    }
+}
+
+__global__ void __launch_bounds__(THREADS, 1)
+tc_pairs_kernel(const __grid_constant__ CUtensorMap mapAb, const __grid_constant__ CUtensorMap mapAs,
+                const __grid_constant__ CUtensorMap mapBb, const __grid_constant__ CUtensorMap mapBs,
+                const Tile* __restrict__ tiles, const int2* __restrict__ pairs, int M, int K,
+                float* __restrict__ Y, int ldy) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    // barriers: full[S], empty[S], acc_full[2], acc_empty[2], corr_full
+    uint64_t* bars = (uint64_t*)(smem + STAGES * STAGE_BYTES);
+    uint64_t* full_b = bars;
+    uint64_t* empty_b = bars + STAGES;
+    uint64_t* accf_b = bars + 2 * STAGES;
+    uint64_t* acce_b = bars + 2 * STAGES + 2;
+    uint64_t* corr_b = bars + 2 * STAGES + 4;
+    uint32_t* tmem_slot = (uint32_t*)(bars + 2 * STAGES + 5);
+    int* s_tgt = (int*)(smem + STAGES * STAGE_BYTES + 256);
+    __shared__ int s_src[BN];
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const Tile tl = tiles[blockIdx.x];
+    const int nk = (K + BK - 1) / BK;
+    const int ngroups = (nk + GROUP - 1) / GROUP;
+
+    if (threadIdx.x < BN) {
+        const int j = threadIdx.x;
+        const int2 pr = pairs[tl.p0 + (j < tl.np ? j : 0)];
+        s_tgt[j] = j < tl.np ? pr.x : -1;
+        s_src[j] = pr.y;
+    }
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(smem_u32(&full_b[s]), 1);
+            mbar_init(smem_u32(&empty_b[s]), 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(smem_u32(&accf_b[b]), 1);
+            mbar_init(smem_u32(&acce_b[b]), 4);
+        }
+        mbar_init(smem_u32(corr_b), 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 2) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(TMEM_COLS));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        // ---------------- producer
+        for (int kc = 0; kc < nk; ++kc) {
+            const int s = kc % STAGES;
+            const uint32_t ph = (kc / STAGES) & 1;
+            mbar_wait(smem_u32(&empty_b[s]), ph ^ 1);
+            uint8_t* st = smem + s * STAGE_BYTES;
+            const uint32_t full = smem_u32(&full_b[s]);
+            if (lane == 0) {
+                mbar_expect_tx(full, STAGE_BYTES);
+                tma_load_3d(smem_u32(st), &mapAb, kc * BK, tl.m0, tl.op, full);
+                tma_load_3d(smem_u32(st + OPND_BYTES), &mapAs, kc * BK, tl.m0, tl.op, full);
+            }
+            __syncwarp();
+            const int r = 4 * lane;
+            tma_gather4(smem_u32(st + 2 * OPND_BYTES + r * 128), &mapBb, kc * BK, s_src[r], s_src[r + 1],
+                        s_src[r + 2], s_src[r + 3], full);
+            tma_gather4(smem_u32(st + 3 * OPND_BYTES + r * 128), &mapBs, kc * BK, s_src[r], s_src[r + 1],
+                        s_src[r + 2], s_src[r + 3], full);
+        }
+    } else if (warp == 1) {
+        // ---------------- MMA issuer (one thread)
+        // instruction descriptor: D f32, A/B tf32, both K-major, N = 128, M = 128
+        const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BN >> 3) << 17) |
+                               ((uint32_t)(BM >> 4) << 24);
+        const uint32_t dcorr = tmem + (uint32_t)(2 * BN);
+        for (int kc = 0; kc < nk; ++kc) {
+            const int s = kc % STAGES;
+            const int g = kc / GROUP, b = g & 1;
+            const bool gfirst = (kc % GROUP) == 0, glast = (kc % GROUP) == GROUP - 1 || kc == nk - 1;
+            if (gfirst) {   // the buffer must have been drained (use n waits for drain n-1)
+                mbar_wait(smem_u32(&acce_b[b]), ((g >> 1) & 1) ^ 1);
+                asm volatile("tcgen05.fence::after_thread_sync;");
+            }
+            mbar_wait(smem_u32(&full_b[s]), (kc / STAGES) & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;");
+            if (lane == 0) {
+                const uint32_t st = smem_u32(smem + s * STAGE_BYTES);
+                const uint64_t ab = smem_desc(st), as = smem_desc(st + OPND_BYTES);
+                const uint64_t bb = smem_desc(st + 2 * OPND_BYTES), bs = smem_desc(st + 3 * OPND_BYTES);
+                const uint32_t dmain = tmem + (uint32_t)(b * BN);
+                const int ksteps = min(BK, K - kc * BK + 7) / 8;     // 8 tf32 (32 B) per MMA
+                for (int k = 0; k < ksteps; ++k) {
+                    const uint64_t off = (uint64_t)(2 * k);          // +32 B in 16-B units
+                    mma_tf32(dmain, ab + off, bb + off, idesc, (!gfirst) | (k != 0));
+                    mma_tf32(dcorr, ab + off, bs + off, idesc, (kc | k) != 0);
+                    mma_tf32(dcorr, as + off, bb + off, idesc, 1);
+                }
+                mma_commit(smem_u32(&empty_b[s]));                   // frees the smem stage
+                if (glast) mma_commit(smem_u32(&accf_b[b]));          // group partial ready
+                if (kc == nk - 1) mma_commit(smem_u32(corr_b));       // corrections ready
+            }
+            __syncwarp();
+        }
+    } else if (warp >= EPI_WARP0) {
+        // ---------------- drain + epilogue: fp32 register accumulation, then atomics into Y
+        const int wq = warp - EPI_WARP0;            // TMEM lane quarter
+        float acc[BN];
+#pragma unroll
+        for (int j = 0; j < BN; ++j) acc[j] = 0.f;
+        for (int g = 0; g < ngroups; ++g) {
+            const int b = g & 1;
+            mbar_wait(smem_u32(&accf_b[b]), (g >> 1) & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;");
+            drain_add(tmem, wq, b * BN, acc);
+            asm volatile("tcgen05.fence::before_thread_sync;");
+            __syncwarp();
+            if (lane == 0) mbar_arrive(smem_u32(&acce_b[b]));
+        }
+        mbar_wait(smem_u32(corr_b), 0);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        drain_add(tmem, wq, 2 * BN, acc);
+        const int row = tl.m0 + 32 * wq + lane;
+        if (row < M) {
+#pragma unroll
+            for (int j = 0; j < BN; ++j) {
+                const int t = s_tgt[j];
+                if (t >= 0) atomicAdd(Y + (int64_t)t * ldy + row, acc[j]);
+            }
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
+}
+
+// round-to-nearest TF32 (low 13 mantissa bits zero): both halves of the split are exact TF32
+// values, so the tensor core's own fp32->tf32 handling (truncation) never applies, and the
+// two rounding errors are unbiased (truncated remainders are one-signed and their dropped
+// product A_s B_s biases long dot products; measured 7e-6 -> see DESIGN.md Sec. 6).
+__device__ __forceinline__ float to_tf32(float x) {
+    uint32_t r;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+    return __uint_as_float(r);
+}
+
+// split fp32 rows into a TF32 head and a TF32 remainder (columns >= K untouched)
+__global__ void split_rows_kernel(const float* __restrict__ X, int ld, int64_t row0, int64_t nrows, int K,
+                                  float* __restrict__ Xb, float* __restrict__ Xs) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= nrows * K) return;
+    const int64_t r = row0 + i / K;
+    const int c = (int)(i % K);
+    const float x = X[r * ld + c];
+    const float b = to_tf32(x);
+    Xb[r * ld + c] = b;
+    Xs[r * ld + c] = to_tf32(x - b);
+}
+
+// ------------------------------------------------------------------ host side
+typedef CUresult (*EncodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiled encoder() {
+    static EncodeTiled fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        EB_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+        EB_REQUIRE(p && q == cudaDriverEntryPointSuccess, "cuTensorMapEncodeTiled not available");
+        fn = (EncodeTiled)p;
+    }
+    return fn;
+}
+
+}  // namespace tc
+
+// A maps: [nops][M][ld] fp32, box {32, 128, 1}
+void tc_make_map_a(CUtensorMap* m, const float* base, int nops, int M, int K, int ld) {
+    cuuint64_t dims[3] = {(cuuint64_t)K, (cuuint64_t)M, (cuuint64_t)nops};
+    cuuint64_t strides[2] = {(cuuint64_t)ld * 4, (cuuint64_t)M * ld * 4};
+    cuuint32_t box[3] = {tc::BK, tc::BM, 1};
+    cuuint32_t es[3] = {1, 1, 1};
+    CUresult r = tc::encoder()(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, (void*)base, dims, strides, box, es,
+                               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    EB_REQUIRE(r == CUDA_SUCCESS, "cuTensorMapEncodeTiled (A) failed: " + std::to_string((int)r));
+}
+
+// B maps: [rows][ld] fp32, gathered 4 rows at a time, box {32, 1}
+void tc_make_map_b(CUtensorMap* m, const float* base, int64_t rows, int K, int ld) {
+    cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)std::max<int64_t>(rows, 1)};
+    cuuint64_t strides[1] = {(cuuint64_t)ld * 4};
+    cuuint32_t box[2] = {tc::BK, 1};
+    cuuint32_t es[2] = {1, 1};
+    CUresult r = tc::encoder()(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void*)base, dims, strides, box, es,
+                               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    EB_REQUIRE(r == CUDA_SUCCESS, "cuTensorMapEncodeTiled (B) failed: " + std::to_string((int)r));
+}
+
+void tc_split_rows(const float* X, int ld, int64_t row0, int64_t nrows, int K, float* Xb, float* Xs,
+                   cudaStream_t s) {
+    if (nrows <= 0) return;
+    tc::split_rows_kernel<<<ceil_div(nrows * K, 256), 256, 0, s>>>(X, ld, row0, nrows, K, Xb, Xs);
+    EB_CHECK_LAUNCH();
+}
+
+void tc_build_tiles(OpPairs& P, int M) {
+    std::vector<tc::Tile> t;
+    for (int o = 0; o < P.nops; ++o)
+        for (int p0 = P.op_ptr_h[o]; p0 < P.op_ptr_h[o + 1]; p0 += tc::BN)
+            for (int m0 = 0; m0 < M; m0 += tc::BM)
+                t.push_back({o, p0, std::min(tc::BN, P.op_ptr_h[o + 1] - p0), m0});
+    P.ntiles = (int)t.size();
+    P.tiles.alloc(std::max<size_t>(t.size(), 1) * sizeof(tc::Tile) / sizeof(int));
+    if (!t.empty()) EB_CUDA(cudaMemcpy(P.tiles.p, t.data(), t.size() * sizeof(tc::Tile), cudaMemcpyHostToDevice));
+}
+
+void tc_pairs_gemm(const OpPairs& P, const CUtensorMap& Ab, const CUtensorMap& As, const CUtensorMap& Bb,
+                   const CUtensorMap& Bs, int M, int K, float* Y, int ldy, cudaStream_t s) {
+    if (P.ntiles == 0) return;
+    static bool attr = false;
+    if (!attr) {
+        EB_CUDA(cudaFuncSetAttribute(tc::tc_pairs_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     tc::SMEM_BYTES));
+        attr = true;
+    }
+    tc::tc_pairs_kernel<<<P.ntiles, tc::THREADS, tc::SMEM_BYTES, s>>>(
+        Ab, As, Bb, Bs, reinterpret_cast<const tc::Tile*>(P.tiles.p), P.pairs.p, M, K, Y, ldy);
+    EB_CHECK_LAUNCH();
+}
+
+}  // namespace ebem

@@ -1,0 +1,35 @@
+"""The tcgen05 3xTF32 translation path against the fp32 SIMT path (same schedule, same
+operators): the two must agree to fp32 rounding, and both against the exact sum."""
+import os
+
+import numpy as np
+import pytest
+
+from oracle import cdirect
+from oracle import kernels as KN
+from workloads import geometry as geo
+from tests.gpu_util import need_gpu, to_dev
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("p,n", [(4, 6000), (6, 20000), (5, 8000)])
+def test_tc_matches_simt(p, n):
+    need_gpu()
+    import paper_1612_04082_b200 as eb
+    d = geo.config2(n=n, seed=11)
+    t = to_dev(d)
+    os.environ["EBEM_SIMT"] = "1"
+    try:
+        simt = eb.fmm_build_tree(t["src"], t["nrm"], t["w"], max_pts=64, p=p, K=d["K"], G=d["G"])
+    finally:
+        del os.environ["EBEM_SIMT"]
+    tc = eb.fmm_build_tree(t["src"], t["nrm"], t["w"], max_pts=64, p=p, K=d["K"], G=d["G"])
+    a = eb.fmm_matvec(simt, eb.KERNEL_UP, t["f"], t["g"]).cpu().numpy().astype(np.float64)
+    b = eb.fmm_matvec(tc, eb.KERNEL_UP, t["f"], t["g"]).cpu().numpy().astype(np.float64)
+    assert np.all(np.isfinite(b))
+    diff = KN.rel_l2(b, a)
+    ref = cdirect.direct_sum(KN.KERNEL_UP, d["src"], d["src"], d["K"], d["G"], w=d["w"], f=d["f"], g=d["g"],
+                             nrm=d["nrm"])
+    print(f"p={p}: |tc - simt| {diff:.2e}, tc err {KN.rel_l2(b, ref):.2e}, simt err {KN.rel_l2(a, ref):.2e}")
+    assert diff < 1e-5
