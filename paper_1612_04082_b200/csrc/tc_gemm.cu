@@ -184,25 +184,32 @@ tc_pairs_kernel(const __grid_constant__ CUtensorMap mapAb, const __grid_constant
     asm volatile("tcgen05.fence::after_thread_sync;");
     const uint32_t tmem = *tmem_slot;
 
-    if (warp == 0) {
-        // ---------------- producer
+    if (warp == 0 || warp == 2 || warp == 3) {
+        // ---------------- producers: warp 0 arms the stage barrier and loads A; the 32
+        // four-row gathers of each B operand are spread over warps 0, 2, 3 (a TMA needs
+        // uniform operands, so each warp issues its lanes' gathers one after another)
+        const int pw = warp == 0 ? 0 : warp - 1;            // 0, 1, 2
+        const int g0 = pw * 11, g1 = min(32, g0 + 11);
         for (int kc = 0; kc < nk; ++kc) {
             const int s = kc % STAGES;
             const uint32_t ph = (kc / STAGES) & 1;
             mbar_wait(smem_u32(&empty_b[s]), ph ^ 1);
             uint8_t* st = smem + s * STAGE_BYTES;
             const uint32_t full = smem_u32(&full_b[s]);
-            if (lane == 0) {
+            if (warp == 0 && lane == 0) {
                 mbar_expect_tx(full, STAGE_BYTES);
                 tma_load_3d(smem_u32(st), &mapAb, kc * BK, tl.m0, tl.op, full);
                 tma_load_3d(smem_u32(st + OPND_BYTES), &mapAs, kc * BK, tl.m0, tl.op, full);
             }
             __syncwarp();
-            const int r = 4 * lane;
-            tma_gather4(smem_u32(st + 2 * OPND_BYTES + r * 128), &mapBb, kc * BK, s_src[r], s_src[r + 1],
-                        s_src[r + 2], s_src[r + 3], full);
-            tma_gather4(smem_u32(st + 3 * OPND_BYTES + r * 128), &mapBs, kc * BK, s_src[r], s_src[r + 1],
-                        s_src[r + 2], s_src[r + 3], full);
+            const int gi = g0 + lane;
+            if (gi < g1) {
+                const int r = 4 * gi;
+                tma_gather4(smem_u32(st + 2 * OPND_BYTES + r * 128), &mapBb, kc * BK, s_src[r], s_src[r + 1],
+                            s_src[r + 2], s_src[r + 3], full);
+                tma_gather4(smem_u32(st + 3 * OPND_BYTES + r * 128), &mapBs, kc * BK, s_src[r], s_src[r + 1],
+                            s_src[r + 2], s_src[r + 3], full);
+            }
         }
     } else if (warp == 1) {
         // ---------------- MMA issuer (one thread)
