@@ -28,9 +28,9 @@ constexpr int BM = 128, BN = 128, BK = 32;     // tile: 128 rows x 128 pairs x 3
 constexpr int STAGES = 3;
 constexpr int OPND_BYTES = BM * BK * 4;        // 16 KB per operand tile (BM == BN)
 constexpr int STAGE_BYTES = 4 * OPND_BYTES;    // Ab, As, Bb, Bs
-constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/ + BN * 4;
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
 constexpr int THREADS = 256;
-constexpr int TMEM_COLS = 4 * BN;              // 3 accumulators used (power-of-2 allocation)
+constexpr int TMEM_COLS = 4 * BN;              // 2 main (ping-pong) + 2 correction accumulators
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -133,35 +133,32 @@ __device__ __forceinline__ void drain_add(uint32_t tmem, int wq, int col, float*
     }
 }
 
+// Persistent: grid = #SMs, CTA b takes tiles b, b + grid, ... (op-major order, so the
+// concurrently running tiles share operators in L2).  The smem ring, the ping-pong main
+// accumulators and the two per-tile correction accumulators all continue across tiles,
+// so the producers load tile i+1 while the MMA finishes tile i and the epilogue of tile
+// i-1 does its atomics.
 __global__ void __launch_bounds__(THREADS, 1)
 tc_pairs_kernel(const __grid_constant__ CUtensorMap mapAb, const __grid_constant__ CUtensorMap mapAs,
                 const __grid_constant__ CUtensorMap mapBb, const __grid_constant__ CUtensorMap mapBs,
-                const Tile* __restrict__ tiles, const int2* __restrict__ pairs, int M, int K,
+                const Tile* __restrict__ tiles, int ntiles, const int2* __restrict__ pairs, int M, int K,
                 float* __restrict__ Y, int ldy) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-    // barriers: full[S], empty[S], acc_full[2], acc_empty[2], corr_full
+    // barriers: full[S], empty[S], acc_full[2], acc_empty[2], corr_full[2], corr_empty[2]
     uint64_t* bars = (uint64_t*)(smem + STAGES * STAGE_BYTES);
     uint64_t* full_b = bars;
     uint64_t* empty_b = bars + STAGES;
     uint64_t* accf_b = bars + 2 * STAGES;
     uint64_t* acce_b = bars + 2 * STAGES + 2;
-    uint64_t* corr_b = bars + 2 * STAGES + 4;
-    uint32_t* tmem_slot = (uint32_t*)(bars + 2 * STAGES + 5);
-    int* s_tgt = (int*)(smem + STAGES * STAGE_BYTES + 256);
-    __shared__ int s_src[BN];
+    uint64_t* corf_b = bars + 2 * STAGES + 4;
+    uint64_t* core_b = bars + 2 * STAGES + 6;
+    uint32_t* tmem_slot = (uint32_t*)(bars + 2 * STAGES + 8);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const Tile tl = tiles[blockIdx.x];
     const int nk = (K + BK - 1) / BK;
     const int ngroups = (nk + GROUP - 1) / GROUP;
 
-    if (threadIdx.x < BN) {
-        const int j = threadIdx.x;
-        const int2 pr = pairs[tl.p0 + (j < tl.np ? j : 0)];
-        s_tgt[j] = j < tl.np ? pr.x : -1;
-        s_src[j] = pr.y;
-    }
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(smem_u32(&full_b[s]), 1);
@@ -170,8 +167,9 @@ tc_pairs_kernel(const __grid_constant__ CUtensorMap mapAb, const __grid_constant
         for (int b = 0; b < 2; ++b) {
             mbar_init(smem_u32(&accf_b[b]), 1);
             mbar_init(smem_u32(&acce_b[b]), 4);
+            mbar_init(smem_u32(&corf_b[b]), 1);
+            mbar_init(smem_u32(&core_b[b]), 4);
         }
-        mbar_init(smem_u32(corr_b), 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 2) {
@@ -189,26 +187,32 @@ tc_pairs_kernel(const __grid_constant__ CUtensorMap mapAb, const __grid_constant
         // four-row gathers of each B operand are spread over warps 0, 2, 3 (a TMA needs
         // uniform operands, so each warp issues its lanes' gathers one after another)
         const int pw = warp == 0 ? 0 : warp - 1;            // 0, 1, 2
-        const int g0 = pw * 11, g1 = min(32, g0 + 11);
-        for (int kc = 0; kc < nk; ++kc) {
-            const int s = kc % STAGES;
-            const uint32_t ph = (kc / STAGES) & 1;
-            mbar_wait(smem_u32(&empty_b[s]), ph ^ 1);
-            uint8_t* st = smem + s * STAGE_BYTES;
-            const uint32_t full = smem_u32(&full_b[s]);
-            if (warp == 0 && lane == 0) {
-                mbar_expect_tx(full, STAGE_BYTES);
-                tma_load_3d(smem_u32(st), &mapAb, kc * BK, tl.m0, tl.op, full);
-                tma_load_3d(smem_u32(st + OPND_BYTES), &mapAs, kc * BK, tl.m0, tl.op, full);
-            }
-            __syncwarp();
-            const int gi = g0 + lane;
-            if (gi < g1) {
-                const int r = 4 * gi;
-                tma_gather4(smem_u32(st + 2 * OPND_BYTES + r * 128), &mapBb, kc * BK, s_src[r], s_src[r + 1],
-                            s_src[r + 2], s_src[r + 3], full);
-                tma_gather4(smem_u32(st + 3 * OPND_BYTES + r * 128), &mapBs, kc * BK, s_src[r], s_src[r + 1],
-                            s_src[r + 2], s_src[r + 3], full);
+        const int gi = pw * 11 + lane;
+        const bool gact = lane < 11 && gi < 32;
+        int c = 0;
+        for (int ti = blockIdx.x; ti < ntiles; ti += gridDim.x) {
+            const Tile tl = tiles[ti];
+            int r[4] = {0, 0, 0, 0};
+            if (gact)
+#pragma unroll
+                for (int q = 0; q < 4; ++q) r[q] = pairs[tl.p0 + min(4 * gi + q, tl.np - 1)].y;
+            for (int kc = 0; kc < nk; ++kc, ++c) {
+                const int s = c % STAGES;
+                mbar_wait(smem_u32(&empty_b[s]), ((c / STAGES) & 1) ^ 1);
+                uint8_t* st = smem + s * STAGE_BYTES;
+                const uint32_t full = smem_u32(&full_b[s]);
+                if (warp == 0 && lane == 0) {
+                    mbar_expect_tx(full, STAGE_BYTES);
+                    tma_load_3d(smem_u32(st), &mapAb, kc * BK, tl.m0, tl.op, full);
+                    tma_load_3d(smem_u32(st + OPND_BYTES), &mapAs, kc * BK, tl.m0, tl.op, full);
+                }
+                __syncwarp();
+                if (gact) {
+                    tma_gather4(smem_u32(st + 2 * OPND_BYTES + 4 * gi * 128), &mapBb, kc * BK, r[0], r[1], r[2],
+                                r[3], full);
+                    tma_gather4(smem_u32(st + 3 * OPND_BYTES + 4 * gi * 128), &mapBs, kc * BK, r[0], r[1], r[2],
+                                r[3], full);
+                }
             }
         }
     } else if (warp == 1) {
@@ -216,59 +220,73 @@ tc_pairs_kernel(const __grid_constant__ CUtensorMap mapAb, const __grid_constant
         // instruction descriptor: D f32, A/B tf32, both K-major, N = 128, M = 128
         const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BN >> 3) << 17) |
                                ((uint32_t)(BM >> 4) << 24);
-        const uint32_t dcorr = tmem + (uint32_t)(2 * BN);
-        for (int kc = 0; kc < nk; ++kc) {
-            const int s = kc % STAGES;
-            const int g = kc / GROUP, b = g & 1;
-            const bool gfirst = (kc % GROUP) == 0, glast = (kc % GROUP) == GROUP - 1 || kc == nk - 1;
-            if (gfirst) {   // the buffer must have been drained (use n waits for drain n-1)
-                mbar_wait(smem_u32(&acce_b[b]), ((g >> 1) & 1) ^ 1);
-                asm volatile("tcgen05.fence::after_thread_sync;");
-            }
-            mbar_wait(smem_u32(&full_b[s]), (kc / STAGES) & 1);
+        int c = 0, G = 0, it = 0;
+        for (int ti = blockIdx.x; ti < ntiles; ti += gridDim.x, ++it) {
+            const int cb = it & 1;
+            mbar_wait(smem_u32(&core_b[cb]), ((it >> 1) & 1) ^ 1);   // correction buffer drained
             asm volatile("tcgen05.fence::after_thread_sync;");
-            if (lane == 0) {
-                const uint32_t st = smem_u32(smem + s * STAGE_BYTES);
-                const uint64_t ab = smem_desc(st), as = smem_desc(st + OPND_BYTES);
-                const uint64_t bb = smem_desc(st + 2 * OPND_BYTES), bs = smem_desc(st + 3 * OPND_BYTES);
-                const uint32_t dmain = tmem + (uint32_t)(b * BN);
-                const int ksteps = min(BK, K - kc * BK + 7) / 8;     // 8 tf32 (32 B) per MMA
-                for (int k = 0; k < ksteps; ++k) {
-                    const uint64_t off = (uint64_t)(2 * k);          // +32 B in 16-B units
-                    mma_tf32(dmain, ab + off, bb + off, idesc, (!gfirst) | (k != 0));
-                    mma_tf32(dcorr, ab + off, bs + off, idesc, (kc | k) != 0);
-                    mma_tf32(dcorr, as + off, bb + off, idesc, 1);
+            const uint32_t dcorr = tmem + (uint32_t)((2 + cb) * BN);
+            for (int kc = 0; kc < nk; ++kc, ++c) {
+                const int s = c % STAGES;
+                const int b = G & 1;
+                const bool gfirst = (kc % GROUP) == 0, glast = (kc % GROUP) == GROUP - 1 || kc == nk - 1;
+                if (gfirst) {   // the main buffer must have been drained
+                    mbar_wait(smem_u32(&acce_b[b]), ((G >> 1) & 1) ^ 1);
+                    asm volatile("tcgen05.fence::after_thread_sync;");
                 }
-                mma_commit(smem_u32(&empty_b[s]));                   // frees the smem stage
-                if (glast) mma_commit(smem_u32(&accf_b[b]));          // group partial ready
-                if (kc == nk - 1) mma_commit(smem_u32(corr_b));       // corrections ready
+                mbar_wait(smem_u32(&full_b[s]), (c / STAGES) & 1);
+                asm volatile("tcgen05.fence::after_thread_sync;");
+                if (lane == 0) {
+                    const uint32_t st = smem_u32(smem + s * STAGE_BYTES);
+                    const uint64_t ab = smem_desc(st), as = smem_desc(st + OPND_BYTES);
+                    const uint64_t bb = smem_desc(st + 2 * OPND_BYTES), bs = smem_desc(st + 3 * OPND_BYTES);
+                    const uint32_t dmain = tmem + (uint32_t)(b * BN);
+                    const int ksteps = min(BK, K - kc * BK + 7) / 8;     // 8 tf32 (32 B) per MMA
+                    for (int k = 0; k < ksteps; ++k) {
+                        const uint64_t off = (uint64_t)(2 * k);          // +32 B in 16-B units
+                        mma_tf32(dmain, ab + off, bb + off, idesc, (!gfirst) | (k != 0));
+                        mma_tf32(dcorr, ab + off, bs + off, idesc, (kc | k) != 0);
+                        mma_tf32(dcorr, as + off, bb + off, idesc, 1);
+                    }
+                    mma_commit(smem_u32(&empty_b[s]));                   // frees the smem stage
+                    if (glast) mma_commit(smem_u32(&accf_b[b]));          // group partial ready
+                    if (kc == nk - 1) mma_commit(smem_u32(&corf_b[cb]));  // corrections ready
+                }
+                __syncwarp();
+                if (glast) ++G;
             }
-            __syncwarp();
         }
     } else if (warp >= EPI_WARP0) {
         // ---------------- drain + epilogue: fp32 register accumulation, then atomics into Y
         const int wq = warp - EPI_WARP0;            // TMEM lane quarter
-        float acc[BN];
+        int G = 0, it = 0;
+        for (int ti = blockIdx.x; ti < ntiles; ti += gridDim.x, ++it) {
+            const Tile tl = tiles[ti];
+            const int cb = it & 1;
+            float acc[BN];
 #pragma unroll
-        for (int j = 0; j < BN; ++j) acc[j] = 0.f;
-        for (int g = 0; g < ngroups; ++g) {
-            const int b = g & 1;
-            mbar_wait(smem_u32(&accf_b[b]), (g >> 1) & 1);
+            for (int j = 0; j < BN; ++j) acc[j] = 0.f;
+            for (int g = 0; g < ngroups; ++g, ++G) {
+                const int b = G & 1;
+                mbar_wait(smem_u32(&accf_b[b]), (G >> 1) & 1);
+                asm volatile("tcgen05.fence::after_thread_sync;");
+                drain_add(tmem, wq, b * BN, acc);
+                asm volatile("tcgen05.fence::before_thread_sync;");
+                __syncwarp();
+                if (lane == 0) mbar_arrive(smem_u32(&acce_b[b]));
+            }
+            mbar_wait(smem_u32(&corf_b[cb]), (it >> 1) & 1);
             asm volatile("tcgen05.fence::after_thread_sync;");
-            drain_add(tmem, wq, b * BN, acc);
+            drain_add(tmem, wq, (2 + cb) * BN, acc);
             asm volatile("tcgen05.fence::before_thread_sync;");
             __syncwarp();
-            if (lane == 0) mbar_arrive(smem_u32(&acce_b[b]));
-        }
-        mbar_wait(smem_u32(corr_b), 0);
-        asm volatile("tcgen05.fence::after_thread_sync;");
-        drain_add(tmem, wq, 2 * BN, acc);
-        const int row = tl.m0 + 32 * wq + lane;
-        if (row < M) {
+            if (lane == 0) mbar_arrive(smem_u32(&core_b[cb]));
+            const int row = tl.m0 + 32 * wq + lane;
+            if (row < M) {
+                const int2* pp = pairs + tl.p0;
 #pragma unroll
-            for (int j = 0; j < BN; ++j) {
-                const int t = s_tgt[j];
-                if (t >= 0) atomicAdd(Y + (int64_t)t * ldy + row, acc[j]);
+                for (int j = 0; j < BN; ++j)
+                    if (j < tl.np) atomicAdd(Y + (int64_t)__ldg(&pp[j].x) * ldy + row, acc[j]);
             }
         }
     }
@@ -370,8 +388,9 @@ void tc_pairs_gemm(const OpPairs& P, const CUtensorMap& Ab, const CUtensorMap& A
                                      tc::SMEM_BYTES));
         attr = true;
     }
-    tc::tc_pairs_kernel<<<P.ntiles, tc::THREADS, tc::SMEM_BYTES, s>>>(
-        Ab, As, Bb, Bs, reinterpret_cast<const tc::Tile*>(P.tiles.p), P.pairs.p, M, K, Y, ldy);
+    const int grid = std::min(P.ntiles, num_sms());
+    tc::tc_pairs_kernel<<<grid, tc::THREADS, tc::SMEM_BYTES, s>>>(
+        Ab, As, Bb, Bs, reinterpret_cast<const tc::Tile*>(P.tiles.p), P.ntiles, P.pairs.p, M, K, Y, ldy);
     EB_CHECK_LAUNCH();
 }
 
