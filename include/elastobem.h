@@ -181,26 +181,41 @@ int fmm_tree_info(const ebem_tree *tree, ebem_tree_info *info);
 int64_t fmm_tree_export(const ebem_tree *tree, int what, void *buf, int64_t cap);
 
 /*
- * bem_gmres_solve -- restarted GMRES (Saad) with device-side
- * Arnoldi for the collocation system A x = b of the mixed BVP (Eqs. num, num2),
- * whose operator is applied matrix-free by the FMM above (lines 184-189).
- *   tree     built on collocation points = sources (panel centroids)
- *   bc_type  [n] per panel: 0 = displacement prescribed (Dirichlet), 1 = traction
- *            prescribed (Neumann)
- *   self_U   [n*9] row-major 3x3 singular self-integral of U over the panel at its
- *            centroid ("evaluated analytically"); NULL = 0
- *   self_P   [n*9] the panel's own principal-value term of (1/2 I + P) (the jump
- *            1/2 I included); NULL = 1/2 I
- *   bc_val   [n*3] prescribed value (displacement or traction) per panel
- *   x        [n*3] in: initial guess (device) / out: unknown per panel (traction on
- *            Dirichlet panels, displacement on Neumann panels)
- *   restart, max_iter, tol (relative residual)
- *   iters_out, resid_out: iterations done and final relative residual (host)
+ * Collocation BEM operator of PAPER.md Eqs. (num), (coef), (num2) (l. 159-191): piecewise-
+ * constant displacement u and traction p on flat triangles, collocation at centroids,
+ * off-diagonal panel integrals by the panels' quadrature points as FMM sources ("Each
+ * triangular element contains 16 quadrature points", l. 187; nq = 1: centroid rule), and
+ * the "second, local, pass" (l. 189): own-panel quadrature contributions replaced by the
+ * singular integrals ("evaluated analytically", l. 179) and the free term 1/2 I.
+ *
+ * bem_create -- vertices [npanels*9]: v0, v1, v2 (xyz each) per flat triangle, ordered
+ *   counter-clockwise seen from outside the material (outward normal by the right-hand
+ *   rule); nq in {1, 16}; max_pts, p: FMM leaf size and order; K, G material.
+ *   Builds quadrature points, the FMM tree over them (targets = centroids), and the local
+ *   3x3 correction blocks.  Synchronises `stream`.
+ * bem_apply  -- y = A x for the mixed BVP with per-panel bc_type (0 = displacement
+ *   prescribed / traction unknown, 1 = traction prescribed / displacement unknown);
+ *   x, y [npanels*3].
+ * bem_rhs    -- b = right-hand side of Eq. num2 for prescribed values bc_val [npanels*3].
+ * bem_gmres_solve -- restarted GMRES(restart) (Saad) with device-side
+ *   Arnoldi (classical Gram-Schmidt + one re-orthogonalisation, fp64 Krylov basis on the
+ *   device, Givens rotations on the host), every A v through bem_apply (one KIFMM matvec).
+ *   x [npanels*3]: initial guess in, solution out (traction on Dirichlet panels,
+ *   displacement on Neumann panels).  Stops at |b - A x| / |b| <= tol or max_iter;
+ *   returns EBEM_ERR_NOCONV (x still written) if the tolerance was not reached.
+ *   iters_out / resid_out (host, may be NULL): iterations and final relative residual.
+ * Array arguments of bem_apply / bem_rhs / bem_gmres_solve must be device pointers.
  */
-int bem_gmres_solve(ebem_tree *tree, const int32_t *bc_type, const float *self_U,
-                    const float *self_P, const float *bc_val, float *x, int restart,
-                    int max_iter, double tol, int32_t *iters_out, double *resid_out,
+typedef struct ebem_bem ebem_bem;
+
+int bem_create(const float *vertices, int64_t npanels, int nq, int max_pts, int p, double K,
+               double G, ebem_bem **bem, void *stream);
+int bem_apply(ebem_bem *bem, const int32_t *bc_type, const float *x, float *y, void *stream);
+int bem_rhs(ebem_bem *bem, const int32_t *bc_type, const float *bc_val, float *b, void *stream);
+int bem_gmres_solve(ebem_bem *bem, const int32_t *bc_type, const float *bc_val, float *x,
+                    int restart, int max_iter, double tol, int32_t *iters_out, double *resid_out,
                     void *stream);
+int bem_free(ebem_bem *bem);
 
 #ifdef __cplusplus
 }

@@ -37,9 +37,13 @@ _lib.fmm_eval_stress.argtypes = [_VP, ctypes.c_int, _VP, _VP, _VP, _VP]
 _lib.fmm_tree_free.argtypes = [_VP]
 _lib.fmm_tree_export.argtypes = [_VP, ctypes.c_int, _VP, _I64]
 _lib.fmm_tree_export.restype = _I64
-_lib.bem_gmres_solve.argtypes = [_VP, _VP, _VP, _VP, _VP, _VP, ctypes.c_int, ctypes.c_int,
-                                 ctypes.c_double, ctypes.POINTER(ctypes.c_int32),
-                                 ctypes.POINTER(ctypes.c_double), _VP]
+_lib.bem_create.argtypes = [_VP, _I64, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_double,
+                            ctypes.c_double, ctypes.POINTER(_VP), _VP]
+_lib.bem_apply.argtypes = [_VP, _VP, _VP, _VP, _VP]
+_lib.bem_rhs.argtypes = [_VP, _VP, _VP, _VP, _VP]
+_lib.bem_gmres_solve.argtypes = [_VP, _VP, _VP, _VP, ctypes.c_int, ctypes.c_int, ctypes.c_double,
+                                 ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_double), _VP]
+_lib.bem_free.argtypes = [_VP]
 
 
 class TreeInfo(ctypes.Structure):
@@ -238,17 +242,62 @@ def ebem_launch_count():
     return int(_lib.ebem_launch_count())
 
 
-def bem_gmres_solve(tree, bc_type, self_U, self_P, bc_val, x, restart=50, max_iter=1000, tol=1e-6):
+class BemOperator:
+    """owning wrapper of an ebem_bem* (bem_create / bem_free): the collocation BEM operator."""
+
+    def __init__(self, handle, npanels):
+        self.handle, self.n = handle, npanels
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        self.handle = None
+        if h and _lib is not None:
+            try:
+                _lib.bem_free(h)
+            except Exception:
+                pass
+
+
+def bem_create(vertices, nq=16, max_pts=64, p=6, K=1.0, G=0.5):
+    """vertices: (n, 3, 3) or (n, 9) float32, counter-clockwise seen from outside."""
+    v = _f32(vertices)
+    n = int(v.shape[0])
+    h = _VP()
+    keep = []
+    _check(_lib.bem_create(_ptr(v, keep), n, int(nq), int(max_pts), int(p), float(K), float(G),
+                           ctypes.byref(h), _stream(v)))
+    return BemOperator(h.value, n)
+
+
+def bem_apply(bem, bc_type, x, out=None):
+    import torch
+    out = torch.empty_like(x) if out is None else out
+    keep = []
+    _check(_lib.bem_apply(bem.handle, _ptr(bc_type, keep), _ptr(x, keep), _ptr(out, keep), _stream(x)))
+    return out
+
+
+def bem_rhs(bem, bc_type, bc_val, out=None):
+    import torch
+    out = torch.empty_like(bc_val) if out is None else out
+    keep = []
+    _check(_lib.bem_rhs(bem.handle, _ptr(bc_type, keep), _ptr(bc_val, keep), _ptr(out, keep), _stream(bc_val)))
+    return out
+
+
+def bem_gmres_solve(bem, bc_type, bc_val, x, restart=50, max_iter=1000, tol=1e-6, check=True):
+    """solves A x = b in place; returns (x, iterations, relative residual)."""
     keep = []
     it = ctypes.c_int32(0)
     res = ctypes.c_double(0)
-    _check(_lib.bem_gmres_solve(tree.handle, _ptr(bc_type, keep), _ptr(self_U, keep), _ptr(self_P, keep),
-                                _ptr(bc_val, keep), _ptr(x, keep), int(restart), int(max_iter), float(tol),
-                                ctypes.byref(it), ctypes.byref(res), _stream(x)))
+    rc = _lib.bem_gmres_solve(bem.handle, _ptr(bc_type, keep), _ptr(bc_val, keep), _ptr(x, keep), int(restart),
+                              int(max_iter), float(tol), ctypes.byref(it), ctypes.byref(res), _stream(x))
+    if check or rc not in (0, -4):
+        _check(rc)
     return x, int(it.value), float(res.value)
 
 
 __all__ = ["bem_kernel_direct", "fmm_build_tree", "fmm_matvec", "fmm_eval_stress", "fmm_tree_info",
-           "fmm_tree_export", "bem_gmres_solve", "fmm_set_profiling", "fmm_phase_stats",
+           "fmm_tree_export", "bem_create", "bem_apply", "bem_rhs", "bem_gmres_solve", "BemOperator", "fmm_set_profiling", "fmm_phase_stats",
            "ebem_launch_count", "FmmTree", "EbemError", "LIB_PATH",
            "KERNEL_U", "KERNEL_P", "KERNEL_UP", "KERNEL_D", "KERNEL_S", "KERNEL_DS"]

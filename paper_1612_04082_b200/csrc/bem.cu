@@ -1,0 +1,441 @@
+// Collocation BEM operator and restarted GMRES with device-side Arnoldi
+// (Sec. 2.2, "Discretization of BIE" and "Matrix-vector products", l. 159-191).
+//
+// Row i of Eq. (num) (piecewise-constant u, p on flat triangles, collocation at centroids):
+//   (1/2 I + P_self_i) u_i + sum_{j} sum_{q in j, y_q != xi_i} w_q P(xi_i, y_q) u_j
+//       = U_self_i p_i + sum_{j} sum_{q in j, y_q != xi_i} w_q U(xi_i, y_q) p_j
+// The double sum is one KIFMM evaluation with the panels' quadrature points as sources
+// (l. 186-187: 16 points per triangle; or the centroid rule, reading R9) and the centroids
+// as targets.  The "second, local, pass" (l. 189) subtracts the own panel's quadrature
+// contributions and adds the singular integrals: per panel two 3x3 blocks
+//   CU_i = U_self_i - sum_{q in i} w_q U(xi_i, y_q),
+//   CP_i = 1/2 I + P_self_i - sum_{q in i} w_q P(xi_i, y_q),
+// with U_self (weakly singular) and the CPV P_self evaluated in polar coordinates about the
+// centroid (radial integral in closed form, angular integral by Gauss-Legendre along the
+// edges: "evaluated analytically", l. 179).
+// The mixed BVP moves the unknowns (p on Dirichlet panels, u on Neumann panels) to the left:
+// A x = b (Eq. num2), applied matrix-free as L(u, p) = P u - U p.
+#include <cmath>
+
+#include "fmm.cuh"
+#include "p2p.cuh"
+
+namespace ebem {
+
+constexpr int NGL = 32;   // Gauss-Legendre points per edge for the self integrals
+__constant__ double c_gl_x[NGL], c_gl_w[NGL];
+
+static void gauss_legendre(int n, std::vector<double>& x, std::vector<double>& w) {
+    x.resize(n);
+    w.resize(n);
+    for (int i = 0; i < n; ++i) {
+        double z = std::cos(3.14159265358979323846 * (i + 0.75) / (n + 0.5)), pp = 0;
+        for (int it = 0; it < 100; ++it) {
+            double p1 = 1, p2 = 0;
+            for (int k = 1; k <= n; ++k) {
+                double p3 = p2;
+                p2 = p1;
+                p1 = ((2.0 * k - 1.0) * z * p2 - (k - 1.0) * p3) / k;
+            }
+            pp = n * (z * p1 - p2) / (z * z - 1.0);
+            double z1 = z;
+            z = z1 - p1 / pp;
+            if (std::fabs(z - z1) < 1e-16) break;
+        }
+        x[i] = z;
+        w[i] = 2.0 / ((1.0 - z * z) * pp * pp);
+    }
+}
+
+struct Bem {
+    int64_t n = 0;          // panels
+    int nq = 16;
+    Material mat{};
+    Tree* tree = nullptr;
+    DBuf<float> cent, nrm, area, qpts, qnrm, qw;
+    DBuf<float> CU, CP;     // [n x 9] local correction blocks (row-major 3x3)
+    DBuf<float> f, g, y;    // expanded densities [n nq x 3], FMM output [n x 3]
+    ~Bem() { delete tree; }
+};
+
+// ------------------------------------------------------------------ geometry
+__device__ __forceinline__ void cross3(const double* a, const double* b, double* c) {
+    c[0] = a[1] * b[2] - a[2] * b[1];
+    c[1] = a[2] * b[0] - a[0] * b[2];
+    c[2] = a[0] * b[1] - a[1] * b[0];
+}
+
+// centroid, unit normal (right-hand rule), area, and the nq quadrature points / weights:
+// nq = 16: midpoint subdivision into 4 congruent triangles x the 4-point degree-3 rule
+// (barycentric (1/3,1/3,1/3) weight -27/48, (3/5,1/5,1/5) x 3 weight 25/48); the middle
+// sub-triangle's centre point is the panel centroid itself and is copied bit-exactly so
+// the FMM's r == 0 exclusion removes it.
+__global__ void panels_kernel(const float* __restrict__ V, int64_t n, int nq, float* cent, float* nrm, float* area,
+                              float* qp, float* qn, float* qw) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double v[3][3];
+    for (int a = 0; a < 3; ++a)
+        for (int c = 0; c < 3; ++c) v[a][c] = V[9 * i + 3 * a + c];
+    double e1[3], e2[3], cr[3];
+    for (int c = 0; c < 3; ++c) {
+        e1[c] = v[1][c] - v[0][c];
+        e2[c] = v[2][c] - v[0][c];
+    }
+    cross3(e1, e2, cr);
+    const double a2 = sqrt(cr[0] * cr[0] + cr[1] * cr[1] + cr[2] * cr[2]);
+    float ctr[3], nn[3];
+    for (int c = 0; c < 3; ++c) {
+        ctr[c] = (float)((v[0][c] + v[1][c] + v[2][c]) / 3.0);
+        nn[c] = (float)(cr[c] / a2);
+        cent[3 * i + c] = ctr[c];
+        nrm[3 * i + c] = nn[c];
+    }
+    const double A = 0.5 * a2;
+    area[i] = (float)A;
+    if (nq == 1) {
+        for (int c = 0; c < 3; ++c) {
+            qp[3 * i + c] = ctr[c];
+            qn[3 * i + c] = nn[c];
+        }
+        qw[i] = (float)A;
+        return;
+    }
+    double m01[3], m12[3], m20[3];
+    for (int c = 0; c < 3; ++c) {
+        m01[c] = 0.5 * (v[0][c] + v[1][c]);
+        m12[c] = 0.5 * (v[1][c] + v[2][c]);
+        m20[c] = 0.5 * (v[2][c] + v[0][c]);
+    }
+    const double* sub[4][3] = {{v[0], m01, m20}, {m01, v[1], m12}, {m20, m12, v[2]}, {m01, m12, m20}};
+    const double bary[4][4] = {{1.0 / 3, 1.0 / 3, 1.0 / 3, -27.0 / 48},
+                               {0.6, 0.2, 0.2, 25.0 / 48},
+                               {0.2, 0.6, 0.2, 25.0 / 48},
+                               {0.2, 0.2, 0.6, 25.0 / 48}};
+    int q = 0;
+    for (int t = 0; t < 4; ++t)
+        for (int k = 0; k < 4; ++k, ++q) {
+            const int64_t o = i * 16 + q;
+            for (int c = 0; c < 3; ++c) {
+                const double x = bary[k][0] * sub[t][0][c] + bary[k][1] * sub[t][1][c] + bary[k][2] * sub[t][2][c];
+                qp[3 * o + c] = (t == 3 && k == 0) ? ctr[c] : (float)x;
+                qn[3 * o + c] = nn[c];
+            }
+            qw[o] = (float)(bary[k][3] * A / 4.0);
+        }
+}
+
+// local correction blocks CU, CP (see the file header), fp64
+__global__ void self_terms_kernel(const float* __restrict__ V, int64_t n, int nq, const float* __restrict__ qp,
+                                  const float* __restrict__ qw, const float* __restrict__ cent,
+                                  const float* __restrict__ nrm, double G, double nu, float* CU, float* CP) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const double PI = 3.14159265358979323846;
+    double v[3][3], xi[3], nn[3];
+    for (int a = 0; a < 3; ++a)
+        for (int c = 0; c < 3; ++c) v[a][c] = V[9 * i + 3 * a + c];
+    for (int c = 0; c < 3; ++c) {
+        xi[c] = (v[0][c] + v[1][c] + v[2][c]) / 3.0;
+        nn[c] = nrm[3 * i + c];
+    }
+    const double cU = 1.0 / (16.0 * PI * (1.0 - nu) * G), a1 = 3.0 - 4.0 * nu;
+    double Us[9] = {0}, Ie[3] = {0};   // int U dS ; int e ln R dtheta (= CPV int e / rho^2 dS)
+    for (int k = 0; k < 3; ++k) {
+        double a[3], b[3], ab[3];
+        for (int c = 0; c < 3; ++c) {
+            a[c] = v[k][c] - xi[c];
+            b[c] = v[(k + 1) % 3][c] - xi[c];
+        }
+        cross3(a, b, ab);
+        const double cr = sqrt(ab[0] * ab[0] + ab[1] * ab[1] + ab[2] * ab[2]);
+        for (int q = 0; q < NGL; ++q) {
+            const double s = 0.5 * (c_gl_x[q] + 1.0), w = 0.5 * c_gl_w[q];
+            double P[3];
+            for (int c = 0; c < 3; ++c) P[c] = a[c] + s * (b[c] - a[c]);
+            const double R = sqrt(P[0] * P[0] + P[1] * P[1] + P[2] * P[2]);
+            const double e[3] = {P[0] / R, P[1] / R, P[2] / R};
+            const double dth = w * cr / (R * R);          // d theta
+            // int_0^R U rho drho = R U(e) rho -> U(e) (homogeneous of degree -1)
+            for (int r = 0; r < 3; ++r)
+                for (int c = 0; c < 3; ++c) Us[3 * r + c] += dth * R * cU * ((r == c ? a1 : 0.0) + e[r] * e[c]);
+            for (int c = 0; c < 3; ++c) Ie[c] += dth * log(R) * e[c];
+        }
+    }
+    // CPV P_self: r = -e, P_ij = -(1-2nu)(r_i n_j - r_j n_i) / (8 pi (1-nu) rho^2)
+    const double cp = -(1.0 - 2.0 * nu) / (8.0 * PI * (1.0 - nu));
+    double Ps[9];
+    for (int r = 0; r < 3; ++r)
+        for (int c = 0; c < 3; ++c) Ps[3 * r + c] = cp * (-Ie[r] * nn[c] + Ie[c] * nn[r]) + (r == c ? 0.5 : 0.0);
+    // subtract what the FMM adds from the panel's own quadrature points (y_q != xi)
+    const float cx = cent[3 * i], cy = cent[3 * i + 1], cz = cent[3 * i + 2];
+    for (int q = 0; q < nq; ++q) {
+        const int64_t o = i * nq + q;
+        const double dx = (double)(cx - qp[3 * o]), dy = (double)(cy - qp[3 * o + 1]), dz = (double)(cz - qp[3 * o + 2]);
+        const double r2 = dx * dx + dy * dy + dz * dz;
+        if (r2 == 0.0) continue;
+        const double rr = sqrt(r2), w = qw[o];
+        const double e[3] = {dx / rr, dy / rr, dz / rr};
+        const double dn = e[0] * nn[0] + e[1] * nn[1] + e[2] * nn[2];
+        const double a = 1.0 - 2.0 * nu;
+        for (int r = 0; r < 3; ++r)
+            for (int c = 0; c < 3; ++c) {
+                Us[3 * r + c] -= w * cU / rr * ((r == c ? a1 : 0.0) + e[r] * e[c]);
+                Ps[3 * r + c] -= w / (8.0 * PI * (1.0 - nu) * r2) *
+                                 (dn * ((r == c ? a : 0.0) + 3.0 * e[r] * e[c]) - a * (e[r] * nn[c] - e[c] * nn[r]));
+            }
+    }
+    for (int k = 0; k < 9; ++k) {
+        CU[9 * i + k] = (float)Us[k];
+        CP[9 * i + k] = (float)Ps[k];
+    }
+}
+
+// ------------------------------------------------------------------ operator L(u, p) = P u - U p
+// mode 0 (A x): p = x on Dirichlet panels, u = x on Neumann panels
+// mode 1 (rhs): u = value on Dirichlet panels, p = value on Neumann panels
+__device__ __forceinline__ void split_up(int mode, int bc, const float* xv, float* u, float* p) {
+    const bool dir = bc == 0;
+    const bool is_p = mode == 0 ? dir : !dir;
+    for (int c = 0; c < 3; ++c) {
+        u[c] = is_p ? 0.f : xv[c];
+        p[c] = is_p ? xv[c] : 0.f;
+    }
+}
+
+__global__ void expand_kernel(int mode, const int32_t* __restrict__ bc, const float* __restrict__ x, int64_t n, int nq,
+                              float* __restrict__ f, float* __restrict__ g) {
+    const int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (o >= n * nq) return;
+    const int64_t j = o / nq;
+    float u[3], p[3];
+    split_up(mode, bc[j], x + 3 * j, u, p);
+    for (int c = 0; c < 3; ++c) {
+        f[3 * o + c] = -p[c];      // single layer enters as - U p
+        g[3 * o + c] = u[c];       // double layer as + P u
+    }
+}
+
+template <class T>
+__global__ void local_kernel(int mode, double sign, const int32_t* __restrict__ bc, const float* __restrict__ x,
+                             int64_t n, const float* __restrict__ CU, const float* __restrict__ CP,
+                             const float* __restrict__ y, T* __restrict__ out) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    float u[3], p[3];
+    split_up(mode, bc[i], x + 3 * i, u, p);
+    for (int r = 0; r < 3; ++r) {
+        double s = y[3 * i + r];
+        for (int c = 0; c < 3; ++c) s += (double)CP[9 * i + 3 * r + c] * u[c] - (double)CU[9 * i + 3 * r + c] * p[c];
+        out[3 * i + r] = (T)(sign * s);
+    }
+}
+
+template <class T>
+static void apply_L(Bem& B, int mode, double sign, const int32_t* bc, const float* x, T* out, cudaStream_t s) {
+    const int64_t n = B.n;
+    expand_kernel<<<ceil_div(n * B.nq, 256), 256, 0, s>>>(mode, bc, x, n, B.nq, B.f.p, B.g.p);
+    EB_CHECK_LAUNCH();
+    fmm_evaluate(*B.tree, K_UP, B.f.p, B.g.p, B.y.p, s);
+    local_kernel<T><<<ceil_div(n, 256), 256, 0, s>>>(mode, sign, bc, x, n, B.CU.p, B.CP.p, B.y.p, out);
+    EB_CHECK_LAUNCH();
+}
+
+Bem* bem_create(const float* verts, int64_t n, int nq, int max_pts, int p, const Material& m, cudaStream_t s) {
+    EB_REQUIRE(nq == 1 || nq == 16, "nq must be 1 or 16");
+    static bool gl_ready = false;
+    if (!gl_ready) {
+        std::vector<double> x, w;
+        gauss_legendre(NGL, x, w);
+        EB_CUDA(cudaMemcpyToSymbol(c_gl_x, x.data(), sizeof(double) * NGL));
+        EB_CUDA(cudaMemcpyToSymbol(c_gl_w, w.data(), sizeof(double) * NGL));
+        gl_ready = true;
+    }
+    auto B = std::make_unique<Bem>();
+    B->n = n;
+    B->nq = nq;
+    B->mat = m;
+    const int64_t ns = n * nq;
+    B->cent.alloc(3 * n);
+    B->nrm.alloc(3 * n);
+    B->area.alloc(n);
+    B->qpts.alloc(3 * ns);
+    B->qnrm.alloc(3 * ns);
+    B->qw.alloc(ns);
+    panels_kernel<<<ceil_div(n, 128), 128, 0, s>>>(verts, n, nq, B->cent.p, B->nrm.p, B->area.p, B->qpts.p, B->qnrm.p,
+                                                   B->qw.p);
+    EB_CHECK_LAUNCH();
+    B->CU.alloc(9 * n);
+    B->CP.alloc(9 * n);
+    self_terms_kernel<<<ceil_div(n, 128), 128, 0, s>>>(verts, n, nq, B->qpts.p, B->qw.p, B->cent.p, B->nrm.p, m.G, m.nu,
+                                                       B->CU.p, B->CP.p);
+    EB_CHECK_LAUNCH();
+    B->tree = build_tree(B->qpts.p, B->qnrm.p, B->qw.p, ns, B->cent.p, n, max_pts, p, m, s);
+    B->f.alloc(3 * ns);
+    B->g.alloc(3 * ns);
+    B->y.alloc(3 * n);
+    EB_CUDA(cudaStreamSynchronize(s));
+    return B.release();
+}
+
+void bem_free(Bem* B) { delete B; }
+
+void bem_apply(Bem& B, const int32_t* bc, const float* x, float* y, cudaStream_t s) {
+    apply_L<float>(B, 0, 1.0, bc, x, y, s);
+}
+
+void bem_rhs(Bem& B, const int32_t* bc, const float* val, float* b, cudaStream_t s) {
+    apply_L<float>(B, 1, -1.0, bc, val, b, s);
+}
+
+// ------------------------------------------------------------------ GMRES (fp64 Krylov basis)
+__global__ void dots_kernel(const double* __restrict__ V, int64_t ld, int k, const double* __restrict__ w,
+                            int64_t n, double* __restrict__ h) {
+    // h[j] = V_j . w for j < k; block j, fixed-order reduction
+    const int j = blockIdx.x;
+    __shared__ double sh[256];
+    double acc = 0;
+    for (int64_t i = threadIdx.x; i < n; i += 256) acc += V[j * ld + i] * w[i];
+    sh[threadIdx.x] = acc;
+    __syncthreads();
+    for (int o = 128; o > 0; o >>= 1) {
+        if (threadIdx.x < o) sh[threadIdx.x] += sh[threadIdx.x + o];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) h[j] = sh[0];
+}
+
+__global__ void axpy_basis(const double* __restrict__ V, int64_t ld, int k, const double* __restrict__ h, double sgn,
+                           double* __restrict__ w, int64_t n) {
+    // w += sgn * sum_{j<k} h[j] V_j
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double s = 0;
+    for (int j = 0; j < k; ++j) s += h[j] * V[j * ld + i];
+    w[i] += sgn * s;
+}
+
+__global__ void scale_copy(const double* __restrict__ a, double sc, double* __restrict__ b, int64_t n) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) b[i] = sc * a[i];
+}
+__global__ void to_f32_kernel(const double* __restrict__ a, float* __restrict__ b, int64_t n) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) b[i] = (float)a[i];
+}
+__global__ void to_f64_kernel(const float* __restrict__ a, double* __restrict__ b, int64_t n) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) b[i] = (double)a[i];
+}
+__global__ void sub_kernel(const double* __restrict__ a, double* __restrict__ b, int64_t n) {   // b = a - b
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) b[i] = a[i] - b[i];
+}
+
+static double dnorm(const double* v, int64_t n, double* tmp, cudaStream_t s) {
+    dots_kernel<<<1, 256, 0, s>>>(v, 0, 1, v, n, tmp);
+    EB_CHECK_LAUNCH();
+    double h = 0;
+    d2h(&h, tmp, 1, s);
+    EB_CUDA(cudaStreamSynchronize(s));
+    return std::sqrt(h);
+}
+
+int bem_gmres(Bem& B, const int32_t* bc, const float* val, float* x, int m, int max_iter, double tol, int32_t* iters,
+              double* resid, cudaStream_t s) {
+    const int64_t n3 = 3 * B.n;
+    DBuf<double> V((size_t)(m + 1) * n3), w(n3), b(n3), xd(n3), hd(m + 2);
+    DBuf<float> xf(n3), yf(n3);
+    // right-hand side b = -L(known values)
+    apply_L<double>(B, 1, -1.0, bc, val, b.p, s);
+    const double bn = dnorm(b.p, n3, hd.p, s);
+    to_f64_kernel<<<ceil_div(n3, 256), 256, 0, s>>>(x, xd.p, n3);
+    EB_CHECK_LAUNCH();
+    auto matvec = [&](const double* v, double* out) {   // out = A v
+        to_f32_kernel<<<ceil_div(n3, 256), 256, 0, s>>>(v, xf.p, n3);
+        EB_CHECK_LAUNCH();
+        apply_L<double>(B, 0, 1.0, bc, xf.p, out, s);
+    };
+    int it = 0;
+    double rel = 1.0;
+    if (bn == 0.0) {
+        EB_CUDA(cudaMemsetAsync(x, 0, sizeof(float) * n3, s));
+        if (iters) *iters = 0;
+        if (resid) *resid = 0;
+        return EBEM_OK;
+    }
+    std::vector<double> H((size_t)(m + 1) * m), cs(m), sn(m), g(m + 1), h(m + 1), h2(m + 1);
+    while (true) {
+        matvec(xd.p, w.p);
+        sub_kernel<<<ceil_div(n3, 256), 256, 0, s>>>(b.p, w.p, n3);   // w = b - A x
+        EB_CHECK_LAUNCH();
+        const double beta = dnorm(w.p, n3, hd.p, s);
+        rel = beta / bn;
+        if (rel <= tol || it >= max_iter) break;
+        scale_copy<<<ceil_div(n3, 256), 256, 0, s>>>(w.p, 1.0 / beta, V.p, n3);
+        EB_CHECK_LAUNCH();
+        std::fill(g.begin(), g.end(), 0.0);
+        g[0] = beta;
+        int k = 0;
+        for (int j = 0; j < m; ++j) {
+            matvec(V.p + (int64_t)j * n3, w.p);
+            // classical Gram-Schmidt with one re-orthogonalisation, on the device
+            for (int pass = 0; pass < 2; ++pass) {
+                dots_kernel<<<j + 1, 256, 0, s>>>(V.p, n3, j + 1, w.p, n3, hd.p);
+                axpy_basis<<<ceil_div(n3, 256), 256, 0, s>>>(V.p, n3, j + 1, hd.p, -1.0, w.p, n3);
+                EB_CHECK_LAUNCH();
+                d2h((pass ? h2 : h).data(), hd.p, j + 1, s);
+            }
+            const double hn = dnorm(w.p, n3, hd.p, s);
+            for (int i = 0; i <= j; ++i) H[(size_t)i * m + j] = h[i] + h2[i];
+            H[(size_t)(j + 1) * m + j] = hn;
+            if (hn > 0) {
+                scale_copy<<<ceil_div(n3, 256), 256, 0, s>>>(w.p, 1.0 / hn, V.p + (int64_t)(j + 1) * n3, n3);
+                EB_CHECK_LAUNCH();
+            }
+            for (int i = 0; i < j; ++i) {   // previous Givens rotations
+                const double a = H[(size_t)i * m + j], c = H[(size_t)(i + 1) * m + j];
+                H[(size_t)i * m + j] = cs[i] * a + sn[i] * c;
+                H[(size_t)(i + 1) * m + j] = -sn[i] * a + cs[i] * c;
+            }
+            const double a = H[(size_t)j * m + j], c = H[(size_t)(j + 1) * m + j];
+            const double den = std::hypot(a, c);
+            cs[j] = a / den;
+            sn[j] = c / den;
+            H[(size_t)j * m + j] = den;
+            H[(size_t)(j + 1) * m + j] = 0;
+            g[j + 1] = -sn[j] * g[j];
+            g[j] = cs[j] * g[j];
+            ++it;
+            k = j + 1;
+            rel = std::fabs(g[j + 1]) / bn;
+            if (rel <= tol || it >= max_iter || hn == 0) break;
+        }
+        // y = H^-1 g (upper triangular), x += V y
+        std::vector<double> y(k);
+        for (int i = k - 1; i >= 0; --i) {
+            double sum = g[i];
+            for (int l = i + 1; l < k; ++l) sum -= H[(size_t)i * m + l] * y[l];
+            y[i] = sum / H[(size_t)i * m + i];
+        }
+        h2d(hd.p, y.data(), k, s);
+        axpy_basis<<<ceil_div(n3, 256), 256, 0, s>>>(V.p, n3, k, hd.p, 1.0, xd.p, n3);
+        EB_CHECK_LAUNCH();
+        if (it >= max_iter) {
+            // true residual of the final iterate
+            matvec(xd.p, w.p);
+            sub_kernel<<<ceil_div(n3, 256), 256, 0, s>>>(b.p, w.p, n3);
+            EB_CHECK_LAUNCH();
+            rel = dnorm(w.p, n3, hd.p, s) / bn;
+            break;
+        }
+    }
+    to_f32_kernel<<<ceil_div(n3, 256), 256, 0, s>>>(xd.p, x, n3);
+    EB_CHECK_LAUNCH();
+    EB_CUDA(cudaStreamSynchronize(s));
+    if (iters) *iters = it;
+    if (resid) *resid = rel;
+    return rel <= tol ? EBEM_OK : EBEM_ERR_NOCONV;
+}
+
+}  // namespace ebem

@@ -238,15 +238,57 @@ extern "C" int64_t fmm_tree_export(const ebem_tree* tree, int what, void* buf, i
     EB_API_END
 }
 
-extern "C" int bem_gmres_solve(ebem_tree* tree, const int32_t* bc_type, const float* self_U,
-                               const float* self_P, const float* bc_val, float* x, int restart,
-                               int max_iter, double tol, int32_t* iters_out, double* resid_out,
-                               void* stream) {
+extern "C" int bem_create(const float* vertices, int64_t npanels, int nq, int max_pts, int p, double K, double G,
+                          ebem_bem** bem, void* stream) {
     EB_API_BEGIN
-    EB_REQUIRE(tree && bc_type && bc_val && x, "NULL argument");
+    set_last_error("");
+    EB_REQUIRE(bem && vertices && npanels > 0, "bad argument");
+    EB_REQUIRE(max_pts >= 1 && p >= 3 && p <= 12, "bad FMM parameters");
+    check_material(K, G);
+    cudaStream_t s = (cudaStream_t)stream;
+    Staged st(s);
+    const float* dv = is_device_ptr(vertices) ? vertices : st.in(vertices, npanels * 9);
+    *bem = reinterpret_cast<ebem_bem*>(ebem::bem_create(dv, npanels, nq, max_pts, p, make_material(K, G), s));
+    return EBEM_OK;
+    EB_API_END
+}
+
+extern "C" int bem_apply(ebem_bem* bem, const int32_t* bc_type, const float* x, float* y, void* stream) {
+    EB_API_BEGIN
+    EB_REQUIRE(bem && bc_type && x && y, "NULL argument");
+    EB_REQUIRE(is_device_ptr(x) && is_device_ptr(y) && is_device_ptr(bc_type), "bem_apply needs device pointers");
+    ebem::bem_apply(*reinterpret_cast<Bem*>(bem), bc_type, x, y, (cudaStream_t)stream);
+    return EBEM_OK;
+    EB_API_END
+}
+
+extern "C" int bem_rhs(ebem_bem* bem, const int32_t* bc_type, const float* bc_val, float* b, void* stream) {
+    EB_API_BEGIN
+    EB_REQUIRE(bem && bc_type && bc_val && b, "NULL argument");
+    EB_REQUIRE(is_device_ptr(bc_val) && is_device_ptr(b) && is_device_ptr(bc_type), "bem_rhs needs device pointers");
+    ebem::bem_rhs(*reinterpret_cast<Bem*>(bem), bc_type, bc_val, b, (cudaStream_t)stream);
+    return EBEM_OK;
+    EB_API_END
+}
+
+extern "C" int bem_gmres_solve(ebem_bem* bem, const int32_t* bc_type, const float* bc_val, float* x, int restart,
+                               int max_iter, double tol, int32_t* iters_out, double* resid_out, void* stream) {
+    EB_API_BEGIN
+    set_last_error("");
+    EB_REQUIRE(bem && bc_type && bc_val && x, "NULL argument");
     EB_REQUIRE(restart >= 1 && max_iter >= 1 && tol > 0, "bad GMRES parameters");
-    Tree* t = reinterpret_cast<Tree*>(tree);
-    return gmres_solve(*t, bc_type, self_U, self_P, bc_val, x, restart, max_iter, tol, iters_out,
-                       resid_out, (cudaStream_t)stream);
+    EB_REQUIRE(is_device_ptr(x) && is_device_ptr(bc_val) && is_device_ptr(bc_type),
+               "bem_gmres_solve needs device pointers");
+    const int rc = ebem::bem_gmres(*reinterpret_cast<Bem*>(bem), bc_type, bc_val, x, restart, max_iter, tol, iters_out,
+                                   resid_out, (cudaStream_t)stream);
+    if (rc != EBEM_OK) set_last_error("GMRES did not reach the tolerance");
+    return rc;
+    EB_API_END
+}
+
+extern "C" int bem_free(ebem_bem* bem) {
+    EB_API_BEGIN
+    ebem::bem_free(reinterpret_cast<Bem*>(bem));
+    return EBEM_OK;
     EB_API_END
 }

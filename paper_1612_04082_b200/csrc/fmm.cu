@@ -608,9 +608,5 @@ int phase_stats(Tree& t, int kernel, ebem_phase_stat* out, int cap) {
     return Tree::NPHASE;
 }
 
-int gmres_solve(Tree&, const int32_t*, const float*, const float*, const float*, float*, int, int, double, int32_t*,
-                double*, cudaStream_t) {
-    throw Error("bem_gmres_solve: not available in this build");
-}
 
 }  // namespace ebem

@@ -150,9 +150,13 @@ void fmm_evaluate(Tree& t, int kernel, const float* f, const float* g, float* ou
 void tree_info(const Tree& t, ebem_tree_info* info);
 int64_t tree_export(const Tree& t, int what, void* buf, int64_t cap);
 int phase_stats(Tree& t, int kernel, ebem_phase_stat* out, int cap);
-int gmres_solve(Tree& t, const int32_t* bc_type, const float* self_U, const float* self_P,
-                const float* bc_val, float* x, int restart, int max_iter, double tol,
-                int32_t* iters_out, double* resid_out, cudaStream_t s);
+struct Bem;
+Bem* bem_create(const float* verts, int64_t n, int nq, int max_pts, int p, const Material& m, cudaStream_t s);
+void bem_free(Bem* B);
+void bem_apply(Bem& B, const int32_t* bc, const float* x, float* y, cudaStream_t s);
+void bem_rhs(Bem& B, const int32_t* bc, const float* val, float* b, cudaStream_t s);
+int bem_gmres(Bem& B, const int32_t* bc, const float* val, float* x, int m, int max_iter, double tol,
+              int32_t* iters, double* resid, cudaStream_t s);
 
 // ------------------------------------------------------------------ primitives (linalg.cu)
 // exclusive scan of n ints (out may alias in); returns the total on the host (syncs)
