@@ -175,6 +175,47 @@ def p2p_bench(eb, torch, pk, reps=5):
             "frac_fp32_peak": tf / pk["fp32_tflops"], "flops_per_interaction": 44}
 
 
+def gmres_workload(args, eb, torch):
+    """configs[4]: mixed-BVP BEM GMRES solve on the metamaterial cell (64 voids, ~1.93M
+    triangles), restart 50, tol 1e-6, p = 8.  Reports iterations, solve time (device
+    events), operator set-up time and the global equilibrium of the solved tractions
+    (sum of traction x area over the closed surface; exact solution: 0)."""
+    from workloads import geometry as geo
+    d = geo.metamaterial_cell(nc=args.cell_nc, level=args.cell_level, nvoids=args.cell_voids)
+    verts = torch.from_numpy(d["verts"]).cuda()
+    bc = torch.from_numpy(d["bc_type"]).cuda()
+    val = torch.from_numpy(d["bc_val"]).cuda()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    op = eb.bem_create(verts, nq=args.nq, max_pts=args.max_pts, p=args.p, K=d["K"], G=d["G"])
+    torch.cuda.synchronize()
+    setup = time.perf_counter() - t0
+    x = torch.zeros((d["verts"].shape[0], 3), device="cuda")
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches0 = eb.ebem_launch_count()
+    with ClockSampler(0) as clk:
+        a.record()
+        x, it, res = eb.bem_gmres_solve(op, bc, val, x, restart=50, max_iter=args.max_iter, tol=1e-6,
+                                        precond=args.precond, check=False)
+        b.record()
+        torch.cuda.synchronize()
+    ms = a.elapsed_time(b)
+    V = d["verts"].astype(np.float64)
+    area = 0.5 * np.linalg.norm(np.cross(V[:, 1] - V[:, 0], V[:, 2] - V[:, 0]), axis=1)
+    t = np.where(d["bc_type"][:, None] == 0, x.cpu().numpy(), d["bc_val"])
+    force = (t * area[:, None]).sum(0)
+    line = {"metric": "BEM GMRES solve time (configs[4])", "value": ms / 1e3, "unit": "s", "n_gpus": 1,
+            "steps": 1, "warmup": 0, "ms_per_step": ms, "higher_is_better": False, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32 FMM, f64 Krylov", "data": "synthetic",
+            "config": {"workload": f"metamaterial cell, {d['verts'].shape[0]} triangles, {args.cell_voids} voids",
+                       "nq": args.nq, "p": args.p, "max_pts": args.max_pts, "restart": 50, "tol": 1e-6,
+                       "precond": ["none (paper)", "block-Jacobi"][args.precond]},
+            "iterations": it, "rel_residual": res, "ms_per_iteration": ms / max(it, 1),
+            "setup_s": setup, "gpu_launches": int(eb.ebem_launch_count() - launches0),
+            "equilibrium_residual": float(np.linalg.norm(force)), "applied_load": 1.0, "clocks": clk.summary()}
+    print(json.dumps(line), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -188,6 +229,13 @@ def main():
     ap.add_argument("--cpu-sample", type=int, default=3072)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-p2p", action="store_true")
+    ap.add_argument("--workload", default="matvec", choices=["matvec", "gmres"])
+    ap.add_argument("--nq", type=int, default=16)
+    ap.add_argument("--cell-nc", type=int, default=160)
+    ap.add_argument("--cell-level", type=int, default=5)
+    ap.add_argument("--cell-voids", type=int, default=64)
+    ap.add_argument("--max-iter", type=int, default=1000)
+    ap.add_argument("--precond", type=int, default=0)
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -204,6 +252,8 @@ def main():
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     pk = peaks()
+    if args.workload == "gmres":
+        return gmres_workload(args, eb, torch)
 
     d = workload(args.n)
     n = d["src"].shape[0]

@@ -203,6 +203,10 @@ int64_t fmm_tree_export(const ebem_tree *tree, int what, void *buf, int64_t cap)
  *   x [npanels*3]: initial guess in, solution out (traction on Dirichlet panels,
  *   displacement on Neumann panels).  Stops at |b - A x| / |b| <= tol or max_iter;
  *   returns EBEM_ERR_NOCONV (x still written) if the tolerance was not reached.
+ *   precond: 0 = none (the paper's solver, l. 181, "In the future this shortcoming should be
+ *   addressed with ... the appropriate preconditioner", l. 369); 1 = block-Jacobi right
+ *   preconditioner with the panels' own 3x3 blocks (-U_self on Dirichlet panels,
+ *   1/2 I + P_self on Neumann panels).  The solution of A x = b is the same.
  *   iters_out / resid_out (host, may be NULL): iterations and final relative residual.
  * Array arguments of bem_apply / bem_rhs / bem_gmres_solve must be device pointers.
  */
@@ -213,8 +217,8 @@ int bem_create(const float *vertices, int64_t npanels, int nq, int max_pts, int 
 int bem_apply(ebem_bem *bem, const int32_t *bc_type, const float *x, float *y, void *stream);
 int bem_rhs(ebem_bem *bem, const int32_t *bc_type, const float *bc_val, float *b, void *stream);
 int bem_gmres_solve(ebem_bem *bem, const int32_t *bc_type, const float *bc_val, float *x,
-                    int restart, int max_iter, double tol, int32_t *iters_out, double *resid_out,
-                    void *stream);
+                    int restart, int max_iter, double tol, int precond, int32_t *iters_out,
+                    double *resid_out, void *stream);
 int bem_free(ebem_bem *bem);
 
 #ifdef __cplusplus

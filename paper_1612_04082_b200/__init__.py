@@ -41,7 +41,7 @@ _lib.bem_create.argtypes = [_VP, _I64, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                             ctypes.c_double, ctypes.POINTER(_VP), _VP]
 _lib.bem_apply.argtypes = [_VP, _VP, _VP, _VP, _VP]
 _lib.bem_rhs.argtypes = [_VP, _VP, _VP, _VP, _VP]
-_lib.bem_gmres_solve.argtypes = [_VP, _VP, _VP, _VP, ctypes.c_int, ctypes.c_int, ctypes.c_double,
+_lib.bem_gmres_solve.argtypes = [_VP, _VP, _VP, _VP, ctypes.c_int, ctypes.c_int, ctypes.c_double, ctypes.c_int,
                                  ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_double), _VP]
 _lib.bem_free.argtypes = [_VP]
 
@@ -285,13 +285,15 @@ def bem_rhs(bem, bc_type, bc_val, out=None):
     return out
 
 
-def bem_gmres_solve(bem, bc_type, bc_val, x, restart=50, max_iter=1000, tol=1e-6, check=True):
-    """solves A x = b in place; returns (x, iterations, relative residual)."""
+def bem_gmres_solve(bem, bc_type, bc_val, x, restart=50, max_iter=1000, tol=1e-6, precond=0, check=True):
+    """solves A x = b in place; returns (x, iterations, relative residual).
+    precond: 0 none (the paper's GMRES), 1 block-Jacobi right preconditioner."""
     keep = []
     it = ctypes.c_int32(0)
     res = ctypes.c_double(0)
     rc = _lib.bem_gmres_solve(bem.handle, _ptr(bc_type, keep), _ptr(bc_val, keep), _ptr(x, keep), int(restart),
-                              int(max_iter), float(tol), ctypes.byref(it), ctypes.byref(res), _stream(x))
+                              int(max_iter), float(tol), int(precond), ctypes.byref(it), ctypes.byref(res),
+                              _stream(x))
     if check or rc not in (0, -4):
         _check(rc)
     return x, int(it.value), float(res.value)

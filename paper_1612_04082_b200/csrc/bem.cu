@@ -54,6 +54,7 @@ struct Bem {
     Tree* tree = nullptr;
     DBuf<float> cent, nrm, area, qpts, qnrm, qw;
     DBuf<float> CU, CP;     // [n x 9] local correction blocks (row-major 3x3)
+    DBuf<double> DU, DP;    // [n x 9] diagonal blocks U_self, 1/2 I + P_self (preconditioner)
     DBuf<float> f, g, y;    // expanded densities [n nq x 3], FMM output [n x 3]
     ~Bem() { delete tree; }
 };
@@ -128,7 +129,8 @@ __global__ void panels_kernel(const float* __restrict__ V, int64_t n, int nq, fl
 // local correction blocks CU, CP (see the file header), fp64
 __global__ void self_terms_kernel(const float* __restrict__ V, int64_t n, int nq, const float* __restrict__ qp,
                                   const float* __restrict__ qw, const float* __restrict__ cent,
-                                  const float* __restrict__ nrm, double G, double nu, float* CU, float* CP) {
+                                  const float* __restrict__ nrm, double G, double nu, float* CU, float* CP,
+                                  double* DU, double* DP) {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= n) return;
     const double PI = 3.14159265358979323846;
@@ -167,6 +169,10 @@ __global__ void self_terms_kernel(const float* __restrict__ V, int64_t n, int nq
     double Ps[9];
     for (int r = 0; r < 3; ++r)
         for (int c = 0; c < 3; ++c) Ps[3 * r + c] = cp * (-Ie[r] * nn[c] + Ie[c] * nn[r]) + (r == c ? 0.5 : 0.0);
+    for (int k = 0; k < 9; ++k) {
+        DU[9 * i + k] = Us[k];
+        DP[9 * i + k] = Ps[k];
+    }
     // subtract what the FMM adds from the panel's own quadrature points (y_q != xi)
     const float cx = cent[3 * i], cy = cent[3 * i + 1], cz = cent[3 * i + 2];
     for (int q = 0; q < nq; ++q) {
@@ -267,8 +273,10 @@ Bem* bem_create(const float* verts, int64_t n, int nq, int max_pts, int p, const
     EB_CHECK_LAUNCH();
     B->CU.alloc(9 * n);
     B->CP.alloc(9 * n);
+    B->DU.alloc(9 * n);
+    B->DP.alloc(9 * n);
     self_terms_kernel<<<ceil_div(n, 128), 128, 0, s>>>(verts, n, nq, B->qpts.p, B->qw.p, B->cent.p, B->nrm.p, m.G, m.nu,
-                                                       B->CU.p, B->CP.p);
+                                                       B->CU.p, B->CP.p, B->DU.p, B->DP.p);
     EB_CHECK_LAUNCH();
     B->tree = build_tree(B->qpts.p, B->qnrm.p, B->qw.p, ns, B->cent.p, n, max_pts, p, m, s);
     B->f.alloc(3 * ns);
@@ -327,9 +335,46 @@ __global__ void to_f64_kernel(const float* __restrict__ a, double* __restrict__ 
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i < n) b[i] = (double)a[i];
 }
+__global__ void add_kernel(const double* __restrict__ a, double* __restrict__ b, int64_t n) {   // b += a
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) b[i] += a[i];
+}
 __global__ void sub_kernel(const double* __restrict__ a, double* __restrict__ b, int64_t n) {   // b = a - b
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i < n) b[i] = a[i] - b[i];
+}
+
+// block-Jacobi right preconditioner: M_i = diagonal block of A (-U_self on Dirichlet panels,
+// 1/2 I + P_self on Neumann panels); Minv_i by 3x3 cofactors in fp64
+__global__ void prec_setup(const int32_t* __restrict__ bc, const double* __restrict__ DU,
+                           const double* __restrict__ DP, int64_t n, double* __restrict__ Minv) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double a[9];
+    const bool dir = bc[i] == 0;
+    for (int k = 0; k < 9; ++k) a[k] = dir ? -DU[9 * i + k] : DP[9 * i + k];
+    const double c00 = a[4] * a[8] - a[5] * a[7], c01 = a[5] * a[6] - a[3] * a[8], c02 = a[3] * a[7] - a[4] * a[6];
+    const double det = a[0] * c00 + a[1] * c01 + a[2] * c02;
+    const double id = 1.0 / det;
+    double* m = Minv + 9 * i;
+    m[0] = c00 * id;
+    m[3] = c01 * id;
+    m[6] = c02 * id;
+    m[1] = (a[2] * a[7] - a[1] * a[8]) * id;
+    m[4] = (a[0] * a[8] - a[2] * a[6]) * id;
+    m[7] = (a[1] * a[6] - a[0] * a[7]) * id;
+    m[2] = (a[1] * a[5] - a[2] * a[4]) * id;
+    m[5] = (a[2] * a[3] - a[0] * a[5]) * id;
+    m[8] = (a[0] * a[4] - a[1] * a[3]) * id;
+}
+
+__global__ void prec_apply(const double* __restrict__ Minv, const double* __restrict__ v, int64_t n,
+                           double* __restrict__ out) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    for (int r = 0; r < 3; ++r)
+        out[3 * i + r] = Minv[9 * i + 3 * r] * v[3 * i] + Minv[9 * i + 3 * r + 1] * v[3 * i + 1] +
+                         Minv[9 * i + 3 * r + 2] * v[3 * i + 2];
 }
 
 static double dnorm(const double* v, int64_t n, double* tmp, cudaStream_t s) {
@@ -342,10 +387,16 @@ static double dnorm(const double* v, int64_t n, double* tmp, cudaStream_t s) {
 }
 
 int bem_gmres(Bem& B, const int32_t* bc, const float* val, float* x, int m, int max_iter, double tol, int32_t* iters,
-              double* resid, cudaStream_t s) {
+              double* resid, int precond, cudaStream_t s) {
     const int64_t n3 = 3 * B.n;
-    DBuf<double> V((size_t)(m + 1) * n3), w(n3), b(n3), xd(n3), hd(m + 2);
+    DBuf<double> V((size_t)(m + 1) * n3), w(n3), b(n3), xd(n3), hd(m + 2), Minv, tp;
     DBuf<float> xf(n3), yf(n3);
+    if (precond) {
+        Minv.alloc(9 * B.n);
+        tp.alloc(n3);
+        prec_setup<<<ceil_div(B.n, 256), 256, 0, s>>>(bc, B.DU.p, B.DP.p, B.n, Minv.p);
+        EB_CHECK_LAUNCH();
+    }
     // right-hand side b = -L(known values)
     apply_L<double>(B, 1, -1.0, bc, val, b.p, s);
     const double bn = dnorm(b.p, n3, hd.p, s);
@@ -355,6 +406,12 @@ int bem_gmres(Bem& B, const int32_t* bc, const float* val, float* x, int m, int 
         to_f32_kernel<<<ceil_div(n3, 256), 256, 0, s>>>(v, xf.p, n3);
         EB_CHECK_LAUNCH();
         apply_L<double>(B, 0, 1.0, bc, xf.p, out, s);
+    };
+    auto pmatvec = [&](const double* v, double* out) {  // out = A M^-1 v (right preconditioning)
+        if (!precond) return matvec(v, out);
+        prec_apply<<<ceil_div(B.n, 256), 256, 0, s>>>(Minv.p, v, B.n, tp.p);
+        EB_CHECK_LAUNCH();
+        matvec(tp.p, out);
     };
     int it = 0;
     double rel = 1.0;
@@ -378,7 +435,7 @@ int bem_gmres(Bem& B, const int32_t* bc, const float* val, float* x, int m, int 
         g[0] = beta;
         int k = 0;
         for (int j = 0; j < m; ++j) {
-            matvec(V.p + (int64_t)j * n3, w.p);
+            pmatvec(V.p + (int64_t)j * n3, w.p);
             // classical Gram-Schmidt with one re-orthogonalisation, on the device
             for (int pass = 0; pass < 2; ++pass) {
                 dots_kernel<<<j + 1, 256, 0, s>>>(V.p, n3, j + 1, w.p, n3, hd.p);
@@ -419,7 +476,14 @@ int bem_gmres(Bem& B, const int32_t* bc, const float* val, float* x, int m, int 
             y[i] = sum / H[(size_t)i * m + i];
         }
         h2d(hd.p, y.data(), k, s);
-        axpy_basis<<<ceil_div(n3, 256), 256, 0, s>>>(V.p, n3, k, hd.p, 1.0, xd.p, n3);
+        if (precond) {     // x += M^-1 (V y)
+            EB_CUDA(cudaMemsetAsync(w.p, 0, sizeof(double) * n3, s));
+            axpy_basis<<<ceil_div(n3, 256), 256, 0, s>>>(V.p, n3, k, hd.p, 1.0, w.p, n3);
+            prec_apply<<<ceil_div(B.n, 256), 256, 0, s>>>(Minv.p, w.p, B.n, tp.p);
+            add_kernel<<<ceil_div(n3, 256), 256, 0, s>>>(tp.p, xd.p, n3);
+        } else {
+            axpy_basis<<<ceil_div(n3, 256), 256, 0, s>>>(V.p, n3, k, hd.p, 1.0, xd.p, n3);
+        }
         EB_CHECK_LAUNCH();
         if (it >= max_iter) {
             // true residual of the final iterate

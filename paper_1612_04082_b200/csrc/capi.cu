@@ -272,7 +272,8 @@ extern "C" int bem_rhs(ebem_bem* bem, const int32_t* bc_type, const float* bc_va
 }
 
 extern "C" int bem_gmres_solve(ebem_bem* bem, const int32_t* bc_type, const float* bc_val, float* x, int restart,
-                               int max_iter, double tol, int32_t* iters_out, double* resid_out, void* stream) {
+                               int max_iter, double tol, int precond, int32_t* iters_out, double* resid_out,
+                               void* stream) {
     EB_API_BEGIN
     set_last_error("");
     EB_REQUIRE(bem && bc_type && bc_val && x, "NULL argument");
@@ -280,7 +281,7 @@ extern "C" int bem_gmres_solve(ebem_bem* bem, const int32_t* bc_type, const floa
     EB_REQUIRE(is_device_ptr(x) && is_device_ptr(bc_val) && is_device_ptr(bc_type),
                "bem_gmres_solve needs device pointers");
     const int rc = ebem::bem_gmres(*reinterpret_cast<Bem*>(bem), bc_type, bc_val, x, restart, max_iter, tol, iters_out,
-                                   resid_out, (cudaStream_t)stream);
+                                   resid_out, precond, (cudaStream_t)stream);
     if (rc != EBEM_OK) set_last_error("GMRES did not reach the tolerance");
     return rc;
     EB_API_END

@@ -156,7 +156,7 @@ void bem_free(Bem* B);
 void bem_apply(Bem& B, const int32_t* bc, const float* x, float* y, cudaStream_t s);
 void bem_rhs(Bem& B, const int32_t* bc, const float* val, float* b, cudaStream_t s);
 int bem_gmres(Bem& B, const int32_t* bc, const float* val, float* x, int m, int max_iter, double tol,
-              int32_t* iters, double* resid, cudaStream_t s);
+              int32_t* iters, double* resid, int precond, cudaStream_t s);
 
 // ------------------------------------------------------------------ primitives (linalg.cu)
 // exclusive scan of n ints (out may alias in); returns the total on the host (syncs)

@@ -183,3 +183,78 @@ def config3(n_src: int = 500_000, grid=(200, 50, 100), seed: int = 3):
     trg = interior_grid(*grid)
     c, nrm, a, f, g, trg = _f32(c, nrm, a, f, g, trg)
     return dict(src=c, trg=trg, nrm=nrm, w=a, f=f, g=g, K=1.67, G=0.77)
+
+
+# ------------------------------------------------------------------ config 4 (GMRES)
+def icosphere(level: int):
+    """unit icosphere: icosahedron, each face split into 4 `level` times, vertices projected
+    to the sphere.  Returns (V0, V1, V2) counter-clockwise seen from outside."""
+    t = (1.0 + 5 ** 0.5) / 2.0
+    verts = [(-1, t, 0), (1, t, 0), (-1, -t, 0), (1, -t, 0), (0, -1, t), (0, 1, t), (0, -1, -t), (0, 1, -t),
+             (t, 0, -1), (t, 0, 1), (-t, 0, -1), (-t, 0, 1)]
+    faces = [(0, 11, 5), (0, 5, 1), (0, 1, 7), (0, 7, 10), (0, 10, 11), (1, 5, 9), (5, 11, 4), (11, 10, 2),
+             (10, 7, 6), (7, 1, 8), (3, 9, 4), (3, 4, 2), (3, 2, 6), (3, 6, 8), (3, 8, 9), (4, 9, 5), (2, 4, 11),
+             (6, 2, 10), (8, 6, 7), (9, 8, 1)]
+    V = np.array(verts, np.float64)
+    V /= np.linalg.norm(V, axis=1, keepdims=True)
+    F = np.array(faces)
+    for _ in range(level):
+        a, b, c = V[F[:, 0]], V[F[:, 1]], V[F[:, 2]]
+        ab, bc, ca = (a + b), (b + c), (c + a)
+        ab /= np.linalg.norm(ab, axis=1, keepdims=True)
+        bc /= np.linalg.norm(bc, axis=1, keepdims=True)
+        ca /= np.linalg.norm(ca, axis=1, keepdims=True)
+        nv = len(V)
+        nf = len(F)
+        V = np.concatenate([V, ab, bc, ca])
+        iab, ibc, ica = nv + np.arange(nf), nv + nf + np.arange(nf), nv + 2 * nf + np.arange(nf)
+        F = np.concatenate([np.stack([F[:, 0], iab, ica], 1), np.stack([F[:, 1], ibc, iab], 1),
+                            np.stack([F[:, 2], ica, ibc], 1), np.stack([iab, ibc, ica], 1)])
+    V0, V1, V2 = V[F[:, 0]], V[F[:, 1]], V[F[:, 2]]
+    # orient counter-clockwise seen from outside (outward normal)
+    flip = np.einsum("ij,ij->i", np.cross(V1 - V0, V2 - V0), V0 + V1 + V2) < 0
+    V1, V2 = np.where(flip[:, None], V2, V1), np.where(flip[:, None], V1, V2)
+    return V0, V1, V2
+
+
+def metamaterial_cell(nc=160, level=5, nvoids=64, rmin=0.05, rmax=0.1, gap=0.01, seed=4):
+    """configs[4]: unit cube with `nvoids` seeded non-overlapping spherical voids of radius
+    in [rmin, rmax], each an icosphere of `level`; the outer cube is meshed like configs[1]
+    (nc cells per edge, 4-triangle fan).  Void surfaces are oriented with the normal out
+    of the material (into the void).  Boundary conditions: Dirichlet u = 0 on the bottom
+    face z = 0, Neumann traction (0, 0, -1) on the top face z = 1, traction free elsewhere.
+    Returns dict(verts (n,3,3) float32, bc_type int32, bc_val float32 (n,3), K, G)."""
+    rng = np.random.default_rng(seed)
+    centers, radii = [], []
+    tries = 0
+    while len(centers) < nvoids:
+        tries += 1
+        if tries > 200000:
+            raise RuntimeError("could not place the voids")
+        r = rng.uniform(rmin, rmax)
+        c = rng.uniform(r + gap, 1 - r - gap, 3)
+        if all(np.linalg.norm(c - c2) > r + r2 + gap for c2, r2 in zip(centers, radii)):
+            centers.append(c)
+            radii.append(r)
+    C0, C1, C2 = cube_voxel_faces(nc)
+    S0, S1, S2 = icosphere(level)
+    parts0, parts1, parts2 = [C0], [C1], [C2]
+    for c, r in zip(centers, radii):
+        # into the void: reverse the sphere's outward orientation
+        parts0.append(c + r * S0)
+        parts1.append(c + r * S2)
+        parts2.append(c + r * S1)
+    V0, V1, V2 = (np.concatenate(p) for p in (parts0, parts1, parts2))
+    cen = (V0 + V1 + V2) / 3.0
+    ncube = len(C0)
+    bc = np.ones(len(V0), np.int32)
+    val = np.zeros((len(V0), 3))
+    bottom = np.zeros(len(V0), bool)
+    bottom[:ncube] = cen[:ncube, 2] < 1e-9
+    top = np.zeros(len(V0), bool)
+    top[:ncube] = cen[:ncube, 2] > 1 - 1e-9
+    bc[bottom] = 0
+    val[top] = (0.0, 0.0, -1.0)
+    verts = np.stack([V0, V1, V2], 1).astype(np.float32)
+    return dict(verts=verts, bc_type=bc, bc_val=val.astype(np.float32), K=1.67, G=0.77,
+                centers=np.array(centers), radii=np.array(radii))
