@@ -74,86 +74,139 @@ check_potential_kernel(const int* __restrict__ tbox, const int* __restrict__ sof
 }
 
 // ------------------------------------------------------------------ leaf evaluation
-// One CTA per target leaf: L2T (own downward equivalent density) and M2T (W list) in
-// fp64 from phi, near field over the U list in fp32, result scattered to caller order.
-constexpr int EV_T = 64, EV_TILE = 64;
+// Two warp-per-leaf kernels (a CTA holds EV_WARPS independent leaves; leaves carry ~24
+// targets on surfaces, so a whole CTA per leaf left most lanes idle):
+//   far_eval : L2T (own downward equivalent density) + M2T (W list) in fp64 from phi,
+//              result (fp32) into the sorted far-field buffer;
+//   near_eval: U-list near field in fp32 (sources staged per warp in shared memory),
+//              plus the far field, scattered to the caller's target order.
+constexpr int EV_WARPS = 4;
+// far field (L2T, M2T) in fp64 from this multipole order on; fp32 below (its rounding,
+// amplified by the cancelling equivalent densities, stays under the truncation error).
+// Inside GMRES the BEM operator always uses fp64: the fp32 rounding is not linear in the
+// density, and Krylov iterations stall at that level (observed at tol 1e-6).
+constexpr int FAR_FP64_MIN_P = 9;
 
-template <bool SL, bool DL, bool STRESS>
-__global__ void __launch_bounds__(EV_T)
-leaf_eval_kernel(const int* __restrict__ eval_box, const int* __restrict__ l2t_slot,
-                 const double* __restrict__ PHID, const double* __restrict__ PHIU, const int* __restrict__ phiu_slot,
-                 const int* __restrict__ woff, const int* __restrict__ widx, const int* __restrict__ uoff,
-                 const int* __restrict__ uidx, const int* __restrict__ sbeg, const int* __restrict__ send,
-                 const int* __restrict__ tbeg, const int* __restrict__ tend, const int* __restrict__ anchor,
-                 const int* __restrict__ level, BoxGeo geo, const double* __restrict__ se, int ne,
-                 const float* __restrict__ trg, const int* __restrict__ trg_perm, const float4* __restrict__ rec,
-                 KConst kc, double cfar, float* __restrict__ out) {
+// T = double: fp64 evaluation (p >= 9, where fp32 rounding of the cancelling terms
+// sum_k K(x, y_k) phi_k would exceed the truncation error); T = float for p <= 8.
+template <class T>
+__device__ __forceinline__ T far_rinv(T r2);
+template <>
+__device__ __forceinline__ float far_rinv<float>(float r2) { return rsqrtf(r2); }
+template <>
+__device__ __forceinline__ double far_rinv<double>(double r2) {
+    // fp32 seed + two Newton steps (r2 > 0: the equivalent surfaces never reach a target)
+    double ri = (double)rsqrtf((float)r2);
+    ri = ri * (1.5 - 0.5 * r2 * ri * ri);
+    return ri * (1.5 - 0.5 * r2 * ri * ri);
+}
+
+template <bool STRESS, class T>
+__global__ void __launch_bounds__(32 * EV_WARPS)
+far_eval_kernel(int n_eval, const int* __restrict__ eval_box, const int* __restrict__ l2t_slot,
+                const double* __restrict__ PHID, const double* __restrict__ PHIU, const int* __restrict__ phiu_slot,
+                const int* __restrict__ woff, const int* __restrict__ widx, const int* __restrict__ tbeg,
+                const int* __restrict__ tend, const int* __restrict__ anchor, const int* __restrict__ level, BoxGeo geo,
+                const double* __restrict__ se, int ne, const float* __restrict__ trg, KConst kc, double cfar,
+                float* __restrict__ far) {
     constexpr int NC = STRESS ? 6 : 3;
-    constexpr int R = STRESS ? REC_STRESS : REC_DISP;
     extern __shared__ double dsm[];
-    double* ey = dsm;                   // [3 ne] equivalent points
-    double* ephi = dsm + 3 * ne;        // [3 ne] prepared equivalent densities
-    float4* srec = reinterpret_cast<float4*>(dsm + 6 * ne);   // [EV_TILE * R]
-    const int b = eval_box[blockIdx.x];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int i = blockIdx.x * EV_WARPS + warp;
+    if (i >= n_eval) return;                       // warp-uniform; no CTA barriers below
+    T* ey = reinterpret_cast<T*>(dsm) + (size_t)warp * 6 * ne;   // [3 ne] equivalent points
+    T* ephi = ey + 3 * ne;                                         // [3 ne] prepared densities
+    const int b = eval_box[i];
     const int t_beg = tbeg[b], t_end = tend[b];
-    for (int t0 = t_beg; t0 < t_end; t0 += EV_T) {
-        const int t = t0 + threadIdx.x;
-        const bool act = t < t_end;
-        const int tc = act ? t : t_beg;
-        const float x = trg[3 * tc], y = trg[3 * tc + 1], z = trg[3 * tc + 2];
+    const int own = l2t_slot[i] >= 0 ? 1 : 0;
+    const int nfar = own + (woff[b + 1] - woff[b]);
+    const T a1 = (T)kc.a1d, aa = (T)kc.ad;
+    for (int t0 = t_beg; t0 < t_end; t0 += 32) {
+        const int t = t0 + lane;
+        const int tc = t < t_end ? t : t_beg;
         double acc64[NC];
-        float acc32[NC];
 #pragma unroll
-        for (int c = 0; c < NC; ++c) {
-            acc64[c] = 0.0;
-            acc32[c] = 0.f;
-        }
-        // far field: own local expansion (L2T) then the W list (M2T)
-        const int nfar = (l2t_slot[blockIdx.x] >= 0 ? 1 : 0) + (woff[b + 1] - woff[b]);
+        for (int c = 0; c < NC; ++c) acc64[c] = 0.0;
         for (int e = 0; e < nfar; ++e) {
-            const bool own = (l2t_slot[blockIdx.x] >= 0) && e == 0;
-            const int a = own ? b : widx[woff[b] + e - (l2t_slot[blockIdx.x] >= 0 ? 1 : 0)];
-            const double* phi = own ? PHID + (int64_t)l2t_slot[blockIdx.x] * 3 * ne
-                                    : (phiu_slot[a] >= 0 ? PHIU + (int64_t)phiu_slot[a] * 3 * ne : nullptr);
-            if (!phi) continue;   // box without sources: zero multipole
+            const bool is_own = own && e == 0;
+            const int a = is_own ? b : widx[woff[b] + e - own];
+            const double* phi = is_own ? PHID + (int64_t)l2t_slot[i] * 3 * ne
+                                       : (phiu_slot[a] >= 0 ? PHIU + (int64_t)phiu_slot[a] * 3 * ne : nullptr);
+            if (!phi) continue;
             double cx, cy, cz, r;
             geo.center(anchor, level, a, cx, cy, cz, r);
-            const double Rr = (own ? RAD_DE : RAD_UE) * r;
-            __syncthreads();
-            for (int k = threadIdx.x; k < ne; k += EV_T) {
-                ey[3 * k] = cx + Rr * se[3 * k];
-                ey[3 * k + 1] = cy + Rr * se[3 * k + 1];
-                ey[3 * k + 2] = cz + Rr * se[3 * k + 2];
-                ephi[3 * k] = cfar * phi[3 * k];
-                ephi[3 * k + 1] = cfar * phi[3 * k + 1];
-                ephi[3 * k + 2] = cfar * phi[3 * k + 2];
+            const double Rr = (is_own ? RAD_DE : RAD_UE) * r;
+            __syncwarp();
+            // coordinates relative to the box centre (keeps fp32 differences well scaled)
+            for (int k = lane; k < ne; k += 32) {
+                ey[3 * k] = (T)(Rr * se[3 * k]);
+                ey[3 * k + 1] = (T)(Rr * se[3 * k + 1]);
+                ey[3 * k + 2] = (T)(Rr * se[3 * k + 2]);
+                ephi[3 * k] = (T)(cfar * phi[3 * k]);
+                ephi[3 * k + 1] = (T)(cfar * phi[3 * k + 1]);
+                ephi[3 * k + 2] = (T)(cfar * phi[3 * k + 2]);
             }
-            __syncthreads();
-            const double xd = x, yd = y, zd = z;
+            __syncwarp();
+            const T x = (T)((double)trg[3 * tc] - cx), y = (T)((double)trg[3 * tc + 1] - cy),
+                    z = (T)((double)trg[3 * tc + 2] - cz);
+            T acc[NC];
+#pragma unroll
+            for (int c = 0; c < NC; ++c) acc[c] = (T)0;
+#pragma unroll 2
             for (int k = 0; k < ne; ++k) {
-                double dx = xd - ey[3 * k], dy = yd - ey[3 * k + 1], dz = zd - ey[3 * k + 2];
-                double ri = safe_rinv(dx * dx + dy * dy + dz * dz);
+                const T dx = x - ey[3 * k], dy = y - ey[3 * k + 1], dz = z - ey[3 * k + 2];
+                const T ri = far_rinv<T>(dx * dx + dy * dy + dz * dz);
                 if (!STRESS)
-                    acc_U<double>(dx, dy, dz, ri, ephi[3 * k], ephi[3 * k + 1], ephi[3 * k + 2], kc.a1d, acc64);
+                    acc_U<T>(dx, dy, dz, ri, ephi[3 * k], ephi[3 * k + 1], ephi[3 * k + 2], a1, acc);
                 else
-                    acc_D<double>(dx, dy, dz, ri, ephi[3 * k], ephi[3 * k + 1], ephi[3 * k + 2], kc.ad, acc64);
+                    acc_D<T>(dx, dy, dz, ri, ephi[3 * k], ephi[3 * k + 1], ephi[3 * k + 2], aa, acc);
             }
+#pragma unroll
+            for (int c = 0; c < NC; ++c) acc64[c] += (double)acc[c];
         }
-        // near field over the U list
+        if (t < t_end)
+#pragma unroll
+            for (int c = 0; c < NC; ++c) far[(int64_t)t * NC + c] = (float)acc64[c];
+    }
+}
+
+template <bool SL, bool DL, bool STRESS>
+__global__ void __launch_bounds__(32 * EV_WARPS)
+near_eval_kernel(int n_eval, const int* __restrict__ eval_box, const int* __restrict__ uoff,
+                 const int* __restrict__ uidx, const int* __restrict__ sbeg, const int* __restrict__ send,
+                 const int* __restrict__ tbeg, const int* __restrict__ tend, const float* __restrict__ trg,
+                 const int* __restrict__ trg_perm, const float4* __restrict__ rec, KConst kc,
+                 const float* __restrict__ far, float* __restrict__ out) {
+    constexpr int NC = STRESS ? 6 : 3;
+    constexpr int R = STRESS ? REC_STRESS : REC_DISP;
+    __shared__ float4 srec_all[EV_WARPS][32 * R];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int i = blockIdx.x * EV_WARPS + warp;
+    if (i >= n_eval) return;
+    float4* srec = srec_all[warp];
+    const int b = eval_box[i];
+    const int t_beg = tbeg[b], t_end = tend[b];
+    for (int t0 = t_beg; t0 < t_end; t0 += 32) {
+        const int t = t0 + lane;
+        const int tc = t < t_end ? t : t_beg;
+        const float x = trg[3 * tc], y = trg[3 * tc + 1], z = trg[3 * tc + 2];
+        float acc[NC];
+#pragma unroll
+        for (int c = 0; c < NC; ++c) acc[c] = 0.f;
         for (int e = uoff[b]; e < uoff[b + 1]; ++e) {
             const int a = uidx[e];
-            for (int s0 = sbeg[a]; s0 < send[a]; s0 += EV_TILE) {
-                const int cnt = min(EV_TILE, send[a] - s0);
-                __syncthreads();
-                for (int q = threadIdx.x; q < cnt * R; q += EV_T) srec[q] = rec[(int64_t)s0 * R + q];
-                __syncthreads();
-                pair_loop<SL, DL, STRESS>(srec, cnt, x, y, z, kc, acc32);
+            for (int s0 = sbeg[a]; s0 < send[a]; s0 += 32) {
+                const int cnt = min(32, send[a] - s0);
+                __syncwarp();
+                for (int q = lane; q < cnt * R; q += 32) srec[q] = rec[(int64_t)s0 * R + q];
+                __syncwarp();
+                pair_loop<SL, DL, STRESS>(srec, cnt, x, y, z, kc, acc);
             }
         }
-        if (act) {
+        if (t < t_end) {
             float* o = out + (int64_t)trg_perm[t] * NC;
 #pragma unroll
-            for (int c = 0; c < NC; ++c) o[c] = (float)(acc64[c] + (double)acc32[c]);
+            for (int c = 0; c < NC; ++c) o[c] = acc[c] + far[(int64_t)t * NC + c];
         }
     }
 }
@@ -376,6 +429,7 @@ void schedule_tree(Tree& t, cudaStream_t s) {
     t.Z.alloc((size_t)std::max(1, t.n_up) * lde);
     t.W.alloc((size_t)std::max(1, t.n_dn) * lde);
     if (const char* e = std::getenv("EBEM_SIMT")) t.use_tc = std::atoi(e) == 0;
+    t.far64 = P.p >= FAR_FP64_MIN_P;
     if (t.use_tc) {
         t.Qb.alloc(t.Q.n); t.Qs.alloc(t.Q.n);
         t.Zb.alloc(t.Z.n); t.Zs.alloc(t.Z.n);
@@ -394,6 +448,7 @@ void schedule_tree(Tree& t, cudaStream_t s) {
         for (auto& x : t.l2l) tc_build_tiles(x, me);
     }
     t.PHID.alloc((size_t)std::max(1, t.n_phid) * me);
+    t.out_sorted.alloc((size_t)std::max<int64_t>(1, t.ntrg) * 6);
     t.PHIU.alloc((size_t)std::max(1, t.n_phiu) * me);
     EB_CUDA(cudaStreamSynchronize(s));
 
@@ -427,16 +482,20 @@ static void launch_eval(const Tree& t, float* out, cudaStream_t s) {
     if (t.n_eval == 0) return;
     const Plan& P = *t.plan;
     BoxGeo geo{t.origin[0], t.origin[1], t.origin[2], t.side};
-    constexpr int R = STRESS ? REC_STRESS : REC_DISP;
-    size_t sm = sizeof(double) * 6 * P.ne + sizeof(float4) * EV_TILE * R;
     KConst kc = make_kconst(t.mat);
     const double cfar = STRESS ? t.mat.cD : t.mat.cU;
-    auto kfn = leaf_eval_kernel<SL, DL, STRESS>;
-    if (sm > 48 * 1024) EB_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    kfn<<<t.n_eval, EV_T, sm, s>>>(t.eval_box.p, t.eval_l2t_slot.p, t.PHID.p, t.PHIU.p, t.phiu_slot.p,
-                                   t.lst_off[2].p, t.lst_idx[2].p, t.lst_off[0].p, t.lst_idx[0].p, t.sbeg.p,
-                                   t.send.p, t.tbeg.p, t.tend.p, t.anchor.p, t.level.p, geo, P.s_e64.p, P.ne,
-                                   t.trg_xyz.p, t.trg_perm.p, STRESS ? t.rec_stress.p : t.rec_disp.p, kc, cfar, out);
+    const int grid = ceil_div(t.n_eval, EV_WARPS);
+    const bool fp64 = t.far64;
+    const size_t sm = (fp64 ? sizeof(double) : sizeof(float)) * 6 * P.ne * EV_WARPS;
+    auto ffn = fp64 ? far_eval_kernel<STRESS, double> : far_eval_kernel<STRESS, float>;
+    if (sm > 48 * 1024) EB_CUDA(cudaFuncSetAttribute(ffn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    ffn<<<grid, 32 * EV_WARPS, sm, s>>>(t.n_eval, t.eval_box.p, t.eval_l2t_slot.p, t.PHID.p, t.PHIU.p, t.phiu_slot.p,
+                                        t.lst_off[2].p, t.lst_idx[2].p, t.tbeg.p, t.tend.p, t.anchor.p, t.level.p, geo,
+                                        P.s_e64.p, P.ne, t.trg_xyz.p, kc, cfar, t.out_sorted.p);
+    EB_CHECK_LAUNCH();
+    near_eval_kernel<SL, DL, STRESS><<<grid, 32 * EV_WARPS, 0, s>>>(
+        t.n_eval, t.eval_box.p, t.lst_off[0].p, t.lst_idx[0].p, t.sbeg.p, t.send.p, t.tbeg.p, t.tend.p, t.trg_xyz.p,
+        t.trg_perm.p, STRESS ? t.rec_stress.p : t.rec_disp.p, kc, t.out_sorted.p, out);
     EB_CHECK_LAUNCH();
 }
 

@@ -116,6 +116,7 @@ struct Tree {
     DBuf<double> phid_scale, phiu_scale; // half-width r of the box of each PHI row
     std::vector<int> up_lstart, dn_lstart;  // per level: first Z / W row (rows are level-major)
     bool use_tc = true;                  // tcgen05 3xTF32 translations (else SIMT fp32)
+    bool far64 = false;                  // L2T / M2T in fp64 (set for p >= 9 and by the BEM operator)
 
     // profiling (fmm_set_profiling / fmm_phase_stats)
     static constexpr int NPHASE = 10;
@@ -136,7 +137,8 @@ struct Tree {
     // workspace (allocated at build time; evaluation allocates nothing)
     DBuf<float4> rec_disp, rec_stress;   // prepared sources, tree order
     DBuf<float> Q;                       // check potentials [max(n_s2m, n_s2l) x mc]
-    DBuf<float> Z, W;                    // [n_up x lde], [n_dn x lde]
+    DBuf<double> Z, W;                   // [n_up x lde], [n_dn x lde] accumulators: fp64 atomics make
+                                         // the sum order-independent at fp32 precision (deterministic)
     DBuf<float> Qb, Qs, Zb, Zs, Wb, Ws;  // TF32 head / remainder copies (B operands)
     CUtensorMap mQb, mQs, mZb, mZs, mWb, mWs;
     DBuf<double> PHID, PHIU;             // [n_phid x me], [n_phiu x me]
@@ -169,18 +171,20 @@ void gemm_f64(int m, int n, int k, double alpha, const double* A, int64_t sA, in
               int batch, cudaStream_t s);
 // pairs GEMM: Y[t] += Mat[op] * X[src] for every pair (t, src) of every op; Mat row-major
 // [M x K]; X rows of length ldx >= K; Y rows of length ldy >= M.  fp32.
-void gemm_pairs_f32(const OpPairs& P, const float* mats, int M, int K, int ldm, const float* X, int ldx,
-                    float* Y, int ldy, cudaStream_t s);
+template <class XT>
+void gemm_pairs_f32(const OpPairs& P, const float* mats, int M, int K, int ldm, const XT* X, int ldx,
+                    double* Y, int ldy, cudaStream_t s);
 // tensor-core path (tc_gemm.cu)
 void tc_make_map_a(CUtensorMap* m, const float* base, int nops, int M, int K, int ld);
 void tc_make_map_b(CUtensorMap* m, const float* base, int64_t rows, int K, int ld);
-void tc_split_rows(const float* X, int ld, int64_t row0, int64_t nrows, int K, float* Xb, float* Xs,
+template <class XT>
+void tc_split_rows(const XT* X, int ld, int64_t row0, int64_t nrows, int K, float* Xb, float* Xs,
                    cudaStream_t s);
 void tc_build_tiles(OpPairs& P, int M);
 void tc_pairs_gemm(const OpPairs& P, const CUtensorMap& Ab, const CUtensorMap& As, const CUtensorMap& Bb,
-                   const CUtensorMap& Bs, int M, int K, float* Y, int ldy, cudaStream_t s);
+                   const CUtensorMap& Bs, int M, int K, double* Y, int ldy, cudaStream_t s);
 // fp64 variant with per-pair scale (r of the box, looked up from scale[t])
-void gemm_pairs_f64(const OpPairs& P, const double* mat, int M, int K, const float* X, int ldx,
+void gemm_pairs_f64(const OpPairs& P, const double* mat, int M, int K, const double* X, int ldx,
                     const double* scale, double* Y, int ldy, cudaStream_t s);
 void build_op_pairs(OpPairs& P, int nops, const std::vector<int>& op, const std::vector<int2>& pr,
                     cudaStream_t s);

@@ -268,10 +268,11 @@ constexpr int PG_M = 64, PG_N = 64, PG_K = 16;
 // Y[t] += Mat[op] X[src] for the 64 pairs of one tile: 64 rows of Mat x 64 pairs.
 // Accumulates with atomicAdd (one pair per target per op, but different ops of the same
 // target land on the same rows).
+template <class XT>
 __global__ void __launch_bounds__(256)
 gemm_pairs_f32_kernel(const int* __restrict__ op_ptr, const int2* __restrict__ pairs, int nops,
-                      const float* __restrict__ mats, int M, int K, int ldm, const float* __restrict__ X,
-                      int ldx, float* __restrict__ Y, int ldy) {
+                      const float* __restrict__ mats, int M, int K, int ldm, const XT* __restrict__ X,
+                      int ldx, double* __restrict__ Y, int ldy) {
     const int op = blockIdx.z;
     const int p0 = op_ptr[op] + blockIdx.y * PG_N;
     const int p1 = op_ptr[op + 1];
@@ -293,7 +294,7 @@ gemm_pairs_f32_kernel(const int* __restrict__ op_ptr, const int2* __restrict__ p
             As[c][r] = (gm < M && gk < K) ? Mt[(int64_t)gm * ldm + gk] : 0.f;
             int j = e / PG_K;                      // pair j, k offset c
             int src = pr[j].y;
-            Bs[c][j] = (src >= 0 && gk < K) ? X[(int64_t)src * ldx + gk] : 0.f;
+            Bs[c][j] = (src >= 0 && gk < K) ? (float)X[(int64_t)src * ldx + gk] : 0.f;
         }
         __syncthreads();
 #pragma unroll
@@ -314,27 +315,32 @@ gemm_pairs_f32_kernel(const int* __restrict__ op_ptr, const int2* __restrict__ p
     for (int j = 0; j < 4; ++j) {
         int pj = tx + 16 * j;
         if (pj >= np) continue;
-        float* y = Y + (int64_t)pr[pj].x * ldy;
+        double* y = Y + (int64_t)pr[pj].x * ldy;
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
             int gm = m0 + ty + 16 * i;
-            if (gm < M) atomicAdd(y + gm, acc[i][j]);
+            if (gm < M) atomicAdd(y + gm, (double)acc[i][j]);
         }
     }
 }
 
-void gemm_pairs_f32(const OpPairs& P, const float* mats, int M, int K, int ldm, const float* X, int ldx,
-                    float* Y, int ldy, cudaStream_t s) {
+template <class XT>
+void gemm_pairs_f32(const OpPairs& P, const float* mats, int M, int K, int ldm, const XT* X, int ldx,
+                    double* Y, int ldy, cudaStream_t s) {
     if (P.npairs == 0) return;
     dim3 grid(ceil_div(M, PG_M), ceil_div(P.max_per_op, PG_N), P.nops);
-    gemm_pairs_f32_kernel<<<grid, 256, 0, s>>>(P.op_ptr.p, P.pairs.p, P.nops, mats, M, K, ldm, X, ldx, Y, ldy);
+    gemm_pairs_f32_kernel<XT><<<grid, 256, 0, s>>>(P.op_ptr.p, P.pairs.p, P.nops, mats, M, K, ldm, X, ldx, Y, ldy);
     EB_CHECK_LAUNCH();
 }
+template void gemm_pairs_f32<float>(const OpPairs&, const float*, int, int, int, const float*, int, double*, int,
+                                    cudaStream_t);
+template void gemm_pairs_f32<double>(const OpPairs&, const float*, int, int, int, const double*, int, double*, int,
+                                     cudaStream_t);
 
 // fp64: Y[t] = scale[t] * Mat X[src] (one op; plain store)
 __global__ void __launch_bounds__(256)
 gemm_pairs_f64_kernel(const int2* __restrict__ pairs, int npairs, const double* __restrict__ Mt, int M,
-                      int K, const float* __restrict__ X, int ldx, const double* __restrict__ scale,
+                      int K, const double* __restrict__ X, int ldx, const double* __restrict__ scale,
                       double* __restrict__ Y, int ldy) {
     const int p0 = blockIdx.y * PG_N;
     const int np = min(PG_N, npairs - p0);
@@ -352,7 +358,7 @@ gemm_pairs_f64_kernel(const int2* __restrict__ pairs, int npairs, const double* 
             int gm = m0 + r, gk = k0 + c;
             As[c][r] = (gm < M && gk < K) ? Mt[(int64_t)gm * K + gk] : 0.0;
             int src = pr[r].y;
-            Bs[c][r] = (src >= 0 && gk < K) ? (double)X[(int64_t)src * ldx + gk] : 0.0;
+            Bs[c][r] = (src >= 0 && gk < K) ? X[(int64_t)src * ldx + gk] : 0.0;
         }
         __syncthreads();
 #pragma unroll
@@ -384,7 +390,7 @@ gemm_pairs_f64_kernel(const int2* __restrict__ pairs, int npairs, const double* 
     }
 }
 
-void gemm_pairs_f64(const OpPairs& P, const double* mat, int M, int K, const float* X, int ldx,
+void gemm_pairs_f64(const OpPairs& P, const double* mat, int M, int K, const double* X, int ldx,
                     const double* scale, double* Y, int ldy, cudaStream_t s) {
     if (P.npairs == 0) return;
     dim3 grid(ceil_div(M, PG_M), ceil_div(P.npairs, PG_N), 1);

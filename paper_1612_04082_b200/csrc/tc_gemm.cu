@@ -142,7 +142,7 @@ __global__ void __launch_bounds__(THREADS, 1)
 tc_pairs_kernel(const __grid_constant__ CUtensorMap mapAb, const __grid_constant__ CUtensorMap mapAs,
                 const __grid_constant__ CUtensorMap mapBb, const __grid_constant__ CUtensorMap mapBs,
                 const Tile* __restrict__ tiles, int ntiles, const int2* __restrict__ pairs, int M, int K,
-                float* __restrict__ Y, int ldy) {
+                double* __restrict__ Y, int ldy) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     // barriers: full[S], empty[S], acc_full[2], acc_empty[2], corr_full[2], corr_empty[2]
@@ -286,7 +286,7 @@ tc_pairs_kernel(const __grid_constant__ CUtensorMap mapAb, const __grid_constant
                 const int2* pp = pairs + tl.p0;
 #pragma unroll
                 for (int j = 0; j < BN; ++j)
-                    if (j < tl.np) atomicAdd(Y + (int64_t)__ldg(&pp[j].x) * ldy + row, acc[j]);
+                    if (j < tl.np) atomicAdd(Y + (int64_t)__ldg(&pp[j].x) * ldy + row, (double)acc[j]);
             }
         }
     }
@@ -304,18 +304,20 @@ __device__ __forceinline__ float to_tf32(float x) {
     asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
     return __uint_as_float(r);
 }
+__device__ __forceinline__ float to_tf32(double x) { return to_tf32((float)x); }
 
 // split fp32 rows into a TF32 head and a TF32 remainder (columns >= K untouched)
-__global__ void split_rows_kernel(const float* __restrict__ X, int ld, int64_t row0, int64_t nrows, int K,
+template <class XT>
+__global__ void split_rows_kernel(const XT* __restrict__ X, int ld, int64_t row0, int64_t nrows, int K,
                                   float* __restrict__ Xb, float* __restrict__ Xs) {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= nrows * K) return;
     const int64_t r = row0 + i / K;
     const int c = (int)(i % K);
-    const float x = X[r * ld + c];
+    const XT x = X[r * ld + c];
     const float b = to_tf32(x);
     Xb[r * ld + c] = b;
-    Xs[r * ld + c] = to_tf32(x - b);
+    Xs[r * ld + c] = to_tf32(x - (XT)b);
 }
 
 // ------------------------------------------------------------------ host side
@@ -361,12 +363,14 @@ void tc_make_map_b(CUtensorMap* m, const float* base, int64_t rows, int K, int l
     EB_REQUIRE(r == CUDA_SUCCESS, "cuTensorMapEncodeTiled (B) failed: " + std::to_string((int)r));
 }
 
-void tc_split_rows(const float* X, int ld, int64_t row0, int64_t nrows, int K, float* Xb, float* Xs,
-                   cudaStream_t s) {
+template <class XT>
+void tc_split_rows(const XT* X, int ld, int64_t row0, int64_t nrows, int K, float* Xb, float* Xs, cudaStream_t s) {
     if (nrows <= 0) return;
-    tc::split_rows_kernel<<<ceil_div(nrows * K, 256), 256, 0, s>>>(X, ld, row0, nrows, K, Xb, Xs);
+    tc::split_rows_kernel<XT><<<ceil_div(nrows * K, 256), 256, 0, s>>>(X, ld, row0, nrows, K, Xb, Xs);
     EB_CHECK_LAUNCH();
 }
+template void tc_split_rows<float>(const float*, int, int64_t, int64_t, int, float*, float*, cudaStream_t);
+template void tc_split_rows<double>(const double*, int, int64_t, int64_t, int, float*, float*, cudaStream_t);
 
 void tc_build_tiles(OpPairs& P, int M) {
     std::vector<tc::Tile> t;
@@ -380,7 +384,7 @@ void tc_build_tiles(OpPairs& P, int M) {
 }
 
 void tc_pairs_gemm(const OpPairs& P, const CUtensorMap& Ab, const CUtensorMap& As, const CUtensorMap& Bb,
-                   const CUtensorMap& Bs, int M, int K, float* Y, int ldy, cudaStream_t s) {
+                   const CUtensorMap& Bs, int M, int K, double* Y, int ldy, cudaStream_t s) {
     if (P.ntiles == 0) return;
     static bool attr = false;
     if (!attr) {

@@ -96,3 +96,14 @@ def test_fmm_kernels_and_separate_targets(eb, kern):
     err = KN.rel_l2(out, ref)
     print("kernel", kern, "rel-L2", err)
     assert err <= 1e-5
+
+
+def test_fmm_deterministic(eb, beam20k):
+    """fp64 accumulation of the translation outputs makes repeated evaluations identical
+    (GMRES needs a consistent operator)."""
+    d, ref = beam20k
+    t = to_dev(d)
+    tree = eb.fmm_build_tree(t["src"], t["nrm"], t["w"], max_pts=64, p=6, K=d["K"], G=d["G"])
+    a = eb.fmm_matvec(tree, eb.KERNEL_UP, t["f"], t["g"]).cpu().numpy()
+    b = eb.fmm_matvec(tree, eb.KERNEL_UP, t["f"], t["g"]).cpu().numpy()
+    assert np.array_equal(a, b)
