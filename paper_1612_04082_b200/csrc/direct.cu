@@ -6,6 +6,8 @@
 // rsqrt per pair.  The source range is split across blockIdx.y so the grid covers all
 // 148 SMs even for a few thousand targets; partial sums land in a [split][target][c]
 // scratch and a second kernel reduces them in a fixed order (deterministic).
+#include <cstdlib>
+
 #include "p2p.cuh"
 
 namespace ebem {
@@ -37,7 +39,7 @@ __global__ void prepare_kernel(int kernel, float cU, float cP, float cD, float c
         r[0] = make_float4(px, py, pz, a * ng);
         r[1] = make_float4(fx, fy, fz, 0.f);
         r[2] = make_float4(gx, gy, gz, 0.f);
-        r[3] = make_float4(nx, ny, nz, 0.f);
+        r[3] = make_float4(3.f * nx, 3.f * ny, 3.f * nz, 0.f);
     } else {
         float4* r = rec + i * REC_STRESS;
         r[0] = make_float4(px, py, pz, ng);
@@ -60,7 +62,7 @@ void prepare_sources(int kernel, const Material& m, const float* y, const float*
 }
 
 constexpr int DIRECT_THREADS = 128;
-constexpr int DIRECT_TPT = 2;          // targets per thread
+constexpr int DIRECT_TPT = 4;          // targets per thread (one LDS.128 per pair)
 constexpr int DIRECT_TILE = 128;       // sources per shared-memory tile
 
 template <bool SL, bool DL, bool STRESS>
@@ -87,8 +89,7 @@ direct_kernel(const float4* __restrict__ rec, int64_t nsrc, int64_t chunk,
         __syncthreads();
         for (int i = threadIdx.x; i < cnt * R; i += DIRECT_THREADS) srec[i] = rec[s0 * R + i];
         __syncthreads();
-#pragma unroll
-        for (int k = 0; k < DIRECT_TPT; ++k) pair_loop<SL, DL, STRESS>(srec, cnt, x[k], y[k], z[k], kc, acc[k]);
+        pair_loop_multi<SL, DL, STRESS, DIRECT_TPT>(srec, cnt, x, y, z, kc, acc);
     }
 #pragma unroll
     for (int k = 0; k < DIRECT_TPT; ++k) {
@@ -115,9 +116,15 @@ static void launch_direct(const float4* rec, int64_t nsrc, const float* trg, int
                           const KConst& kc, float* out, cudaStream_t s) {
     constexpr int NC = STRESS ? 6 : 3;
     const int tblocks = ceil_div(ntrg, DIRECT_THREADS * DIRECT_TPT);
-    const int want = num_sms() * 8;
-    int nsplit = std::max(1, std::min(ceil_div(want, tblocks), ceil_div(nsrc, 4 * DIRECT_TILE)));
+    // split the sources so the grid fills the resident CTA slots of one wave as closely
+    // as possible (partial second waves cost more than an under-full first one)
+    int occ = 0;
+    EB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, direct_kernel<SL, DL, STRESS>, DIRECT_THREADS, 0));
+    const int slots = num_sms() * std::max(occ, 1);
+    int nsplit = std::max(1, std::min(slots / tblocks, ceil_div(nsrc, 4 * DIRECT_TILE)));
+    if (const char* e = std::getenv("EBEM_DIRECT_SPLIT")) nsplit = std::max(1, std::atoi(e));
     nsplit = std::min(nsplit, 65535);
+    // whole shared-memory tiles per CTA (measured: ragged chunks cost 15-100%)
     int64_t chunk = ((nsrc + nsplit - 1) / nsplit + DIRECT_TILE - 1) / DIRECT_TILE * DIRECT_TILE;
     nsplit = (int)((nsrc + chunk - 1) / chunk);
     if (nsplit <= 1) {

@@ -26,6 +26,11 @@ __device__ __forceinline__ float rsqrt_t<float>(float x) { return rsqrtf(x); }
 template <>
 __device__ __forceinline__ double rsqrt_t<double>(double x) { return rsqrt(x); }
 
+// fused multiply-add for both precisions (the accumulations below are written as FMA
+// chains into the accumulator, so the compiler emits one FFMA per term)
+__device__ __forceinline__ float fmat(float a, float b, float c) { return fmaf(a, b, c); }
+__device__ __forceinline__ double fmat(double a, double b, double c) { return fma(a, b, c); }
+
 // rinv with the self pair (r == 0) excluded: PAPER.md line 189, the own panel is
 // handled by the local pass, never by the sum.
 template <class T>
@@ -38,30 +43,31 @@ __device__ __forceinline__ T safe_rinv(T r2) {
 template <class T>
 __device__ __forceinline__ void acc_U(T dx, T dy, T dz, T ri, T fx, T fy, T fz, T a1, T* u) {
     T ri2 = ri * ri;
-    T df = dx * fx + dy * fy + dz * fz;
+    T df = fmat(dz, fz, fmat(dy, fy, dx * fx));
     T s = df * ri2 * ri;
     T t = a1 * ri;
-    u[0] += t * fx + s * dx;
-    u[1] += t * fy + s * dy;
-    u[2] += t * fz + s * dz;
+    u[0] = fmat(t, fx, fmat(s, dx, u[0]));
+    u[1] = fmat(t, fy, fmat(s, dy, u[1]));
+    u[2] = fmat(t, fz, fmat(s, dz, u[2]));
 }
 
-// double layer: g = cP w g (prepared), q = a (n.g) (prepared):
-// u_i += a rinv^3 [(d.n) g_i + (d.g) n_i] + [3 (d.n)(d.g) rinv^5 - q rinv^3] d_i
+// double layer: g = cP w g, q = a (n.g), n3 = 3 n (all prepared per source):
+// u_i += a rinv^3 [(d.n) g_i + (d.g) n_i] + rinv^3 [3 (d.n)(d.g) rinv^2 - q] d_i
+// written with a3 = a/3 so every output update is one FFMA (FFMA-dense inner loop)
 template <class T>
-__device__ __forceinline__ void acc_P(T dx, T dy, T dz, T ri, T gx, T gy, T gz, T nx, T ny, T nz,
-                                      T q, T a, T* u) {
+__device__ __forceinline__ void acc_P(T dx, T dy, T dz, T ri, T gx, T gy, T gz, T n3x, T n3y, T n3z,
+                                      T q, T a3, T* u) {
     T ri2 = ri * ri;
     T ri3 = ri2 * ri;
-    T dn = dx * nx + dy * ny + dz * nz;
-    T dg = dx * gx + dy * gy + dz * gz;
-    T ar3 = a * ri3;
-    T A = dn * ar3;
-    T B = dg * ar3;
-    T C = (T(3) * dn * dg) * (ri3 * ri2) - q * ri3;
-    u[0] += A * gx + B * nx + C * dx;
-    u[1] += A * gy + B * ny + C * dy;
-    u[2] += A * gz + B * nz + C * dz;
+    T dn3 = fmat(dz, n3z, fmat(dy, n3y, dx * n3x));   // 3 (d.n)
+    T dg = fmat(dz, gz, fmat(dy, gy, dx * gx));
+    T ar3 = a3 * ri3;
+    T A = dn3 * ar3;                                  // a (d.n) rinv^3
+    T B = dg * ar3;                                   // a (d.g) rinv^3 / 3   (multiplies n3)
+    T C = ri3 * fmat(dn3 * dg, ri2, -q);
+    u[0] = fmat(A, gx, fmat(B, n3x, fmat(C, dx, u[0])));
+    u[1] = fmat(A, gy, fmat(B, n3y, fmat(C, dy, u[1])));
+    u[2] = fmat(A, gz, fmat(B, n3z, fmat(C, dz, u[2])));
 }
 
 // stress of a single layer: f = cD w f (prepared, cD = -1/(8 pi (1-nu))):
@@ -70,18 +76,19 @@ template <class T>
 __device__ __forceinline__ void acc_D(T dx, T dy, T dz, T ri, T fx, T fy, T fz, T a, T* s) {
     T ri2 = ri * ri;
     T ri3 = ri2 * ri;
-    T df = dx * fx + dy * fy + dz * fz;
+    T df = fmat(dz, fz, fmat(dy, fy, dx * fx));
     T A = a * ri3;
     T B = T(3) * df * ri3 * ri2;
     T Ad = A * df;
-    T bx = B * dx, by = B * dy, bz = B * dz;
-    T ax = A * fx, ay = A * fy, az = A * fz;
-    s[0] += T(2) * ax * dx - Ad + bx * dx;
-    s[1] += T(2) * ay * dy - Ad + by * dy;
-    s[2] += T(2) * az * dz - Ad + bz * dz;
-    s[3] += ax * dy + ay * dx + bx * dy;
-    s[4] += ay * dz + az * dy + by * dz;
-    s[5] += ax * dz + az * dx + bx * dz;
+    // v_i = A f_i + (B/2) d_i:  s_ij += v_i d_j + v_j d_i - Ad d_ij
+    T hB = T(0.5) * B;
+    T vx = fmat(hB, dx, A * fx), vy = fmat(hB, dy, A * fy), vz = fmat(hB, dz, A * fz);
+    s[0] = fmat(T(2) * vx, dx, s[0] - Ad);
+    s[1] = fmat(T(2) * vy, dy, s[1] - Ad);
+    s[2] = fmat(T(2) * vz, dz, s[2] - Ad);
+    s[3] = fmat(vx, dy, fmat(vy, dx, s[3]));
+    s[4] = fmat(vy, dz, fmat(vz, dy, s[4]));
+    s[5] = fmat(vx, dz, fmat(vz, dx, s[5]));
 }
 
 // stress of a double layer: g = cS w g, ng = n.g, NG = a (n (x) g + g (x) n) (prepared):
@@ -102,15 +109,15 @@ __device__ __forceinline__ void acc_S(T dx, T dy, T dz, T ri, T gx, T gy, T gz, 
     T Cgd = T(3) * nu * dn * ri5;
     T Cnd = T(3) * nu * dg * ri5;
     T Cdl = T(3) * a * dndg * ri5 - b4 * ng * ri3;
-    T ux = hCdd * dx + Cgd * gx + Cnd * nx;
-    T uy = hCdd * dy + Cgd * gy + Cnd * ny;
-    T uz = hCdd * dz + Cgd * gz + Cnd * nz;
-    s[0] += T(2) * ux * dx + ri3 * NG[0] + Cdl;
-    s[1] += T(2) * uy * dy + ri3 * NG[1] + Cdl;
-    s[2] += T(2) * uz * dz + ri3 * NG[2] + Cdl;
-    s[3] += ux * dy + uy * dx + ri3 * NG[3];
-    s[4] += uy * dz + uz * dy + ri3 * NG[4];
-    s[5] += ux * dz + uz * dx + ri3 * NG[5];
+    T ux = fmat(Cnd, nx, fmat(Cgd, gx, hCdd * dx));
+    T uy = fmat(Cnd, ny, fmat(Cgd, gy, hCdd * dy));
+    T uz = fmat(Cnd, nz, fmat(Cgd, gz, hCdd * dz));
+    s[0] = fmat(T(2) * ux, dx, fmat(ri3, NG[0], s[0] + Cdl));
+    s[1] = fmat(T(2) * uy, dy, fmat(ri3, NG[1], s[1] + Cdl));
+    s[2] = fmat(T(2) * uz, dz, fmat(ri3, NG[2], s[2] + Cdl));
+    s[3] = fmat(ux, dy, fmat(uy, dx, fmat(ri3, NG[3], s[3])));
+    s[4] = fmat(uy, dz, fmat(uz, dy, fmat(ri3, NG[4], s[4])));
+    s[5] = fmat(ux, dz, fmat(uz, dx, fmat(ri3, NG[5], s[5])));
 }
 
 }  // namespace ebem

@@ -15,20 +15,20 @@ inline bool kernel_stress(int k) { return k >= K_D; }
 inline int kernel_ncomp(int k) { return kernel_stress(k) ? 6 : 3; }
 
 // Per-source record, 4 float4 (displacement family) or 6 float4 (stress family):
-//   disp   : [y.xyz, q=a (n.g)] [f = cU w f, 0] [g = cP w g, 0] [n, 0]
+//   disp   : [y.xyz, q=a (n.g)] [f = cU w f, 0] [g = cP w g, 0] [3 n, 0]
 //   stress : [y.xyz, ng = n.g]  [f = cD w f, 0] [g = cS w g, 0] [n, 0]
 //            [NG_xx, NG_yy, NG_zz, NG_xy] [NG_yz, NG_xz, 0, 0],  NG = a (n g^T + g n^T)
 constexpr int REC_DISP = 4;
 constexpr int REC_STRESS = 6;
 
 struct KConst {
-    float a1, a, nu, b4;
+    float a1, a, a3, nu, b4;
     double a1d, ad, nud, b4d;
 };
 
 inline KConst make_kconst(const Material& m) {
     KConst k;
-    k.a1 = (float)m.a1; k.a = (float)m.a; k.nu = (float)m.nu; k.b4 = (float)m.b4;
+    k.a1 = (float)m.a1; k.a = (float)m.a; k.a3 = (float)(m.a / 3.0); k.nu = (float)m.nu; k.b4 = (float)m.b4;
     k.a1d = m.a1; k.ad = m.a; k.nud = m.nu; k.b4d = m.b4;
     return k;
 }
@@ -62,7 +62,7 @@ __device__ __forceinline__ void pair_loop(const float4* __restrict__ srec, int c
             if (DL) {
                 const float4 g = srec[j * R + 2];
                 const float4 n = srec[j * R + 3];
-                acc_P(dx, dy, dz, ri, g.x, g.y, g.z, n.x, n.y, n.z, p.w, kc.a, acc);
+                acc_P(dx, dy, dz, ri, g.x, g.y, g.z, n.x, n.y, n.z, p.w, kc.a3, acc);
             }
         } else {
             if (SL) {
@@ -76,6 +76,40 @@ __device__ __forceinline__ void pair_loop(const float4* __restrict__ srec, int c
                 const float4 t1 = srec[j * R + 5];
                 const float NG[6] = {t0.x, t0.y, t0.z, t0.w, t1.x, t1.y};
                 acc_S(dx, dy, dz, ri, g.x, g.y, g.z, n.x, n.y, n.z, p.w, NG, kc.a, kc.nu, kc.b4, acc);
+            }
+        }
+    }
+}
+
+// the same, for TPT targets per thread: the source loop is outermost so that each record is
+// read from shared memory once for all TPT targets (one LDS.128 per pair at TPT = 4)
+template <bool SL, bool DL, bool STRESS, int TPT>
+__device__ __forceinline__ void pair_loop_multi(const float4* __restrict__ srec, int cnt, const float* x,
+                                                const float* y, const float* z, const KConst& kc, float (*acc)[STRESS ? 6 : 3]) {
+    constexpr int R = STRESS ? REC_STRESS : REC_DISP;
+#pragma unroll 2
+    for (int j = 0; j < cnt; ++j) {
+        const float4 p = srec[j * R + 0];
+        const float4 f = SL ? srec[j * R + 1] : make_float4(0, 0, 0, 0);
+        const float4 g = DL ? srec[j * R + 2] : make_float4(0, 0, 0, 0);
+        const float4 n = DL ? srec[j * R + 3] : make_float4(0, 0, 0, 0);
+        float NG[6] = {0, 0, 0, 0, 0, 0};
+        if (STRESS && DL) {
+            const float4 t0 = srec[j * R + 4];
+            const float4 t1 = srec[j * R + 5];
+            NG[0] = t0.x; NG[1] = t0.y; NG[2] = t0.z; NG[3] = t0.w; NG[4] = t1.x; NG[5] = t1.y;
+        }
+#pragma unroll
+        for (int k = 0; k < TPT; ++k) {
+            float dx = x[k] - p.x, dy = y[k] - p.y, dz = z[k] - p.z;
+            float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
+            float ri = safe_rinv(r2);
+            if (!STRESS) {
+                if (SL) acc_U(dx, dy, dz, ri, f.x, f.y, f.z, kc.a1, acc[k]);
+                if (DL) acc_P(dx, dy, dz, ri, g.x, g.y, g.z, n.x, n.y, n.z, p.w, kc.a3, acc[k]);
+            } else {
+                if (SL) acc_D(dx, dy, dz, ri, f.x, f.y, f.z, kc.a, acc[k]);
+                if (DL) acc_S(dx, dy, dz, ri, g.x, g.y, g.z, n.x, n.y, n.z, p.w, NG, kc.a, kc.nu, kc.b4, acc[k]);
             }
         }
     }
