@@ -34,23 +34,31 @@ struct BoxGeo {
 // sources of boxes sidx[soff[i] .. soff[i+1]) (or of tbox[i] itself when soff is null).
 // Output Q[i][3 nc] (fp32).  PAPER.md line 147: the approximation sum_i phi_i K(x_i, y)
 // is fitted to the sources' field on a check surface.
-constexpr int CP_T = 128, CP_TILE = 64;
+constexpr int CP_T = 256, CP_TILE = 64;
 
-template <bool SL, bool DL>
+// one thread per check point (KPT points per thread when the surface has more than CP_T),
+// accumulators in registers, sources streamed through shared memory
+template <bool SL, bool DL, int KPT>
 __global__ void __launch_bounds__(CP_T)
 check_potential_kernel(const int* __restrict__ tbox, const int* __restrict__ soff, const int* __restrict__ sidx,
                        const int* __restrict__ sbeg, const int* __restrict__ send, const int* __restrict__ anchor,
                        const int* __restrict__ level, BoxGeo geo, double rad, const float* __restrict__ sc, int nc,
                        const float4* __restrict__ rec, KConst kc, float* __restrict__ Q, int ldq) {
-    extern __shared__ float smem[];
-    float* acc = smem;                                                  // [3 nc]
-    float4* srec = reinterpret_cast<float4*>(smem + ((3 * nc + 3) & ~3));   // [CP_TILE * 4]
+    __shared__ float4 srec[CP_TILE * REC_DISP];
     const int i = blockIdx.x;
     const int b = tbox[i];
     double cx, cy, cz, r;
     geo.center(anchor, level, b, cx, cy, cz, r);
     const float R = (float)(rad * r);
-    for (int k = threadIdx.x; k < 3 * nc; k += CP_T) acc[k] = 0.f;
+    float x[KPT], y[KPT], z[KPT], acc[KPT][3];
+#pragma unroll
+    for (int q = 0; q < KPT; ++q) {
+        const int k = min((int)threadIdx.x + q * CP_T, nc - 1);
+        x[q] = (float)cx + R * sc[3 * k];
+        y[q] = (float)cy + R * sc[3 * k + 1];
+        z[q] = (float)cz + R * sc[3 * k + 2];
+        acc[q][0] = acc[q][1] = acc[q][2] = 0.f;
+    }
     const int e0 = soff ? soff[i] : 0, e1 = soff ? soff[i + 1] : 1;
     for (int e = e0; e < e1; ++e) {
         const int a = soff ? sidx[e] : b;
@@ -59,18 +67,19 @@ check_potential_kernel(const int* __restrict__ tbox, const int* __restrict__ sof
             __syncthreads();
             for (int q = threadIdx.x; q < cnt * REC_DISP; q += CP_T) srec[q] = rec[(int64_t)s0 * REC_DISP + q];
             __syncthreads();
-            for (int k = threadIdx.x; k < nc; k += CP_T) {
-                float u[3] = {0.f, 0.f, 0.f};
-                float x = (float)cx + R * sc[3 * k], y = (float)cy + R * sc[3 * k + 1], z = (float)cz + R * sc[3 * k + 2];
-                pair_loop<SL, DL, false>(srec, cnt, x, y, z, kc, u);
-                acc[3 * k] += u[0];
-                acc[3 * k + 1] += u[1];
-                acc[3 * k + 2] += u[2];
-            }
+            pair_loop_multi<SL, DL, false, KPT>(srec, cnt, x, y, z, kc, acc);
         }
     }
-    __syncthreads();
-    for (int k = threadIdx.x; k < 3 * nc; k += CP_T) Q[(int64_t)i * ldq + k] = acc[k];
+#pragma unroll
+    for (int q = 0; q < KPT; ++q) {
+        const int k = threadIdx.x + q * CP_T;
+        if (k < nc) {
+            float* o = Q + (int64_t)i * ldq + 3 * k;
+            o[0] = acc[q][0];
+            o[1] = acc[q][1];
+            o[2] = acc[q][2];
+        }
+    }
 }
 
 // ------------------------------------------------------------------ leaf evaluation
@@ -470,10 +479,19 @@ static void launch_check(const Tree& t, const int* tbox, int n, const int* soff,
     if (n == 0) return;
     const Plan& P = *t.plan;
     BoxGeo geo{t.origin[0], t.origin[1], t.origin[2], t.side};
-    size_t sm = sizeof(float) * ((3 * P.nc + 3) & ~3) + sizeof(float4) * CP_TILE * REC_DISP;
     KConst kc = make_kconst(t.mat);
-    check_potential_kernel<SL, DL><<<n, CP_T, sm, s>>>(tbox, soff, sidx, t.sbeg.p, t.send.p, t.anchor.p, t.level.p,
-                                                       geo, rad, P.s_c.p, P.nc, t.rec_disp.p, kc, t.Q.p, P.ldc);
+    const int kpt = ceil_div(P.nc, CP_T);
+#define EB_CHECK_LAUNCH_KPT(K)                                                                                     \
+    check_potential_kernel<SL, DL, K><<<n, CP_T, 0, s>>>(tbox, soff, sidx, t.sbeg.p, t.send.p, t.anchor.p,         \
+                                                         t.level.p, geo, rad, P.s_c.p, P.nc, t.rec_disp.p, kc,    \
+                                                         t.Q.p, P.ldc)
+    switch (kpt) {
+        case 1: EB_CHECK_LAUNCH_KPT(1); break;
+        case 2: EB_CHECK_LAUNCH_KPT(2); break;
+        case 3: EB_CHECK_LAUNCH_KPT(3); break;
+        default: EB_REQUIRE(kpt <= 4, "check surface too large"); EB_CHECK_LAUNCH_KPT(4); break;
+    }
+#undef EB_CHECK_LAUNCH_KPT
     EB_CHECK_LAUNCH();
 }
 

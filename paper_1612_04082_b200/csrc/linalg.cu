@@ -337,7 +337,7 @@ template void gemm_pairs_f32<float>(const OpPairs&, const float*, int, int, int,
 template void gemm_pairs_f32<double>(const OpPairs&, const float*, int, int, int, const double*, int, double*, int,
                                      cudaStream_t);
 
-// fp64: Y[t] = scale[t] * Mat X[src] (one op; plain store)
+// fp64: Y[t] = scale[t] * Mat X[src] (one op; plain store; Mat upper triangular)
 __global__ void __launch_bounds__(256)
 gemm_pairs_f64_kernel(const int2* __restrict__ pairs, int npairs, const double* __restrict__ Mt, int M,
                       int K, const double* __restrict__ X, int ldx, const double* __restrict__ scale,
@@ -352,7 +352,8 @@ gemm_pairs_f64_kernel(const int2* __restrict__ pairs, int npairs, const double* 
     __syncthreads();
     const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
     double acc[4][4] = {};
-    for (int k0 = 0; k0 < K; k0 += PG_K) {
+    // Mt is upper triangular (R^-1): rows m0.. only see columns k >= m0
+    for (int k0 = (m0 / PG_K) * PG_K; k0 < K; k0 += PG_K) {
         for (int e = threadIdx.x; e < PG_K * PG_M; e += 256) {
             int r = e / PG_K, c = e % PG_K;
             int gm = m0 + r, gk = k0 + c;
