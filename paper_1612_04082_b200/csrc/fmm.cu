@@ -439,6 +439,7 @@ void schedule_tree(Tree& t, cudaStream_t s) {
     t.W.alloc((size_t)std::max(1, t.n_dn) * lde);
     if (const char* e = std::getenv("EBEM_SIMT")) t.use_tc = std::atoi(e) == 0;
     t.far64 = P.p >= FAR_FP64_MIN_P;
+    t.tc_fast = t.use_tc && !t.far64 && !(std::getenv("EBEM_TC_PRECISE") && std::atoi(std::getenv("EBEM_TC_PRECISE")));
     if (t.use_tc) {
         t.Qb.alloc(t.Q.n); t.Qs.alloc(t.Q.n);
         t.Zb.alloc(t.Z.n); t.Zs.alloc(t.Z.n);
@@ -450,11 +451,11 @@ void schedule_tree(Tree& t, cudaStream_t s) {
         tc_make_map_b(&t.mZs, t.Zs.p, std::max(1, t.n_up), me, lde);
         tc_make_map_b(&t.mWb, t.Wb.p, std::max(1, t.n_dn), me, lde);
         tc_make_map_b(&t.mWs, t.Ws.p, std::max(1, t.n_dn), me, lde);
-        tc_build_tiles(t.q2z_up, me);
-        tc_build_tiles(t.q2z_dn, me);
-        tc_build_tiles(t.m2l, me);
-        for (auto& x : t.m2m) tc_build_tiles(x, me);
-        for (auto& x : t.l2l) tc_build_tiles(x, me);
+        tc_build_tiles(t.q2z_up, me, false);
+        tc_build_tiles(t.q2z_dn, me, false);
+        tc_build_tiles(t.m2l, me, t.tc_fast);
+        for (auto& x : t.m2m) tc_build_tiles(x, me, false);
+        for (auto& x : t.l2l) tc_build_tiles(x, me, false);
     }
     t.PHID.alloc((size_t)std::max(1, t.n_phid) * me);
     t.out_sorted.alloc((size_t)std::max<int64_t>(1, t.ntrg) * 6);
@@ -589,7 +590,8 @@ void fmm_evaluate(Tree& t, int kernel, const float* f, const float* g, float* ou
         }
     }
     mark(phase++);
-    if (t.use_tc) tc_pairs_gemm(t.m2l, P.mM2L_b, P.mM2L_s, t.mZb, t.mZs, me, me, t.W.p, lde, s);
+    if (t.use_tc && t.tc_fast) tc_pairs_gemm_fast(t.m2l, P.mM2L_b, P.mM2L_s, t.Zb.p, t.Zs.p, lde, me, me, t.W.p, lde, s);
+    else if (t.use_tc) tc_pairs_gemm(t.m2l, P.mM2L_b, P.mM2L_s, t.mZb, t.mZs, me, me, t.W.p, lde, s);
     else gemm_pairs_f32(t.m2l, P.M2L.p, me, me, lde, t.Z.p, lde, t.W.p, lde, s);
     mark(phase++);
     for (int l = 3; l < t.nlevels; ++l) {

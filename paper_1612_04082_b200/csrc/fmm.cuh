@@ -117,6 +117,7 @@ struct Tree {
     std::vector<int> up_lstart, dn_lstart;  // per level: first Z / W row (rows are level-major)
     bool use_tc = true;                  // tcgen05 3xTF32 translations (else SIMT fp32)
     bool far64 = false;                  // L2T / M2T in fp64 (set for p >= 9 and by the BEM operator)
+    bool tc_fast = false;                // p <= 8 plain matvec: two-slice full-K tensor-core kernel
 
     // profiling (fmm_set_profiling / fmm_phase_stats)
     static constexpr int NPHASE = 10;
@@ -180,7 +181,9 @@ void tc_make_map_b(CUtensorMap* m, const float* base, int64_t rows, int K, int l
 template <class XT>
 void tc_split_rows(const XT* X, int ld, int64_t row0, int64_t nrows, int K, float* Xb, float* Xs,
                    cudaStream_t s);
-void tc_build_tiles(OpPairs& P, int M);
+void tc_build_tiles(OpPairs& P, int M, bool fast);
+void tc_pairs_gemm_fast(const OpPairs& P, const CUtensorMap& Ab, const CUtensorMap& As, const float* Bb,
+                        const float* Bs, int ldb, int M, int K, double* Y, int ldy, cudaStream_t s);
 void tc_pairs_gemm(const OpPairs& P, const CUtensorMap& Ab, const CUtensorMap& As, const CUtensorMap& Bb,
                    const CUtensorMap& Bs, int M, int K, double* Y, int ldy, cudaStream_t s);
 // fp64 variant with per-pair scale (r of the box, looked up from scale[t])

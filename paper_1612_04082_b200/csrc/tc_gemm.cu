@@ -295,6 +295,180 @@ tc_pairs_kernel(const __grid_constant__ CUtensorMap mapAb, const __grid_constant
     if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
 }
 
+// ------------------------------------------------------------------ fast variant (p <= 8)
+// Same contraction, tuned for throughput where the full-K tensor-core accumulation chain
+// (error ~1e-6 relative, see the precise kernel's note) is far below the FMM truncation
+// error: each CTA tile is TWO 128-row operator slices x 128 pairs, so the gathered B rows
+// (the expensive, L2-missing operand) are loaded once for 256 output rows, each K chunk
+// carries 24 MMAs (half the per-stage pipeline overhead per MMA), and whole-K accumulators
+// live in TMEM (2 tiles in flight = 4 x 128 columns) read straight into the atomics.
+// B comes from the precomputed TF32 head/remainder copies by coalesced 16-B cp.async
+// (8 lanes per 128-B row piece): a TMA gather4 issues only ~1 per 32 cycles per SM.
+namespace fast {
+constexpr int MT = 2;                                   // operator row slices per CTA tile
+constexpr int STAGES = 2;
+constexpr int STAGE_BYTES = (2 * MT + 2) * OPND_BYTES;  // A_b,A_s per slice + B_b,B_s = 96 KB
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256;
+constexpr int TMEM_COLS = 512;                          // 2 tiles x MT slices x 128 columns
+}  // namespace fast
+
+__global__ void __launch_bounds__(THREADS, 1)
+tc_pairs_fast_kernel(const __grid_constant__ CUtensorMap mapAb, const __grid_constant__ CUtensorMap mapAs,
+                     const float* __restrict__ Bb, const float* __restrict__ Bs, int ldb,
+                     const Tile* __restrict__ tiles, int ntiles, const int2* __restrict__ pairs, int M, int K,
+                     double* __restrict__ Y, int ldy) {
+    constexpr int MT = fast::MT, STAGES = fast::STAGES, STAGE_BYTES = fast::STAGE_BYTES, TMEM_COLS = fast::TMEM_COLS;
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    uint64_t* bars = (uint64_t*)(smem + STAGES * STAGE_BYTES);
+    uint64_t* full_b = bars;                     // [STAGES]
+    uint64_t* empty_b = bars + STAGES;           // [STAGES]
+    uint64_t* accf_b = bars + 2 * STAGES;        // [2]
+    uint64_t* acce_b = bars + 2 * STAGES + 2;    // [2]
+    uint32_t* tmem_slot = (uint32_t*)(bars + 2 * STAGES + 4);
+    __shared__ int s_src[BN];
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nk = (K + BK - 1) / BK;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(smem_u32(&full_b[s]), 1 + 32);    // A expect_tx + 32 cp.async arrivals
+            mbar_init(smem_u32(&empty_b[s]), 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(smem_u32(&accf_b[b]), 1);
+            mbar_init(smem_u32(&acce_b[b]), 4);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 2) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(TMEM_COLS));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        // ---------------- producer
+        const int piece = lane & 7, rsub = lane >> 3;
+        int c = 0;
+        for (int ti = blockIdx.x; ti < ntiles; ti += gridDim.x) {
+            const Tile tl = tiles[ti];
+            __syncwarp();
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int r = lane + 32 * q;
+                s_src[r] = pairs[tl.p0 + min(r, tl.np - 1)].y;
+            }
+            __syncwarp();
+            for (int kc = 0; kc < nk; ++kc, ++c) {
+                const int s = c % STAGES;
+                mbar_wait(smem_u32(&empty_b[s]), ((c / STAGES) & 1) ^ 1);
+                uint8_t* st = smem + s * STAGE_BYTES;
+                const uint32_t full = smem_u32(&full_b[s]);
+                if (lane == 0) {
+                    mbar_expect_tx(full, 2 * MT * OPND_BYTES);
+#pragma unroll
+                    for (int mt = 0; mt < MT; ++mt) {
+                        tma_load_3d(smem_u32(st + (2 * mt) * OPND_BYTES), &mapAb, kc * BK, tl.m0 + mt * BM, tl.op, full);
+                        tma_load_3d(smem_u32(st + (2 * mt + 1) * OPND_BYTES), &mapAs, kc * BK, tl.m0 + mt * BM, tl.op,
+                                    full);
+                    }
+                }
+                const int col = kc * BK + 4 * piece;
+                const uint32_t nb = col < ldb ? 16u : 0u;      // zero-fill past the row
+                const uint32_t b0 = smem_u32(st + 2 * MT * OPND_BYTES);
+                const uint32_t b1 = b0 + OPND_BYTES;
+#pragma unroll 4
+                for (int j = 0; j < BN / 4; ++j) {
+                    const int r = rsub + 4 * j;
+                    const int64_t off = (int64_t)s_src[r] * ldb + col;
+                    const uint32_t so = (uint32_t)(r * 128 + ((piece ^ (r & 7)) * 16));
+                    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(b0 + so),
+                                 "l"(nb ? Bb + off : Bb), "r"(nb)
+                                 : "memory");
+                    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(b1 + so),
+                                 "l"(nb ? Bs + off : Bs), "r"(nb)
+                                 : "memory");
+                }
+                asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(full) : "memory");
+            }
+        }
+    } else if (warp == 1) {
+        // ---------------- MMA issuer
+        const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BN >> 3) << 17) |
+                               ((uint32_t)(BM >> 4) << 24);
+        int c = 0, it = 0;
+        for (int ti = blockIdx.x; ti < ntiles; ti += gridDim.x, ++it) {
+            const int ab = it & 1;
+            mbar_wait(smem_u32(&acce_b[ab]), ((it >> 1) & 1) ^ 1);
+            asm volatile("tcgen05.fence::after_thread_sync;");
+            for (int kc = 0; kc < nk; ++kc, ++c) {
+                const int s = c % STAGES;
+                mbar_wait(smem_u32(&full_b[s]), (c / STAGES) & 1);
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // cp.async data -> tensor core
+                asm volatile("tcgen05.fence::after_thread_sync;");
+                if (lane == 0) {
+                    const uint32_t st = smem_u32(smem + s * STAGE_BYTES);
+                    const uint64_t bb = smem_desc(st + 2 * MT * OPND_BYTES), bs = smem_desc(st + (2 * MT + 1) * OPND_BYTES);
+                    const int ksteps = min(BK, K - kc * BK + 7) / 8;
+                    for (int k = 0; k < ksteps; ++k) {
+                        const uint64_t off = (uint64_t)(2 * k);
+#pragma unroll
+                        for (int mt = 0; mt < MT; ++mt) {
+                            const uint64_t a_b = smem_desc(st + (2 * mt) * OPND_BYTES) + off;
+                            const uint64_t a_s = smem_desc(st + (2 * mt + 1) * OPND_BYTES) + off;
+                            const uint32_t d = tmem + (uint32_t)((ab * MT + mt) * BN);
+                            mma_tf32(d, a_b, bb + off, idesc, (kc | k) != 0);
+                            mma_tf32(d, a_b, bs + off, idesc, 1);
+                            mma_tf32(d, a_s, bb + off, idesc, 1);
+                        }
+                    }
+                    mma_commit(smem_u32(&empty_b[s]));
+                    if (kc == nk - 1) mma_commit(smem_u32(&accf_b[ab]));
+                }
+                __syncwarp();
+            }
+        }
+    } else if (warp >= EPI_WARP0) {
+        // ---------------- epilogue: TMEM -> fp64 atomics, 32 columns at a time
+        const int wq = warp - EPI_WARP0;
+        int it = 0;
+        for (int ti = blockIdx.x; ti < ntiles; ti += gridDim.x, ++it) {
+            const Tile tl = tiles[ti];
+            const int ab = it & 1;
+            mbar_wait(smem_u32(&accf_b[ab]), (it >> 1) & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;");
+            const int2* pp = pairs + tl.p0;
+#pragma unroll
+            for (int mt = 0; mt < MT; ++mt) {
+                const int row = tl.m0 + mt * BM + 32 * wq + lane;
+#pragma unroll 1
+                for (int c0 = 0; c0 < BN; c0 += 32) {
+                    uint32_t v[32];
+                    tmem_ld32(tmem + ((uint32_t)(32 * wq) << 16) + (uint32_t)((ab * MT + mt) * BN + c0), v);
+                    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                    if (row < M) {
+#pragma unroll
+                        for (int j = 0; j < 32; ++j)
+                            if (c0 + j < tl.np)
+                                atomicAdd(Y + (int64_t)__ldg(&pp[c0 + j].x) * ldy + row, (double)__uint_as_float(v[j]));
+                    }
+                }
+            }
+            asm volatile("tcgen05.fence::before_thread_sync;");
+            __syncwarp();
+            if (lane == 0) mbar_arrive(smem_u32(&acce_b[ab]));
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
+}
+
 // round-to-nearest TF32 (low 13 mantissa bits zero): both halves of the split are exact TF32
 // values, so the tensor core's own fp32->tf32 handling (truncation) never applies, and the
 // two rounding errors are unbiased (truncated remainders are one-signed and their dropped
@@ -372,15 +546,31 @@ void tc_split_rows(const XT* X, int ld, int64_t row0, int64_t nrows, int K, floa
 template void tc_split_rows<float>(const float*, int, int64_t, int64_t, int, float*, float*, cudaStream_t);
 template void tc_split_rows<double>(const double*, int, int64_t, int64_t, int, float*, float*, cudaStream_t);
 
-void tc_build_tiles(OpPairs& P, int M) {
+void tc_build_tiles(OpPairs& P, int M, bool fast) {
     std::vector<tc::Tile> t;
+    const int mstep = fast ? tc::fast::MT * tc::BM : tc::BM;
     for (int o = 0; o < P.nops; ++o)
         for (int p0 = P.op_ptr_h[o]; p0 < P.op_ptr_h[o + 1]; p0 += tc::BN)
-            for (int m0 = 0; m0 < M; m0 += tc::BM)
+            for (int m0 = 0; m0 < M; m0 += mstep)
                 t.push_back({o, p0, std::min(tc::BN, P.op_ptr_h[o + 1] - p0), m0});
     P.ntiles = (int)t.size();
     P.tiles.alloc(std::max<size_t>(t.size(), 1) * sizeof(tc::Tile) / sizeof(int));
     if (!t.empty()) EB_CUDA(cudaMemcpy(P.tiles.p, t.data(), t.size() * sizeof(tc::Tile), cudaMemcpyHostToDevice));
+}
+
+void tc_pairs_gemm_fast(const OpPairs& P, const CUtensorMap& Ab, const CUtensorMap& As, const float* Bb,
+                        const float* Bs, int ldb, int M, int K, double* Y, int ldy, cudaStream_t s) {
+    if (P.ntiles == 0) return;
+    static bool attr = false;
+    if (!attr) {
+        EB_CUDA(cudaFuncSetAttribute(tc::tc_pairs_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     tc::fast::SMEM_BYTES));
+        attr = true;
+    }
+    const int grid = std::min(P.ntiles, num_sms());
+    tc::tc_pairs_fast_kernel<<<grid, tc::THREADS, tc::fast::SMEM_BYTES, s>>>(
+        Ab, As, Bb, Bs, ldb, reinterpret_cast<const tc::Tile*>(P.tiles.p), P.ntiles, P.pairs.p, M, K, Y, ldy);
+    EB_CHECK_LAUNCH();
 }
 
 void tc_pairs_gemm(const OpPairs& P, const CUtensorMap& Ab, const CUtensorMap& As, const CUtensorMap& Bb,
