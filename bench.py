@@ -306,12 +306,18 @@ def main():
     phases = eb.fmm_phase_stats(tree, eb.KERNEL_UP)
     eb.fmm_set_profiling(tree, False)
     ph_out = []
+    tensor_phases = ("Q2Z_up", "M2M", "Q2Z_dn", "M2L", "L2L")   # 3xTF32 tcgen05 path
+    pk["tf32x3_tflops"] = pk["tf32_tflops"] / 3.0                # fp32-equivalent peak of 3xTF32
     for ph in phases:
         f64, f32 = ph["flops_fp64"], ph["flops"] - ph["flops_fp64"]
-        tmin = f32 / (pk["fp32_tflops"] * 1e12) + f64 / (pk["fp64_tflops"] * 1e12)   # ALU lower bound (s)
-        tmem = ph["bytes"] / (pk["hbm_gbs"] * 1e9)
         sec = ph["ms"] * 1e-3
-        bound = "alu" if tmin >= tmem else "hbm"
+        tmem = ph["bytes"] / (pk["hbm_gbs"] * 1e9)
+        if ph["name"] in tensor_phases:
+            tmin, bound = ph["flops"] / (pk["tf32x3_tflops"] * 1e12), "tensor"
+        else:
+            tmin, bound = f32 / (pk["fp32_tflops"] * 1e12) + f64 / (pk["fp64_tflops"] * 1e12), "alu"
+        if tmem > tmin:
+            bound = "hbm"
         frac = (max(tmin, tmem) / sec) if sec > 0 else None
         ph_out.append({"name": ph["name"], "ms": ph["ms"], "launches": ph["launches"], "bound": bound,
                        "gflop": ph["flops"] / 1e9, "gflop_fp64": f64 / 1e9, "interactions": ph["interactions"],
@@ -319,7 +325,13 @@ def main():
     dom = max(ph_out, key=lambda x: x["ms"])
     dph = next(p for p in phases if p["name"] == dom["name"])
     sec = dom["ms"] * 1e-3
-    if dom["bound"] == "alu":
+    if dom["bound"] == "tensor":
+        roof = {"bound": "tensor", "phase": dom["name"], "achieved": dph["flops"] / sec / 1e12,
+                "peak": pk["tf32x3_tflops"], "unit": "TFLOP/s", "frac": dph["flops"] / sec / 1e12 / pk["tf32x3_tflops"],
+                "traffic": None,
+                "peak_source": "measured bf16 GEMM / 2 (TF32) / 3 (3xTF32 = fp32-accurate); achieved counts "
+                               "algorithmic fp32 flops 2*M*K per pair"}
+    elif dom["bound"] == "alu":
         f64, f32 = dph["flops_fp64"], dph["flops"] - dph["flops_fp64"]
         peak = dph["flops"] / (f32 / pk["fp32_tflops"] + f64 / pk["fp64_tflops"]) if dph["flops"] else pk["fp32_tflops"]
         roof = {"bound": "alu", "phase": dom["name"], "achieved": dph["flops"] / sec / 1e12, "peak": peak,
