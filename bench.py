@@ -106,6 +106,17 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def max_over_ranks(value, dist=None):
+    """max of a per-rank timing over all ranks (device tensor under NCCL, host under gloo)."""
+    if dist is None or not dist.is_initialized() or dist.get_world_size() == 1:
+        return float(value)
+    import torch
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([float(value)], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 def workload(n):
     from workloads import geometry as geo
     return geo.config2(n=n)
@@ -301,10 +312,7 @@ def main():
     launches = (eb.ebem_launch_count() - launches0) // args.steps
     ms_steps = [a.elapsed_time(b) for a, b in ev]
     ms = float(np.mean(ms_steps))
-    if dist:
-        tt = torch.tensor([ms], device="cuda")
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        ms = float(tt.item())
+    ms = max_over_ranks(ms, dist)
 
     # ---- per-phase device times (native profiler, one more L2-flushed step)
     eb.fmm_set_profiling(tree, True)
