@@ -54,9 +54,12 @@ check_potential_kernel(const int* __restrict__ tbox, const int* __restrict__ sof
 #pragma unroll
     for (int q = 0; q < KPT; ++q) {
         const int k = min((int)threadIdx.x + q * CP_T, nc - 1);
-        x[q] = (float)cx + R * sc[3 * k];
-        y[q] = (float)cy + R * sc[3 * k + 1];
-        z[q] = (float)cz + R * sc[3 * k + 2];
+        // coordinates relative to the box centre: absolute fp32 check points would carry an
+        // error of ulp(|x|), which is not small against a deep box (a level-20 box is
+        // ~1e-6 of the root)
+        x[q] = R * sc[3 * k];
+        y[q] = R * sc[3 * k + 1];
+        z[q] = R * sc[3 * k + 2];
         acc[q][0] = acc[q][1] = acc[q][2] = 0.f;
     }
     const int e0 = soff ? soff[i] : 0, e1 = soff ? soff[i + 1] : 1;
@@ -65,7 +68,15 @@ check_potential_kernel(const int* __restrict__ tbox, const int* __restrict__ sof
         for (int s0 = sbeg[a]; s0 < send[a]; s0 += CP_TILE) {
             const int cnt = min(CP_TILE, send[a] - s0);
             __syncthreads();
-            for (int q = threadIdx.x; q < cnt * REC_DISP; q += CP_T) srec[q] = rec[(int64_t)s0 * REC_DISP + q];
+            for (int q = threadIdx.x; q < cnt * REC_DISP; q += CP_T) {
+                float4 v = rec[(int64_t)s0 * REC_DISP + q];
+                if (q % REC_DISP == 0) {            // source position, shifted in fp64
+                    v.x = (float)((double)v.x - cx);
+                    v.y = (float)((double)v.y - cy);
+                    v.z = (float)((double)v.z - cz);
+                }
+                srec[q] = v;
+            }
             __syncthreads();
             pair_loop_multi<SL, DL, false, KPT>(srec, cnt, x, y, z, kc, acc);
         }
