@@ -23,6 +23,9 @@
  *     target in Voigt order (xx, yy, zz, xy, yz, xz).
  *   - Pairs with r == 0 are excluded (the own panel's singular
  *     contribution is the job of the local pass, not of the sum).
+ *   - Empty inputs: nsrc = 0 gives zero outputs, ntrg = 0 writes nothing; a tree
+ *     needs nsrc + ntrg >= 1 (either may be 0).  Coincident points are allowed: the
+ *     tree stops refining at level 20 and such a leaf may exceed max_pts.
  *   - Material: bulk modulus K > 0 and shear modulus G > 0 (PAPER.md Eq. elast,
  *     line 37); the kernels use nu = (3K - 2G) / (2 (3K + G)).
  *   - Memory: unless stated otherwise, array arguments of one call must be either

@@ -166,3 +166,21 @@ def test_argument_errors_are_reported(eb):
         eb.fmm_matvec(tree, eb.KERNEL_D, F)
     with pytest.raises(eb.EbemError):
         eb.bem_kernel_direct(eb.KERNEL_U, S, S, f=None)
+
+
+def test_empty_inputs(eb):
+    p, n, w, f, g = _rand(500, 16)
+    e3 = np.zeros((0, 3), np.float32)
+    # direct: no sources -> zeros; no targets -> empty output
+    out = eb.bem_kernel_direct(eb.KERNEL_UP, p, e3, nrm=e3, w=np.zeros(0, np.float32), f=e3, g=e3)
+    assert out.shape == (500, 3) and not np.any(np.asarray(out))
+    out = eb.bem_kernel_direct(eb.KERNEL_DS, e3, p, nrm=n, w=w, f=f, g=g)
+    assert np.asarray(out).shape == (0, 6)
+    # FMM: targets without sources, sources without targets
+    tree = eb.fmm_build_tree(e3, e3, np.zeros(0, np.float32), trg=p, max_pts=16, p=4)
+    out = eb.fmm_matvec(tree, eb.KERNEL_UP, e3, e3)
+    assert out.shape == (500, 3) and not np.any(np.asarray(out))
+    tree = eb.fmm_build_tree(p, n, w, trg=e3, max_pts=16, p=4)
+    assert np.asarray(eb.fmm_eval_stress(tree, eb.KERNEL_DS, f, g)).shape == (0, 6)
+    with pytest.raises(eb.EbemError):
+        eb.fmm_build_tree(e3, e3, trg=e3, max_pts=16, p=4)
