@@ -310,9 +310,12 @@ constexpr int STAGES = 2;
 constexpr int STAGE_BYTES = (2 * MT + 2) * OPND_BYTES;  // A_b,A_s per slice + B_b,B_s = 96 KB
 constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256;
 constexpr int TMEM_COLS = 512;                          // 2 tiles x MT slices x 128 columns
+constexpr int NPROD = 3;                                // B-gather warps (0, 2, 3); 5 or 7 were no faster
+constexpr int THREADS = 256;
+constexpr int NG = (BN / 4 + NPROD - 1) / NPROD;        // 4-row groups per producer warp
 }  // namespace fast
 
-__global__ void __launch_bounds__(THREADS, 1)
+__global__ void __launch_bounds__(fast::THREADS, 1)
 tc_pairs_fast_kernel(const __grid_constant__ CUtensorMap mapAb, const __grid_constant__ CUtensorMap mapAs,
                      const float* __restrict__ Bb, const float* __restrict__ Bs, int ldb,
                      const Tile* __restrict__ tiles, int ntiles, const int2* __restrict__ pairs, int M, int K,
@@ -326,13 +329,12 @@ tc_pairs_fast_kernel(const __grid_constant__ CUtensorMap mapAb, const __grid_con
     uint64_t* accf_b = bars + 2 * STAGES;        // [2]
     uint64_t* acce_b = bars + 2 * STAGES + 2;    // [2]
     uint32_t* tmem_slot = (uint32_t*)(bars + 2 * STAGES + 4);
-    __shared__ int s_src[BN];
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nk = (K + BK - 1) / BK;
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) {
-            mbar_init(smem_u32(&full_b[s]), 1 + 32);    // A expect_tx + 32 cp.async arrivals
+            mbar_init(smem_u32(&full_b[s]), 1 + 32 * fast::NPROD);   // A expect_tx + cp.async arrivals
             mbar_init(smem_u32(&empty_b[s]), 1);
         }
         for (int b = 0; b < 2; ++b) {
@@ -351,25 +353,27 @@ tc_pairs_fast_kernel(const __grid_constant__ CUtensorMap mapAb, const __grid_con
     asm volatile("tcgen05.fence::after_thread_sync;");
     const uint32_t tmem = *tmem_slot;
 
-    if (warp == 0) {
-        // ---------------- producer
+    if (warp == 0 || warp == 2 || warp == 3) {
+        // ---------------- producers: warp 0 lane 0 issues the A tiles (TMA); warps 0, 2, 3
+        // gather the B rows with 16-B cp.async (one warp could not issue them fast enough:
+        // the loads are latency bound per instruction, the MMA warp waited on full barriers)
+        const int pi = warp == 0 ? 0 : warp - 1;
         const int piece = lane & 7, rsub = lane >> 3;
         int c = 0;
         for (int ti = blockIdx.x; ti < ntiles; ti += gridDim.x) {
             const Tile tl = tiles[ti];
-            __syncwarp();
+            int64_t srow[fast::NG];                      // this lane's source rows x ldb
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const int r = lane + 32 * q;
-                s_src[r] = pairs[tl.p0 + min(r, tl.np - 1)].y;
+            for (int g = 0; g < fast::NG; ++g) {
+                const int r = rsub + 4 * (pi + fast::NPROD * g);
+                srow[g] = (int64_t)__ldg(&pairs[tl.p0 + min(r, tl.np - 1)].y) * ldb;
             }
-            __syncwarp();
             for (int kc = 0; kc < nk; ++kc, ++c) {
                 const int s = c % STAGES;
                 mbar_wait(smem_u32(&empty_b[s]), ((c / STAGES) & 1) ^ 1);
                 uint8_t* st = smem + s * STAGE_BYTES;
                 const uint32_t full = smem_u32(&full_b[s]);
-                if (lane == 0) {
+                if (pi == 0 && lane == 0) {
                     mbar_expect_tx(full, 2 * MT * OPND_BYTES);
 #pragma unroll
                     for (int mt = 0; mt < MT; ++mt) {
@@ -382,17 +386,20 @@ tc_pairs_fast_kernel(const __grid_constant__ CUtensorMap mapAb, const __grid_con
                 const uint32_t nb = col < ldb ? 16u : 0u;      // zero-fill past the row
                 const uint32_t b0 = smem_u32(st + 2 * MT * OPND_BYTES);
                 const uint32_t b1 = b0 + OPND_BYTES;
-#pragma unroll 4
-                for (int j = 0; j < BN / 4; ++j) {
-                    const int r = rsub + 4 * j;
-                    const int64_t off = (int64_t)s_src[r] * ldb + col;
-                    const uint32_t so = (uint32_t)(r * 128 + ((piece ^ (r & 7)) * 16));
-                    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(b0 + so),
-                                 "l"(nb ? Bb + off : Bb), "r"(nb)
-                                 : "memory");
-                    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(b1 + so),
-                                 "l"(nb ? Bs + off : Bs), "r"(nb)
-                                 : "memory");
+#pragma unroll
+                for (int g = 0; g < fast::NG; ++g) {
+                    const int grp = pi + fast::NPROD * g;
+                    if (grp < BN / 4) {
+                        const int r = rsub + 4 * grp;
+                        const int64_t off = srow[g] + col;
+                        const uint32_t so = (uint32_t)(r * 128 + ((piece ^ (r & 7)) * 16));
+                        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(b0 + so),
+                                     "l"(nb ? Bb + off : Bb), "r"(nb)
+                                     : "memory");
+                        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(b1 + so),
+                                     "l"(nb ? Bs + off : Bs), "r"(nb)
+                                     : "memory");
+                    }
                 }
                 asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(full) : "memory");
             }
@@ -568,7 +575,7 @@ void tc_pairs_gemm_fast(const OpPairs& P, const CUtensorMap& Ab, const CUtensorM
         attr = true;
     }
     const int grid = std::min(P.ntiles, num_sms());
-    tc::tc_pairs_fast_kernel<<<grid, tc::THREADS, tc::fast::SMEM_BYTES, s>>>(
+    tc::tc_pairs_fast_kernel<<<grid, tc::fast::THREADS, tc::fast::SMEM_BYTES, s>>>(
         Ab, As, Bb, Bs, ldb, reinterpret_cast<const tc::Tile*>(P.tiles.p), P.ntiles, P.pairs.p, M, K, Y, ldy);
     EB_CHECK_LAUNCH();
 }
