@@ -279,11 +279,9 @@ Bem* bem_create(const float* verts, int64_t n, int nq, int max_pts, int p, const
                                                        B->CU.p, B->CP.p, B->DU.p, B->DP.p);
     EB_CHECK_LAUNCH();
     B->tree = build_tree(B->qpts.p, B->qnrm.p, B->qw.p, ns, B->cent.p, n, max_pts, p, m, s);
-    B->tree->far64 = true;     // GMRES needs an operator linear to ~1e-8 (see fmm.cu)
-    if (B->tree->tc_fast) {    // and the precise (drained) tensor-core accumulation
-        B->tree->tc_fast = false;
-        tc_build_tiles(B->tree->m2l, B->tree->plan->me, false);
-    }
+    // GMRES needs an operator linear to ~1e-8: fp64 far field and the precise (drained)
+    // tensor-core accumulation (see fmm.cu)
+    tree_precise(*B->tree, s);
     B->f.alloc(3 * ns);
     B->g.alloc(3 * ns);
     B->y.alloc(3 * n);

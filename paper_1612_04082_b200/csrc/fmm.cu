@@ -21,7 +21,7 @@ struct BoxGeo {
     double ox, oy, oz, side;
     __device__ __forceinline__ void center(const int* anchor, const int* level, int b, double& cx, double& cy,
                                            double& cz, double& r) const {
-        const double h = side / (double)(1 << level[b]);
+        const double h = side * __hiloint2double((1023 - level[b]) << 20, 0);   // side 2^-level, exact
         cx = ox + (anchor[3 * b] + 0.5) * h;
         cy = oy + (anchor[3 * b + 1] + 0.5) * h;
         cz = oz + (anchor[3 * b + 2] + 0.5) * h;
@@ -190,6 +190,152 @@ far_eval_kernel(int n_eval, const int* __restrict__ eval_box, const int* __restr
     }
 }
 
+// fp32 far field (p <= 8 matvec): phi arrives pre-scaled in fp32 (PHI GEMM epilogue), so a
+// box costs one coalesced copy of its equivalent points / densities into the warp's shared
+// slice; each lane then evaluates TPT targets against them (TPT = 2 for leaves with more
+// than 32 targets: every staged point is read once for both).
+template <bool STRESS, int TPT>
+__device__ __forceinline__ void far_round_f32(int t0, int t_beg, int t_end, int b, int own, int nfar,
+                                              const int* __restrict__ widx, int wbeg, const float4* __restrict__ PHIDF,
+                                              int l2t, const float4* __restrict__ PHIUF,
+                                              const int* __restrict__ phiu_slot, const int* __restrict__ anchor,
+                                              const int* __restrict__ level, const BoxGeo& geo,
+                                              const float4* __restrict__ se4, int ne, const float* __restrict__ trg,
+                                              const KConst& kc, float4* ey, float4* ph, int lane,
+                                              float* __restrict__ far) {
+    constexpr int NC = STRESS ? 6 : 3;
+    int tc[TPT];
+#pragma unroll
+    for (int j = 0; j < TPT; ++j) {
+        const int t = t0 + lane + 32 * j;
+        tc[j] = t < t_end ? t : t_beg;
+    }
+    float acc[TPT][NC];
+#pragma unroll
+    for (int j = 0; j < TPT; ++j)
+#pragma unroll
+        for (int c = 0; c < NC; ++c) acc[j][c] = 0.f;
+    for (int e = 0; e < nfar; ++e) {
+        const bool is_own = own && e == 0;
+        const int a = is_own ? b : widx[wbeg + e - own];
+        const float4* phi = is_own ? PHIDF + (int64_t)l2t * ne
+                                   : (phiu_slot[a] >= 0 ? PHIUF + (int64_t)phiu_slot[a] * ne : nullptr);
+        if (!phi) continue;
+        double cx, cy, cz, r;
+        geo.center(anchor, level, a, cx, cy, cz, r);
+        const float R = (float)((is_own ? RAD_DE : RAD_UE) * r);
+        __syncwarp();
+        for (int k = lane; k < ne; k += 32) {
+            const float4 u = se4[k];
+            ey[k] = make_float4(R * u.x, R * u.y, R * u.z, 0.f);
+            ph[k] = phi[k];
+        }
+        __syncwarp();
+        float x[TPT], y[TPT], z[TPT];
+#pragma unroll
+        for (int j = 0; j < TPT; ++j) {          // relative to the box centre, in fp64
+            x[j] = (float)((double)trg[3 * tc[j]] - cx);
+            y[j] = (float)((double)trg[3 * tc[j] + 1] - cy);
+            z[j] = (float)((double)trg[3 * tc[j] + 2] - cz);
+        }
+#pragma unroll 2
+        for (int k = 0; k < ne; ++k) {
+            const float4 q = ey[k], f = ph[k];
+#pragma unroll
+            for (int j = 0; j < TPT; ++j) {
+                const float dx = x[j] - q.x, dy = y[j] - q.y, dz = z[j] - q.z;
+                const float ri = rsqrtf(fmaf(dz, dz, fmaf(dy, dy, dx * dx)));
+                if (!STRESS)
+                    acc_U<float>(dx, dy, dz, ri, f.x, f.y, f.z, kc.a1, acc[j]);
+                else
+                    acc_D<float>(dx, dy, dz, ri, f.x, f.y, f.z, kc.a, acc[j]);
+            }
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < TPT; ++j) {
+        const int t = t0 + lane + 32 * j;
+        if (t < t_end)
+#pragma unroll
+            for (int c = 0; c < NC; ++c) far[(int64_t)t * NC + c] = acc[j][c];
+    }
+}
+
+template <bool STRESS>
+__global__ void __launch_bounds__(32 * EV_WARPS)
+far_eval_f32_kernel(int n_eval, const int* __restrict__ eval_box, const int* __restrict__ l2t_slot,
+                    const float4* __restrict__ PHIDF, const float4* __restrict__ PHIUF,
+                    const int* __restrict__ phiu_slot, const int* __restrict__ woff, const int* __restrict__ widx,
+                    const int* __restrict__ tbeg, const int* __restrict__ tend, const int* __restrict__ anchor,
+                    const int* __restrict__ level, BoxGeo geo, const float4* __restrict__ se4, int ne,
+                    const float* __restrict__ trg, KConst kc, float* __restrict__ far) {
+    extern __shared__ float4 fsm[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int i = blockIdx.x * EV_WARPS + warp;
+    if (i >= n_eval) return;                       // warp-uniform; no CTA barriers below
+    float4* ey = fsm + (size_t)warp * 2 * ne;
+    float4* ph = ey + ne;
+    const int b = eval_box[i];
+    const int t_beg = tbeg[b], t_end = tend[b];
+    const int l2t = l2t_slot[i];
+    const int own = l2t >= 0 ? 1 : 0;
+    const int nfar = own + (woff[b + 1] - woff[b]);
+    for (int t0 = t_beg; t0 < t_end;) {
+        if (t_end - t0 > 32) {
+            far_round_f32<STRESS, 2>(t0, t_beg, t_end, b, own, nfar, widx, woff[b], PHIDF, l2t, PHIUF, phiu_slot,
+                                     anchor, level, geo, se4, ne, trg, kc, ey, ph, lane, far);
+            t0 += 64;
+        } else {
+            far_round_f32<STRESS, 1>(t0, t_beg, t_end, b, own, nfar, widx, woff[b], PHIDF, l2t, PHIUF, phiu_slot,
+                                     anchor, level, geo, se4, ne, trg, kc, ey, ph, lane, far);
+            t0 += 32;
+        }
+    }
+}
+
+// near field: U-list sources staged 32 at a time per warp; TPT targets per lane (2 when
+// the leaf has more than 32 targets, so each staged record serves both)
+template <bool SL, bool DL, bool STRESS, int TPT>
+__device__ __forceinline__ void near_round(int t0, int t_beg, int t_end, int b, const int* __restrict__ uoff,
+                                           const int* __restrict__ uidx, const int* __restrict__ sbeg,
+                                           const int* __restrict__ send, const float* __restrict__ trg,
+                                           const int* __restrict__ trg_perm, const float4* __restrict__ rec,
+                                           const KConst& kc, const float* __restrict__ far, float* __restrict__ out,
+                                           float4* srec, int lane) {
+    constexpr int NC = STRESS ? 6 : 3;
+    constexpr int R = STRESS ? REC_STRESS : REC_DISP;
+    float x[TPT], y[TPT], z[TPT], acc[TPT][NC];
+#pragma unroll
+    for (int j = 0; j < TPT; ++j) {
+        const int t = t0 + lane + 32 * j;
+        const int tc = t < t_end ? t : t_beg;
+        x[j] = trg[3 * tc];
+        y[j] = trg[3 * tc + 1];
+        z[j] = trg[3 * tc + 2];
+#pragma unroll
+        for (int c = 0; c < NC; ++c) acc[j][c] = 0.f;
+    }
+    for (int e = uoff[b]; e < uoff[b + 1]; ++e) {
+        const int a = uidx[e];
+        for (int s0 = sbeg[a]; s0 < send[a]; s0 += 32) {
+            const int cnt = min(32, send[a] - s0);
+            __syncwarp();
+            for (int q = lane; q < cnt * R; q += 32) srec[q] = rec[(int64_t)s0 * R + q];
+            __syncwarp();
+            pair_loop_multi<SL, DL, STRESS, TPT>(srec, cnt, x, y, z, kc, acc);
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < TPT; ++j) {
+        const int t = t0 + lane + 32 * j;
+        if (t < t_end) {
+            float* o = out + (int64_t)trg_perm[t] * NC;
+#pragma unroll
+            for (int c = 0; c < NC; ++c) o[c] = acc[j][c] + far[(int64_t)t * NC + c];
+        }
+    }
+}
+
 template <bool SL, bool DL, bool STRESS>
 __global__ void __launch_bounds__(32 * EV_WARPS)
 near_eval_kernel(int n_eval, const int* __restrict__ eval_box, const int* __restrict__ uoff,
@@ -197,7 +343,6 @@ near_eval_kernel(int n_eval, const int* __restrict__ eval_box, const int* __rest
                  const int* __restrict__ tbeg, const int* __restrict__ tend, const float* __restrict__ trg,
                  const int* __restrict__ trg_perm, const float4* __restrict__ rec, KConst kc,
                  const float* __restrict__ far, float* __restrict__ out) {
-    constexpr int NC = STRESS ? 6 : 3;
     constexpr int R = STRESS ? REC_STRESS : REC_DISP;
     __shared__ float4 srec_all[EV_WARPS][32 * R];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -206,27 +351,15 @@ near_eval_kernel(int n_eval, const int* __restrict__ eval_box, const int* __rest
     float4* srec = srec_all[warp];
     const int b = eval_box[i];
     const int t_beg = tbeg[b], t_end = tend[b];
-    for (int t0 = t_beg; t0 < t_end; t0 += 32) {
-        const int t = t0 + lane;
-        const int tc = t < t_end ? t : t_beg;
-        const float x = trg[3 * tc], y = trg[3 * tc + 1], z = trg[3 * tc + 2];
-        float acc[NC];
-#pragma unroll
-        for (int c = 0; c < NC; ++c) acc[c] = 0.f;
-        for (int e = uoff[b]; e < uoff[b + 1]; ++e) {
-            const int a = uidx[e];
-            for (int s0 = sbeg[a]; s0 < send[a]; s0 += 32) {
-                const int cnt = min(32, send[a] - s0);
-                __syncwarp();
-                for (int q = lane; q < cnt * R; q += 32) srec[q] = rec[(int64_t)s0 * R + q];
-                __syncwarp();
-                pair_loop<SL, DL, STRESS>(srec, cnt, x, y, z, kc, acc);
-            }
-        }
-        if (t < t_end) {
-            float* o = out + (int64_t)trg_perm[t] * NC;
-#pragma unroll
-            for (int c = 0; c < NC; ++c) o[c] = acc[c] + far[(int64_t)t * NC + c];
+    for (int t0 = t_beg; t0 < t_end;) {
+        if (t_end - t0 > 32) {
+            near_round<SL, DL, STRESS, 2>(t0, t_beg, t_end, b, uoff, uidx, sbeg, send, trg, trg_perm, rec, kc, far,
+                                          out, srec, lane);
+            t0 += 64;
+        } else {
+            near_round<SL, DL, STRESS, 1>(t0, t_beg, t_end, b, uoff, uidx, sbeg, send, trg, trg_perm, rec, kc, far,
+                                          out, srec, lane);
+            t0 += 32;
         }
     }
 }
@@ -468,9 +601,16 @@ void schedule_tree(Tree& t, cudaStream_t s) {
         for (auto& x : t.m2m) tc_build_tiles(x, me, false);
         for (auto& x : t.l2l) tc_build_tiles(x, me, false);
     }
-    t.PHID.alloc((size_t)std::max(1, t.n_phid) * me);
+    if (t.far64) {
+        t.PHID.alloc((size_t)std::max(1, t.n_phid) * me);
+        t.PHIU.alloc((size_t)std::max(1, t.n_phiu) * me);
+    } else {
+        t.PHIDF.alloc((size_t)std::max(1, t.n_phid) * P.ne);
+        t.PHIUF.alloc((size_t)std::max(1, t.n_phiu) * P.ne);
+        t.PHIDF.zero(s);
+        t.PHIUF.zero(s);
+    }
     t.out_sorted.alloc((size_t)std::max<int64_t>(1, t.ntrg) * 6);
-    t.PHIU.alloc((size_t)std::max(1, t.n_phiu) * me);
     EB_CUDA(cudaStreamSynchronize(s));
 
     int64_t bytes = 0;
@@ -479,7 +619,7 @@ void schedule_tree(Tree& t, cudaStream_t s) {
     bytes += (int64_t)nb * 4 * 40;
     for (int k = 0; k < 4; ++k) bytes += t.lst_off[k].bytes() + t.lst_idx[k].bytes();
     bytes += t.rec_disp.bytes() + t.rec_stress.bytes() + t.Q.bytes() + t.Z.bytes() + t.W.bytes() + t.PHID.bytes() +
-             t.PHIU.bytes();
+             t.PHIU.bytes() + t.PHIDF.bytes() + t.PHIUF.bytes();
     bytes += t.m2l.pairs.bytes();
     t.device_bytes = bytes;
 }
@@ -507,6 +647,24 @@ static void launch_check(const Tree& t, const int* tbox, int n, const int* soff,
     EB_CHECK_LAUNCH();
 }
 
+// switch a built tree to the precise configuration (fp64 far field, drained tensor-core
+// accumulation): the BEM operator inside GMRES
+void tree_precise(Tree& t, cudaStream_t s) {
+    const Plan& P = *t.plan;
+    if (!t.far64) {
+        t.far64 = true;
+        t.PHIDF.release();
+        t.PHIUF.release();
+        t.PHID.alloc((size_t)std::max(1, t.n_phid) * P.me);
+        t.PHIU.alloc((size_t)std::max(1, t.n_phiu) * P.me);
+    }
+    if (t.tc_fast) {
+        t.tc_fast = false;
+        tc_build_tiles(t.m2l, P.me, false);
+    }
+    EB_CUDA(cudaStreamSynchronize(s));
+}
+
 template <bool SL, bool DL, bool STRESS>
 static void launch_eval(const Tree& t, float* out, cudaStream_t s) {
     if (t.n_eval == 0) return;
@@ -515,13 +673,23 @@ static void launch_eval(const Tree& t, float* out, cudaStream_t s) {
     KConst kc = make_kconst(t.mat);
     const double cfar = STRESS ? t.mat.cD : t.mat.cU;
     const int grid = ceil_div(t.n_eval, EV_WARPS);
-    const bool fp64 = t.far64;
-    const size_t sm = (fp64 ? sizeof(double) : sizeof(float)) * 6 * P.ne * EV_WARPS;
-    auto ffn = fp64 ? far_eval_kernel<STRESS, double> : far_eval_kernel<STRESS, float>;
-    if (sm > 48 * 1024) EB_CUDA(cudaFuncSetAttribute(ffn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    ffn<<<grid, 32 * EV_WARPS, sm, s>>>(t.n_eval, t.eval_box.p, t.eval_l2t_slot.p, t.PHID.p, t.PHIU.p, t.phiu_slot.p,
-                                        t.lst_off[2].p, t.lst_idx[2].p, t.tbeg.p, t.tend.p, t.anchor.p, t.level.p, geo,
-                                        P.s_e64.p, P.ne, t.trg_xyz.p, kc, cfar, t.out_sorted.p);
+    if (t.far64) {
+        const size_t sm = sizeof(double) * 6 * P.ne * EV_WARPS;
+        auto ffn = far_eval_kernel<STRESS, double>;
+        if (sm > 48 * 1024) EB_CUDA(cudaFuncSetAttribute(ffn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        ffn<<<grid, 32 * EV_WARPS, sm, s>>>(t.n_eval, t.eval_box.p, t.eval_l2t_slot.p, t.PHID.p, t.PHIU.p,
+                                            t.phiu_slot.p, t.lst_off[2].p, t.lst_idx[2].p, t.tbeg.p, t.tend.p,
+                                            t.anchor.p, t.level.p, geo, P.s_e64.p, P.ne, t.trg_xyz.p, kc, cfar,
+                                            t.out_sorted.p);
+    } else {
+        const size_t sm = sizeof(float4) * 2 * P.ne * EV_WARPS;
+        auto ffn = far_eval_f32_kernel<STRESS>;
+        if (sm > 48 * 1024) EB_CUDA(cudaFuncSetAttribute(ffn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        ffn<<<grid, 32 * EV_WARPS, sm, s>>>(t.n_eval, t.eval_box.p, t.eval_l2t_slot.p, t.PHIDF.p, t.PHIUF.p,
+                                            t.phiu_slot.p, t.lst_off[2].p, t.lst_idx[2].p, t.tbeg.p, t.tend.p,
+                                            t.anchor.p, t.level.p, geo, P.s_e4.p, P.ne, t.trg_xyz.p, kc,
+                                            t.out_sorted.p);
+    }
     EB_CHECK_LAUNCH();
     near_eval_kernel<SL, DL, STRESS><<<grid, 32 * EV_WARPS, 0, s>>>(
         t.n_eval, t.eval_box.p, t.lst_off[0].p, t.lst_idx[0].p, t.sbeg.p, t.send.p, t.tbeg.p, t.tend.p, t.trg_xyz.p,
@@ -616,8 +784,14 @@ void fmm_evaluate(Tree& t, int kernel, const float* f, const float* g, float* ou
     mark(phase++);
 
     // equivalent densities (fp64) and leaf evaluation
-    gemm_pairs_f64(t.phid_pairs, P.Rdinv.p, me, me, t.W.p, lde, t.phid_scale.p, t.PHID.p, me, s);
-    gemm_pairs_f64(t.phiu_pairs, P.Ruinv.p, me, me, t.Z.p, lde, t.phiu_scale.p, t.PHIU.p, me, s);
+    if (t.far64) {
+        gemm_pairs_f64(t.phid_pairs, P.Rdinv.p, me, me, t.W.p, lde, t.phid_scale.p, t.PHID.p, me, s);
+        gemm_pairs_f64(t.phiu_pairs, P.Ruinv.p, me, me, t.Z.p, lde, t.phiu_scale.p, t.PHIU.p, me, s);
+    } else {
+        const double cfar = stress ? t.mat.cD : t.mat.cU;
+        gemm_pairs_f64_to_f32(t.phid_pairs, P.Rdinv.p, me, me, t.W.p, lde, t.phid_scale.p, cfar, t.PHIDF.p, P.ne, s);
+        gemm_pairs_f64_to_f32(t.phiu_pairs, P.Ruinv.p, me, me, t.Z.p, lde, t.phiu_scale.p, cfar, t.PHIUF.p, P.ne, s);
+    }
     mark(phase++);
     switch (kernel) {
         case K_U: launch_eval<true, false, false>(t, out, s); break;

@@ -39,6 +39,7 @@ struct Plan {
     Material mat{};
     DBuf<float> s_e, s_c;       // unit surface grids [ne*3], [nc*3] (fp32 copies)
     DBuf<double> s_e64, s_c64;
+    DBuf<float4> s_e4;          // unit equivalent surface as float4 (fp32 far field)
     DBuf<float> Qu1T, Qd1T;     // [me x ldc] row-major: z = Qu1T q
     DBuf<double> Ruinv, Rdinv;  // [me x me] row-major upper triangular: phi = r Rinv z
     DBuf<float> M2M, L2L;       // [8][me x lde]
@@ -142,7 +143,8 @@ struct Tree {
                                          // the sum order-independent at fp32 precision (deterministic)
     DBuf<float> Qb, Qs, Zb, Zs, Wb, Ws;  // TF32 head / remainder copies (B operands)
     CUtensorMap mQb, mQs, mZb, mZs, mWb, mWs;
-    DBuf<double> PHID, PHIU;             // [n_phid x me], [n_phiu x me]
+    DBuf<double> PHID, PHIU;             // [n_phid x me], [n_phiu x me] (fp64 far field)
+    DBuf<float4> PHIDF, PHIUF;           // [n_phid x ne], [n_phiu x ne] (fp32 far field, scaled)
     DBuf<float> out_sorted;              // [ntrg x 6]
     int64_t device_bytes = 0;
 };
@@ -181,6 +183,7 @@ void tc_make_map_b(CUtensorMap* m, const float* base, int64_t rows, int K, int l
 template <class XT>
 void tc_split_rows(const XT* X, int ld, int64_t row0, int64_t nrows, int K, float* Xb, float* Xs,
                    cudaStream_t s);
+void tree_precise(Tree& t, cudaStream_t s);
 void tc_build_tiles(OpPairs& P, int M, bool fast);
 void tc_pairs_gemm_fast(const OpPairs& P, const CUtensorMap& Ab, const CUtensorMap& As, const float* Bb,
                         const float* Bs, int ldb, int M, int K, double* Y, int ldy, cudaStream_t s);
@@ -189,6 +192,9 @@ void tc_pairs_gemm(const OpPairs& P, const CUtensorMap& Ab, const CUtensorMap& A
 // fp64 variant with per-pair scale (r of the box, looked up from scale[t])
 void gemm_pairs_f64(const OpPairs& P, const double* mat, int M, int K, const double* X, int ldx,
                     const double* scale, double* Y, int ldy, cudaStream_t s);
+// the same with fp32 output in the far-field layout: row t = M/3 float4 (cf * value, 0)
+void gemm_pairs_f64_to_f32(const OpPairs& P, const double* mat, int M, int K, const double* X, int ldx,
+                           const double* scale, double cf, float4* Y, int ldy, cudaStream_t s);
 void build_op_pairs(OpPairs& P, int nops, const std::vector<int>& op, const std::vector<int2>& pr,
                     cudaStream_t s);
 

@@ -337,11 +337,14 @@ template void gemm_pairs_f32<float>(const OpPairs&, const float*, int, int, int,
 template void gemm_pairs_f32<double>(const OpPairs&, const float*, int, int, int, const double*, int, double*, int,
                                      cudaStream_t);
 
-// fp64: Y[t] = scale[t] * Mat X[src] (one op; plain store; Mat upper triangular)
+// fp64: Y[t] = scale[t] * Mat X[src] (one op; plain store; Mat upper triangular).
+// OutT = double: Y row-major [t][ldy].  OutT = float4: the fp32 far-field layout, row t holds
+// M/3 float4 (x, y, z, 0) = (float)(cf * scale[t] * (Mat X)[3k .. 3k+2]) (ldy in float4).
+template <class OutT>
 __global__ void __launch_bounds__(256)
 gemm_pairs_f64_kernel(const int2* __restrict__ pairs, int npairs, const double* __restrict__ Mt, int M,
-                      int K, const double* __restrict__ X, int ldx, const double* __restrict__ scale,
-                      double* __restrict__ Y, int ldy) {
+                      int K, const double* __restrict__ X, int ldx, const double* __restrict__ scale, double cf,
+                      OutT* __restrict__ Y, int ldy) {
     const int p0 = blockIdx.y * PG_N;
     const int np = min(PG_N, npairs - p0);
     const int m0 = blockIdx.x * PG_M;
@@ -382,11 +385,16 @@ gemm_pairs_f64_kernel(const int2* __restrict__ pairs, int npairs, const double* 
         if (pj >= np) continue;
         int t = pr[pj].x;
         double sc = scale[t];
-        double* y = Y + (int64_t)t * ldy;
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
             int gm = m0 + ty + 16 * i;
-            if (gm < M) y[gm] = sc * acc[i][j];
+            if (gm >= M) continue;
+            if constexpr (sizeof(OutT) == sizeof(double)) {
+                Y[(int64_t)t * ldy + gm] = sc * acc[i][j];
+            } else {
+                float* y = reinterpret_cast<float*>(Y + (int64_t)t * ldy);
+                y[4 * (gm / 3) + gm % 3] = (float)(cf * sc * acc[i][j]);
+            }
         }
     }
 }
@@ -395,7 +403,17 @@ void gemm_pairs_f64(const OpPairs& P, const double* mat, int M, int K, const dou
                     const double* scale, double* Y, int ldy, cudaStream_t s) {
     if (P.npairs == 0) return;
     dim3 grid(ceil_div(M, PG_M), ceil_div(P.npairs, PG_N), 1);
-    gemm_pairs_f64_kernel<<<grid, 256, 0, s>>>(P.pairs.p, (int)P.npairs, mat, M, K, X, ldx, scale, Y, ldy);
+    gemm_pairs_f64_kernel<double><<<grid, 256, 0, s>>>(P.pairs.p, (int)P.npairs, mat, M, K, X, ldx, scale, 1.0, Y,
+                                                       ldy);
+    EB_CHECK_LAUNCH();
+}
+
+void gemm_pairs_f64_to_f32(const OpPairs& P, const double* mat, int M, int K, const double* X, int ldx,
+                           const double* scale, double cf, float4* Y, int ldy, cudaStream_t s) {
+    if (P.npairs == 0) return;
+    dim3 grid(ceil_div(M, PG_M), ceil_div(P.npairs, PG_N), 1);
+    gemm_pairs_f64_kernel<float4><<<grid, 256, 0, s>>>(P.pairs.p, (int)P.npairs, mat, M, K, X, ldx, scale, cf, Y,
+                                                       ldy);
     EB_CHECK_LAUNCH();
 }
 

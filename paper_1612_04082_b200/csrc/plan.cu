@@ -263,6 +263,10 @@ static std::shared_ptr<Plan> make_plan(int p, const Material& m, cudaStream_t s)
     P->s_c.alloc(scf.size());
     h2d(P->s_e.p, sef.data(), sef.size(), s);
     h2d(P->s_c.p, scf.data(), scf.size(), s);
+    std::vector<float4> se4(P->ne);
+    for (int k = 0; k < P->ne; ++k) se4[k] = make_float4((float)se[3 * k], (float)se[3 * k + 1], (float)se[3 * k + 2], 0.f);
+    P->s_e4.alloc(P->ne);
+    h2d(P->s_e4.p, se4.data(), P->ne, s);
 
     DBuf<double> Qu1T, Qd1T;
     factor_solve(*P, P->s_c64, RAD_UC, P->s_e64, RAD_UE, Qu1T, P->Ruinv, s);
