@@ -3,9 +3,9 @@
 //
 // Layout: prepared source records (p2p.cuh) are streamed through shared memory in
 // tiles of 128; each thread owns TPT targets in registers and does fp32 FFMA with one
-// rsqrt per pair.  The source range is split across blockIdx.y so the grid covers all
-// 148 SMs even for a few thousand targets; partial sums land in a [split][target][c]
-// scratch and a second kernel reduces them in a fixed order (deterministic).
+// rsqrt per pair.  A one-wave persistent grid splits the (target block, source tile)
+// units evenly over all resident CTA slots; partial sums of a target block from the CTAs
+// that covered it are reduced in a fixed order (deterministic).
 #include <cstdlib>
 
 #include "p2p.cuh"
@@ -62,83 +62,94 @@ void prepare_sources(int kernel, const Material& m, const float* y, const float*
 }
 
 constexpr int DIRECT_THREADS = 128;
-constexpr int DIRECT_TPT = 4;          // targets per thread (one LDS.128 per pair)
+constexpr int DIRECT_TPT = 4;          // targets per thread (measured best of 3..8)
 constexpr int DIRECT_TILE = 128;       // sources per shared-memory tile
+constexpr int DIRECT_TB = DIRECT_THREADS * DIRECT_TPT;   // targets per target block
+
+// Work = (target block, source tile) units, target-block major.  The grid is exactly the
+// resident CTA slots of one wave and CTA c takes the contiguous unit range
+// [c U / G, (c+1) U / G): every SM gets the same number of pair interactions to within one
+// tile (a 2-D grid of whole source chunks left 14% of the slots idle on configs[1]).
+// A CTA flushes its accumulators whenever its range leaves a target block, into slot
+// (c - first CTA of that block) of that block's partial sums; reduce_blocks adds the slots
+// of each target in a fixed order (deterministic).
+__device__ __forceinline__ int64_t first_cta(int64_t u, int64_t U, int64_t G) {
+    return ((u + 1) * G + U - 1) / U - 1;          // CTA whose range contains unit u
+}
 
 template <bool SL, bool DL, bool STRESS>
 __global__ void __launch_bounds__(DIRECT_THREADS)
-direct_kernel(const float4* __restrict__ rec, int64_t nsrc, int64_t chunk,
-              const float* __restrict__ trg, int64_t ntrg, KConst kc, float* __restrict__ partial) {
+direct_kernel(const float4* __restrict__ rec, int64_t nsrc, int64_t ntiles, const float* __restrict__ trg,
+              int64_t ntrg, int64_t U, int kslots, KConst kc, float* __restrict__ partial) {
     constexpr int R = STRESS ? REC_STRESS : REC_DISP;
     constexpr int NC = STRESS ? 6 : 3;
     __shared__ float4 srec[DIRECT_TILE * R];
-    const int64_t t0 = (int64_t)blockIdx.x * DIRECT_THREADS * DIRECT_TPT + threadIdx.x;
-    float x[DIRECT_TPT], y[DIRECT_TPT], z[DIRECT_TPT], acc[DIRECT_TPT][NC];
+    const int64_t G = gridDim.x, c = blockIdx.x;
+    const int64_t u_beg = c * U / G, u_end = (c + 1) * U / G;
+    int64_t u = u_beg;
+    while (u < u_end) {
+        const int64_t tb = u / ntiles;
+        const int64_t u_stop = min(u_end, (tb + 1) * ntiles);
+        const int64_t t0 = tb * DIRECT_TB + threadIdx.x;
+        float x[DIRECT_TPT], y[DIRECT_TPT], z[DIRECT_TPT], acc[DIRECT_TPT][NC];
 #pragma unroll
-    for (int k = 0; k < DIRECT_TPT; ++k) {
-        int64_t t = t0 + k * DIRECT_THREADS;
-        int64_t tc = t < ntrg ? t : ntrg - 1;
-        x[k] = trg[3 * tc]; y[k] = trg[3 * tc + 1]; z[k] = trg[3 * tc + 2];
+        for (int k = 0; k < DIRECT_TPT; ++k) {
+            const int64_t t = t0 + k * DIRECT_THREADS;
+            const int64_t tc = t < ntrg ? t : ntrg - 1;
+            x[k] = trg[3 * tc]; y[k] = trg[3 * tc + 1]; z[k] = trg[3 * tc + 2];
 #pragma unroll
-        for (int c = 0; c < NC; ++c) acc[k][c] = 0.f;
-    }
-    const int64_t s_begin = blockIdx.y * chunk;
-    const int64_t s_end = min(nsrc, s_begin + chunk);
-    for (int64_t s0 = s_begin; s0 < s_end; s0 += DIRECT_TILE) {
-        const int cnt = (int)min((int64_t)DIRECT_TILE, s_end - s0);
-        __syncthreads();
-        for (int i = threadIdx.x; i < cnt * R; i += DIRECT_THREADS) srec[i] = rec[s0 * R + i];
-        __syncthreads();
-        pair_loop_multi<SL, DL, STRESS, DIRECT_TPT>(srec, cnt, x, y, z, kc, acc);
-    }
-#pragma unroll
-    for (int k = 0; k < DIRECT_TPT; ++k) {
-        int64_t t = t0 + k * DIRECT_THREADS;
-        if (t < ntrg) {
-            float* o = partial + ((int64_t)blockIdx.y * ntrg + t) * NC;
-#pragma unroll
-            for (int c = 0; c < NC; ++c) o[c] = acc[k][c];
+            for (int q = 0; q < NC; ++q) acc[k][q] = 0.f;
         }
+        for (; u < u_stop; ++u) {
+            const int64_t s0 = (u - tb * ntiles) * DIRECT_TILE;
+            const int cnt = (int)min((int64_t)DIRECT_TILE, nsrc - s0);
+            __syncthreads();
+            for (int i = threadIdx.x; i < cnt * R; i += DIRECT_THREADS) srec[i] = rec[s0 * R + i];
+            __syncthreads();
+            pair_loop_multi<SL, DL, STRESS, DIRECT_TPT>(srec, cnt, x, y, z, kc, acc);
+        }
+        const int slot = (int)(c - first_cta(tb * ntiles, U, G));
+        float* o = partial + ((int64_t)tb * kslots + slot) * DIRECT_TB * NC;
+#pragma unroll
+        for (int k = 0; k < DIRECT_TPT; ++k)
+#pragma unroll
+            for (int q = 0; q < NC; ++q) o[(threadIdx.x + k * DIRECT_THREADS) * NC + q] = acc[k][q];
     }
 }
 
-__global__ void reduce_splits(const float* __restrict__ partial, int nsplit, int64_t m,
-                              float* __restrict__ out) {
-    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i >= m) return;
-    float s = 0.f;
-    for (int k = 0; k < nsplit; ++k) s += partial[k * m + i];
-    out[i] = s;
+// out[t] = sum over the CTAs that covered t's target block, in CTA order
+__global__ void reduce_blocks(const float* __restrict__ partial, int64_t ntrg, int nc, int64_t ntiles, int64_t U,
+                              int64_t G, int kslots, float* __restrict__ out) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= ntrg * nc) return;
+    const int64_t t = i / nc, q = i % nc, tb = t / DIRECT_TB, r = t % DIRECT_TB;
+    const int64_t c0 = first_cta(tb * ntiles, U, G), c1 = first_cta((tb + 1) * ntiles - 1, U, G);
+    const float* p = partial + (int64_t)tb * kslots * DIRECT_TB * nc + r * nc + q;
+    float sum = 0.f;
+    for (int64_t k = 0; k <= c1 - c0; ++k) sum += p[k * DIRECT_TB * nc];
+    out[i] = sum;
 }
 
 template <bool SL, bool DL, bool STRESS>
 static void launch_direct(const float4* rec, int64_t nsrc, const float* trg, int64_t ntrg,
                           const KConst& kc, float* out, cudaStream_t s) {
     constexpr int NC = STRESS ? 6 : 3;
-    const int tblocks = ceil_div(ntrg, DIRECT_THREADS * DIRECT_TPT);
-    // split the sources so the grid fills the resident CTA slots of one wave as closely
-    // as possible (partial second waves cost more than an under-full first one)
+    const int64_t tblocks = (ntrg + DIRECT_TB - 1) / DIRECT_TB;
+    const int64_t ntiles = (nsrc + DIRECT_TILE - 1) / DIRECT_TILE;
+    const int64_t U = tblocks * ntiles;
     int occ = 0;
     EB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, direct_kernel<SL, DL, STRESS>, DIRECT_THREADS, 0));
-    const int slots = num_sms() * std::max(occ, 1);
-    int nsplit = std::max(1, std::min(slots / tblocks, ceil_div(nsrc, 4 * DIRECT_TILE)));
-    if (const char* e = std::getenv("EBEM_DIRECT_SPLIT")) nsplit = std::max(1, std::atoi(e));
-    nsplit = std::min(nsplit, 65535);
-    // whole shared-memory tiles per CTA (measured: ragged chunks cost 15-100%)
-    int64_t chunk = ((nsrc + nsplit - 1) / nsplit + DIRECT_TILE - 1) / DIRECT_TILE * DIRECT_TILE;
-    nsplit = (int)((nsrc + chunk - 1) / chunk);
-    if (nsplit <= 1) {
-        dim3 grid(tblocks, 1);
-        direct_kernel<SL, DL, STRESS><<<grid, DIRECT_THREADS, 0, s>>>(rec, nsrc, nsrc, trg, ntrg, kc, out);
-        EB_CHECK_LAUNCH();
-        return;
-    }
+    int64_t G = std::min<int64_t>(U, (int64_t)num_sms() * std::max(occ, 1));
+    if (const char* e = std::getenv("EBEM_DIRECT_GRID")) G = std::max<int64_t>(1, std::min<int64_t>(U, std::atoll(e)));
+    // CTAs per target block: at most ceil(ntiles / floor(U / G)) + 1
+    const int64_t per = std::max<int64_t>(1, U / G);
+    const int kslots = (int)std::min<int64_t>(G, (ntiles + per - 1) / per + 1);
     float* partial = nullptr;
-    EB_CUDA(cudaMallocAsync(&partial, sizeof(float) * nsplit * ntrg * NC, s));
-    dim3 grid(tblocks, nsplit);
-    direct_kernel<SL, DL, STRESS><<<grid, DIRECT_THREADS, 0, s>>>(rec, nsrc, chunk, trg, ntrg, kc, partial);
+    EB_CUDA(cudaMallocAsync(&partial, sizeof(float) * tblocks * kslots * DIRECT_TB * NC, s));
+    direct_kernel<SL, DL, STRESS><<<(unsigned)G, DIRECT_THREADS, 0, s>>>(rec, nsrc, ntiles, trg, ntrg, U, kslots, kc,
+                                                                         partial);
     EB_CHECK_LAUNCH();
-    reduce_splits<<<ceil_div(ntrg * NC, 256), 256, 0, s>>>(partial, nsplit, ntrg * NC, out);
+    reduce_blocks<<<(unsigned)ceil_div(ntrg * NC, 256), 256, 0, s>>>(partial, ntrg, NC, ntiles, U, G, kslots, out);
     EB_CHECK_LAUNCH();
     EB_CUDA(cudaFreeAsync(partial, s));
 }
