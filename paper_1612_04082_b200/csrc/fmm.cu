@@ -53,7 +53,7 @@ check_potential_kernel(const int* __restrict__ tbox, const int* __restrict__ sof
     float x[KPT], y[KPT], z[KPT], acc[KPT][3];
 #pragma unroll
     for (int q = 0; q < KPT; ++q) {
-        const int k = min((int)threadIdx.x + q * CP_T, nc - 1);
+        const int k = min((int)(threadIdx.x + q * blockDim.x), nc - 1);
         // coordinates relative to the box centre: absolute fp32 check points would carry an
         // error of ulp(|x|), which is not small against a deep box (a level-20 box is
         // ~1e-6 of the root)
@@ -68,7 +68,7 @@ check_potential_kernel(const int* __restrict__ tbox, const int* __restrict__ sof
         for (int s0 = sbeg[a]; s0 < send[a]; s0 += CP_TILE) {
             const int cnt = min(CP_TILE, send[a] - s0);
             __syncthreads();
-            for (int q = threadIdx.x; q < cnt * REC_DISP; q += CP_T) {
+            for (int q = threadIdx.x; q < cnt * REC_DISP; q += blockDim.x) {
                 float4 v = rec[(int64_t)s0 * REC_DISP + q];
                 if (q % REC_DISP == 0) {            // source position, shifted in fp64
                     v.x = (float)((double)v.x - cx);
@@ -83,7 +83,7 @@ check_potential_kernel(const int* __restrict__ tbox, const int* __restrict__ sof
     }
 #pragma unroll
     for (int q = 0; q < KPT; ++q) {
-        const int k = threadIdx.x + q * CP_T;
+        const int k = threadIdx.x + q * blockDim.x;
         if (k < nc) {
             float* o = Q + (int64_t)i * ldq + 3 * k;
             o[0] = acc[q][0];
@@ -632,9 +632,12 @@ static void launch_check(const Tree& t, const int* tbox, int n, const int* soff,
     const Plan& P = *t.plan;
     BoxGeo geo{t.origin[0], t.origin[1], t.origin[2], t.side};
     KConst kc = make_kconst(t.mat);
-    const int kpt = ceil_div(P.nc, CP_T);
+    const int kpt = ceil_div(P.nc, CP_T);      // 2 or 3 points per thread measured slower
+    // the fewest whole warps that cover the surface with kpt points per thread (p = 6:
+    // 218 points -> 224 threads, not 256)
+    const int nthr = 32 * ceil_div(ceil_div(P.nc, kpt), 32);
 #define EB_CHECK_LAUNCH_KPT(K)                                                                                     \
-    check_potential_kernel<SL, DL, K><<<n, CP_T, 0, s>>>(tbox, soff, sidx, t.sbeg.p, t.send.p, t.anchor.p,         \
+    check_potential_kernel<SL, DL, K><<<n, nthr, 0, s>>>(tbox, soff, sidx, t.sbeg.p, t.send.p, t.anchor.p,         \
                                                          t.level.p, geo, rad, P.s_c.p, P.nc, t.rec_disp.p, kc,    \
                                                          t.Q.p, P.ldc)
     switch (kpt) {
