@@ -595,11 +595,11 @@ void schedule_tree(Tree& t, cudaStream_t s) {
         tc_make_map_b(&t.mZs, t.Zs.p, std::max(1, t.n_up), me, lde);
         tc_make_map_b(&t.mWb, t.Wb.p, std::max(1, t.n_dn), me, lde);
         tc_make_map_b(&t.mWs, t.Ws.p, std::max(1, t.n_dn), me, lde);
-        tc_build_tiles(t.q2z_up, me, false);
-        tc_build_tiles(t.q2z_dn, me, false);
-        tc_build_tiles(t.m2l, me, t.tc_fast);
-        for (auto& x : t.m2m) tc_build_tiles(x, me, false);
-        for (auto& x : t.l2l) tc_build_tiles(x, me, false);
+        tc_build_tiles(t.q2z_up, me, mc, false);
+        tc_build_tiles(t.q2z_dn, me, mc, false);
+        tc_build_tiles(t.m2l, me, me, t.tc_fast);
+        for (auto& x : t.m2m) tc_build_tiles(x, me, me, false);
+        for (auto& x : t.l2l) tc_build_tiles(x, me, me, false);
     }
     if (t.far64) {
         t.PHID.alloc((size_t)std::max(1, t.n_phid) * me);
@@ -663,7 +663,7 @@ void tree_precise(Tree& t, cudaStream_t s) {
     }
     if (t.tc_fast) {
         t.tc_fast = false;
-        tc_build_tiles(t.m2l, P.me, false);
+        tc_build_tiles(t.m2l, P.me, P.me, false);
     }
     EB_CUDA(cudaStreamSynchronize(s));
 }

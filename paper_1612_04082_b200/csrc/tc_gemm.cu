@@ -92,6 +92,7 @@ __device__ __forceinline__ void mma_commit(uint32_t bar) {
 
 struct Tile {
     int op, p0, np, m0;
+    int kc0, kc1;        // K chunks [kc0, kc1) of this tile (split K on small launches)
 };
 
 // The tensor core's fp32 accumulation is not round-to-nearest: chaining all K/8 MMAs
@@ -156,8 +157,7 @@ tc_pairs_kernel(const __grid_constant__ CUtensorMap mapAb, const __grid_constant
     uint32_t* tmem_slot = (uint32_t*)(bars + 2 * STAGES + 8);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int nk = (K + BK - 1) / BK;
-    const int ngroups = (nk + GROUP - 1) / GROUP;
+    (void)K;
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) {
@@ -196,7 +196,7 @@ tc_pairs_kernel(const __grid_constant__ CUtensorMap mapAb, const __grid_constant
             if (gact)
 #pragma unroll
                 for (int q = 0; q < 4; ++q) r[q] = pairs[tl.p0 + min(4 * gi + q, tl.np - 1)].y;
-            for (int kc = 0; kc < nk; ++kc, ++c) {
+            for (int kc = tl.kc0; kc < tl.kc1; ++kc, ++c) {
                 const int s = c % STAGES;
                 mbar_wait(smem_u32(&empty_b[s]), ((c / STAGES) & 1) ^ 1);
                 uint8_t* st = smem + s * STAGE_BYTES;
@@ -226,10 +226,12 @@ tc_pairs_kernel(const __grid_constant__ CUtensorMap mapAb, const __grid_constant
             mbar_wait(smem_u32(&core_b[cb]), ((it >> 1) & 1) ^ 1);   // correction buffer drained
             asm volatile("tcgen05.fence::after_thread_sync;");
             const uint32_t dcorr = tmem + (uint32_t)((2 + cb) * BN);
-            for (int kc = 0; kc < nk; ++kc, ++c) {
+            const int kc0 = tiles[ti].kc0, kc1 = tiles[ti].kc1;
+            for (int kc = kc0; kc < kc1; ++kc, ++c) {
                 const int s = c % STAGES;
                 const int b = G & 1;
-                const bool gfirst = (kc % GROUP) == 0, glast = (kc % GROUP) == GROUP - 1 || kc == nk - 1;
+                const bool gfirst = ((kc - kc0) % GROUP) == 0,
+                           glast = ((kc - kc0) % GROUP) == GROUP - 1 || kc == kc1 - 1;
                 if (gfirst) {   // the main buffer must have been drained
                     mbar_wait(smem_u32(&acce_b[b]), ((G >> 1) & 1) ^ 1);
                     asm volatile("tcgen05.fence::after_thread_sync;");
@@ -245,12 +247,12 @@ tc_pairs_kernel(const __grid_constant__ CUtensorMap mapAb, const __grid_constant
                     for (int k = 0; k < ksteps; ++k) {
                         const uint64_t off = (uint64_t)(2 * k);          // +32 B in 16-B units
                         mma_tf32(dmain, ab + off, bb + off, idesc, (!gfirst) | (k != 0));
-                        mma_tf32(dcorr, ab + off, bs + off, idesc, (kc | k) != 0);
+                        mma_tf32(dcorr, ab + off, bs + off, idesc, kc != kc0 || k != 0);
                         mma_tf32(dcorr, as + off, bb + off, idesc, 1);
                     }
                     mma_commit(smem_u32(&empty_b[s]));                   // frees the smem stage
                     if (glast) mma_commit(smem_u32(&accf_b[b]));          // group partial ready
-                    if (kc == nk - 1) mma_commit(smem_u32(&corf_b[cb]));  // corrections ready
+                    if (kc == kc1 - 1) mma_commit(smem_u32(&corf_b[cb]));  // corrections ready
                 }
                 __syncwarp();
                 if (glast) ++G;
@@ -266,6 +268,7 @@ tc_pairs_kernel(const __grid_constant__ CUtensorMap mapAb, const __grid_constant
             float acc[BN];
 #pragma unroll
             for (int j = 0; j < BN; ++j) acc[j] = 0.f;
+            const int ngroups = (tl.kc1 - tl.kc0 + GROUP - 1) / GROUP;
             for (int g = 0; g < ngroups; ++g, ++G) {
                 const int b = G & 1;
                 mbar_wait(smem_u32(&accf_b[b]), (G >> 1) & 1);
@@ -331,7 +334,6 @@ tc_pairs_fast_kernel(const __grid_constant__ CUtensorMap mapAb, const __grid_con
     uint32_t* tmem_slot = (uint32_t*)(bars + 2 * STAGES + 4);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int nk = (K + BK - 1) / BK;
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(smem_u32(&full_b[s]), 1 + 32 * fast::NPROD);   // A expect_tx + cp.async arrivals
@@ -368,7 +370,7 @@ tc_pairs_fast_kernel(const __grid_constant__ CUtensorMap mapAb, const __grid_con
                 const int r = rsub + 4 * (pi + fast::NPROD * g);
                 srow[g] = (int64_t)__ldg(&pairs[tl.p0 + min(r, tl.np - 1)].y) * ldb;
             }
-            for (int kc = 0; kc < nk; ++kc, ++c) {
+            for (int kc = tl.kc0; kc < tl.kc1; ++kc, ++c) {
                 const int s = c % STAGES;
                 mbar_wait(smem_u32(&empty_b[s]), ((c / STAGES) & 1) ^ 1);
                 uint8_t* st = smem + s * STAGE_BYTES;
@@ -413,7 +415,8 @@ tc_pairs_fast_kernel(const __grid_constant__ CUtensorMap mapAb, const __grid_con
             const int ab = it & 1;
             mbar_wait(smem_u32(&acce_b[ab]), ((it >> 1) & 1) ^ 1);
             asm volatile("tcgen05.fence::after_thread_sync;");
-            for (int kc = 0; kc < nk; ++kc, ++c) {
+            const int kc0 = tiles[ti].kc0, kc1 = tiles[ti].kc1;
+            for (int kc = kc0; kc < kc1; ++kc, ++c) {
                 const int s = c % STAGES;
                 mbar_wait(smem_u32(&full_b[s]), (c / STAGES) & 1);
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // cp.async data -> tensor core
@@ -429,13 +432,13 @@ tc_pairs_fast_kernel(const __grid_constant__ CUtensorMap mapAb, const __grid_con
                             const uint64_t a_b = smem_desc(st + (2 * mt) * OPND_BYTES) + off;
                             const uint64_t a_s = smem_desc(st + (2 * mt + 1) * OPND_BYTES) + off;
                             const uint32_t d = tmem + (uint32_t)((ab * MT + mt) * BN);
-                            mma_tf32(d, a_b, bb + off, idesc, (kc | k) != 0);
+                            mma_tf32(d, a_b, bb + off, idesc, kc != kc0 || k != 0);
                             mma_tf32(d, a_b, bs + off, idesc, 1);
                             mma_tf32(d, a_s, bb + off, idesc, 1);
                         }
                     }
                     mma_commit(smem_u32(&empty_b[s]));
-                    if (kc == nk - 1) mma_commit(smem_u32(&accf_b[ab]));
+                    if (kc == kc1 - 1) mma_commit(smem_u32(&accf_b[ab]));
                 }
                 __syncwarp();
             }
@@ -553,13 +556,29 @@ void tc_split_rows(const XT* X, int ld, int64_t row0, int64_t nrows, int K, floa
 template void tc_split_rows<float>(const float*, int, int64_t, int64_t, int, float*, float*, cudaStream_t);
 template void tc_split_rows<double>(const double*, int, int64_t, int64_t, int, float*, float*, cudaStream_t);
 
-void tc_build_tiles(OpPairs& P, int M, bool fast) {
+// Tiles in operator-major order.  Launches with fewer tiles than SMs (the coarse M2M/L2L
+// levels) split K over several CTAs: a lone tile streams its 15 K chunks through one SM in
+// ~20 us, while its partial sums are added by the fp64 atomics of the epilogue anyway.
+void tc_build_tiles(OpPairs& P, int M, int K, bool fast) {
     std::vector<tc::Tile> t;
     const int mstep = fast ? tc::fast::MT * tc::BM : tc::BM;
+    const int nk = (K + tc::BK - 1) / tc::BK;
     for (int o = 0; o < P.nops; ++o)
         for (int p0 = P.op_ptr_h[o]; p0 < P.op_ptr_h[o + 1]; p0 += tc::BN)
             for (int m0 = 0; m0 < M; m0 += mstep)
-                t.push_back({o, p0, std::min(tc::BN, P.op_ptr_h[o + 1] - p0), m0});
+                t.push_back({o, p0, std::min(tc::BN, P.op_ptr_h[o + 1] - p0), m0, 0, nk});
+    const int nsplit = fast || t.empty() ? 1 : std::max(1, std::min(nk / 3, num_sms() / (int)t.size()));
+    if (nsplit > 1) {
+        std::vector<tc::Tile> u;
+        for (const tc::Tile& x : t)
+            for (int q = 0; q < nsplit; ++q) {
+                tc::Tile y = x;
+                y.kc0 = nk * q / nsplit;
+                y.kc1 = nk * (q + 1) / nsplit;
+                u.push_back(y);
+            }
+        t.swap(u);
+    }
     P.ntiles = (int)t.size();
     P.tiles.alloc(std::max<size_t>(t.size(), 1) * sizeof(tc::Tile) / sizeof(int));
     if (!t.empty()) EB_CUDA(cudaMemcpy(P.tiles.p, t.data(), t.size() * sizeof(tc::Tile), cudaMemcpyHostToDevice));
