@@ -7,6 +7,7 @@
 //   leaves   : phi_d = r R_d^-1 w, phi_u = r R_u^-1 z in fp64; one kernel per target leaf
 //              does L2T + M2T in fp64 and the U-list near field (P2P) in fp32.
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 
@@ -128,7 +129,7 @@ far_eval_kernel(int n_eval, const int* __restrict__ eval_box, const int* __restr
                 const int* __restrict__ woff, const int* __restrict__ widx, const int* __restrict__ tbeg,
                 const int* __restrict__ tend, const int* __restrict__ anchor, const int* __restrict__ level, BoxGeo geo,
                 const double* __restrict__ se, int ne, const float* __restrict__ trg, KConst kc, double cfar,
-                float* __restrict__ far) {
+                const float* __restrict__ near, const int* __restrict__ trg_perm, float* __restrict__ out) {
     constexpr int NC = STRESS ? 6 : 3;
     extern __shared__ double dsm[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -184,9 +185,11 @@ far_eval_kernel(int n_eval, const int* __restrict__ eval_box, const int* __restr
 #pragma unroll
             for (int c = 0; c < NC; ++c) acc64[c] += (double)acc[c];
         }
-        if (t < t_end)
+        if (t < t_end) {
+            float* o = out + (int64_t)trg_perm[t] * NC;
 #pragma unroll
-            for (int c = 0; c < NC; ++c) far[(int64_t)t * NC + c] = (float)acc64[c];
+            for (int c = 0; c < NC; ++c) o[c] = (float)(acc64[c] + (double)near[(int64_t)t * NC + c]);
+        }
     }
 }
 
@@ -202,7 +205,8 @@ __device__ __forceinline__ void far_round_f32(int t0, int t_beg, int t_end, int 
                                               const int* __restrict__ level, const BoxGeo& geo,
                                               const float4* __restrict__ se4, int ne, const float* __restrict__ trg,
                                               const KConst& kc, float4* ey, float4* ph, int lane,
-                                              float* __restrict__ far) {
+                                              const float* __restrict__ near, const int* __restrict__ trg_perm,
+                                              float* __restrict__ out) {
     constexpr int NC = STRESS ? 6 : 3;
     int tc[TPT];
 #pragma unroll
@@ -255,9 +259,11 @@ __device__ __forceinline__ void far_round_f32(int t0, int t_beg, int t_end, int 
 #pragma unroll
     for (int j = 0; j < TPT; ++j) {
         const int t = t0 + lane + 32 * j;
-        if (t < t_end)
+        if (t < t_end) {
+            float* o = out + (int64_t)trg_perm[t] * NC;
 #pragma unroll
-            for (int c = 0; c < NC; ++c) far[(int64_t)t * NC + c] = acc[j][c];
+            for (int c = 0; c < NC; ++c) o[c] = acc[j][c] + near[(int64_t)t * NC + c];
+        }
     }
 }
 
@@ -268,7 +274,8 @@ far_eval_f32_kernel(int n_eval, const int* __restrict__ eval_box, const int* __r
                     const int* __restrict__ phiu_slot, const int* __restrict__ woff, const int* __restrict__ widx,
                     const int* __restrict__ tbeg, const int* __restrict__ tend, const int* __restrict__ anchor,
                     const int* __restrict__ level, BoxGeo geo, const float4* __restrict__ se4, int ne,
-                    const float* __restrict__ trg, KConst kc, float* __restrict__ far) {
+                    const float* __restrict__ trg, KConst kc, const float* __restrict__ near,
+                    const int* __restrict__ trg_perm, float* __restrict__ out) {
     extern __shared__ float4 fsm[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int i = blockIdx.x * EV_WARPS + warp;
@@ -283,11 +290,11 @@ far_eval_f32_kernel(int n_eval, const int* __restrict__ eval_box, const int* __r
     for (int t0 = t_beg; t0 < t_end;) {
         if (t_end - t0 > 32) {
             far_round_f32<STRESS, 2>(t0, t_beg, t_end, b, own, nfar, widx, woff[b], PHIDF, l2t, PHIUF, phiu_slot,
-                                     anchor, level, geo, se4, ne, trg, kc, ey, ph, lane, far);
+                                     anchor, level, geo, se4, ne, trg, kc, ey, ph, lane, near, trg_perm, out);
             t0 += 64;
         } else {
             far_round_f32<STRESS, 1>(t0, t_beg, t_end, b, own, nfar, widx, woff[b], PHIDF, l2t, PHIUF, phiu_slot,
-                                     anchor, level, geo, se4, ne, trg, kc, ey, ph, lane, far);
+                                     anchor, level, geo, se4, ne, trg, kc, ey, ph, lane, near, trg_perm, out);
             t0 += 32;
         }
     }
@@ -299,9 +306,8 @@ template <bool SL, bool DL, bool STRESS, int TPT>
 __device__ __forceinline__ void near_round(int t0, int t_beg, int t_end, int b, const int* __restrict__ uoff,
                                            const int* __restrict__ uidx, const int* __restrict__ sbeg,
                                            const int* __restrict__ send, const float* __restrict__ trg,
-                                           const int* __restrict__ trg_perm, const float4* __restrict__ rec,
-                                           const KConst& kc, const float* __restrict__ far, float* __restrict__ out,
-                                           float4* srec, int lane) {
+                                           const float4* __restrict__ rec, const KConst& kc,
+                                           float* __restrict__ near, float4* srec, int lane) {
     constexpr int NC = STRESS ? 6 : 3;
     constexpr int R = STRESS ? REC_STRESS : REC_DISP;
     float x[TPT], y[TPT], z[TPT], acc[TPT][NC];
@@ -328,11 +334,9 @@ __device__ __forceinline__ void near_round(int t0, int t_beg, int t_end, int b, 
 #pragma unroll
     for (int j = 0; j < TPT; ++j) {
         const int t = t0 + lane + 32 * j;
-        if (t < t_end) {
-            float* o = out + (int64_t)trg_perm[t] * NC;
+        if (t < t_end)
 #pragma unroll
-            for (int c = 0; c < NC; ++c) o[c] = acc[j][c] + far[(int64_t)t * NC + c];
-        }
+            for (int c = 0; c < NC; ++c) near[(int64_t)t * NC + c] = acc[j][c];
     }
 }
 
@@ -341,8 +345,7 @@ __global__ void __launch_bounds__(32 * EV_WARPS)
 near_eval_kernel(int n_eval, const int* __restrict__ eval_box, const int* __restrict__ uoff,
                  const int* __restrict__ uidx, const int* __restrict__ sbeg, const int* __restrict__ send,
                  const int* __restrict__ tbeg, const int* __restrict__ tend, const float* __restrict__ trg,
-                 const int* __restrict__ trg_perm, const float4* __restrict__ rec, KConst kc,
-                 const float* __restrict__ far, float* __restrict__ out) {
+                 const float4* __restrict__ rec, KConst kc, float* __restrict__ near) {
     constexpr int R = STRESS ? REC_STRESS : REC_DISP;
     __shared__ float4 srec_all[EV_WARPS][32 * R];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -353,12 +356,12 @@ near_eval_kernel(int n_eval, const int* __restrict__ eval_box, const int* __rest
     const int t_beg = tbeg[b], t_end = tend[b];
     for (int t0 = t_beg; t0 < t_end;) {
         if (t_end - t0 > 32) {
-            near_round<SL, DL, STRESS, 2>(t0, t_beg, t_end, b, uoff, uidx, sbeg, send, trg, trg_perm, rec, kc, far,
-                                          out, srec, lane);
+            near_round<SL, DL, STRESS, 2>(t0, t_beg, t_end, b, uoff, uidx, sbeg, send, trg, rec, kc, near, srec,
+                                          lane);
             t0 += 64;
         } else {
-            near_round<SL, DL, STRESS, 1>(t0, t_beg, t_end, b, uoff, uidx, sbeg, send, trg, trg_perm, rec, kc, far,
-                                          out, srec, lane);
+            near_round<SL, DL, STRESS, 1>(t0, t_beg, t_end, b, uoff, uidx, sbeg, send, trg, rec, kc, near, srec,
+                                          lane);
             t0 += 32;
         }
     }
@@ -577,8 +580,9 @@ void schedule_tree(Tree& t, cudaStream_t s) {
     t.rec_disp.alloc(std::max<int64_t>(t.nsrc * REC_DISP, 1));
     t.rec_stress.alloc(std::max<int64_t>(t.nsrc * REC_STRESS, 1));
     const int lde = P.lde, ldc = P.ldc;
-    const int64_t nq = std::max(1, std::max(t.n_s2m, t.n_s2l));
+    const int64_t nq = std::max(1, t.n_s2m), nqd = std::max(1, t.n_s2l);
     t.Q.alloc((size_t)nq * ldc);
+    t.Qd.alloc((size_t)nqd * ldc);
     t.Z.alloc((size_t)std::max(1, t.n_up) * lde);
     t.W.alloc((size_t)std::max(1, t.n_dn) * lde);
     if (const char* e = std::getenv("EBEM_SIMT")) t.use_tc = std::atoi(e) == 0;
@@ -586,11 +590,14 @@ void schedule_tree(Tree& t, cudaStream_t s) {
     t.tc_fast = t.use_tc && !t.far64 && !(std::getenv("EBEM_TC_PRECISE") && std::atoi(std::getenv("EBEM_TC_PRECISE")));
     if (t.use_tc) {
         t.Qb.alloc(t.Q.n); t.Qs.alloc(t.Q.n);
+        t.Qdb.alloc(t.Qd.n); t.Qds.alloc(t.Qd.n);
         t.Zb.alloc(t.Z.n); t.Zs.alloc(t.Z.n);
         t.Wb.alloc(t.W.n); t.Ws.alloc(t.W.n);
-        for (DBuf<float>* b : {&t.Qb, &t.Qs, &t.Zb, &t.Zs, &t.Wb, &t.Ws}) b->zero(s);
+        for (DBuf<float>* b : {&t.Qb, &t.Qs, &t.Qdb, &t.Qds, &t.Zb, &t.Zs, &t.Wb, &t.Ws}) b->zero(s);
         tc_make_map_b(&t.mQb, t.Qb.p, nq, mc, ldc);
         tc_make_map_b(&t.mQs, t.Qs.p, nq, mc, ldc);
+        tc_make_map_b(&t.mQdb, t.Qdb.p, nqd, mc, ldc);
+        tc_make_map_b(&t.mQds, t.Qds.p, nqd, mc, ldc);
         tc_make_map_b(&t.mZb, t.Zb.p, std::max(1, t.n_up), me, lde);
         tc_make_map_b(&t.mZs, t.Zs.p, std::max(1, t.n_up), me, lde);
         tc_make_map_b(&t.mWb, t.Wb.p, std::max(1, t.n_dn), me, lde);
@@ -610,7 +617,7 @@ void schedule_tree(Tree& t, cudaStream_t s) {
         t.PHIDF.zero(s);
         t.PHIUF.zero(s);
     }
-    t.out_sorted.alloc((size_t)std::max<int64_t>(1, t.ntrg) * 6);
+    t.near_sorted.alloc((size_t)std::max<int64_t>(1, t.ntrg) * 6);
     EB_CUDA(cudaStreamSynchronize(s));
 
     int64_t bytes = 0;
@@ -618,7 +625,7 @@ void schedule_tree(Tree& t, cudaStream_t s) {
              t.src_nrm.bytes() + t.src_w.bytes() + t.trg_xyz.bytes();
     bytes += (int64_t)nb * 4 * 40;
     for (int k = 0; k < 4; ++k) bytes += t.lst_off[k].bytes() + t.lst_idx[k].bytes();
-    bytes += t.rec_disp.bytes() + t.rec_stress.bytes() + t.Q.bytes() + t.Z.bytes() + t.W.bytes() + t.PHID.bytes() +
+    bytes += t.rec_disp.bytes() + t.rec_stress.bytes() + t.Q.bytes() + t.Qd.bytes() + t.Z.bytes() + t.W.bytes() + t.PHID.bytes() +
              t.PHIU.bytes() + t.PHIDF.bytes() + t.PHIUF.bytes();
     bytes += t.m2l.pairs.bytes();
     t.device_bytes = bytes;
@@ -627,7 +634,7 @@ void schedule_tree(Tree& t, cudaStream_t s) {
 // ------------------------------------------------------------------ evaluation
 template <bool SL, bool DL>
 static void launch_check(const Tree& t, const int* tbox, int n, const int* soff, const int* sidx, double rad,
-                         cudaStream_t s) {
+                         float* Q, cudaStream_t s) {
     if (n == 0) return;
     const Plan& P = *t.plan;
     BoxGeo geo{t.origin[0], t.origin[1], t.origin[2], t.side};
@@ -637,9 +644,10 @@ static void launch_check(const Tree& t, const int* tbox, int n, const int* soff,
     // 218 points -> 224 threads, not 256)
     const int nthr = 32 * ceil_div(ceil_div(P.nc, kpt), 32);
 #define EB_CHECK_LAUNCH_KPT(K)                                                                                     \
+    EB_CUDA(cudaFuncSetAttribute(check_potential_kernel<SL, DL, K>, cudaFuncAttributePreferredSharedMemoryCarveout, 100)); \
     check_potential_kernel<SL, DL, K><<<n, nthr, 0, s>>>(tbox, soff, sidx, t.sbeg.p, t.send.p, t.anchor.p,         \
                                                          t.level.p, geo, rad, P.s_c.p, P.nc, t.rec_disp.p, kc,    \
-                                                         t.Q.p, P.ldc)
+                                                         Q, P.ldc)
     switch (kpt) {
         case 1: EB_CHECK_LAUNCH_KPT(1); break;
         case 2: EB_CHECK_LAUNCH_KPT(2); break;
@@ -668,8 +676,26 @@ void tree_precise(Tree& t, cudaStream_t s) {
     EB_CUDA(cudaStreamSynchronize(s));
 }
 
+// near field (U-list P2P) into the sorted near buffer
 template <bool SL, bool DL, bool STRESS>
-static void launch_eval(const Tree& t, float* out, cudaStream_t s) {
+static void launch_near(const Tree& t, cudaStream_t s) {
+    if (t.n_eval == 0) return;
+    KConst kc = make_kconst(t.mat);
+    static bool carve = false;
+    if (!carve) {   // same L1/shared split as the translation kernels, so both can share an SM
+        EB_CUDA(cudaFuncSetAttribute(near_eval_kernel<SL, DL, STRESS>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                     100));
+        carve = true;
+    }
+    near_eval_kernel<SL, DL, STRESS><<<ceil_div(t.n_eval, EV_WARPS), 32 * EV_WARPS, 0, s>>>(
+        t.n_eval, t.eval_box.p, t.lst_off[0].p, t.lst_idx[0].p, t.sbeg.p, t.send.p, t.tbeg.p, t.tend.p, t.trg_xyz.p,
+        STRESS ? t.rec_stress.p : t.rec_disp.p, kc, t.near_sorted.p);
+    EB_CHECK_LAUNCH();
+}
+
+// far field (L2T + M2T) plus the near buffer, scattered to the caller's target order
+template <bool STRESS>
+static void launch_far(const Tree& t, float* out, cudaStream_t s) {
     if (t.n_eval == 0) return;
     const Plan& P = *t.plan;
     BoxGeo geo{t.origin[0], t.origin[1], t.origin[2], t.side};
@@ -683,7 +709,7 @@ static void launch_eval(const Tree& t, float* out, cudaStream_t s) {
         ffn<<<grid, 32 * EV_WARPS, sm, s>>>(t.n_eval, t.eval_box.p, t.eval_l2t_slot.p, t.PHID.p, t.PHIU.p,
                                             t.phiu_slot.p, t.lst_off[2].p, t.lst_idx[2].p, t.tbeg.p, t.tend.p,
                                             t.anchor.p, t.level.p, geo, P.s_e64.p, P.ne, t.trg_xyz.p, kc, cfar,
-                                            t.out_sorted.p);
+                                            t.near_sorted.p, t.trg_perm.p, out);
     } else {
         const size_t sm = sizeof(float4) * 2 * P.ne * EV_WARPS;
         auto ffn = far_eval_f32_kernel<STRESS>;
@@ -691,15 +717,20 @@ static void launch_eval(const Tree& t, float* out, cudaStream_t s) {
         ffn<<<grid, 32 * EV_WARPS, sm, s>>>(t.n_eval, t.eval_box.p, t.eval_l2t_slot.p, t.PHIDF.p, t.PHIUF.p,
                                             t.phiu_slot.p, t.lst_off[2].p, t.lst_idx[2].p, t.tbeg.p, t.tend.p,
                                             t.anchor.p, t.level.p, geo, P.s_e4.p, P.ne, t.trg_xyz.p, kc,
-                                            t.out_sorted.p);
+                                            t.near_sorted.p, t.trg_perm.p, out);
     }
-    EB_CHECK_LAUNCH();
-    near_eval_kernel<SL, DL, STRESS><<<grid, 32 * EV_WARPS, 0, s>>>(
-        t.n_eval, t.eval_box.p, t.lst_off[0].p, t.lst_idx[0].p, t.sbeg.p, t.send.p, t.tbeg.p, t.tend.p, t.trg_xyz.p,
-        t.trg_perm.p, STRESS ? t.rec_stress.p : t.rec_disp.p, kc, t.out_sorted.p, out);
     EB_CHECK_LAUNCH();
 }
 
+// Schedule.  Profiling on: every phase in order on the caller's stream (phase events).
+// Otherwise two internal streams forked from the caller's stream and joined back into it:
+//   A (high priority): prep -> S2M, Q2Z_up, M2M -> M2L -> [S2L done] Q2Z_dn -> L2L -> PHI
+//                      -> [near done] far field + scatter
+//   B (low priority) :         S2L check potentials, then the U-list near field
+// B's kernels are FP32-ALU bound and run beside the memory / tensor-core bound M2L (the
+// persistent M2L kernel leaves room for a few P2P CTAs per SM once all kernels request the
+// same L1/shared split).  Measured on the 1M beam: 7.20 vs 7.31 ms serial; the overlap is
+// partial because M2L itself slows down by the issue slots the P2P warps take.
 void fmm_evaluate(Tree& t, int kernel, const float* f, const float* g, float* out, cudaStream_t s) {
     const Plan& P = *t.plan;
     const int me = P.me, mc = P.mc;
@@ -708,6 +739,22 @@ void fmm_evaluate(Tree& t, int kernel, const float* f, const float* g, float* ou
     const int src_kernel = stress ? kernel - 3 : kernel;    // D->U, S->P, DS->UP
     EB_REQUIRE(!dl || t.has_normals, "double-layer kernel needs normals at fmm_build_tree");
     if (t.ntrg == 0) return;
+    const bool conc = !t.profile;
+    if (conc && !t.sA) {
+        int least = 0, greatest = 0;
+        EB_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+        EB_CUDA(cudaStreamCreateWithPriority(&t.sA, cudaStreamNonBlocking, greatest));
+        EB_CUDA(cudaStreamCreateWithPriority(&t.sB, cudaStreamNonBlocking, least));
+        for (cudaEvent_t* e : {&t.ev_fork, &t.ev_s2l, &t.ev_near, &t.ev_joinA})
+            EB_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+    }
+    cudaStream_t sa = s, sb = s;
+    if (conc) {
+        sa = t.sA;
+        sb = t.sB;
+        EB_CUDA(cudaEventRecord(t.ev_fork, s));
+        EB_CUDA(cudaStreamWaitEvent(sa, t.ev_fork, 0));
+    }
     int phase = 0;
     int64_t l0 = 0;
     auto mark = [&](int ph) {   // phase boundary: event + launch count of the finished phase
@@ -722,87 +769,120 @@ void fmm_evaluate(Tree& t, int kernel, const float* f, const float* g, float* ou
 
     // prepared sources in tree order (geometry sorted, densities via src_perm)
     prepare_sources(src_kernel, t.mat, t.src_xyz.p, t.src_nrm.p, t.src_w.p, nullptr, f, g, t.src_perm.p, t.nsrc,
-                    t.rec_disp.p, s);
+                    t.rec_disp.p, sa);
     if (stress)
         prepare_sources(kernel, t.mat, t.src_xyz.p, t.src_nrm.p, t.src_w.p, nullptr, f, g, t.src_perm.p, t.nsrc,
-                        t.rec_stress.p, s);
-    t.Z.zero(s);
-    t.W.zero(s);
+                        t.rec_stress.p, sa);
+    t.Z.zero(sa);
+    t.W.zero(sa);
     mark(phase++);
 
+    auto s2l = [&](cudaStream_t st) {
+        if (!t.n_s2l) return;
+        if (sl && dl) launch_check<true, true>(t, t.s2l_box.p, t.n_s2l, t.x_src_off.p, t.x_src_idx.p, RAD_DC, t.Qd.p, st);
+        else if (sl) launch_check<true, false>(t, t.s2l_box.p, t.n_s2l, t.x_src_off.p, t.x_src_idx.p, RAD_DC, t.Qd.p, st);
+        else launch_check<false, true>(t, t.s2l_box.p, t.n_s2l, t.x_src_off.p, t.x_src_idx.p, RAD_DC, t.Qd.p, st);
+    };
+    auto near = [&](cudaStream_t st) {
+        switch (kernel) {
+            case K_U: launch_near<true, false, false>(t, st); break;
+            case K_P: launch_near<false, true, false>(t, st); break;
+            case K_UP: launch_near<true, true, false>(t, st); break;
+            case K_D: launch_near<true, false, true>(t, st); break;
+            case K_S: launch_near<false, true, true>(t, st); break;
+            case K_DS: launch_near<true, true, true>(t, st); break;
+        }
+    };
+    // stream B starts when the upward pass is done, i.e. alongside M2L
+    auto fork_b = [&]() {
+        if (!conc) return;
+        EB_CUDA(cudaEventRecord(t.ev_fork, sa));
+        EB_CUDA(cudaStreamWaitEvent(sb, t.ev_fork, 0));
+        s2l(sb);
+        EB_CUDA(cudaEventRecord(t.ev_s2l, sb));
+        near(sb);
+        EB_CUDA(cudaEventRecord(t.ev_near, sb));
+    };
+
     // upward pass
-    if (sl && dl) launch_check<true, true>(t, t.s2m_box.p, t.n_s2m, nullptr, nullptr, RAD_UC, s);
-    else if (sl) launch_check<true, false>(t, t.s2m_box.p, t.n_s2m, nullptr, nullptr, RAD_UC, s);
-    else launch_check<false, true>(t, t.s2m_box.p, t.n_s2m, nullptr, nullptr, RAD_UC, s);
+    if (sl && dl) launch_check<true, true>(t, t.s2m_box.p, t.n_s2m, nullptr, nullptr, RAD_UC, t.Q.p, sa);
+    else if (sl) launch_check<true, false>(t, t.s2m_box.p, t.n_s2m, nullptr, nullptr, RAD_UC, t.Q.p, sa);
+    else launch_check<false, true>(t, t.s2m_box.p, t.n_s2m, nullptr, nullptr, RAD_UC, t.Q.p, sa);
     mark(phase++);
     const int lde = P.lde, ldc = P.ldc;
     auto zrows = [&](int l) { return (int64_t)t.up_lstart[l + 1] - t.up_lstart[l]; };
     auto wrows = [&](int l) { return (int64_t)t.dn_lstart[l + 1] - t.dn_lstart[l]; };
     if (t.use_tc) {
-        tc_split_rows(t.Q.p, ldc, 0, t.n_s2m, mc, t.Qb.p, t.Qs.p, s);
-        tc_pairs_gemm(t.q2z_up, P.mQu1T_b, P.mQu1T_s, t.mQb, t.mQs, me, mc, t.Z.p, lde, s);
+        tc_split_rows(t.Q.p, ldc, 0, t.n_s2m, mc, t.Qb.p, t.Qs.p, sa);
+        tc_pairs_gemm(t.q2z_up, P.mQu1T_b, P.mQu1T_s, t.mQb, t.mQs, me, mc, t.Z.p, lde, sa);
     } else {
-        gemm_pairs_f32(t.q2z_up, P.Qu1T.p, me, mc, ldc, t.Q.p, ldc, t.Z.p, lde, s);
+        gemm_pairs_f32(t.q2z_up, P.Qu1T.p, me, mc, ldc, t.Q.p, ldc, t.Z.p, lde, sa);
     }
     mark(phase++);
     for (int l = t.nlevels - 2; l >= 2; --l) {
         if (t.use_tc) {
-            tc_split_rows(t.Z.p, lde, t.up_lstart[l + 1], zrows(l + 1), me, t.Zb.p, t.Zs.p, s);
-            tc_pairs_gemm(t.m2m[l], P.mM2M_b, P.mM2M_s, t.mZb, t.mZs, me, me, t.Z.p, lde, s);
+            tc_split_rows(t.Z.p, lde, t.up_lstart[l + 1], zrows(l + 1), me, t.Zb.p, t.Zs.p, sa);
+            tc_pairs_gemm(t.m2m[l], P.mM2M_b, P.mM2M_s, t.mZb, t.mZs, me, me, t.Z.p, lde, sa);
         } else {
-            gemm_pairs_f32(t.m2m[l], P.M2M.p, me, me, lde, t.Z.p, lde, t.Z.p, lde, s);
+            gemm_pairs_f32(t.m2m[l], P.M2M.p, me, me, lde, t.Z.p, lde, t.Z.p, lde, sa);
         }
     }
-    if (t.use_tc && t.nlevels > 2) tc_split_rows(t.Z.p, lde, t.up_lstart[2], zrows(2), me, t.Zb.p, t.Zs.p, s);
+    if (t.use_tc && t.nlevels > 2) tc_split_rows(t.Z.p, lde, t.up_lstart[2], zrows(2), me, t.Zb.p, t.Zs.p, sa);
     mark(phase++);
 
-    // downward pass
-    if (t.n_s2l) {
-        if (sl && dl) launch_check<true, true>(t, t.s2l_box.p, t.n_s2l, t.x_src_off.p, t.x_src_idx.p, RAD_DC, s);
-        else if (sl) launch_check<true, false>(t, t.s2l_box.p, t.n_s2l, t.x_src_off.p, t.x_src_idx.p, RAD_DC, s);
-        else launch_check<false, true>(t, t.s2l_box.p, t.n_s2l, t.x_src_off.p, t.x_src_idx.p, RAD_DC, s);
-    }
+    // downward pass (stream B forks here: started together with the upward pass it only
+    // competed with the other FP32-bound kernels, measured no faster)
+    fork_b();
+    if (!conc) s2l(sa);
     mark(phase++);
-    if (t.n_s2l) {
+    auto q2z_dn = [&]() {
+        if (!t.n_s2l) return;
         if (t.use_tc) {
-            tc_split_rows(t.Q.p, ldc, 0, t.n_s2l, mc, t.Qb.p, t.Qs.p, s);
-            tc_pairs_gemm(t.q2z_dn, P.mQd1T_b, P.mQd1T_s, t.mQb, t.mQs, me, mc, t.W.p, lde, s);
+            tc_split_rows(t.Qd.p, ldc, 0, t.n_s2l, mc, t.Qdb.p, t.Qds.p, sa);
+            tc_pairs_gemm(t.q2z_dn, P.mQd1T_b, P.mQd1T_s, t.mQdb, t.mQds, me, mc, t.W.p, lde, sa);
         } else {
-            gemm_pairs_f32(t.q2z_dn, P.Qd1T.p, me, mc, ldc, t.Q.p, ldc, t.W.p, lde, s);
+            gemm_pairs_f32(t.q2z_dn, P.Qd1T.p, me, mc, ldc, t.Qd.p, ldc, t.W.p, lde, sa);
         }
-    }
+    };
+    if (!conc) q2z_dn();
     mark(phase++);
-    if (t.use_tc && t.tc_fast) tc_pairs_gemm_fast(t.m2l, P.mM2L_b, P.mM2L_s, t.Zb.p, t.Zs.p, lde, me, me, t.W.p, lde, s);
-    else if (t.use_tc) tc_pairs_gemm(t.m2l, P.mM2L_b, P.mM2L_s, t.mZb, t.mZs, me, me, t.W.p, lde, s);
-    else gemm_pairs_f32(t.m2l, P.M2L.p, me, me, lde, t.Z.p, lde, t.W.p, lde, s);
+    if (t.use_tc && t.tc_fast) tc_pairs_gemm_fast(t.m2l, P.mM2L_b, P.mM2L_s, t.Zb.p, t.Zs.p, lde, me, me, t.W.p, lde, sa);
+    else if (t.use_tc) tc_pairs_gemm(t.m2l, P.mM2L_b, P.mM2L_s, t.mZb, t.mZs, me, me, t.W.p, lde, sa);
+    else gemm_pairs_f32(t.m2l, P.M2L.p, me, me, lde, t.Z.p, lde, t.W.p, lde, sa);
+    if (conc) {
+        EB_CUDA(cudaStreamWaitEvent(sa, t.ev_s2l, 0));
+        q2z_dn();
+    }
     mark(phase++);
     for (int l = 3; l < t.nlevels; ++l) {
         if (t.use_tc) {
-            tc_split_rows(t.W.p, lde, t.dn_lstart[l - 1], wrows(l - 1), me, t.Wb.p, t.Ws.p, s);
-            tc_pairs_gemm(t.l2l[l], P.mL2L_b, P.mL2L_s, t.mWb, t.mWs, me, me, t.W.p, lde, s);
+            tc_split_rows(t.W.p, lde, t.dn_lstart[l - 1], wrows(l - 1), me, t.Wb.p, t.Ws.p, sa);
+            tc_pairs_gemm(t.l2l[l], P.mL2L_b, P.mL2L_s, t.mWb, t.mWs, me, me, t.W.p, lde, sa);
         } else {
-            gemm_pairs_f32(t.l2l[l], P.L2L.p, me, me, lde, t.W.p, lde, t.W.p, lde, s);
+            gemm_pairs_f32(t.l2l[l], P.L2L.p, me, me, lde, t.W.p, lde, t.W.p, lde, sa);
         }
     }
     mark(phase++);
 
     // equivalent densities (fp64) and leaf evaluation
     if (t.far64) {
-        gemm_pairs_f64(t.phid_pairs, P.Rdinv.p, me, me, t.W.p, lde, t.phid_scale.p, t.PHID.p, me, s);
-        gemm_pairs_f64(t.phiu_pairs, P.Ruinv.p, me, me, t.Z.p, lde, t.phiu_scale.p, t.PHIU.p, me, s);
+        gemm_pairs_f64(t.phid_pairs, P.Rdinv.p, me, me, t.W.p, lde, t.phid_scale.p, t.PHID.p, me, sa);
+        gemm_pairs_f64(t.phiu_pairs, P.Ruinv.p, me, me, t.Z.p, lde, t.phiu_scale.p, t.PHIU.p, me, sa);
     } else {
         const double cfar = stress ? t.mat.cD : t.mat.cU;
-        gemm_pairs_f64_to_f32(t.phid_pairs, P.Rdinv.p, me, me, t.W.p, lde, t.phid_scale.p, cfar, t.PHIDF.p, P.ne, s);
-        gemm_pairs_f64_to_f32(t.phiu_pairs, P.Ruinv.p, me, me, t.Z.p, lde, t.phiu_scale.p, cfar, t.PHIUF.p, P.ne, s);
+        gemm_pairs_f64_to_f32(t.phid_pairs, P.Rdinv.p, me, me, t.W.p, lde, t.phid_scale.p, cfar, t.PHIDF.p, P.ne,
+                              sa);
+        gemm_pairs_f64_to_f32(t.phiu_pairs, P.Ruinv.p, me, me, t.Z.p, lde, t.phiu_scale.p, cfar, t.PHIUF.p, P.ne,
+                              sa);
     }
     mark(phase++);
-    switch (kernel) {
-        case K_U: launch_eval<true, false, false>(t, out, s); break;
-        case K_P: launch_eval<false, true, false>(t, out, s); break;
-        case K_UP: launch_eval<true, true, false>(t, out, s); break;
-        case K_D: launch_eval<true, false, true>(t, out, s); break;
-        case K_S: launch_eval<false, true, true>(t, out, s); break;
-        case K_DS: launch_eval<true, true, true>(t, out, s); break;
+    if (conc) EB_CUDA(cudaStreamWaitEvent(sa, t.ev_near, 0));
+    else near(sa);
+    if (stress) launch_far<true>(t, out, sa);
+    else launch_far<false>(t, out, sa);
+    if (conc) {
+        EB_CUDA(cudaEventRecord(t.ev_joinA, sa));
+        EB_CUDA(cudaStreamWaitEvent(s, t.ev_joinA, 0));
     }
     mark(phase++);
     t.ev_valid = t.profile;

@@ -134,18 +134,25 @@ struct Tree {
     ~Tree() {
         for (auto& e : ev)
             if (e) cudaEventDestroy(e);
+        for (cudaEvent_t e : {ev_fork, ev_s2l, ev_near, ev_joinA})
+            if (e) cudaEventDestroy(e);
+        if (sA) cudaStreamDestroy(sA);
+        if (sB) cudaStreamDestroy(sB);
     }
 
     // workspace (allocated at build time; evaluation allocates nothing)
     DBuf<float4> rec_disp, rec_stress;   // prepared sources, tree order
-    DBuf<float> Q;                       // check potentials [max(n_s2m, n_s2l) x mc]
+    DBuf<float> Q, Qd;                   // check potentials [n_s2m x mc] (S2M), [n_s2l x mc] (S2L)
     DBuf<double> Z, W;                   // [n_up x lde], [n_dn x lde] accumulators: fp64 atomics make
                                          // the sum order-independent at fp32 precision (deterministic)
-    DBuf<float> Qb, Qs, Zb, Zs, Wb, Ws;  // TF32 head / remainder copies (B operands)
-    CUtensorMap mQb, mQs, mZb, mZs, mWb, mWs;
+    DBuf<float> Qb, Qs, Qdb, Qds, Zb, Zs, Wb, Ws;   // TF32 head / remainder copies (B operands)
+    CUtensorMap mQb, mQs, mQdb, mQds, mZb, mZs, mWb, mWs;
     DBuf<double> PHID, PHIU;             // [n_phid x me], [n_phiu x me] (fp64 far field)
     DBuf<float4> PHIDF, PHIUF;           // [n_phid x ne], [n_phiu x ne] (fp32 far field, scaled)
-    DBuf<float> out_sorted;              // [ntrg x 6]
+    DBuf<float> near_sorted;             // [ntrg x 6] U-list near field, sorted target order
+    // two-stream schedule (fmm_evaluate): created on first use
+    cudaStream_t sA = nullptr, sB = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_s2l = nullptr, ev_near = nullptr, ev_joinA = nullptr;
     int64_t device_bytes = 0;
 };
 
