@@ -107,3 +107,27 @@ def test_fmm_deterministic(eb, beam20k):
     a = eb.fmm_matvec(tree, eb.KERNEL_UP, t["f"], t["g"]).cpu().numpy()
     b = eb.fmm_matvec(tree, eb.KERNEL_UP, t["f"], t["g"]).cpu().numpy()
     assert np.array_equal(a, b)
+
+
+def test_fmm_matvec_in_cuda_graph(eb, beam20k):
+    """the evaluation allocates nothing and only enqueues work (two internal streams forked
+    from and joined back into the caller's stream), so it can be captured and replayed."""
+    d, _ = beam20k
+    t = to_dev(d)
+    tree = eb.fmm_build_tree(t["src"], t["nrm"], t["w"], max_pts=64, p=6, K=d["K"], G=d["G"])
+    f, g = t["f"].clone(), t["g"].clone()
+    eager = eb.fmm_matvec(tree, eb.KERNEL_UP, f, g).cpu().numpy()
+    out = torch.empty_like(t["f"])
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):                      # warm-up on the capture stream
+        eb.fmm_matvec(tree, eb.KERNEL_UP, f, g, out=out)
+    torch.cuda.current_stream().wait_stream(s)
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        eb.fmm_matvec(tree, eb.KERNEL_UP, f, g, out=out)
+    f.mul_(2.0)
+    g.mul_(2.0)
+    graph.replay()
+    torch.cuda.synchronize()
+    np.testing.assert_allclose(out.cpu().numpy(), 2.0 * eager, rtol=0, atol=1e-6 * np.abs(eager).max())
