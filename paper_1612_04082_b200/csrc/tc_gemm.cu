@@ -386,12 +386,13 @@ tc_pairs_fast_kernel(const __grid_constant__ CUtensorMap mapAb, const __grid_con
                 }
                 const int col = kc * BK + 4 * piece;
                 const uint32_t nb = col < ldb ? 16u : 0u;      // zero-fill past the row
+                const int ngrp = ((tl.np + 15) & ~15) / 4;     // row groups the MMA reads (N)
                 const uint32_t b0 = smem_u32(st + 2 * MT * OPND_BYTES);
                 const uint32_t b1 = b0 + OPND_BYTES;
 #pragma unroll
                 for (int g = 0; g < fast::NG; ++g) {
                     const int grp = pi + fast::NPROD * g;
-                    if (grp < BN / 4) {
+                    if (grp < ngrp) {
                         const int r = rsub + 4 * grp;
                         const int64_t off = srow[g] + col;
                         const uint32_t so = (uint32_t)(r * 128 + ((piece ^ (r & 7)) * 16));
@@ -408,11 +409,13 @@ tc_pairs_fast_kernel(const __grid_constant__ CUtensorMap mapAb, const __grid_con
         }
     } else if (warp == 1) {
         // ---------------- MMA issuer
-        const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BN >> 3) << 17) |
-                               ((uint32_t)(BM >> 4) << 24);
         int c = 0, it = 0;
         for (int ti = blockIdx.x; ti < ntiles; ti += gridDim.x, ++it) {
             const int ab = it & 1;
+            // N = the tile's pairs rounded up to 16: partial tiles cost in proportion
+            const uint32_t nmma = (uint32_t)((tiles[ti].np + 15) & ~15);
+            const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((nmma >> 3) << 17) |
+                                   ((uint32_t)(BM >> 4) << 24);
             mbar_wait(smem_u32(&acce_b[ab]), ((it >> 1) & 1) ^ 1);
             asm volatile("tcgen05.fence::after_thread_sync;");
             const int kc0 = tiles[ti].kc0, kc1 = tiles[ti].kc1;
@@ -457,7 +460,7 @@ tc_pairs_fast_kernel(const __grid_constant__ CUtensorMap mapAb, const __grid_con
             for (int mt = 0; mt < MT; ++mt) {
                 const int row = tl.m0 + mt * BM + 32 * wq + lane;
 #pragma unroll 1
-                for (int c0 = 0; c0 < BN; c0 += 32) {
+                for (int c0 = 0; c0 < tl.np; c0 += 32) {
                     uint32_t v[32];
                     tmem_ld32(tmem + ((uint32_t)(32 * wq) << 16) + (uint32_t)((ab * MT + mt) * BN + c0), v);
                     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
@@ -556,7 +559,8 @@ void tc_split_rows(const XT* X, int ld, int64_t row0, int64_t nrows, int K, floa
 template void tc_split_rows<float>(const float*, int, int64_t, int64_t, int, float*, float*, cudaStream_t);
 template void tc_split_rows<double>(const double*, int, int64_t, int64_t, int, float*, float*, cudaStream_t);
 
-// Tiles in operator-major order.  Launches with fewer tiles than SMs (the coarse M2M/L2L
+// Tiles in operator-major order (ordering the M2L tiles by target-row chunks first kept W
+// and Z rows in L2 across operators but re-read the operators per chunk: no faster).  Launches with fewer tiles than SMs (the coarse M2M/L2L
 // levels) split K over several CTAs: a lone tile streams its 15 K chunks through one SM in
 // ~20 us, while its partial sums are added by the fp64 atomics of the epilogue anyway.
 void tc_build_tiles(OpPairs& P, int M, int K, bool fast) {
