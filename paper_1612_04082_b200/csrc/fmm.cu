@@ -888,16 +888,17 @@ void fmm_evaluate(Tree& t, int kernel, const float* f, const float* g, float* ou
     t.ev_valid = t.profile;
 }
 
-// flops per pair interaction of the fp32 pair loop, counted from elastic.cuh as written
-// (FFMA = 2, FADD/FMUL = 1; rsqrt not counted): d and r^2 8, then U 18, P 36, D 54, S 89.
+// flops per pair interaction of the fp32 pair loop, counted in the SASS of the compiled
+// direct kernel (tools/count_flops.sh): FFMA = 2, FMUL / FADD = 1 per pair; the rsqrt (MUFU)
+// and the r = 0 select are not counted.
 static double flops_per_pair(int kernel) {
     switch (kernel) {
-        case K_U: return 26;
-        case K_P: return 44;
-        case K_UP: return 62;
-        case K_D: return 62;
-        case K_S: return 97;
-        default: return 151;
+        case K_U: return 29;
+        case K_P: return 45;
+        case K_UP: return 65;
+        case K_D: return 54;
+        case K_S: return 87;
+        default: return 131;
     }
 }
 

@@ -81,13 +81,18 @@ __device__ __forceinline__ void pair_loop(const float4* __restrict__ srec, int c
     }
 }
 
+#ifndef EBEM_PL_UNROLL
+#define EBEM_PL_UNROLL 4
+#endif
+constexpr int PL_UNROLL = EBEM_PL_UNROLL;
+
 // the same, for TPT targets per thread: the source loop is outermost so that each record is
 // read from shared memory once for all TPT targets (one LDS.128 per pair at TPT = 4)
 template <bool SL, bool DL, bool STRESS, int TPT>
 __device__ __forceinline__ void pair_loop_multi(const float4* __restrict__ srec, int cnt, const float* x,
                                                 const float* y, const float* z, const KConst& kc, float (*acc)[STRESS ? 6 : 3]) {
     constexpr int R = STRESS ? REC_STRESS : REC_DISP;
-#pragma unroll 2
+#pragma unroll PL_UNROLL
     for (int j = 0; j < cnt; ++j) {
         const float4 p = srec[j * R + 0];
         const float4 f = SL ? srec[j * R + 1] : make_float4(0, 0, 0, 0);
