@@ -193,12 +193,45 @@ far_eval_kernel(int n_eval, const int* __restrict__ eval_box, const int* __restr
     }
 }
 
+// Lane groups for the warp-per-leaf kernels.  A leaf holds nt targets (~31 on average on
+// the benchmark surfaces, 1..64 in general); one lane per target left a quarter of the lanes
+// idle.  The warp is split into G = 32 / L groups of L lanes; each group takes every G-th
+// source and each lane TPT targets (t0 + l + L j), with L * TPT >= nt as tight as possible,
+// and the groups' partial sums are added by shuffles at the end.  Returns TPT (1..4; 0 when
+// nt exceeds 128, then a 32 x 4 round is used and repeated).
+__device__ __forceinline__ int lane_groups(int nt, int& L) {
+    if (nt > 128) {
+        L = 32;
+        return 4;
+    }
+    int best = 1 << 30, tpt = 4;
+    L = 32;
+    for (int l = 32; l >= 4; l >>= 1) {
+        const int t = (nt + l - 1) / l;
+        if (t <= 4 && l * t < best) {      // strict: ties keep the larger group (fewer shuffles)
+            best = l * t;
+            L = l;
+            tpt = t;
+        }
+    }
+    return tpt;
+}
+
+template <int NC, int TPT>
+__device__ __forceinline__ void reduce_groups(float (*acc)[NC], int L) {
+    for (int off = L; off < 32; off <<= 1)
+#pragma unroll
+        for (int j = 0; j < TPT; ++j)
+#pragma unroll
+            for (int c = 0; c < NC; ++c) acc[j][c] += __shfl_xor_sync(0xffffffffu, acc[j][c], off);
+}
+
 // fp32 far field (p <= 8 matvec): phi arrives pre-scaled in fp32 (PHI GEMM epilogue), so a
 // box costs one coalesced copy of its equivalent points / densities into the warp's shared
 // slice; each lane then evaluates TPT targets against them (TPT = 2 for leaves with more
 // than 32 targets: every staged point is read once for both).
 template <bool STRESS, int TPT>
-__device__ __forceinline__ void far_round_f32(int t0, int t_beg, int t_end, int b, int own, int nfar,
+__device__ __forceinline__ void far_round_f32(int t0, int t_beg, int t_end, int L, int b, int own, int nfar,
                                               const int* __restrict__ widx, int wbeg, const float4* __restrict__ PHIDF,
                                               int l2t, const float4* __restrict__ PHIUF,
                                               const int* __restrict__ phiu_slot, const int* __restrict__ anchor,
@@ -208,10 +241,11 @@ __device__ __forceinline__ void far_round_f32(int t0, int t_beg, int t_end, int 
                                               const float* __restrict__ near, const int* __restrict__ trg_perm,
                                               float* __restrict__ out) {
     constexpr int NC = STRESS ? 6 : 3;
+    const int G = 32 / L, grp = lane / L, l = lane % L;
     int tc[TPT];
 #pragma unroll
     for (int j = 0; j < TPT; ++j) {
-        const int t = t0 + lane + 32 * j;
+        const int t = t0 + l + L * j;
         tc[j] = t < t_end ? t : t_beg;
     }
     float acc[TPT][NC];
@@ -243,7 +277,7 @@ __device__ __forceinline__ void far_round_f32(int t0, int t_beg, int t_end, int 
             z[j] = (float)((double)trg[3 * tc[j] + 2] - cz);
         }
 #pragma unroll 2
-        for (int k = 0; k < ne; ++k) {
+        for (int k = grp; k < ne; k += G) {      // this group's share of the equivalent points
             const float4 q = ey[k], f = ph[k];
 #pragma unroll
             for (int j = 0; j < TPT; ++j) {
@@ -256,15 +290,17 @@ __device__ __forceinline__ void far_round_f32(int t0, int t_beg, int t_end, int 
             }
         }
     }
+    reduce_groups<NC, TPT>(acc, L);
+    if (grp == 0)
 #pragma unroll
-    for (int j = 0; j < TPT; ++j) {
-        const int t = t0 + lane + 32 * j;
-        if (t < t_end) {
-            float* o = out + (int64_t)trg_perm[t] * NC;
+        for (int j = 0; j < TPT; ++j) {
+            const int t = t0 + l + L * j;
+            if (t < t_end) {
+                float* o = out + (int64_t)trg_perm[t] * NC;
 #pragma unroll
-            for (int c = 0; c < NC; ++c) o[c] = acc[j][c] + near[(int64_t)t * NC + c];
+                for (int c = 0; c < NC; ++c) o[c] = acc[j][c] + near[(int64_t)t * NC + c];
+            }
         }
-    }
 }
 
 template <bool STRESS>
@@ -288,32 +324,38 @@ far_eval_f32_kernel(int n_eval, const int* __restrict__ eval_box, const int* __r
     const int own = l2t >= 0 ? 1 : 0;
     const int nfar = own + (woff[b + 1] - woff[b]);
     for (int t0 = t_beg; t0 < t_end;) {
-        if (t_end - t0 > 32) {
-            far_round_f32<STRESS, 2>(t0, t_beg, t_end, b, own, nfar, widx, woff[b], PHIDF, l2t, PHIUF, phiu_slot,
-                                     anchor, level, geo, se4, ne, trg, kc, ey, ph, lane, near, trg_perm, out);
-            t0 += 64;
-        } else {
-            far_round_f32<STRESS, 1>(t0, t_beg, t_end, b, own, nfar, widx, woff[b], PHIDF, l2t, PHIUF, phiu_slot,
-                                     anchor, level, geo, se4, ne, trg, kc, ey, ph, lane, near, trg_perm, out);
-            t0 += 32;
+        int L;
+        const int tpt = lane_groups(t_end - t0, L);
+#define EB_FAR(T)                                                                                                   \
+    far_round_f32<STRESS, T>(t0, t_beg, t_end, L, b, own, nfar, widx, woff[b], PHIDF, l2t, PHIUF, phiu_slot, anchor, \
+                             level, geo, se4, ne, trg, kc, ey, ph, lane, near, trg_perm, out)
+        switch (tpt) {
+            case 1: EB_FAR(1); break;
+            case 2: EB_FAR(2); break;
+            case 3: EB_FAR(3); break;
+            default: EB_FAR(4); break;
         }
+#undef EB_FAR
+        t0 += L * tpt;
     }
 }
 
-// near field: U-list sources staged 32 at a time per warp; TPT targets per lane (2 when
-// the leaf has more than 32 targets, so each staged record serves both)
+// near field: U-list sources staged 32 at a time per warp (record stride R + 1 float4, so
+// the groups' different records fall in different banks); lane groups as above
 template <bool SL, bool DL, bool STRESS, int TPT>
-__device__ __forceinline__ void near_round(int t0, int t_beg, int t_end, int b, const int* __restrict__ uoff,
+__device__ __forceinline__ void near_round(int t0, int t_beg, int t_end, int L, int b, const int* __restrict__ uoff,
                                            const int* __restrict__ uidx, const int* __restrict__ sbeg,
                                            const int* __restrict__ send, const float* __restrict__ trg,
                                            const float4* __restrict__ rec, const KConst& kc,
                                            float* __restrict__ near, float4* srec, int lane) {
     constexpr int NC = STRESS ? 6 : 3;
     constexpr int R = STRESS ? REC_STRESS : REC_DISP;
+    constexpr int RS = R + 1;
+    const int G = 32 / L, grp = lane / L, l = lane % L;
     float x[TPT], y[TPT], z[TPT], acc[TPT][NC];
 #pragma unroll
     for (int j = 0; j < TPT; ++j) {
-        const int t = t0 + lane + 32 * j;
+        const int t = t0 + l + L * j;
         const int tc = t < t_end ? t : t_beg;
         x[j] = trg[3 * tc];
         y[j] = trg[3 * tc + 1];
@@ -326,18 +368,20 @@ __device__ __forceinline__ void near_round(int t0, int t_beg, int t_end, int b, 
         for (int s0 = sbeg[a]; s0 < send[a]; s0 += 32) {
             const int cnt = min(32, send[a] - s0);
             __syncwarp();
-            for (int q = lane; q < cnt * R; q += 32) srec[q] = rec[(int64_t)s0 * R + q];
+            for (int q = lane; q < cnt * R; q += 32) srec[(q / R) * RS + q % R] = rec[(int64_t)s0 * R + q];
             __syncwarp();
-            pair_loop_multi<SL, DL, STRESS, TPT>(srec, cnt, x, y, z, kc, acc);
+            pair_loop_strided<SL, DL, STRESS, TPT, RS>(srec, cnt, grp, G, x, y, z, kc, acc);
         }
     }
+    reduce_groups<NC, TPT>(acc, L);
+    if (grp == 0)
 #pragma unroll
-    for (int j = 0; j < TPT; ++j) {
-        const int t = t0 + lane + 32 * j;
-        if (t < t_end)
+        for (int j = 0; j < TPT; ++j) {
+            const int t = t0 + l + L * j;
+            if (t < t_end)
 #pragma unroll
-            for (int c = 0; c < NC; ++c) near[(int64_t)t * NC + c] = acc[j][c];
-    }
+                for (int c = 0; c < NC; ++c) near[(int64_t)t * NC + c] = acc[j][c];
+        }
 }
 
 template <bool SL, bool DL, bool STRESS>
@@ -347,7 +391,7 @@ near_eval_kernel(int n_eval, const int* __restrict__ eval_box, const int* __rest
                  const int* __restrict__ tbeg, const int* __restrict__ tend, const float* __restrict__ trg,
                  const float4* __restrict__ rec, KConst kc, float* __restrict__ near) {
     constexpr int R = STRESS ? REC_STRESS : REC_DISP;
-    __shared__ float4 srec_all[EV_WARPS][32 * R];
+    __shared__ float4 srec_all[EV_WARPS][32 * (R + 1)];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int i = blockIdx.x * EV_WARPS + warp;
     if (i >= n_eval) return;
@@ -355,15 +399,18 @@ near_eval_kernel(int n_eval, const int* __restrict__ eval_box, const int* __rest
     const int b = eval_box[i];
     const int t_beg = tbeg[b], t_end = tend[b];
     for (int t0 = t_beg; t0 < t_end;) {
-        if (t_end - t0 > 32) {
-            near_round<SL, DL, STRESS, 2>(t0, t_beg, t_end, b, uoff, uidx, sbeg, send, trg, rec, kc, near, srec,
-                                          lane);
-            t0 += 64;
-        } else {
-            near_round<SL, DL, STRESS, 1>(t0, t_beg, t_end, b, uoff, uidx, sbeg, send, trg, rec, kc, near, srec,
-                                          lane);
-            t0 += 32;
+        int L;
+        const int tpt = lane_groups(t_end - t0, L);
+#define EB_NEAR(T)                                                                                                   \
+    near_round<SL, DL, STRESS, T>(t0, t_beg, t_end, L, b, uoff, uidx, sbeg, send, trg, rec, kc, near, srec, lane)
+        switch (tpt) {
+            case 1: EB_NEAR(1); break;
+            case 2: EB_NEAR(2); break;
+            case 3: EB_NEAR(3); break;
+            default: EB_NEAR(4); break;
         }
+#undef EB_NEAR
+        t0 += L * tpt;
     }
 }
 

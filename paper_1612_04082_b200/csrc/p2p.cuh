@@ -120,4 +120,39 @@ __device__ __forceinline__ void pair_loop_multi(const float4* __restrict__ srec,
     }
 }
 
+
+// the same for a lane group: records j = g, g + G, ... of the staged tile (stride RS float4),
+// TPT targets per thread
+template <bool SL, bool DL, bool STRESS, int TPT, int RS>
+__device__ __forceinline__ void pair_loop_strided(const float4* __restrict__ srec, int cnt, int g, int G,
+                                                  const float* x, const float* y, const float* z, const KConst& kc,
+                                                  float (*acc)[STRESS ? 6 : 3]) {
+#pragma unroll 2
+    for (int j = g; j < cnt; j += G) {
+        const float4 p = srec[j * RS + 0];
+        const float4 f = SL ? srec[j * RS + 1] : make_float4(0, 0, 0, 0);
+        const float4 gg = DL ? srec[j * RS + 2] : make_float4(0, 0, 0, 0);
+        const float4 n = DL ? srec[j * RS + 3] : make_float4(0, 0, 0, 0);
+        float NG[6] = {0, 0, 0, 0, 0, 0};
+        if (STRESS && DL) {
+            const float4 t0 = srec[j * RS + 4];
+            const float4 t1 = srec[j * RS + 5];
+            NG[0] = t0.x; NG[1] = t0.y; NG[2] = t0.z; NG[3] = t0.w; NG[4] = t1.x; NG[5] = t1.y;
+        }
+#pragma unroll
+        for (int k = 0; k < TPT; ++k) {
+            float dx = x[k] - p.x, dy = y[k] - p.y, dz = z[k] - p.z;
+            float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
+            float ri = safe_rinv(r2);
+            if (!STRESS) {
+                if (SL) acc_U(dx, dy, dz, ri, f.x, f.y, f.z, kc.a1, acc[k]);
+                if (DL) acc_P(dx, dy, dz, ri, gg.x, gg.y, gg.z, n.x, n.y, n.z, p.w, kc.a3, acc[k]);
+            } else {
+                if (SL) acc_D(dx, dy, dz, ri, f.x, f.y, f.z, kc.a, acc[k]);
+                if (DL) acc_S(dx, dy, dz, ri, gg.x, gg.y, gg.z, n.x, n.y, n.z, p.w, NG, kc.a, kc.nu, kc.b4, acc[k]);
+            }
+        }
+    }
+}
+
 }  // namespace ebem
