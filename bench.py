@@ -241,8 +241,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--n", type=int, default=1_000_000)
-    ap.add_argument("--p", type=int, default=6)
-    ap.add_argument("--max-pts", type=int, default=64)
+    ap.add_argument("--p", type=int, default=None, help="multipole order (default: 6 matvec, 8 gmres)")
+    ap.add_argument("--max-pts", type=int, default=None,
+                    help="leaf capacity (default: 64 for the matvec (configs[2]), 1024 for gmres)")
     ap.add_argument("--ref-sample", type=int, default=512)
     ap.add_argument("--cpu-sample", type=int, default=3072)
     ap.add_argument("--no-cpu", action="store_true")
@@ -255,6 +256,11 @@ def main():
     ap.add_argument("--max-iter", type=int, default=1000)
     ap.add_argument("--precond", type=int, default=0)
     args = ap.parse_args()
+    gm = args.workload == "gmres"
+    if args.max_pts is None:
+        args.max_pts = 1024 if gm else 64     # gmres: fastest leaf size for 16 sources per panel
+    if args.p is None:
+        args.p = 8 if gm else 6
     if args.impl == "reference":
         return run_reference(args)
 

@@ -490,11 +490,21 @@ void schedule_tree(Tree& t, cudaStream_t s) {
         build_op_pairs(t.m2m[l], 8, op, p2, s);
     }
 
+    // X- and W-list interactions that are cheaper done directly (reading in DESIGN.md):
+    // X (source leaf A -> box B): when B is a leaf with fewer targets than check points, A's
+    // sources go straight to B's targets instead of to B's check surface; W (A's equivalent
+    // density -> B's targets): when A holds fewer sources than equivalent points, its sources
+    // go straight to B's targets.  Exact, and fewer pair interactions either way.
+    // EBEM_XW_DIRECT=0 keeps the paper's S2L / M2T for every entry.
+    const bool xw_direct = !(std::getenv("EBEM_XW_DIRECT") && std::atoi(std::getenv("EBEM_XW_DIRECT")) == 0);
+    auto x_direct = [&](int b) { return xw_direct && leaf[b] && tsub[b] < P.nc; };
+    auto w_direct = [&](int a) { return xw_direct && nsub[a] < P.ne; };
+
     // S2L: boxes with X-list leaves that hold sources
     std::vector<int> s2l, xoff(1, 0), xidx;
     pr.clear();
     for (int b = 0; b < nb; ++b) {
-        if (dn[b] < 0) continue;
+        if (dn[b] < 0 || x_direct(b)) continue;
         int cnt = 0;
         for (int e = off[3][b]; e < off[3][b + 1]; ++e)
             if (nsub[idx[3][e]] > 0) {
@@ -554,8 +564,33 @@ void schedule_tree(Tree& t, cudaStream_t s) {
         build_op_pairs(t.l2l[l], 8, op, p2, s);
     }
 
-    // leaf evaluation
+    // leaf evaluation: near list (U + direct X + direct W) and M2T list (the other W entries)
     std::vector<int> ev, l2t, phid_box, phiu_box, phiu(nb, -1);
+    std::vector<int> noff(nb + 1, 0), nidx, moff(nb + 1, 0), midx;
+    for (int b = 0; b < nb; ++b) {
+        if (leaf[b] && tsub[b] > 0) {
+            for (int e = off[0][b]; e < off[0][b + 1]; ++e) nidx.push_back(idx[0][e]);
+            if (x_direct(b))
+                for (int e = off[3][b]; e < off[3][b + 1]; ++e)
+                    if (nsub[idx[3][e]] > 0) nidx.push_back(idx[3][e]);
+            for (int e = off[2][b]; e < off[2][b + 1]; ++e) {
+                const int a = idx[2][e];
+                if (nsub[a] == 0) continue;
+                if (w_direct(a)) nidx.push_back(a);
+                else midx.push_back(a);
+            }
+        }
+        noff[b + 1] = (int)nidx.size();
+        moff[b + 1] = (int)midx.size();
+    }
+    t.near_off.alloc(nb + 1);
+    h2d(t.near_off.p, noff.data(), nb + 1, s);
+    t.near_idx.alloc(std::max<size_t>(nidx.size(), 1));
+    h2d(t.near_idx.p, nidx.data(), nidx.size(), s);
+    t.m2t_off.alloc(nb + 1);
+    h2d(t.m2t_off.p, moff.data(), nb + 1, s);
+    t.m2t_idx.alloc(std::max<size_t>(midx.size(), 1));
+    h2d(t.m2t_idx.p, midx.data(), midx.size(), s);
     std::vector<double> phid_scale, phiu_scale;
     std::vector<int2> prd, pru;
     auto half = [&](int b) { return t.side / (double)(1 << level[b]) * 0.5; };
@@ -570,8 +605,8 @@ void schedule_tree(Tree& t, cudaStream_t s) {
         } else {
             l2t.push_back(-1);
         }
-        for (int e = off[2][b]; e < off[2][b + 1]; ++e) {
-            int a = idx[2][e];
+        for (int e = moff[b]; e < moff[b + 1]; ++e) {
+            int a = midx[e];
             if (up[a] >= 0 && phiu[a] < 0) {
                 phiu[a] = (int)phiu_box.size();
                 pru.push_back(make_int2(phiu[a], up[a]));
@@ -591,12 +626,12 @@ void schedule_tree(Tree& t, cudaStream_t s) {
         for (size_t i = 0; i < ev.size(); ++i) {
             const int b = ev[i];
             double ns = 0;
-            for (int e = off[0][b]; e < off[0][b + 1]; ++e) ns += nsub[idx[0][e]];
+            for (int e = noff[b]; e < noff[b + 1]; ++e) ns += nsub[nidx[e]];
             t.w_p2p_src += ns;
             t.w_p2p_inter += ns * tsub[b];
             if (l2t[i] >= 0) t.w_l2t_inter += ne * tsub[b];
-            for (int e = off[2][b]; e < off[2][b + 1]; ++e)
-                if (phiu[idx[2][e]] >= 0) t.w_m2t_inter += ne * tsub[b];
+            for (int e = moff[b]; e < moff[b + 1]; ++e)
+                if (phiu[midx[e]] >= 0) t.w_m2t_inter += ne * tsub[b];
         }
         t.w_m2m_pairs = t.w_l2l_pairs = 0;
         for (auto& x : t.m2m) t.w_m2m_pairs += x.npairs;
@@ -735,7 +770,7 @@ static void launch_near(const Tree& t, cudaStream_t s) {
         carve = true;
     }
     near_eval_kernel<SL, DL, STRESS><<<ceil_div(t.n_eval, EV_WARPS), 32 * EV_WARPS, 0, s>>>(
-        t.n_eval, t.eval_box.p, t.lst_off[0].p, t.lst_idx[0].p, t.sbeg.p, t.send.p, t.tbeg.p, t.tend.p, t.trg_xyz.p,
+        t.n_eval, t.eval_box.p, t.near_off.p, t.near_idx.p, t.sbeg.p, t.send.p, t.tbeg.p, t.tend.p, t.trg_xyz.p,
         STRESS ? t.rec_stress.p : t.rec_disp.p, kc, t.near_sorted.p);
     EB_CHECK_LAUNCH();
 }
@@ -754,7 +789,7 @@ static void launch_far(const Tree& t, float* out, cudaStream_t s) {
         auto ffn = far_eval_kernel<STRESS, double>;
         if (sm > 48 * 1024) EB_CUDA(cudaFuncSetAttribute(ffn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
         ffn<<<grid, 32 * EV_WARPS, sm, s>>>(t.n_eval, t.eval_box.p, t.eval_l2t_slot.p, t.PHID.p, t.PHIU.p,
-                                            t.phiu_slot.p, t.lst_off[2].p, t.lst_idx[2].p, t.tbeg.p, t.tend.p,
+                                            t.phiu_slot.p, t.m2t_off.p, t.m2t_idx.p, t.tbeg.p, t.tend.p,
                                             t.anchor.p, t.level.p, geo, P.s_e64.p, P.ne, t.trg_xyz.p, kc, cfar,
                                             t.near_sorted.p, t.trg_perm.p, out);
     } else {
@@ -762,7 +797,7 @@ static void launch_far(const Tree& t, float* out, cudaStream_t s) {
         auto ffn = far_eval_f32_kernel<STRESS>;
         if (sm > 48 * 1024) EB_CUDA(cudaFuncSetAttribute(ffn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
         ffn<<<grid, 32 * EV_WARPS, sm, s>>>(t.n_eval, t.eval_box.p, t.eval_l2t_slot.p, t.PHIDF.p, t.PHIUF.p,
-                                            t.phiu_slot.p, t.lst_off[2].p, t.lst_idx[2].p, t.tbeg.p, t.tend.p,
+                                            t.phiu_slot.p, t.m2t_off.p, t.m2t_idx.p, t.tbeg.p, t.tend.p,
                                             t.anchor.p, t.level.p, geo, P.s_e4.p, P.ne, t.trg_xyz.p, kc,
                                             t.near_sorted.p, t.trg_perm.p, out);
     }

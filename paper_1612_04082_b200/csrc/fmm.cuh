@@ -149,7 +149,9 @@ struct Tree {
     CUtensorMap mQb, mQs, mQdb, mQds, mZb, mZs, mWb, mWs;
     DBuf<double> PHID, PHIU;             // [n_phid x me], [n_phiu x me] (fp64 far field)
     DBuf<float4> PHIDF, PHIUF;           // [n_phid x ne], [n_phiu x ne] (fp32 far field, scaled)
-    DBuf<float> near_sorted;             // [ntrg x 6] U-list near field, sorted target order
+    DBuf<float> near_sorted;             // [ntrg x 6] near field, sorted target order
+    DBuf<int> near_off, near_idx;        // per box: source boxes summed directly (U + direct X/W)
+    DBuf<int> m2t_off, m2t_idx;          // per box: W-list boxes evaluated from their equivalent density
     // two-stream schedule (fmm_evaluate): created on first use
     cudaStream_t sA = nullptr, sB = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_s2l = nullptr, ev_near = nullptr, ev_joinA = nullptr;
