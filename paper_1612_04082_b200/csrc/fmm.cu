@@ -499,6 +499,16 @@ void schedule_tree(Tree& t, cudaStream_t s) {
     const bool xw_direct = !(std::getenv("EBEM_XW_DIRECT") && std::atoi(std::getenv("EBEM_XW_DIRECT")) == 0);
     auto x_direct = [&](int b) { return xw_direct && leaf[b] && tsub[b] < P.nc; };
     auto w_direct = [&](int a) { return xw_direct && nsub[a] < P.ne; };
+    // V-list pairs of two leaves with few points: one M2L costs ~ (3 n_e)^2 tensor-core MACs
+    // (x3 for 3xTF32) plus its share of the fp64 state; summing the nsrc x ntrg pairs directly
+    // is cheaper below ~kappa (3 n_e)^2 pair interactions (kappa measured on the 1M beam).
+    static const double kappa = std::getenv("EBEM_V_DIRECT") ? std::atof(std::getenv("EBEM_V_DIRECT")) : 0.006;
+    // (only with the fp32 far field, p <= 8: at p >= 9 the fp32 direct sums would exceed the
+    // fp64 far field's error, measured 1.5e-6 vs 5.5e-7 at p = 10)
+    const bool v_dir_on = xw_direct && P.p < FAR_FP64_MIN_P;
+    auto v_direct = [&](int b, int a) {
+        return v_dir_on && leaf[b] && leaf[a] && (double)nsub[a] * tsub[b] < kappa * (double)P.me * P.me;
+    };
 
     // S2L: boxes with X-list leaves that hold sources
     std::vector<int> s2l, xoff(1, 0), xidx;
@@ -535,7 +545,7 @@ void schedule_tree(Tree& t, cudaStream_t s) {
             if (dn[b] < 0) continue;
             for (int e = off[1][b]; e < off[1][b + 1]; ++e) {
                 int a = idx[1][e];
-                if (up[a] < 0) continue;
+                if (up[a] < 0 || v_direct(b, a)) continue;
                 int ox = anchor[3 * a] - anchor[3 * b], oy = anchor[3 * a + 1] - anchor[3 * b + 1],
                     oz = anchor[3 * a + 2] - anchor[3 * b + 2];
                 int o = P.off_index[(ox + 3) * 49 + (oy + 3) * 7 + (oz + 3)];
@@ -570,6 +580,8 @@ void schedule_tree(Tree& t, cudaStream_t s) {
     for (int b = 0; b < nb; ++b) {
         if (leaf[b] && tsub[b] > 0) {
             for (int e = off[0][b]; e < off[0][b + 1]; ++e) nidx.push_back(idx[0][e]);
+            for (int e = off[1][b]; e < off[1][b + 1]; ++e)
+                if (nsub[idx[1][e]] > 0 && v_direct(b, idx[1][e])) nidx.push_back(idx[1][e]);
             if (x_direct(b))
                 for (int e = off[3][b]; e < off[3][b + 1]; ++e)
                     if (nsub[idx[3][e]] > 0) nidx.push_back(idx[3][e]);
