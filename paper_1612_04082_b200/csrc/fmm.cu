@@ -30,6 +30,13 @@ struct BoxGeo {
     }
 };
 
+// round-to-nearest TF32 (the tensor-core operand split, as tc_gemm.cu's split kernel)
+__device__ __forceinline__ float tf32_rna(float x) {
+    uint32_t r;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+    return __uint_as_float(r);
+}
+
 // ------------------------------------------------------------------ check potentials
 // Entry i: target = check surface of box tbox[i] (radius factor rad), sources = the
 // sources of boxes sidx[soff[i] .. soff[i+1]) (or of tbox[i] itself when soff is null).
@@ -44,7 +51,8 @@ __global__ void __launch_bounds__(CP_T)
 check_potential_kernel(const int* __restrict__ tbox, const int* __restrict__ soff, const int* __restrict__ sidx,
                        const int* __restrict__ sbeg, const int* __restrict__ send, const int* __restrict__ anchor,
                        const int* __restrict__ level, BoxGeo geo, double rad, const float* __restrict__ sc, int nc,
-                       const float4* __restrict__ rec, KConst kc, float* __restrict__ Q, int ldq) {
+                       const float4* __restrict__ rec, KConst kc, float* __restrict__ Q, float* __restrict__ Qb,
+                       float* __restrict__ Qs, int ldq) {
     __shared__ float4 srec[CP_TILE * REC_DISP];
     const int i = blockIdx.x;
     const int b = tbox[i];
@@ -86,10 +94,19 @@ check_potential_kernel(const int* __restrict__ tbox, const int* __restrict__ sof
     for (int q = 0; q < KPT; ++q) {
         const int k = threadIdx.x + q * blockDim.x;
         if (k < nc) {
-            float* o = Q + (int64_t)i * ldq + 3 * k;
-            o[0] = acc[q][0];
-            o[1] = acc[q][1];
-            o[2] = acc[q][2];
+            const int64_t o = (int64_t)i * ldq + 3 * k;
+            if (Qb) {              // tensor-core path: the TF32 head / remainder split, fused
+#pragma unroll
+                for (int c = 0; c < 3; ++c) {
+                    const float h = tf32_rna(acc[q][c]);
+                    Qb[o + c] = h;
+                    Qs[o + c] = tf32_rna(acc[q][c] - h);
+                }
+            } else {
+                Q[o] = acc[q][0];
+                Q[o + 1] = acc[q][1];
+                Q[o + 2] = acc[q][2];
+            }
         }
     }
 }
@@ -728,7 +745,7 @@ void schedule_tree(Tree& t, cudaStream_t s) {
 // ------------------------------------------------------------------ evaluation
 template <bool SL, bool DL>
 static void launch_check(const Tree& t, const int* tbox, int n, const int* soff, const int* sidx, double rad,
-                         float* Q, cudaStream_t s) {
+                         float* Q, float* Qb, float* Qs, cudaStream_t s) {
     if (n == 0) return;
     const Plan& P = *t.plan;
     BoxGeo geo{t.origin[0], t.origin[1], t.origin[2], t.side};
@@ -741,7 +758,7 @@ static void launch_check(const Tree& t, const int* tbox, int n, const int* soff,
     EB_CUDA(cudaFuncSetAttribute(check_potential_kernel<SL, DL, K>, cudaFuncAttributePreferredSharedMemoryCarveout, 100)); \
     check_potential_kernel<SL, DL, K><<<n, nthr, 0, s>>>(tbox, soff, sidx, t.sbeg.p, t.send.p, t.anchor.p,         \
                                                          t.level.p, geo, rad, P.s_c.p, P.nc, t.rec_disp.p, kc,    \
-                                                         Q, P.ldc)
+                                                         Q, Qb, Qs, P.ldc)
     switch (kpt) {
         case 1: EB_CHECK_LAUNCH_KPT(1); break;
         case 2: EB_CHECK_LAUNCH_KPT(2); break;
@@ -873,9 +890,11 @@ void fmm_evaluate(Tree& t, int kernel, const float* f, const float* g, float* ou
 
     auto s2l = [&](cudaStream_t st) {
         if (!t.n_s2l) return;
-        if (sl && dl) launch_check<true, true>(t, t.s2l_box.p, t.n_s2l, t.x_src_off.p, t.x_src_idx.p, RAD_DC, t.Qd.p, st);
-        else if (sl) launch_check<true, false>(t, t.s2l_box.p, t.n_s2l, t.x_src_off.p, t.x_src_idx.p, RAD_DC, t.Qd.p, st);
-        else launch_check<false, true>(t, t.s2l_box.p, t.n_s2l, t.x_src_off.p, t.x_src_idx.p, RAD_DC, t.Qd.p, st);
+        float* qb = t.use_tc ? t.Qdb.p : nullptr;
+        float* qs = t.use_tc ? t.Qds.p : nullptr;
+        if (sl && dl) launch_check<true, true>(t, t.s2l_box.p, t.n_s2l, t.x_src_off.p, t.x_src_idx.p, RAD_DC, t.Qd.p, qb, qs, st);
+        else if (sl) launch_check<true, false>(t, t.s2l_box.p, t.n_s2l, t.x_src_off.p, t.x_src_idx.p, RAD_DC, t.Qd.p, qb, qs, st);
+        else launch_check<false, true>(t, t.s2l_box.p, t.n_s2l, t.x_src_off.p, t.x_src_idx.p, RAD_DC, t.Qd.p, qb, qs, st);
     };
     auto near = [&](cudaStream_t st) {
         switch (kernel) {
@@ -899,15 +918,18 @@ void fmm_evaluate(Tree& t, int kernel, const float* f, const float* g, float* ou
     };
 
     // upward pass
-    if (sl && dl) launch_check<true, true>(t, t.s2m_box.p, t.n_s2m, nullptr, nullptr, RAD_UC, t.Q.p, sa);
-    else if (sl) launch_check<true, false>(t, t.s2m_box.p, t.n_s2m, nullptr, nullptr, RAD_UC, t.Q.p, sa);
-    else launch_check<false, true>(t, t.s2m_box.p, t.n_s2m, nullptr, nullptr, RAD_UC, t.Q.p, sa);
+    {
+        float* qb = t.use_tc ? t.Qb.p : nullptr;
+        float* qs = t.use_tc ? t.Qs.p : nullptr;
+        if (sl && dl) launch_check<true, true>(t, t.s2m_box.p, t.n_s2m, nullptr, nullptr, RAD_UC, t.Q.p, qb, qs, sa);
+        else if (sl) launch_check<true, false>(t, t.s2m_box.p, t.n_s2m, nullptr, nullptr, RAD_UC, t.Q.p, qb, qs, sa);
+        else launch_check<false, true>(t, t.s2m_box.p, t.n_s2m, nullptr, nullptr, RAD_UC, t.Q.p, qb, qs, sa);
+    }
     mark(phase++);
     const int lde = P.lde, ldc = P.ldc;
     auto zrows = [&](int l) { return (int64_t)t.up_lstart[l + 1] - t.up_lstart[l]; };
     auto wrows = [&](int l) { return (int64_t)t.dn_lstart[l + 1] - t.dn_lstart[l]; };
     if (t.use_tc) {
-        tc_split_rows(t.Q.p, ldc, 0, t.n_s2m, mc, t.Qb.p, t.Qs.p, sa);
         tc_pairs_gemm(t.q2z_up, P.mQu1T_b, P.mQu1T_s, t.mQb, t.mQs, me, mc, t.Z.p, lde, sa);
     } else {
         gemm_pairs_f32(t.q2z_up, P.Qu1T.p, me, mc, ldc, t.Q.p, ldc, t.Z.p, lde, sa);
@@ -932,7 +954,6 @@ void fmm_evaluate(Tree& t, int kernel, const float* f, const float* g, float* ou
     auto q2z_dn = [&]() {
         if (!t.n_s2l) return;
         if (t.use_tc) {
-            tc_split_rows(t.Qd.p, ldc, 0, t.n_s2l, mc, t.Qdb.p, t.Qds.p, sa);
             tc_pairs_gemm(t.q2z_dn, P.mQd1T_b, P.mQd1T_s, t.mQdb, t.mQds, me, mc, t.W.p, lde, sa);
         } else {
             gemm_pairs_f32(t.q2z_dn, P.Qd1T.p, me, mc, ldc, t.Qd.p, ldc, t.W.p, lde, sa);
