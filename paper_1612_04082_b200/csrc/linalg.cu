@@ -340,70 +340,111 @@ template void gemm_pairs_f32<double>(const OpPairs&, const float*, int, int, int
 // fp64: Y[t] = scale[t] * Mat X[src] (one op; plain store; Mat upper triangular).
 // OutT = double: Y row-major [t][ldy].  OutT = float4: the fp32 far-field layout, row t holds
 // M/3 float4 (x, y, z, 0) = (float)(cf * scale[t] * (Mat X)[3k .. 3k+2]) (ldy in float4).
+// Computed on the fp64 tensor cores (mma.sync m8n8k4 f64; measured 37 TFLOP/s on B200, the
+// FP64 FMA peak): a SIMT version (4 x 4 register tiles) was bound by shared-memory loads (8 LDS per
+// 16 DFMA) at ~41% of the FP64 pipe.  CTA tile 64 rows x 64 pairs, K step 16 double-buffered
+// in smem (row stride 20 doubles: conflict-free fragment loads); 8 warps of 32 x 16 outputs
+// (4 x 2 mma tiles, 6 fragment loads per 8 MMAs).
+constexpr int DM_M = 64, DM_N = 64, DM_K = 16, DM_LD = 20;
 template <class OutT>
 __global__ void __launch_bounds__(256)
-gemm_pairs_f64_kernel(const int2* __restrict__ pairs, int npairs, const double* __restrict__ Mt, int M,
-                      int K, const double* __restrict__ X, int ldx, const double* __restrict__ scale, double cf,
-                      OutT* __restrict__ Y, int ldy) {
-    const int p0 = blockIdx.y * PG_N;
-    const int np = min(PG_N, npairs - p0);
-    const int m0 = blockIdx.x * PG_M;
-    __shared__ double As[PG_K][PG_M + 1];
-    __shared__ double Bs[PG_K][PG_N + 1];
-    __shared__ int2 pr[PG_N];
-    if (threadIdx.x < PG_N) pr[threadIdx.x] = threadIdx.x < np ? pairs[p0 + threadIdx.x] : make_int2(-1, -1);
+gemm_pairs_dmma_kernel(const int2* __restrict__ pairs, int npairs, const double* __restrict__ Mt, int M, int K,
+                       const double* __restrict__ X, int ldx, const double* __restrict__ scale, double cf,
+                       OutT* __restrict__ Y, int ldy) {
+    const int p0 = blockIdx.y * DM_N;
+    const int np = min(DM_N, npairs - p0);
+    const int m0 = blockIdx.x * DM_M;
+    __shared__ __align__(16) double As[2][DM_M * DM_LD];
+    __shared__ __align__(16) double Bs[2][DM_N * DM_LD];
+    __shared__ int2 pr[DM_N];
+    if (threadIdx.x < DM_N) pr[threadIdx.x] = threadIdx.x < np ? pairs[p0 + threadIdx.x] : make_int2(-1, -1);
     __syncthreads();
-    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
-    double acc[4][4] = {};
-    // Mt is upper triangular (R^-1): rows m0.. only see columns k >= m0
-    for (int k0 = (m0 / PG_K) * PG_K; k0 < K; k0 += PG_K) {
-        for (int e = threadIdx.x; e < PG_K * PG_M; e += 256) {
-            int r = e / PG_K, c = e % PG_K;
-            int gm = m0 + r, gk = k0 + c;
-            As[c][r] = (gm < M && gk < K) ? Mt[(int64_t)gm * K + gk] : 0.0;
-            int src = pr[r].y;
-            Bs[c][r] = (src >= 0 && gk < K) ? X[(int64_t)src * ldx + gk] : 0.0;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int wm = warp >> 2, wn = warp & 3;                 // 2 x 4 warps: 32 rows x 16 pairs each
+    // loader: row r = threadIdx / 4 (0..63), 4 consecutive doubles (2 x double2) at k = 4 (tid % 4)
+    const int lr = threadIdx.x >> 2, lk = 4 * (threadIdx.x & 3);
+    double2 la[2], lb[2];
+    auto load = [&](int k0) {
+        const int gm = m0 + lr, src = pr[lr].y;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int gk = k0 + lk + 2 * h;
+            la[h] = make_double2(gm < M && gk < K ? Mt[(int64_t)gm * K + gk] : 0.0,
+                                 gm < M && gk + 1 < K ? Mt[(int64_t)gm * K + gk + 1] : 0.0);
+            lb[h] = make_double2(src >= 0 && gk < K ? X[(int64_t)src * ldx + gk] : 0.0,
+                                 src >= 0 && gk + 1 < K ? X[(int64_t)src * ldx + gk + 1] : 0.0);
         }
-        __syncthreads();
+    };
+    auto store = [&](int buf) {
 #pragma unroll
-        for (int kk = 0; kk < PG_K; ++kk) {
-            double a[4], b[4];
+        for (int h = 0; h < 2; ++h) {
+            *reinterpret_cast<double2*>(&As[buf][lr * DM_LD + lk + 2 * h]) = la[h];
+            *reinterpret_cast<double2*>(&Bs[buf][lr * DM_LD + lk + 2 * h]) = lb[h];
+        }
+    };
+    double c[4][2][2];
 #pragma unroll
-            for (int i = 0; i < 4; ++i) a[i] = As[kk][ty + 16 * i];
+    for (int i = 0; i < 4; ++i)
 #pragma unroll
-            for (int j = 0; j < 4; ++j) b[j] = Bs[kk][tx + 16 * j];
+        for (int j = 0; j < 2; ++j) c[i][j][0] = c[i][j][1] = 0.0;
+    int k0 = (m0 / DM_K) * DM_K;                              // R^-1 is upper triangular
+    load(k0);
+    store(0);
+    __syncthreads();
+    int buf = 0;
+    const int fr = lane >> 2, fk = lane & 3;                  // fragment row / k of this lane
+    for (; k0 < K; k0 += DM_K) {
+        const bool more = k0 + DM_K < K;
+        if (more) load(k0 + DM_K);
+#pragma unroll
+        for (int kk = 0; kk < DM_K; kk += 4) {
+            double a[4], b[2];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) a[i] = As[buf][(wm * 32 + i * 8 + fr) * DM_LD + kk + fk];
+#pragma unroll
+            for (int j = 0; j < 2; ++j) b[j] = Bs[buf][(wn * 16 + j * 8 + fr) * DM_LD + kk + fk];
 #pragma unroll
             for (int i = 0; i < 4; ++i)
 #pragma unroll
-                for (int j = 0; j < 4; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
+                for (int j = 0; j < 2; ++j)
+                    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                                 : "+d"(c[i][j][0]), "+d"(c[i][j][1])
+                                 : "d"(a[i]), "d"(b[j]));
         }
-        __syncthreads();
+        if (more) {
+            store(buf ^ 1);
+            __syncthreads();
+            buf ^= 1;
+        }
     }
+    // C fragment: row fr of the 8 x 8 tile, columns 2 (lane % 4) + {0, 1}
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-        int pj = tx + 16 * j;
-        if (pj >= np) continue;
-        int t = pr[pj].x;
-        double sc = scale[t];
+    for (int j = 0; j < 2; ++j)
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            int gm = m0 + ty + 16 * i;
-            if (gm >= M) continue;
-            if constexpr (sizeof(OutT) == sizeof(double)) {
-                Y[(int64_t)t * ldy + gm] = sc * acc[i][j];
-            } else {
-                float* y = reinterpret_cast<float*>(Y + (int64_t)t * ldy);
-                y[4 * (gm / 3) + gm % 3] = (float)(cf * sc * acc[i][j]);
+        for (int e = 0; e < 2; ++e) {
+            const int pj = wn * 16 + j * 8 + 2 * fk + e;
+            if (pj >= np) continue;
+            const int t = pr[pj].x;
+            const double sc = scale[t];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int gm = m0 + wm * 32 + i * 8 + fr;
+                if (gm >= M) continue;
+                if constexpr (sizeof(OutT) == sizeof(double)) {
+                    Y[(int64_t)t * ldy + gm] = sc * c[i][j][e];
+                } else {
+                    float* y = reinterpret_cast<float*>(Y + (int64_t)t * ldy);
+                    y[4 * (gm / 3) + gm % 3] = (float)(cf * sc * c[i][j][e]);
+                }
             }
         }
-    }
 }
 
 void gemm_pairs_f64(const OpPairs& P, const double* mat, int M, int K, const double* X, int ldx,
                     const double* scale, double* Y, int ldy, cudaStream_t s) {
     if (P.npairs == 0) return;
-    dim3 grid(ceil_div(M, PG_M), ceil_div(P.npairs, PG_N), 1);
-    gemm_pairs_f64_kernel<double><<<grid, 256, 0, s>>>(P.pairs.p, (int)P.npairs, mat, M, K, X, ldx, scale, 1.0, Y,
+    dim3 grid(ceil_div(M, DM_M), ceil_div(P.npairs, DM_N), 1);
+    gemm_pairs_dmma_kernel<double><<<grid, 256, 0, s>>>(P.pairs.p, (int)P.npairs, mat, M, K, X, ldx, scale, 1.0, Y,
                                                        ldy);
     EB_CHECK_LAUNCH();
 }
@@ -411,8 +452,8 @@ void gemm_pairs_f64(const OpPairs& P, const double* mat, int M, int K, const dou
 void gemm_pairs_f64_to_f32(const OpPairs& P, const double* mat, int M, int K, const double* X, int ldx,
                            const double* scale, double cf, float4* Y, int ldy, cudaStream_t s) {
     if (P.npairs == 0) return;
-    dim3 grid(ceil_div(M, PG_M), ceil_div(P.npairs, PG_N), 1);
-    gemm_pairs_f64_kernel<float4><<<grid, 256, 0, s>>>(P.pairs.p, (int)P.npairs, mat, M, K, X, ldx, scale, cf, Y,
+    dim3 grid(ceil_div(M, DM_M), ceil_div(P.npairs, DM_N), 1);
+    gemm_pairs_dmma_kernel<float4><<<grid, 256, 0, s>>>(P.pairs.p, (int)P.npairs, mat, M, K, X, ldx, scale, cf, Y,
                                                        ldy);
     EB_CHECK_LAUNCH();
 }
