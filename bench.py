@@ -234,6 +234,50 @@ def gmres_workload(args, eb, torch):
     print(json.dumps(line), flush=True)
 
 
+def stress_workload(args, eb, torch):
+    """configs[3]: stress (D + S) of 500k beam-surface sources with smooth densities at 1M
+    interior grid targets, p = 8: the topological-derivative evaluation.  Device time per
+    evaluation (L2-flushed steps), rel-L2 on 1000 sampled targets vs the fp64 oracle."""
+    from oracle import cdirect
+    from oracle import kernels as KN
+    from workloads import geometry as geo
+    d = geo.config3()
+    t = {k: torch.from_numpy(np.ascontiguousarray(v, np.float32)).cuda() for k, v in d.items()
+         if isinstance(v, np.ndarray)}
+    tree = eb.fmm_build_tree(t["src"], t["nrm"], t["w"], trg=t["trg"], max_pts=args.max_pts, p=args.p, K=d["K"],
+                             G=d["G"])
+    nt = d["trg"].shape[0]
+    out = torch.empty((nt, 6), device="cuda")
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+    for _ in range(max(args.warmup, 3)):
+        eb.fmm_eval_stress(tree, eb.KERNEL_DS, t["f"], t["g"], out=out)
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    launches0 = eb.ebem_launch_count()
+    with ClockSampler(0) as clk:
+        for k in range(args.steps):
+            flush.fill_(float(k))
+            ev[k][0].record()
+            eb.fmm_eval_stress(tree, eb.KERNEL_DS, t["f"], t["g"], out=out)
+            ev[k][1].record()
+        torch.cuda.synchronize()
+    launches = (eb.ebem_launch_count() - launches0) // args.steps
+    ms = float(np.mean([a.elapsed_time(b) for a, b in ev]))
+    idx = np.sort(np.random.default_rng(11).choice(nt, 1000, replace=False))
+    ref = cdirect.direct_sum(KN.KERNEL_DS, d["trg"][idx], d["src"], d["K"], d["G"], w=d["w"], f=d["f"], g=d["g"],
+                             nrm=d["nrm"])
+    rel = KN.rel_l2(out.cpu().numpy()[idx].astype(np.float64), ref)
+    line = {"metric": "FMM stress evaluation ms (configs[3])", "value": ms, "unit": "ms", "n_gpus": 1,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32 (fp64 plan / equivalent densities)",
+            "data": "synthetic",
+            "config": {"workload": f"beam surface {d['src'].shape[0]} sources, {nt} interior grid targets, "
+                                   "kernel D+S (6-component stress)", "p": args.p, "max_pts": args.max_pts,
+                       "l2": "flushed between steps (256 MB write)"},
+            "rel_l2": rel, "targets_per_s": nt / (ms * 1e-3), "gpu_launches": launches, "clocks": clk.summary()}
+    print(json.dumps(line), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -248,7 +292,7 @@ def main():
     ap.add_argument("--cpu-sample", type=int, default=3072)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-p2p", action="store_true")
-    ap.add_argument("--workload", default="matvec", choices=["matvec", "gmres"])
+    ap.add_argument("--workload", default="matvec", choices=["matvec", "gmres", "stress"])
     ap.add_argument("--nq", type=int, default=16)
     ap.add_argument("--cell-nc", type=int, default=160)
     ap.add_argument("--cell-level", type=int, default=5)
@@ -260,7 +304,7 @@ def main():
     if args.max_pts is None:
         args.max_pts = 1024 if gm else 64     # gmres: fastest leaf size for 16 sources per panel
     if args.p is None:
-        args.p = 8 if gm else 6
+        args.p = 8 if args.workload in ("gmres", "stress") else 6
     if args.impl == "reference":
         return run_reference(args)
 
@@ -278,6 +322,8 @@ def main():
     pk = peaks()
     if args.workload == "gmres":
         return gmres_workload(args, eb, torch)
+    if args.workload == "stress":
+        return stress_workload(args, eb, torch)
 
     d = workload(args.n)
     n = d["src"].shape[0]
