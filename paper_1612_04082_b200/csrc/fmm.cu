@@ -431,6 +431,13 @@ near_eval_kernel(int n_eval, const int* __restrict__ eval_box, const int* __rest
     }
 }
 
+// precise M2L (p >= 9, GMRES) on the two-slice fast-kernel data flow with drained groups;
+// EBEM_M2L_DRAIN=0 selects the one-slice precise kernel instead
+static bool m2l_drain_fast() {
+    static const bool on = !(std::getenv("EBEM_M2L_DRAIN") && std::atoi(std::getenv("EBEM_M2L_DRAIN")) == 0);
+    return on;
+}
+
 // ------------------------------------------------------------------ schedule (host)
 void schedule_tree(Tree& t, cudaStream_t s) {
     const Plan& P = *t.plan;
@@ -715,7 +722,7 @@ void schedule_tree(Tree& t, cudaStream_t s) {
         tc_make_map_b(&t.mWs, t.Ws.p, std::max(1, t.n_dn), me, lde);
         tc_build_tiles(t.q2z_up, me, mc, false);
         tc_build_tiles(t.q2z_dn, me, mc, false);
-        tc_build_tiles(t.m2l, me, me, t.tc_fast);
+        tc_build_tiles(t.m2l, me, me, t.tc_fast || m2l_drain_fast());
         for (auto& x : t.m2m) tc_build_tiles(x, me, me, false);
         for (auto& x : t.l2l) tc_build_tiles(x, me, me, false);
     }
@@ -782,7 +789,7 @@ void tree_precise(Tree& t, cudaStream_t s) {
     }
     if (t.tc_fast) {
         t.tc_fast = false;
-        tc_build_tiles(t.m2l, P.me, P.me, false);
+        tc_build_tiles(t.m2l, P.me, P.me, m2l_drain_fast());
     }
     EB_CUDA(cudaStreamSynchronize(s));
 }
@@ -961,7 +968,9 @@ void fmm_evaluate(Tree& t, int kernel, const float* f, const float* g, float* ou
     };
     if (!conc) q2z_dn();
     mark(phase++);
-    if (t.use_tc && t.tc_fast) tc_pairs_gemm_fast(t.m2l, P.mM2L_b, P.mM2L_s, t.Zb.p, t.Zs.p, lde, me, me, t.W.p, lde, sa);
+    if (t.use_tc && t.tc_fast) tc_pairs_gemm_fast(t.m2l, P.mM2L_b, P.mM2L_s, t.Zb.p, t.Zs.p, lde, me, me, t.W.p, lde, false, sa);
+    else if (t.use_tc && m2l_drain_fast())   // precise accumulation, two-slice fast-kernel data flow
+        tc_pairs_gemm_fast(t.m2l, P.mM2L_b, P.mM2L_s, t.Zb.p, t.Zs.p, lde, me, me, t.W.p, lde, true, sa);
     else if (t.use_tc) tc_pairs_gemm(t.m2l, P.mM2L_b, P.mM2L_s, t.mZb, t.mZs, me, me, t.W.p, lde, sa);
     else gemm_pairs_f32(t.m2l, P.M2L.p, me, me, lde, t.Z.p, lde, t.W.p, lde, sa);
     if (conc) {

@@ -195,7 +195,7 @@ void tc_split_rows(const XT* X, int ld, int64_t row0, int64_t nrows, int K, floa
 void tree_precise(Tree& t, cudaStream_t s);
 void tc_build_tiles(OpPairs& P, int M, int K, bool fast);
 void tc_pairs_gemm_fast(const OpPairs& P, const CUtensorMap& Ab, const CUtensorMap& As, const float* Bb,
-                        const float* Bs, int ldb, int M, int K, double* Y, int ldy, cudaStream_t s);
+                        const float* Bs, int ldb, int M, int K, double* Y, int ldy, bool drain, cudaStream_t s);
 void tc_pairs_gemm(const OpPairs& P, const CUtensorMap& Ab, const CUtensorMap& As, const CUtensorMap& Bb,
                    const CUtensorMap& Bs, int M, int K, double* Y, int ldy, cudaStream_t s);
 // fp64 variant with per-pair scale (r of the box, looked up from scale[t])

@@ -318,7 +318,13 @@ constexpr int THREADS = 256;
 constexpr int NG = (BN / 4 + NPROD - 1) / NPROD;        // 4-row groups per producer warp
 }  // namespace fast
 
-__global__ void __launch_bounds__(fast::THREADS, 1)
+// DRAIN = true: the precise variant for p >= 9 and GMRES.  The MMAs of every GROUP K chunks go
+// to one of two ping-pong TMEM buffers (2 slices x 128 columns each); eight epilogue warps
+// (one per TMEM lane quarter and slice) add each finished group into fp32 registers (round
+// to nearest) while the MMA fills the other buffer, so no tensor-core accumulation chain is
+// longer than GROUP chunks.
+template <bool DRAIN>
+__global__ void __launch_bounds__(DRAIN ? 384 : fast::THREADS, 1)
 tc_pairs_fast_kernel(const __grid_constant__ CUtensorMap mapAb, const __grid_constant__ CUtensorMap mapAs,
                      const float* __restrict__ Bb, const float* __restrict__ Bs, int ldb,
                      const Tile* __restrict__ tiles, int ntiles, const int2* __restrict__ pairs, int M, int K,
@@ -341,7 +347,7 @@ tc_pairs_fast_kernel(const __grid_constant__ CUtensorMap mapAb, const __grid_con
         }
         for (int b = 0; b < 2; ++b) {
             mbar_init(smem_u32(&accf_b[b]), 1);
-            mbar_init(smem_u32(&acce_b[b]), 4);
+            mbar_init(smem_u32(&acce_b[b]), DRAIN ? 8 : 4);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -407,6 +413,49 @@ tc_pairs_fast_kernel(const __grid_constant__ CUtensorMap mapAb, const __grid_con
                 asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(full) : "memory");
             }
         }
+    } else if (warp == 1 && DRAIN) {
+        // ---------------- MMA issuer, drained groups
+        int c = 0, G = 0;
+        for (int ti = blockIdx.x; ti < ntiles; ti += gridDim.x) {
+            const uint32_t nmma = (uint32_t)((tiles[ti].np + 15) & ~15);
+            const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((nmma >> 3) << 17) |
+                                   ((uint32_t)(BM >> 4) << 24);
+            const int kc0 = tiles[ti].kc0, kc1 = tiles[ti].kc1;
+            for (int kc = kc0; kc < kc1; ++kc, ++c) {
+                const int s = c % STAGES;
+                const int b = G & 1;
+                const bool gfirst = ((kc - kc0) % GROUP) == 0,
+                           glast = ((kc - kc0) % GROUP) == GROUP - 1 || kc == kc1 - 1;
+                if (gfirst) {   // the buffer's previous group has been drained
+                    mbar_wait(smem_u32(&acce_b[b]), ((G >> 1) & 1) ^ 1);
+                    asm volatile("tcgen05.fence::after_thread_sync;");
+                }
+                mbar_wait(smem_u32(&full_b[s]), (c / STAGES) & 1);
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                asm volatile("tcgen05.fence::after_thread_sync;");
+                if (lane == 0) {
+                    const uint32_t st = smem_u32(smem + s * STAGE_BYTES);
+                    const uint64_t bb = smem_desc(st + 2 * MT * OPND_BYTES), bs = smem_desc(st + (2 * MT + 1) * OPND_BYTES);
+                    const int ksteps = min(BK, K - kc * BK + 7) / 8;
+                    for (int k = 0; k < ksteps; ++k) {
+                        const uint64_t off = (uint64_t)(2 * k);
+#pragma unroll
+                        for (int mt = 0; mt < MT; ++mt) {
+                            const uint64_t a_b = smem_desc(st + (2 * mt) * OPND_BYTES) + off;
+                            const uint64_t a_s = smem_desc(st + (2 * mt + 1) * OPND_BYTES) + off;
+                            const uint32_t d = tmem + (uint32_t)((b * MT + mt) * BN);
+                            mma_tf32(d, a_b, bb + off, idesc, !gfirst || k != 0);
+                            mma_tf32(d, a_b, bs + off, idesc, 1);
+                            mma_tf32(d, a_s, bb + off, idesc, 1);
+                        }
+                    }
+                    mma_commit(smem_u32(&empty_b[s]));
+                    if (glast) mma_commit(smem_u32(&accf_b[b]));
+                }
+                __syncwarp();
+                if (glast) ++G;
+            }
+        }
     } else if (warp == 1) {
         // ---------------- MMA issuer
         int c = 0, it = 0;
@@ -446,7 +495,34 @@ tc_pairs_fast_kernel(const __grid_constant__ CUtensorMap mapAb, const __grid_con
                 __syncwarp();
             }
         }
-    } else if (warp >= EPI_WARP0) {
+    } else if (warp >= EPI_WARP0 && DRAIN) {
+        // ---------------- drains: warp -> (lane quarter, slice); fp32 register sums, then atomics
+        const int wq = warp & 3, mt = (warp - EPI_WARP0) >> 2;
+        int G = 0;
+        for (int ti = blockIdx.x; ti < ntiles; ti += gridDim.x) {
+            const Tile tl = tiles[ti];
+            float acc[BN];
+#pragma unroll
+            for (int j = 0; j < BN; ++j) acc[j] = 0.f;
+            const int ngroups = (tl.kc1 - tl.kc0 + GROUP - 1) / GROUP;
+            for (int g = 0; g < ngroups; ++g, ++G) {
+                const int b = G & 1;
+                mbar_wait(smem_u32(&accf_b[b]), (G >> 1) & 1);
+                asm volatile("tcgen05.fence::after_thread_sync;");
+                drain_add(tmem, wq, (b * MT + mt) * BN, acc);
+                asm volatile("tcgen05.fence::before_thread_sync;");
+                __syncwarp();
+                if (lane == 0) mbar_arrive(smem_u32(&acce_b[b]));
+            }
+            const int row = tl.m0 + mt * BM + 32 * wq + lane;
+            if (row < M) {
+                const int2* pp = pairs + tl.p0;
+#pragma unroll
+                for (int j = 0; j < BN; ++j)
+                    if (j < tl.np) atomicAdd(Y + (int64_t)__ldg(&pp[j].x) * ldy + row, (double)acc[j]);
+            }
+        }
+    } else if (warp >= EPI_WARP0 && warp < EPI_WARP0 + 4) {
         // ---------------- epilogue: TMEM -> fp64 atomics, 32 columns at a time
         const int wq = warp - EPI_WARP0;
         int it = 0;
@@ -589,16 +665,16 @@ void tc_build_tiles(OpPairs& P, int M, int K, bool fast) {
 }
 
 void tc_pairs_gemm_fast(const OpPairs& P, const CUtensorMap& Ab, const CUtensorMap& As, const float* Bb,
-                        const float* Bs, int ldb, int M, int K, double* Y, int ldy, cudaStream_t s) {
+                        const float* Bs, int ldb, int M, int K, double* Y, int ldy, bool drain, cudaStream_t s) {
     if (P.ntiles == 0) return;
-    static bool attr = false;
-    if (!attr) {
-        EB_CUDA(cudaFuncSetAttribute(tc::tc_pairs_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     tc::fast::SMEM_BYTES));
-        attr = true;
+    static bool attr[2] = {false, false};
+    auto fn = drain ? tc::tc_pairs_fast_kernel<true> : tc::tc_pairs_fast_kernel<false>;
+    if (!attr[drain]) {
+        EB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::fast::SMEM_BYTES));
+        attr[drain] = true;
     }
     const int grid = std::min(P.ntiles, num_sms());
-    tc::tc_pairs_fast_kernel<<<grid, tc::fast::THREADS, tc::fast::SMEM_BYTES, s>>>(
+    fn<<<grid, drain ? 384 : tc::fast::THREADS, tc::fast::SMEM_BYTES, s>>>(
         Ab, As, Bb, Bs, ldb, reinterpret_cast<const tc::Tile*>(P.tiles.p), P.ntiles, P.pairs.p, M, K, Y, ldy);
     EB_CHECK_LAUNCH();
 }
