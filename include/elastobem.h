@@ -211,6 +211,8 @@ int64_t fmm_tree_export(const ebem_tree *tree, int what, void *buf, int64_t cap)
  *   preconditioner with the panels' own 3x3 blocks (-U_self on Dirichlet panels,
  *   1/2 I + P_self on Neumann panels).  The solution of A x = b is the same.
  *   iters_out / resid_out (host, may be NULL): iterations and final relative residual.
+ *   restart in [1, 63] (EBEM_ERR_ARG otherwise): the Krylov basis is (restart + 1) fp64
+ *   vectors of npanels*3 on the device.
  * Array arguments of bem_apply / bem_rhs / bem_gmres_solve must be device pointers.
  */
 typedef struct ebem_bem ebem_bem;

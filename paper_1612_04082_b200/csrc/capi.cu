@@ -295,7 +295,7 @@ extern "C" int bem_gmres_solve(ebem_bem* bem, const int32_t* bc_type, const floa
     EB_API_BEGIN
     set_last_error("");
     EB_REQUIRE(bem && bc_type && bc_val && x, "NULL argument");
-    EB_REQUIRE(restart >= 1 && max_iter >= 1 && tol > 0, "bad GMRES parameters");
+    EB_REQUIRE(restart >= 1 && restart <= 63 && max_iter >= 1 && tol > 0, "bad GMRES parameters");
     EB_REQUIRE(is_device_ptr(x) && is_device_ptr(bc_val) && is_device_ptr(bc_type),
                "bem_gmres_solve needs device pointers");
     const int rc = ebem::bem_gmres(*reinterpret_cast<Bem*>(bem), bc_type, bc_val, x, restart, max_iter, tol, iters_out,
