@@ -70,6 +70,26 @@ __device__ __forceinline__ void acc_P(T dx, T dy, T dz, T ri, T gx, T gy, T gz, 
     u[2] = fmat(A, gz, fmat(B, n3z, fmat(C, dz, u[2])));
 }
 
+// both layers at once (U + P): the two d-terms share one coefficient, S = (d.f) rinv^3 + C,
+// 37 FP32 instructions per pair with d and r^2 instead of 41 for acc_U + acc_P
+template <class T>
+__device__ __forceinline__ void acc_UP(T dx, T dy, T dz, T ri, T fx, T fy, T fz, T gx, T gy, T gz, T n3x, T n3y,
+                                       T n3z, T q, T a1, T a3, T* u) {
+    T ri2 = ri * ri;
+    T ri3 = ri2 * ri;
+    T df = fmat(dz, fz, fmat(dy, fy, dx * fx));
+    T dn3 = fmat(dz, n3z, fmat(dy, n3y, dx * n3x));
+    T dg = fmat(dz, gz, fmat(dy, gy, dx * gx));
+    T ar3 = a3 * ri3;
+    T A = dn3 * ar3;
+    T B = dg * ar3;
+    T S = fmat(df, ri3, ri3 * fmat(dn3 * dg, ri2, -q));
+    T t = a1 * ri;
+    u[0] = fmat(t, fx, fmat(A, gx, fmat(B, n3x, fmat(S, dx, u[0]))));
+    u[1] = fmat(t, fy, fmat(A, gy, fmat(B, n3y, fmat(S, dy, u[1]))));
+    u[2] = fmat(t, fz, fmat(A, gz, fmat(B, n3z, fmat(S, dz, u[2]))));
+}
+
 // stress of a single layer: f = cD w f (prepared, cD = -1/(8 pi (1-nu))):
 // s_ij += a rinv^3 (f_i d_j + f_j d_i - d_ij (d.f)) + 3 rinv^5 (d.f) d_i d_j
 template <class T>

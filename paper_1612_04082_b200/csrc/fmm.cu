@@ -1019,7 +1019,7 @@ static double flops_per_pair(int kernel) {
     switch (kernel) {
         case K_U: return 29;
         case K_P: return 45;
-        case K_UP: return 65;
+        case K_UP: return 59;
         case K_D: return 54;
         case K_S: return 87;
         default: return 131;

@@ -55,11 +55,15 @@ __device__ __forceinline__ void pair_loop(const float4* __restrict__ srec, int c
         float r2 = dx * dx + dy * dy + dz * dz;
         float ri = safe_rinv(r2);
         if (!STRESS) {
-            if (SL) {
+            if (SL && DL) {
+                const float4 f = srec[j * R + 1];
+                const float4 g = srec[j * R + 2];
+                const float4 n = srec[j * R + 3];
+                acc_UP(dx, dy, dz, ri, f.x, f.y, f.z, g.x, g.y, g.z, n.x, n.y, n.z, p.w, kc.a1, kc.a3, acc);
+            } else if (SL) {
                 const float4 f = srec[j * R + 1];
                 acc_U(dx, dy, dz, ri, f.x, f.y, f.z, kc.a1, acc);
-            }
-            if (DL) {
+            } else {
                 const float4 g = srec[j * R + 2];
                 const float4 n = srec[j * R + 3];
                 acc_P(dx, dy, dz, ri, g.x, g.y, g.z, n.x, n.y, n.z, p.w, kc.a3, acc);
@@ -110,8 +114,9 @@ __device__ __forceinline__ void pair_loop_multi(const float4* __restrict__ srec,
             float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
             float ri = safe_rinv(r2);
             if (!STRESS) {
-                if (SL) acc_U(dx, dy, dz, ri, f.x, f.y, f.z, kc.a1, acc[k]);
-                if (DL) acc_P(dx, dy, dz, ri, g.x, g.y, g.z, n.x, n.y, n.z, p.w, kc.a3, acc[k]);
+                if (SL && DL) acc_UP(dx, dy, dz, ri, f.x, f.y, f.z, g.x, g.y, g.z, n.x, n.y, n.z, p.w, kc.a1, kc.a3, acc[k]);
+                else if (SL) acc_U(dx, dy, dz, ri, f.x, f.y, f.z, kc.a1, acc[k]);
+                else acc_P(dx, dy, dz, ri, g.x, g.y, g.z, n.x, n.y, n.z, p.w, kc.a3, acc[k]);
             } else {
                 if (SL) acc_D(dx, dy, dz, ri, f.x, f.y, f.z, kc.a, acc[k]);
                 if (DL) acc_S(dx, dy, dz, ri, g.x, g.y, g.z, n.x, n.y, n.z, p.w, NG, kc.a, kc.nu, kc.b4, acc[k]);
@@ -145,8 +150,9 @@ __device__ __forceinline__ void pair_loop_strided(const float4* __restrict__ sre
             float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
             float ri = safe_rinv(r2);
             if (!STRESS) {
-                if (SL) acc_U(dx, dy, dz, ri, f.x, f.y, f.z, kc.a1, acc[k]);
-                if (DL) acc_P(dx, dy, dz, ri, gg.x, gg.y, gg.z, n.x, n.y, n.z, p.w, kc.a3, acc[k]);
+                if (SL && DL) acc_UP(dx, dy, dz, ri, f.x, f.y, f.z, gg.x, gg.y, gg.z, n.x, n.y, n.z, p.w, kc.a1, kc.a3, acc[k]);
+                else if (SL) acc_U(dx, dy, dz, ri, f.x, f.y, f.z, kc.a1, acc[k]);
+                else acc_P(dx, dy, dz, ri, gg.x, gg.y, gg.z, n.x, n.y, n.z, p.w, kc.a3, acc[k]);
             } else {
                 if (SL) acc_D(dx, dy, dz, ri, f.x, f.y, f.z, kc.a, acc[k]);
                 if (DL) acc_S(dx, dy, dz, ri, gg.x, gg.y, gg.z, n.x, n.y, n.z, p.w, NG, kc.a, kc.nu, kc.b4, acc[k]);
