@@ -140,4 +140,36 @@ __device__ __forceinline__ void acc_S(T dx, T dy, T dz, T ri, T gx, T gy, T gz, 
     s[5] = fmat(ux, dz, fmat(uz, dx, fmat(ri3, NG[5], s[5])));
 }
 
+// both stress kernels at once (D + S): one symmetric update with w = v (D) + u (S) and one
+// diagonal coefficient (Cdelta - A (d.f)) instead of two
+template <class T>
+__device__ __forceinline__ void acc_DS(T dx, T dy, T dz, T ri, T fx, T fy, T fz, T gx, T gy, T gz, T nx, T ny,
+                                       T nz, T ng, const T* NG, T a, T nu, T b4, T* s) {
+    T ri2 = ri * ri;
+    T ri3 = ri2 * ri;
+    T ri5 = ri3 * ri2;
+    // D part: v = A f + (B/2) d with A = a rinv^3, B = 3 (d.f) rinv^5; diagonal -A (d.f)
+    T df = fmat(dz, fz, fmat(dy, fy, dx * fx));
+    T A = a * ri3;
+    T hB = T(1.5) * df * ri5;
+    // S part
+    T dn = fmat(dz, nz, fmat(dy, ny, dx * nx));
+    T dg = fmat(dz, gz, fmat(dy, gy, dx * gx));
+    T dndg = dn * dg;
+    T hCdd = T(0.5) * ri5 * (T(3) * a * ng - T(15) * dndg * ri2);
+    T Cgd = T(3) * nu * dn * ri5;
+    T Cnd = T(3) * nu * dg * ri5;
+    T Cdl = T(3) * a * dndg * ri5 - b4 * ng * ri3 - A * df;
+    const T hd = hCdd + hB;
+    T wx = fmat(Cnd, nx, fmat(Cgd, gx, fmat(A, fx, hd * dx)));
+    T wy = fmat(Cnd, ny, fmat(Cgd, gy, fmat(A, fy, hd * dy)));
+    T wz = fmat(Cnd, nz, fmat(Cgd, gz, fmat(A, fz, hd * dz)));
+    s[0] = fmat(T(2) * wx, dx, fmat(ri3, NG[0], s[0] + Cdl));
+    s[1] = fmat(T(2) * wy, dy, fmat(ri3, NG[1], s[1] + Cdl));
+    s[2] = fmat(T(2) * wz, dz, fmat(ri3, NG[2], s[2] + Cdl));
+    s[3] = fmat(wx, dy, fmat(wy, dx, fmat(ri3, NG[3], s[3])));
+    s[4] = fmat(wy, dz, fmat(wz, dy, fmat(ri3, NG[4], s[4])));
+    s[5] = fmat(wx, dz, fmat(wz, dx, fmat(ri3, NG[5], s[5])));
+}
+
 }  // namespace ebem

@@ -1022,7 +1022,7 @@ static double flops_per_pair(int kernel) {
         case K_UP: return 59;
         case K_D: return 54;
         case K_S: return 87;
-        default: return 131;
+        default: return 104;
     }
 }
 

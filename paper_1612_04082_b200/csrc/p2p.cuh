@@ -69,11 +69,18 @@ __device__ __forceinline__ void pair_loop(const float4* __restrict__ srec, int c
                 acc_P(dx, dy, dz, ri, g.x, g.y, g.z, n.x, n.y, n.z, p.w, kc.a3, acc);
             }
         } else {
-            if (SL) {
+            if (SL && DL) {
+                const float4 f = srec[j * R + 1];
+                const float4 g = srec[j * R + 2];
+                const float4 n = srec[j * R + 3];
+                const float4 t0 = srec[j * R + 4];
+                const float4 t1 = srec[j * R + 5];
+                const float NG[6] = {t0.x, t0.y, t0.z, t0.w, t1.x, t1.y};
+                acc_DS(dx, dy, dz, ri, f.x, f.y, f.z, g.x, g.y, g.z, n.x, n.y, n.z, p.w, NG, kc.a, kc.nu, kc.b4, acc);
+            } else if (SL) {
                 const float4 f = srec[j * R + 1];
                 acc_D(dx, dy, dz, ri, f.x, f.y, f.z, kc.a, acc);
-            }
-            if (DL) {
+            } else {
                 const float4 g = srec[j * R + 2];
                 const float4 n = srec[j * R + 3];
                 const float4 t0 = srec[j * R + 4];
@@ -118,8 +125,9 @@ __device__ __forceinline__ void pair_loop_multi(const float4* __restrict__ srec,
                 else if (SL) acc_U(dx, dy, dz, ri, f.x, f.y, f.z, kc.a1, acc[k]);
                 else acc_P(dx, dy, dz, ri, g.x, g.y, g.z, n.x, n.y, n.z, p.w, kc.a3, acc[k]);
             } else {
-                if (SL) acc_D(dx, dy, dz, ri, f.x, f.y, f.z, kc.a, acc[k]);
-                if (DL) acc_S(dx, dy, dz, ri, g.x, g.y, g.z, n.x, n.y, n.z, p.w, NG, kc.a, kc.nu, kc.b4, acc[k]);
+                if (SL && DL) acc_DS(dx, dy, dz, ri, f.x, f.y, f.z, g.x, g.y, g.z, n.x, n.y, n.z, p.w, NG, kc.a, kc.nu, kc.b4, acc[k]);
+                else if (SL) acc_D(dx, dy, dz, ri, f.x, f.y, f.z, kc.a, acc[k]);
+                else acc_S(dx, dy, dz, ri, g.x, g.y, g.z, n.x, n.y, n.z, p.w, NG, kc.a, kc.nu, kc.b4, acc[k]);
             }
         }
     }
@@ -154,8 +162,9 @@ __device__ __forceinline__ void pair_loop_strided(const float4* __restrict__ sre
                 else if (SL) acc_U(dx, dy, dz, ri, f.x, f.y, f.z, kc.a1, acc[k]);
                 else acc_P(dx, dy, dz, ri, gg.x, gg.y, gg.z, n.x, n.y, n.z, p.w, kc.a3, acc[k]);
             } else {
-                if (SL) acc_D(dx, dy, dz, ri, f.x, f.y, f.z, kc.a, acc[k]);
-                if (DL) acc_S(dx, dy, dz, ri, gg.x, gg.y, gg.z, n.x, n.y, n.z, p.w, NG, kc.a, kc.nu, kc.b4, acc[k]);
+                if (SL && DL) acc_DS(dx, dy, dz, ri, f.x, f.y, f.z, gg.x, gg.y, gg.z, n.x, n.y, n.z, p.w, NG, kc.a, kc.nu, kc.b4, acc[k]);
+                else if (SL) acc_D(dx, dy, dz, ri, f.x, f.y, f.z, kc.a, acc[k]);
+                else acc_S(dx, dy, dz, ri, gg.x, gg.y, gg.z, n.x, n.y, n.z, p.w, NG, kc.a, kc.nu, kc.b4, acc[k]);
             }
         }
     }
