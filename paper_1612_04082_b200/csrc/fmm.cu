@@ -1059,7 +1059,7 @@ int phase_stats(Tree& t, int kernel, ebem_phase_stat* out, int cap) {
     st[7].flops = 2.0 * me * me * t.w_l2l_pairs;
     st[7].bytes = 4.0 * 8 * me * me + 4.0 * 2 * me * t.w_l2l_pairs;
     st[8].fp64 = 1;
-    st[8].flops = st[8].flops_fp64 = 2.0 * me * me * (t.n_phid + t.n_phiu);
+    st[8].flops = st[8].flops_fp64 = me * (me + 1) * (double)(t.n_phid + t.n_phiu);   // triangular R^-1
     st[8].bytes = 2 * 8.0 * me * me + (4.0 + 8.0) * me * (t.n_phid + t.n_phiu);
     st[9].interactions = t.w_p2p_inter + t.w_l2t_inter + t.w_m2t_inter;
     st[9].fp64 = 1;
