@@ -308,12 +308,21 @@ def main():
     if args.impl == "reference":
         return run_reference(args)
 
-    import torch
-    import paper_1612_04082_b200 as eb
-
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+    ids = vis.split(",") if vis else [str(i) for i in range(64)]
+    smi_index = ids[local]                       # nvidia-smi uses physical indices
+    if world > 1:
+        # one GPU per process, made the only visible device before CUDA starts: the library
+        # (its own static CUDA runtime) then works on device 0 like torch does
+        os.environ["CUDA_VISIBLE_DEVICES"] = ids[local]
+        local = 0
+
+    import torch
+    import paper_1612_04082_b200 as eb
+
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
@@ -352,7 +361,7 @@ def main():
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
-    with ClockSampler(local) as clk:
+    with ClockSampler(smi_index) as clk:
         for k in range(args.steps):
             flush.fill_(float(k))
             ev[k][0].record()
