@@ -292,6 +292,7 @@ def main():
     ap.add_argument("--cpu-sample", type=int, default=3072)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-p2p", action="store_true")
+    ap.add_argument("--no-p10", action="store_true", help="skip the p = 10 line (configs[2]'s second order)")
     ap.add_argument("--workload", default="matvec", choices=["matvec", "gmres", "stress"])
     ap.add_argument("--nq", type=int, default=16)
     ap.add_argument("--cell-nc", type=int, default=160)
@@ -421,8 +422,8 @@ def main():
     try:
         tr = json.load(open(os.path.join(ROOT, "profiles", "r01", "traffic.json")))
         if roof["phase"] in tr:
-            t = tr[roof["phase"]]
-            roof["traffic"] = t["dram_read"] + t["dram_write"]
+            rec = tr[roof["phase"]]
+            roof["traffic"] = rec["dram_read"] + rec["dram_write"]
             roof["traffic_source"] = tr["_source"]
     except Exception:
         pass
@@ -458,17 +459,41 @@ def main():
                "sample": f"{args.cpu_sample} random targets x all {n} sources (fp64 C direct sum), "
                          f"{sec:.1f} s, extrapolated to all {n} targets"}
 
+    # ---- configs[2]'s second order: the same points at p = 10 (fp64 far field, drained
+    # tensor-core accumulation), 5 L2-flushed steps, error on the same oracle sample
+    p10 = None
+    if rank == 0 and world == 1 and not args.no_p10 and args.p != 10:
+        tree10 = eb.fmm_build_tree(t["src"], t["nrm"], t["w"], max_pts=args.max_pts, p=10, K=d["K"], G=d["G"])
+        out10 = torch.empty_like(out)
+        for _ in range(2):
+            eb.fmm_matvec(tree10, eb.KERNEL_UP, t["f"], t["g"], out=out10)
+        ts = []
+        for k in range(5):
+            flush.fill_(float(k))
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            eb.fmm_matvec(tree10, eb.KERNEL_UP, t["f"], t["g"], out=out10)
+            b.record()
+            torch.cuda.synchronize()
+            ts.append(a.elapsed_time(b))
+        p10 = {"p": 10, "ms": float(np.mean(ts)), "steps": 5, "rel_l2": None}
+        if rel is not None:
+            got10 = out10.cpu().numpy().astype(np.float64)[idx]
+            p10["rel_l2"] = float(np.linalg.norm(got10 - ref) / np.linalg.norm(ref))
+        del tree10
+
     if rank == 0:
         line = {"metric": METRIC, "value": ms, "unit": "ms", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False, "scaling": "weak",
-                "vs_baseline": None, "dtype": "f32 (fp64 plan, fp64 L2T/M2T)", "data": "synthetic",
+                "vs_baseline": None, "dtype": "f32 (3xTF32 translations; fp64 plan, fp64 equivalent densities)",
+                "data": "synthetic",
                 "config": {"workload": WORKLOAD, "n_points": n, "p": args.p, "max_pts": args.max_pts,
                            "kernel": "UP", "l2": "flushed between steps (256 MB write)",
                            "nboxes": info["nboxes"], "nlevels": info["nlevels"], "n_v": info["n_v"],
                            "parallelism": "replicas" if world > 1 else "single"},
                 "points_per_s": n / (ms * 1e-3), "rel_l2": rel, "tree_build_s": rebuild_s,
                 "first_build_s_incl_operators": build_s, "gpu_launches": int(launches),
-                "roofline": roof, "phases": ph_out, "p2p": p2p, "cpu_baseline": cpu,
+                "roofline": roof, "phases": ph_out, "p2p": p2p, "p10": p10, "cpu_baseline": cpu,
                 "e2e": {"value": float(np.mean(e2e)), "unit": "ms", "h2d_bytes_per_step": int(fh.nbytes + gh.nbytes),
                         "d2h_bytes_per_step": int(oh.nbytes)},
                 "clocks": clk.summary(), "peaks": pk}
