@@ -216,16 +216,19 @@ far_eval_kernel(int n_eval, const int* __restrict__ eval_box, const int* __restr
 // source and each lane TPT targets (t0 + l + L j), with L * TPT >= nt as tight as possible,
 // and the groups' partial sums are added by shuffles at the end.  Returns TPT (1..4; 0 when
 // nt exceeds 128, then a 32 x 4 round is used and repeated).
+#ifndef LG_TMAX
+#define LG_TMAX 4
+#endif
 __device__ __forceinline__ int lane_groups(int nt, int& L) {
-    if (nt > 128) {
+    if (nt > 32 * LG_TMAX) {
         L = 32;
-        return 4;
+        return LG_TMAX;
     }
-    int best = 1 << 30, tpt = 4;
+    int best = 1 << 30, tpt = LG_TMAX;
     L = 32;
     for (int l = 32; l >= 4; l >>= 1) {
         const int t = (nt + l - 1) / l;
-        if (t <= 4 && l * t < best) {      // strict: ties keep the larger group (fewer shuffles)
+        if (t <= LG_TMAX && l * t < best) {   // strict: ties keep the larger group (fewer shuffles)
             best = l * t;
             L = l;
             tpt = t;
@@ -349,8 +352,19 @@ far_eval_f32_kernel(int n_eval, const int* __restrict__ eval_box, const int* __r
         switch (tpt) {
             case 1: EB_FAR(1); break;
             case 2: EB_FAR(2); break;
+#if LG_TMAX >= 3
             case 3: EB_FAR(3); break;
-            default: EB_FAR(4); break;
+#endif
+#if LG_TMAX >= 4
+            case 4: EB_FAR(4); break;
+#endif
+#if LG_TMAX > 4
+            case 5: EB_FAR(5); break;
+            case 6: EB_FAR(6); break;
+            case 7: EB_FAR(7); break;
+            case 8: EB_FAR(8); break;
+#endif
+            default: EB_FAR(LG_TMAX); break;
         }
 #undef EB_FAR
         t0 += L * tpt;
@@ -423,8 +437,19 @@ near_eval_kernel(int n_eval, const int* __restrict__ eval_box, const int* __rest
         switch (tpt) {
             case 1: EB_NEAR(1); break;
             case 2: EB_NEAR(2); break;
+#if LG_TMAX >= 3
             case 3: EB_NEAR(3); break;
-            default: EB_NEAR(4); break;
+#endif
+#if LG_TMAX >= 4
+            case 4: EB_NEAR(4); break;
+#endif
+#if LG_TMAX > 4
+            case 5: EB_NEAR(5); break;
+            case 6: EB_NEAR(6); break;
+            case 7: EB_NEAR(7); break;
+            case 8: EB_NEAR(8); break;
+#endif
+            default: EB_NEAR(LG_TMAX); break;
         }
 #undef EB_NEAR
         t0 += L * tpt;
