@@ -1,0 +1,106 @@
+"""Parity at BASELINE.json's full sizes, in the launch configurations bench.py times:
+the GPU result on seeded sampled targets against the fp64 oracle computed one target at a
+time (oracle/c/direct_sum.c), the octree and its lists bit-exact against oracle.tree, and
+for the full GMRES solve the properties that hold at any size (residual, equilibrium)."""
+import numpy as np
+import pytest
+
+from oracle import cdirect
+from oracle import kernels as KN
+from oracle import tree as OT
+from workloads import geometry as geo
+from tests.gpu_util import csr_lists, need_gpu, to_dev, torch
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def eb():
+    need_gpu()
+    import paper_1612_04082_b200 as eb
+    return eb
+
+
+def _sampled_err(eb, d, tree, kern, idx, stress=False):
+    t = to_dev(d)
+    fn = eb.fmm_eval_stress if stress else eb.fmm_matvec
+    out = fn(tree, kern, t["f"], t["g"]).cpu().numpy().astype(np.float64)
+    trg = d.get("trg", d["src"])
+    ref = cdirect.direct_sum(kern, trg[idx], d["src"], d["K"], d["G"], w=d["w"], f=d["f"], g=d["g"], nrm=d["nrm"])
+    return KN.rel_l2(out[idx], ref)
+
+
+@pytest.fixture(scope="module")
+def beam200k():
+    return geo.config2(n=200_000, seed=0)
+
+
+def test_config2_tree_and_lists_bit_exact(eb, beam200k):
+    """configs[2]: 200k graded beam points, max 64 per leaf."""
+    d = beam200k
+    tree = eb.fmm_build_tree(torch.from_numpy(d["src"]).cuda(), max_pts=64, p=4)
+    ot = OT.build_tree(d["src"], d["src"], 64)
+    assert np.array_equal(eb.fmm_tree_export(tree, "keys"), ot.keys)
+    assert np.array_equal(eb.fmm_tree_export(tree, "perm"), ot.perm)
+    assert np.array_equal(eb.fmm_tree_export(tree, "level"), ot.level)
+    assert np.array_equal(eb.fmm_tree_export(tree, "anchor"), ot.anchor)
+    ol = OT.build_lists(ot)
+    for k in "UVWX":
+        assert csr_lists(eb.fmm_tree_export(tree, k + "_off"), eb.fmm_tree_export(tree, k)) == ol[k], k
+
+
+def test_config2_p6_and_p10(eb, beam200k):
+    """configs[2] at both of its orders: <= 1e-4 at p = 6, <= 1e-6 at p = 10, decreasing."""
+    d = beam200k
+    t = to_dev(d)
+    idx = np.sort(np.random.default_rng(21).choice(d["src"].shape[0], 1500, replace=False))
+    errs = {}
+    for p in (6, 10):
+        tree = eb.fmm_build_tree(t["src"], t["nrm"], t["w"], max_pts=64, p=p, K=d["K"], G=d["G"])
+        errs[p] = _sampled_err(eb, d, tree, KN.KERNEL_UP, idx)
+    print("configs[2] sampled rel-L2:", errs)
+    assert errs[6] <= 1e-4
+    assert errs[10] <= 1e-6
+    assert errs[10] < errs[6]
+
+
+def test_bench_workload_1m(eb):
+    """the bench line's workload: 1M-point beam, U + P, p = 6, leaf 64."""
+    d = geo.config2(n=1_000_000, seed=0)
+    t = to_dev(d)
+    tree = eb.fmm_build_tree(t["src"], t["nrm"], t["w"], max_pts=64, p=6, K=d["K"], G=d["G"])
+    idx = np.sort(np.random.default_rng(22).choice(d["src"].shape[0], 800, replace=False))
+    err = _sampled_err(eb, d, tree, KN.KERNEL_UP, idx)
+    print("1M beam p=6 sampled rel-L2:", err)
+    assert err <= 1e-4
+
+
+def test_config3_stress_full(eb):
+    """configs[3]: 500k surface sources -> 1M interior grid targets, D + S, p = 8, leaf 256."""
+    d = geo.config3()
+    t = to_dev(d)
+    tree = eb.fmm_build_tree(t["src"], t["nrm"], t["w"], trg=t["trg"], max_pts=256, p=8, K=d["K"], G=d["G"])
+    idx = np.sort(np.random.default_rng(23).choice(d["trg"].shape[0], 400, replace=False))
+    err = _sampled_err(eb, d, tree, KN.KERNEL_DS, idx, stress=True)
+    print("configs[3] sampled rel-L2:", err)
+    assert err <= 1e-5
+
+
+def test_config4_gmres_full(eb):
+    """configs[4]: the 1.93 M-triangle cell, mixed BVP, block-Jacobi GMRES(50) to 1e-6 at
+    p = 8, leaf 1024: converges, and the tractions balance (net force of the solved + given
+    tractions over the closed surface ~ 0 against the applied unit load)."""
+    d = geo.metamaterial_cell(nc=160, level=5, nvoids=64)
+    verts = torch.from_numpy(d["verts"]).cuda()
+    bc = torch.from_numpy(d["bc_type"]).cuda()
+    val = torch.from_numpy(d["bc_val"]).cuda()
+    op = eb.bem_create(verts, nq=16, max_pts=1024, p=8, K=d["K"], G=d["G"])
+    x = torch.zeros((d["verts"].shape[0], 3), device="cuda")
+    x, it, res = eb.bem_gmres_solve(op, bc, val, x, restart=50, max_iter=600, tol=1e-6, precond=1, check=False)
+    V = d["verts"].astype(np.float64)
+    area = 0.5 * np.linalg.norm(np.cross(V[:, 1] - V[:, 0], V[:, 2] - V[:, 0]), axis=1)
+    tr = np.where(d["bc_type"][:, None] == 0, x.cpu().numpy(), d["bc_val"])
+    force = np.linalg.norm((tr * area[:, None]).sum(0))
+    print("configs[4]: iterations", it, "residual", res, "net force", force)
+    assert res <= 1e-6
+    assert force < 2e-3
