@@ -139,75 +139,81 @@ __device__ __forceinline__ double far_rinv<double>(double r2) {
     return ri * (1.5 - 0.5 * r2 * ri * ri);
 }
 
-template <bool STRESS, class T>
-__global__ void __launch_bounds__(32 * EV_WARPS)
-far_eval_kernel(int n_eval, const int* __restrict__ eval_box, const int* __restrict__ l2t_slot,
-                const double* __restrict__ PHID, const double* __restrict__ PHIU, const int* __restrict__ phiu_slot,
-                const int* __restrict__ woff, const int* __restrict__ widx, const int* __restrict__ tbeg,
-                const int* __restrict__ tend, const int* __restrict__ anchor, const int* __restrict__ level, BoxGeo geo,
-                const double* __restrict__ se, int ne, const float* __restrict__ trg, KConst kc, double cfar,
-                const float* __restrict__ near, const int* __restrict__ trg_perm, float* __restrict__ out) {
+// fp64 far field (p >= 9 and GMRES): the unit equivalent surface is held once per CTA in
+// fp64 shared memory and scaled per box in the inner loop, so a warp stages only its box's
+// densities (3 ne doubles); lane groups as in the fp32 kernel.
+template <bool STRESS, int TPT>
+__device__ __forceinline__ void far_round_f64(int t0, int t_beg, int t_end, int L, int b, int own, int nfar,
+                                              const int* __restrict__ widx, int wbeg, const double* __restrict__ PHID,
+                                              int l2t, const double* __restrict__ PHIU,
+                                              const int* __restrict__ phiu_slot, const int* __restrict__ anchor,
+                                              const int* __restrict__ level, const BoxGeo& geo,
+                                              const double* __restrict__ sse, int ne, const float* __restrict__ trg,
+                                              const KConst& kc, double cfar, double* ph, int lane,
+                                              const float* __restrict__ near, const int* __restrict__ trg_perm,
+                                              float* __restrict__ out) {
     constexpr int NC = STRESS ? 6 : 3;
-    extern __shared__ double dsm[];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int i = blockIdx.x * EV_WARPS + warp;
-    if (i >= n_eval) return;                       // warp-uniform; no CTA barriers below
-    T* ey = reinterpret_cast<T*>(dsm) + (size_t)warp * 6 * ne;   // [3 ne] equivalent points
-    T* ephi = ey + 3 * ne;                                         // [3 ne] prepared densities
-    const int b = eval_box[i];
-    const int t_beg = tbeg[b], t_end = tend[b];
-    const int own = l2t_slot[i] >= 0 ? 1 : 0;
-    const int nfar = own + (woff[b + 1] - woff[b]);
-    const T a1 = (T)kc.a1d, aa = (T)kc.ad;
-    for (int t0 = t_beg; t0 < t_end; t0 += 32) {
-        const int t = t0 + lane;
-        const int tc = t < t_end ? t : t_beg;
-        double acc64[NC];
+    const int G = 32 / L, grp = lane / L, l = lane % L;
+    int tc[TPT];
 #pragma unroll
-        for (int c = 0; c < NC; ++c) acc64[c] = 0.0;
-        for (int e = 0; e < nfar; ++e) {
-            const bool is_own = own && e == 0;
-            const int a = is_own ? b : widx[woff[b] + e - own];
-            const double* phi = is_own ? PHID + (int64_t)l2t_slot[i] * 3 * ne
-                                       : (phiu_slot[a] >= 0 ? PHIU + (int64_t)phiu_slot[a] * 3 * ne : nullptr);
-            if (!phi) continue;
-            double cx, cy, cz, r;
-            geo.center(anchor, level, a, cx, cy, cz, r);
-            const double Rr = (is_own ? RAD_DE : RAD_UE) * r;
-            __syncwarp();
-            // coordinates relative to the box centre (keeps fp32 differences well scaled)
-            for (int k = lane; k < ne; k += 32) {
-                ey[3 * k] = (T)(Rr * se[3 * k]);
-                ey[3 * k + 1] = (T)(Rr * se[3 * k + 1]);
-                ey[3 * k + 2] = (T)(Rr * se[3 * k + 2]);
-                ephi[3 * k] = (T)(cfar * phi[3 * k]);
-                ephi[3 * k + 1] = (T)(cfar * phi[3 * k + 1]);
-                ephi[3 * k + 2] = (T)(cfar * phi[3 * k + 2]);
-            }
-            __syncwarp();
-            const T x = (T)((double)trg[3 * tc] - cx), y = (T)((double)trg[3 * tc + 1] - cy),
-                    z = (T)((double)trg[3 * tc + 2] - cz);
-            T acc[NC];
+    for (int j = 0; j < TPT; ++j) {
+        const int t = t0 + l + L * j;
+        tc[j] = t < t_end ? t : t_beg;
+    }
+    double acc[TPT][NC];
 #pragma unroll
-            for (int c = 0; c < NC; ++c) acc[c] = (T)0;
-#pragma unroll 2
-            for (int k = 0; k < ne; ++k) {
-                const T dx = x - ey[3 * k], dy = y - ey[3 * k + 1], dz = z - ey[3 * k + 2];
-                const T ri = far_rinv<T>(dx * dx + dy * dy + dz * dz);
-                if (!STRESS)
-                    acc_U<T>(dx, dy, dz, ri, ephi[3 * k], ephi[3 * k + 1], ephi[3 * k + 2], a1, acc);
-                else
-                    acc_D<T>(dx, dy, dz, ri, ephi[3 * k], ephi[3 * k + 1], ephi[3 * k + 2], aa, acc);
-            }
+    for (int j = 0; j < TPT; ++j)
 #pragma unroll
-            for (int c = 0; c < NC; ++c) acc64[c] += (double)acc[c];
+        for (int c = 0; c < NC; ++c) acc[j][c] = 0.0;
+    const double a1 = kc.a1d, aa = kc.ad;
+    for (int e = 0; e < nfar; ++e) {
+        const bool is_own = own && e == 0;
+        const int a = is_own ? b : widx[wbeg + e - own];
+        const double* phi = is_own ? PHID + (int64_t)l2t * 3 * ne
+                                   : (phiu_slot[a] >= 0 ? PHIU + (int64_t)phiu_slot[a] * 3 * ne : nullptr);
+        if (!phi) continue;
+        double cx, cy, cz, r;
+        geo.center(anchor, level, a, cx, cy, cz, r);
+        const double R = (is_own ? RAD_DE : RAD_UE) * r;
+        __syncwarp();
+        for (int k = lane; k < 3 * ne; k += 32) ph[k] = cfar * phi[k];
+        __syncwarp();
+        double x[TPT], y[TPT], z[TPT];
+#pragma unroll
+        for (int j = 0; j < TPT; ++j) {
+            x[j] = (double)trg[3 * tc[j]] - cx;
+            y[j] = (double)trg[3 * tc[j] + 1] - cy;
+            z[j] = (double)trg[3 * tc[j] + 2] - cz;
         }
-        if (t < t_end) {
-            float* o = out + (int64_t)trg_perm[t] * NC;
+        for (int k = grp; k < ne; k += G) {
+            const double qx = R * sse[3 * k], qy = R * sse[3 * k + 1], qz = R * sse[3 * k + 2];
+            const double fx = ph[3 * k], fy = ph[3 * k + 1], fz = ph[3 * k + 2];
 #pragma unroll
-            for (int c = 0; c < NC; ++c) o[c] = (float)(acc64[c] + (double)near[(int64_t)t * NC + c]);
+            for (int j = 0; j < TPT; ++j) {
+                const double dx = x[j] - qx, dy = y[j] - qy, dz = z[j] - qz;
+                const double ri = far_rinv<double>(dx * dx + dy * dy + dz * dz);
+                if (!STRESS)
+                    acc_U<double>(dx, dy, dz, ri, fx, fy, fz, a1, acc[j]);
+                else
+                    acc_D<double>(dx, dy, dz, ri, fx, fy, fz, aa, acc[j]);
+            }
         }
     }
+#pragma unroll
+    for (int j = 0; j < TPT; ++j)
+#pragma unroll
+        for (int c = 0; c < NC; ++c)
+            for (int off = L; off < 32; off <<= 1) acc[j][c] += __shfl_xor_sync(0xffffffffu, acc[j][c], off);
+    if (grp == 0)
+#pragma unroll
+        for (int j = 0; j < TPT; ++j) {
+            const int t = t0 + l + L * j;
+            if (t < t_end) {
+                float* o = out + (int64_t)trg_perm[t] * NC;
+#pragma unroll
+                for (int c = 0; c < NC; ++c) o[c] = (float)(acc[j][c] + (double)near[(int64_t)t * NC + c]);
+            }
+        }
 }
 
 // Lane groups for the warp-per-leaf kernels.  A leaf holds nt targets (~31 on average on
@@ -229,6 +235,25 @@ __device__ __forceinline__ int lane_groups(int nt, int& L) {
     for (int l = 32; l >= 4; l >>= 1) {
         const int t = (nt + l - 1) / l;
         if (t <= LG_TMAX && l * t < best) {   // strict: ties keep the larger group (fewer shuffles)
+            best = l * t;
+            L = l;
+            tpt = t;
+        }
+    }
+    return tpt;
+}
+
+template <int TM>
+__device__ __forceinline__ int lane_groups_max(int nt, int& L) {
+    if (nt > 32 * TM) {
+        L = 32;
+        return TM;
+    }
+    int best = 1 << 30, tpt = TM;
+    L = 32;
+    for (int l = 32; l >= 4; l >>= 1) {
+        const int t = (nt + l - 1) / l;
+        if (t <= TM && l * t < best) {
             best = l * t;
             L = l;
             tpt = t;
@@ -321,6 +346,41 @@ __device__ __forceinline__ void far_round_f32(int t0, int t_beg, int t_end, int 
                 for (int c = 0; c < NC; ++c) o[c] = acc[j][c] + near[(int64_t)t * NC + c];
             }
         }
+}
+
+template <bool STRESS>
+__global__ void __launch_bounds__(32 * EV_WARPS)
+far_eval_f64_kernel(int n_eval, const int* __restrict__ eval_box, const int* __restrict__ l2t_slot,
+                    const double* __restrict__ PHID, const double* __restrict__ PHIU,
+                    const int* __restrict__ phiu_slot, const int* __restrict__ woff, const int* __restrict__ widx,
+                    const int* __restrict__ tbeg, const int* __restrict__ tend, const int* __restrict__ anchor,
+                    const int* __restrict__ level, BoxGeo geo, const double* __restrict__ se, int ne,
+                    const float* __restrict__ trg, KConst kc, double cfar, const float* __restrict__ near,
+                    const int* __restrict__ trg_perm, float* __restrict__ out) {
+    extern __shared__ double dsm[];
+    double* sse = dsm;                                      // [3 ne] unit surface (CTA)
+    for (int k = threadIdx.x; k < 3 * ne; k += blockDim.x) sse[k] = se[k];
+    __syncthreads();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int i = blockIdx.x * EV_WARPS + warp;
+    if (i >= n_eval) return;                                 // warp-uniform; no CTA barriers below
+    double* ph = dsm + 3 * ne + (size_t)warp * 3 * ne;
+    const int b = eval_box[i];
+    const int t_beg = tbeg[b], t_end = tend[b];
+    const int l2t = l2t_slot[i];
+    const int own = l2t >= 0 ? 1 : 0;
+    const int nfar = own + (woff[b + 1] - woff[b]);
+    for (int t0 = t_beg; t0 < t_end;) {
+        int L;
+        const int tpt = lane_groups_max<2>(t_end - t0, L);   // fp64: at most 2 targets per lane
+#define EB_FAR64(T)                                                                                                  \
+    far_round_f64<STRESS, T>(t0, t_beg, t_end, L, b, own, nfar, widx, woff[b], PHID, l2t, PHIU, phiu_slot, anchor, \
+                             level, geo, sse, ne, trg, kc, cfar, ph, lane, near, trg_perm, out)
+        if (tpt == 1) EB_FAR64(1);
+        else EB_FAR64(2);
+#undef EB_FAR64
+        t0 += L * tpt;
+    }
 }
 
 template <bool STRESS>
@@ -846,8 +906,8 @@ static void launch_far(const Tree& t, float* out, cudaStream_t s) {
     const double cfar = STRESS ? t.mat.cD : t.mat.cU;
     const int grid = ceil_div(t.n_eval, EV_WARPS);
     if (t.far64) {
-        const size_t sm = sizeof(double) * 6 * P.ne * EV_WARPS;
-        auto ffn = far_eval_kernel<STRESS, double>;
+        const size_t sm = sizeof(double) * 3 * P.ne * (EV_WARPS + 1);
+        auto ffn = far_eval_f64_kernel<STRESS>;
         if (sm > 48 * 1024) EB_CUDA(cudaFuncSetAttribute(ffn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
         ffn<<<grid, 32 * EV_WARPS, sm, s>>>(t.n_eval, t.eval_box.p, t.eval_l2t_slot.p, t.PHID.p, t.PHIU.p,
                                             t.phiu_slot.p, t.m2t_off.p, t.m2t_idx.p, t.tbeg.p, t.tend.p,
