@@ -872,7 +872,7 @@ void tree_precise(Tree& t, cudaStream_t s) {
         t.PHID.alloc((size_t)std::max(1, t.n_phid) * P.me);
         t.PHIU.alloc((size_t)std::max(1, t.n_phiu) * P.me);
     }
-    if (t.tc_fast) {
+    if (t.tc_fast && !std::getenv("EBEM_BEM_FAST_M2L")) {
         t.tc_fast = false;
         tc_build_tiles(t.m2l, P.me, P.me, m2l_drain_fast());
     }
