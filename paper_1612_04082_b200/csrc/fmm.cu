@@ -1,3 +1,5 @@
+#include <chrono>
+#include <cstdio>
 // KIFMM evaluation (Sec. 2.2) on the tree built by tree.cu:
 //   upward   : S2M (sources -> upward check potential, fp32 pair loop) -> z = Q_u1^T q
 //              M2M (z_P += M2M_c z_C, level by level, fine to coarse)
@@ -526,6 +528,16 @@ static bool m2l_drain_fast() {
 // ------------------------------------------------------------------ schedule (host)
 void schedule_tree(Tree& t, cudaStream_t s) {
     const Plan& P = *t.plan;
+    static const bool timing = std::getenv("EBEM_BUILD_TIMING") != nullptr;
+    auto tick = std::chrono::steady_clock::now();
+    auto lap = [&](const char* what) {
+        if (!timing) return;
+        EB_CUDA(cudaStreamSynchronize(s));
+        const auto now = std::chrono::steady_clock::now();
+        fprintf(stderr, "[ebem schedule] %-18s %.2f ms\n", what,
+                std::chrono::duration<double, std::milli>(now - tick).count());
+        tick = now;
+    };
     const int nb = t.nboxes;
     auto dl = [&](const DBuf<int>& d, size_t n) {
         std::vector<int> h(n);
@@ -565,6 +577,7 @@ void schedule_tree(Tree& t, cudaStream_t s) {
     h2d(t.up_slot.p, up.data(), nb, s);
     h2d(t.dn_slot.p, dn.data(), nb, s);
 
+    lap("download+slots");
     // S2M on leaves carrying z; check potential rows are s2m indices
     std::vector<int> s2m;
     std::vector<int> op1;
@@ -646,6 +659,7 @@ void schedule_tree(Tree& t, cudaStream_t s) {
     op1.assign(pr.size(), 0);
     build_op_pairs(t.q2z_dn, 1, op1, pr, s);
 
+    lap("s2m/m2m/s2l");
     // M2L, all levels, grouped by translation vector
     {
         std::vector<int> op;
@@ -666,6 +680,7 @@ void schedule_tree(Tree& t, cudaStream_t s) {
         build_op_pairs(t.m2l, NV_OFFSETS, op, p2, s);
     }
 
+    lap("m2l pairs");
     // L2L per child level
     t.l2l.clear();
     t.l2l.resize(t.nlevels);
@@ -683,6 +698,7 @@ void schedule_tree(Tree& t, cudaStream_t s) {
         build_op_pairs(t.l2l[l], 8, op, p2, s);
     }
 
+    lap("l2l");
     // leaf evaluation: near list (U + direct X + direct W) and M2T list (the other W entries)
     std::vector<int> ev, l2t, phid_box, phiu_box, phiu(nb, -1);
     std::vector<int> noff(nb + 1, 0), nidx, moff(nb + 1, 0), midx;
@@ -778,6 +794,7 @@ void schedule_tree(Tree& t, cudaStream_t s) {
     op1.assign(pru.size(), 0);
     build_op_pairs(t.phiu_pairs, 1, op1, pru, s);
 
+    lap("leaf lists/phi");
     // workspace
     const int me = P.me, mc = P.mc;
     t.rec_disp.alloc(std::max<int64_t>(t.nsrc * REC_DISP, 1));
@@ -820,6 +837,7 @@ void schedule_tree(Tree& t, cudaStream_t s) {
         t.PHIDF.zero(s);
         t.PHIUF.zero(s);
     }
+    lap("workspace+tiles");
     t.near_sorted.alloc((size_t)std::max<int64_t>(1, t.ntrg) * 6);
     EB_CUDA(cudaStreamSynchronize(s));
 

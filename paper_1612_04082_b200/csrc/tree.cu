@@ -1,3 +1,6 @@
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 // Adaptive octree and KIFMM interaction lists on the device (Sec. 2.2,
 // "Generation of an octree partitioning of the domain into boxes"; reading R5 in DESIGN.md):
 //   bounding cube (min/max reduction) -> 60-bit Morton keys (fp64 quantisation, one IEEE
@@ -369,6 +372,7 @@ void schedule_tree(Tree& t, cudaStream_t s);   // fmm.cu
 
 Tree* build_tree(const float* src, const float* nrm, const float* w, int64_t nsrc, const float* trg,
                  int64_t ntrg, int max_pts, int p, const Material& m, cudaStream_t s) {
+    const auto t0_build = std::chrono::steady_clock::now();
     auto T = std::make_unique<Tree>();
     Tree& t = *T;
     t.nsrc = nsrc;
@@ -601,8 +605,16 @@ Tree* build_tree(const float* src, const float* nrm, const float* w, int64_t nsr
     EB_CUDA(cudaStreamSynchronize(s));
 
     // ---- operators and execution schedule
+    const auto tb = std::chrono::steady_clock::now();
     t.plan = get_plan(p, m, s);
+    const auto tp = std::chrono::steady_clock::now();
     schedule_tree(t, s);
+    if (std::getenv("EBEM_BUILD_TIMING")) {
+        const auto te = std::chrono::steady_clock::now();
+        auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+        fprintf(stderr, "[ebem build] tree+lists %.2f ms, plan %.2f ms, schedule %.2f ms\n", ms(t0_build, tb),
+                ms(tb, tp), ms(tp, te));
+    }
     return T.release();
 }
 
