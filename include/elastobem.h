@@ -138,7 +138,8 @@ int fmm_tree_free(ebem_tree *tree);
  * elastic.cuh, or 2 M K per GEMM column; bytes: operands read once + results
  * written once), its arithmetic precision and the device time of the last profiled
  * evaluation (ms, -1 if none; synchronises on that evaluation's last event).
- * Phases: prep, S2M, Q2Z_up, M2M, S2L, Q2Z_dn, M2L, L2L, PHI, EVAL.
+ * Phases: prep, S2M, Q2Z_up, M2M, S2L, Q2Z_dn, M2L, L2L, PHI, NEAR, FAR (near field:
+ * U list and the directly summed X/W/V entries; far field: L2T + M2T and the scatter).
  */
 typedef struct ebem_phase_stat {
     char name[16];

@@ -1105,6 +1105,7 @@ void fmm_evaluate(Tree& t, int kernel, const float* f, const float* g, float* ou
     mark(phase++);
     if (conc) EB_CUDA(cudaStreamWaitEvent(sa, t.ev_near, 0));
     else near(sa);
+    mark(phase++);
     if (stress) launch_far<true>(t, out, sa);
     else launch_far<false>(t, out, sa);
     if (conc) {
@@ -1130,7 +1131,8 @@ static double flops_per_pair(int kernel) {
 }
 
 int phase_stats(Tree& t, int kernel, ebem_phase_stat* out, int cap) {
-    static const char* names[Tree::NPHASE] = {"prep", "S2M", "Q2Z_up", "M2M", "S2L", "Q2Z_dn", "M2L", "L2L", "PHI", "EVAL"};
+    static const char* names[Tree::NPHASE] = {"prep", "S2M",    "Q2Z_up", "M2M",  "S2L", "Q2Z_dn",
+                                              "M2L",  "L2L",    "PHI",    "NEAR", "FAR"};
     const Plan& P = *t.plan;
     const double me = P.me, mc = P.mc, ne = P.ne;
     const bool stress = kernel_stress(kernel);
@@ -1164,12 +1166,14 @@ int phase_stats(Tree& t, int kernel, ebem_phase_stat* out, int cap) {
     st[8].fp64 = 1;
     st[8].flops = st[8].flops_fp64 = me * (me + 1) * (double)(t.n_phid + t.n_phiu);   // triangular R^-1
     st[8].bytes = 2 * 8.0 * me * me + (4.0 + 8.0) * me * (t.n_phid + t.n_phiu);
-    st[9].interactions = t.w_p2p_inter + t.w_l2t_inter + t.w_m2t_inter;
-    st[9].fp64 = 1;
-    st[9].flops_fp64 = (t.w_l2t_inter + t.w_m2t_inter) * flops_per_pair(stress ? K_D : K_U);
-    st[9].flops = t.w_p2p_inter * flops_per_pair(kernel) + st[9].flops_fp64;
-    st[9].bytes = t.w_p2p_src * (stress ? rec_sb : rec_b) + t.ntrg * (12.0 + 4.0 * (stress ? 6 : 3)) +
-                  8.0 * me * (t.n_phid + t.n_phiu);
+    st[9].interactions = t.w_p2p_inter;
+    st[9].flops = t.w_p2p_inter * flops_per_pair(kernel);
+    st[9].bytes = t.w_p2p_src * (stress ? rec_sb : rec_b) + t.ntrg * (12.0 + 4.0 * (stress ? 6 : 3));
+    st[10].interactions = t.w_l2t_inter + t.w_m2t_inter;
+    st[10].fp64 = t.far64 ? 1 : 0;
+    st[10].flops = (t.w_l2t_inter + t.w_m2t_inter) * flops_per_pair(stress ? K_D : K_U);
+    st[10].flops_fp64 = t.far64 ? st[10].flops : 0;
+    st[10].bytes = t.ntrg * (12.0 + 4.0 * (stress ? 6 : 3) * 2) + (t.far64 ? 8.0 : 16.0 / 3.0) * me * (t.n_phid + t.n_phiu);
     if (t.ev_valid) {
         EB_CUDA(cudaEventSynchronize(t.ev[Tree::NPHASE]));
         for (int i = 0; i < Tree::NPHASE; ++i) {

@@ -121,7 +121,7 @@ struct Tree {
     bool tc_fast = false;                // p <= 8 plain matvec: two-slice full-K tensor-core kernel
 
     // profiling (fmm_set_profiling / fmm_phase_stats)
-    static constexpr int NPHASE = 10;
+    static constexpr int NPHASE = 11;
     bool profile = false;
     cudaEvent_t ev[NPHASE + 1] = {};
     bool ev_valid = false;

@@ -88,7 +88,7 @@ Other workloads:
 {ph}
 
 The timed steps run the near field on a second stream beside M2L, so the phase sum exceeds
-the {b['value']:.2f} ms step.  "EVAL" = near field + far field.
+the {b["value"]:.2f} ms step.
 
 ## Kernel shares of one matvec (ncu launch list; serialised, cold)
 {shares}
