@@ -491,7 +491,7 @@ def main():
                            "kernel": "UP", "l2": "flushed between steps (256 MB write)",
                            "nboxes": info["nboxes"], "nlevels": info["nlevels"], "n_v": info["n_v"],
                            "parallelism": "replicas" if world > 1 else "single"},
-                "points_per_s": world * n / (ms * 1e-3),   # whole job (replicas) "rel_l2": rel, "tree_build_s": rebuild_s,
+                "points_per_s": world * n / (ms * 1e-3), "rel_l2": rel, "tree_build_s": rebuild_s,
                 "first_build_s_incl_operators": build_s, "gpu_launches": int(launches),
                 "roofline": roof, "phases": ph_out, "p2p": p2p, "p10": p10, "cpu_baseline": cpu,
                 "e2e": {"value": float(np.mean(e2e)), "unit": "ms", "h2d_bytes_per_step": int(fh.nbytes + gh.nbytes),
