@@ -119,6 +119,7 @@ struct Tree {
     bool use_tc = true;                  // tcgen05 3xTF32 translations (else SIMT fp32)
     bool far64 = false;                  // L2T / M2T in fp64 (set for p >= 9 and by the BEM operator)
     bool tc_fast = false;                // p <= 8 plain matvec: two-slice full-K tensor-core kernel
+    bool ml_fast = false;                // Q2Z / M2M / L2L on the fast kernel too
 
     // profiling (fmm_set_profiling / fmm_phase_stats)
     static constexpr int NPHASE = 11;

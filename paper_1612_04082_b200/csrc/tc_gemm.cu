@@ -647,7 +647,7 @@ void tc_build_tiles(OpPairs& P, int M, int K, bool fast) {
         for (int p0 = P.op_ptr_h[o]; p0 < P.op_ptr_h[o + 1]; p0 += tc::BN)
             for (int m0 = 0; m0 < M; m0 += mstep)
                 t.push_back({o, p0, std::min(tc::BN, P.op_ptr_h[o + 1] - p0), m0, 0, nk});
-    const int nsplit = fast || t.empty() ? 1 : std::max(1, std::min(nk / 3, num_sms() / (int)t.size()));
+    const int nsplit = t.empty() ? 1 : std::max(1, std::min(nk / 3, num_sms() / (int)t.size()));
     if (nsplit > 1) {
         std::vector<tc::Tile> u;
         for (const tc::Tile& x : t)
