@@ -1,13 +1,15 @@
-#include <chrono>
-#include <cstdio>
 // KIFMM evaluation (Sec. 2.2) on the tree built by tree.cu:
-//   upward   : S2M (sources -> upward check potential, fp32 pair loop) -> z = Q_u1^T q
-//              M2M (z_P += M2M_c z_C, level by level, fine to coarse)
-//   downward : S2L (X-list sources -> downward check potential) -> w += Q_d1^T q
-//              M2L (w_B += M2L_o z_A, all levels in one launch, grouped by translation o)
+//   upward   : S2M (sources -> upward check potential, fp32 pair loop, TF32 split fused)
+//              -> z = Q_u1^T q;  M2M (z_P += M2M_c z_C, level by level, fine to coarse)
+//   downward : M2L (w_B += M2L_o z_A, all levels in one launch, grouped by translation o),
+//              S2L for the X entries not summed directly -> w += Q_d1^T q,
 //              L2L (w_C += L2L_c w_P, coarse to fine)
-//   leaves   : phi_d = r R_d^-1 w, phi_u = r R_u^-1 z in fp64; one kernel per target leaf
-//              does L2T + M2T in fp64 and the U-list near field (P2P) in fp32.
+//   leaves   : phi = r R^-1 z / w (fp64, DMMA); near field = U list + the X / W / V entries
+//              that are cheaper summed directly (reading R11), on a second stream beside
+//              M2L; far field = L2T + M2T from phi, plus the near buffer, scattered to the
+//              caller's target order.
+// Translations run on tcgen05 3xTF32 (tc_gemm.cu); precision choices in DESIGN.md Sec. 5.
+#include <chrono>
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
