@@ -229,6 +229,9 @@ __device__ __forceinline__ void far_round_f64(int t0, int t_beg, int t_end, int 
 #ifndef LG_TMAX
 #define LG_TMAX 4
 #endif
+#ifndef NEAR_TMAX_STRESS
+#define NEAR_TMAX_STRESS 3
+#endif
 __device__ __forceinline__ int lane_groups(int nt, int& L) {
     if (nt > 32 * LG_TMAX) {
         L = 32;
@@ -495,9 +498,21 @@ near_eval_kernel(int n_eval, const int* __restrict__ eval_box, const int* __rest
     const int t_beg = tbeg[b], t_end = tend[b];
     for (int t0 = t_beg; t0 < t_end;) {
         int L;
-        const int tpt = lane_groups(t_end - t0, L);
 #define EB_NEAR(T)                                                                                                   \
     near_round<SL, DL, STRESS, T>(t0, t_beg, t_end, L, b, uoff, uidx, sbeg, send, trg, rec, kc, near, srec, lane)
+        if constexpr (STRESS) {     // 6-component sums: fewer targets per lane keep registers down
+            const int tpt = lane_groups_max<NEAR_TMAX_STRESS>(t_end - t0, L);
+            if (tpt == 1) EB_NEAR(1);
+#if NEAR_TMAX_STRESS >= 3
+            else if (tpt == 3) EB_NEAR(3);
+#endif
+#if NEAR_TMAX_STRESS >= 4
+            else if (tpt == 4) EB_NEAR(4);
+#endif
+            else EB_NEAR(2);
+            t0 += L * tpt;
+        } else {
+        const int tpt = lane_groups(t_end - t0, L);
         switch (tpt) {
             case 1: EB_NEAR(1); break;
             case 2: EB_NEAR(2); break;
@@ -517,6 +532,7 @@ near_eval_kernel(int n_eval, const int* __restrict__ eval_box, const int* __rest
         }
 #undef EB_NEAR
         t0 += L * tpt;
+        }
     }
 }
 
