@@ -229,6 +229,9 @@ __device__ __forceinline__ void far_round_f64(int t0, int t_beg, int t_end, int 
 #ifndef LG_TMAX
 #define LG_TMAX 4
 #endif
+#ifndef NEAR_TILE
+#define NEAR_TILE 32          // sources staged per warp
+#endif
 #ifndef NEAR_TMAX_STRESS
 #define NEAR_TMAX_STRESS 3
 #endif
@@ -463,8 +466,8 @@ __device__ __forceinline__ void near_round(int t0, int t_beg, int t_end, int L, 
     }
     for (int e = uoff[b]; e < uoff[b + 1]; ++e) {
         const int a = uidx[e];
-        for (int s0 = sbeg[a]; s0 < send[a]; s0 += 32) {
-            const int cnt = min(32, send[a] - s0);
+        for (int s0 = sbeg[a]; s0 < send[a]; s0 += NEAR_TILE) {
+            const int cnt = min(NEAR_TILE, send[a] - s0);
             __syncwarp();
             for (int q = lane; q < cnt * R; q += 32) srec[(q / R) * RS + q % R] = rec[(int64_t)s0 * R + q];
             __syncwarp();
@@ -489,7 +492,7 @@ near_eval_kernel(int n_eval, const int* __restrict__ eval_box, const int* __rest
                  const int* __restrict__ tbeg, const int* __restrict__ tend, const float* __restrict__ trg,
                  const float4* __restrict__ rec, KConst kc, float* __restrict__ near) {
     constexpr int R = STRESS ? REC_STRESS : REC_DISP;
-    __shared__ float4 srec_all[EV_WARPS][32 * (R + 1)];
+    __shared__ float4 srec_all[EV_WARPS][NEAR_TILE * (R + 1)];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int i = blockIdx.x * EV_WARPS + warp;
     if (i >= n_eval) return;
