@@ -11,6 +11,8 @@ d = sys.argv[1] if len(sys.argv) > 1 else "profiles/r01"
 run = lambda *a: subprocess.run([sys.executable, *a], capture_output=True, text=True).stdout
 b = json.load(open(os.path.join(d, "bench_latest.json")))
 hot = run("tools/ncu_summary.py", os.path.join(d, "hot_raw.csv"))
+if os.path.exists(os.path.join(d, "hot2_raw.csv")):
+    hot += "\n" + run("tools/ncu_summary.py", os.path.join(d, "hot2_raw.csv"))
 shares = run("tools/launch_shares.py", os.path.join(d, "launches_bench.csv"))
 tr = json.load(open(os.path.join(d, "traffic.json")))["M2L"]
 ph = "\n".join(f"| {p['name']} | {p['ms']:.3f} | {p['launches']} | {p['bound']} | {p['frac']:.2f} |"
@@ -72,7 +74,8 @@ Regenerate this file with `python tools/make_summary.py {d}`.
 * `launches_bench.csv` — `ncu --metrics gpu__time_duration.sum --clock-control none --csv
   python bench.py --steps 2 --warmup 3 --no-cpu`.
 * `hot_raw.csv`, `hot_details.csv` — `ncu --set full --import-source on -k regex:<hot kernels>
-  python tools/prof_fmm.py --direct --reps 1`.
+  -c 12 python tools/prof_fmm.py --direct --reps 1` (S2M, Q2Z/M2M levels, near field, M2L);
+  `hot2_*` — the same for the PHI (DMMA), far-field and direct kernels.
 * `precise_raw.csv`, `precise_details.csv` — the first `tc_pairs_kernel` launches (Q2Z / M2M).
 * `tree_build_launches.csv` — launch list (time, DRAM bytes) of three 1M-point tree builds
   (the first one includes the one-time operator precompute).

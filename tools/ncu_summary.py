@@ -50,7 +50,8 @@ def main():
             else:
                 cells.append(f"{float(d[k]):.1f}")
         print(f"| `{name}` | " + " | ".join(cells) + " |")
-        if "tc_pairs_fast_kernel" in name and m2l is None:
+        dur = to_base(d["gpu__time_duration.sum"], u["gpu__time_duration.sum"])
+        if "tc_pairs_fast_kernel" in name and (m2l is None or dur * 1e3 > m2l["ms_under_ncu"]):   # M2L: the longest
             m2l = {"kernel": "tc_pairs_fast_kernel",
                    "dram_read": to_base(d["dram__bytes_read.sum"], u["dram__bytes_read.sum"]),
                    "dram_write": to_base(d["dram__bytes_write.sum"], u["dram__bytes_write.sum"]),
