@@ -188,9 +188,30 @@ def p2p_bench(eb, torch, pk, reps=20):
     inter = float(n) * (n - 1)
     flops = inter * 45.0          # P kernel: FFMA=2, FMUL/FADD=1 in the compiled pair loop (tools/count_flops.sh)
     tf = flops / (ms * 1e-3) / 1e12
-    return {"config": "configs[1] cube 24576 triangles, kernel P, all pairs", "ms": ms,
-            "ginteractions_per_s": inter / (ms * 1e-3) / 1e9, "tflops": tf,
-            "frac_fp32_peak": tf / pk["fp32_tflops"], "flops_per_interaction": 45}
+    res = {"config": "configs[1] cube 24576 triangles, kernel P, all pairs", "ms": ms,
+           "ginteractions_per_s": inter / (ms * 1e-3) / 1e9, "tflops": tf,
+           "frac_fp32_peak": tf / pk["fp32_tflops"], "flops_per_interaction": 45}
+    # the same kernel on configs[2]'s 200k beam points (all 4e10 pairs): the sustained rate
+    # without configs[1]'s small-problem tail and block reduction
+    d2 = geo.config2(n=200_000, seed=0)
+    t2 = {k: torch.from_numpy(v).cuda() for k, v in d2.items() if isinstance(v, np.ndarray)}
+    n2 = d2["src"].shape[0]
+    out2 = torch.empty((n2, 3), device="cuda")
+    eb.bem_kernel_direct(eb.KERNEL_P, t2["src"], t2["src"], nrm=t2["nrm"], w=t2["w"], g=t2["g"], K=d2["K"],
+                         G=d2["G"], out=out2)
+    torch.cuda.synchronize()
+    s.record()
+    for _ in range(3):
+        eb.bem_kernel_direct(eb.KERNEL_P, t2["src"], t2["src"], nrm=t2["nrm"], w=t2["w"], g=t2["g"], K=d2["K"],
+                             G=d2["G"], out=out2)
+    e.record()
+    torch.cuda.synchronize()
+    ms2 = s.elapsed_time(e) / 3
+    tf2 = float(n2) * (n2 - 1) * 45.0 / (ms2 * 1e-3) / 1e12
+    res["large"] = {"config": f"configs[2] beam {n2} points, kernel P, all pairs", "ms": ms2,
+                    "ginteractions_per_s": float(n2) * (n2 - 1) / (ms2 * 1e-3) / 1e9, "tflops": tf2,
+                    "frac_fp32_peak": tf2 / pk["fp32_tflops"]}
+    return res
 
 
 def gmres_workload(args, eb, torch):
