@@ -915,10 +915,18 @@ void tree_precise(Tree& t, cudaStream_t s) {
         t.PHID.alloc((size_t)std::max(1, t.n_phid) * P.me);
         t.PHIU.alloc((size_t)std::max(1, t.n_phiu) * P.me);
     }
-    if (t.tc_fast && !std::getenv("EBEM_BEM_FAST_M2L")) {
-        t.tc_fast = false;
-        tc_build_tiles(t.m2l, P.me, P.me, m2l_drain_fast());
-    }
+    tree_m2l_fast(t, false, s);
+    EB_CUDA(cudaStreamSynchronize(s));
+}
+
+// M2L accumulation of a built tree: full-chain (fast) or drained groups (precise).  The fast
+// chain is allowed only where it is below the truncation error (p <= 8).
+void tree_m2l_fast(Tree& t, bool fast, cudaStream_t s) {
+    const Plan& P = *t.plan;
+    fast = fast && t.use_tc && P.p < FAR_FP64_MIN_P;
+    if (fast == t.tc_fast) return;
+    t.tc_fast = fast;
+    tc_build_tiles(t.m2l, P.me, P.me, fast || m2l_drain_fast());
     EB_CUDA(cudaStreamSynchronize(s));
 }
 

@@ -194,6 +194,7 @@ template <class XT>
 void tc_split_rows(const XT* X, int ld, int64_t row0, int64_t nrows, int K, float* Xb, float* Xs,
                    cudaStream_t s);
 void tree_precise(Tree& t, cudaStream_t s);
+void tree_m2l_fast(Tree& t, bool fast, cudaStream_t s);
 void tc_build_tiles(OpPairs& P, int M, int K, bool fast);
 void tc_pairs_gemm_fast(const OpPairs& P, const CUtensorMap& Ab, const CUtensorMap& As, const float* Bb,
                         const float* Bs, int ldb, int M, int K, double* Y, int ldy, bool drain, cudaStream_t s);
