@@ -91,7 +91,7 @@ check_potential_kernel(const int* __restrict__ tbox, const int* __restrict__ sof
                 srec[q] = v;
             }
             __syncthreads();
-            pair_loop_multi<SL, DL, false, KPT>(srec, cnt, x, y, z, kc, acc);
+            pair_loop_multi<SL, DL, false, KPT, false>(srec, cnt, x, y, z, kc, acc);   // check points never coincide
         }
     }
 #pragma unroll
@@ -471,7 +471,8 @@ __device__ __forceinline__ void near_round(int t0, int t_beg, int t_end, int L, 
             __syncwarp();
             for (int q = lane; q < cnt * R; q += 32) srec[(q / R) * RS + q % R] = rec[(int64_t)s0 * R + q];
             __syncwarp();
-            pair_loop_strided<SL, DL, STRESS, TPT, RS>(srec, cnt, grp, G, x, y, z, kc, acc);
+            if (a == b) pair_loop_strided<SL, DL, STRESS, TPT, RS, true>(srec, cnt, grp, G, x, y, z, kc, acc);
+            else pair_loop_strided<SL, DL, STRESS, TPT, RS, false>(srec, cnt, grp, G, x, y, z, kc, acc);
         }
     }
     reduce_groups<NC, TPT>(acc, L);
@@ -1137,7 +1138,6 @@ void fmm_evaluate(Tree& t, int kernel, const float* f, const float* g, float* ou
     // stream B starts when the upward pass is done, i.e. alongside M2L
     auto fork_b = [&]() {
         if (!conc) return;
-        EB_CUDA(cudaEventRecord(t.ev_fork, sa));
         EB_CUDA(cudaStreamWaitEvent(sb, t.ev_fork, 0));
         s2l(sb);
         EB_CUDA(cudaEventRecord(t.ev_s2l, sb));
@@ -1178,6 +1178,7 @@ void fmm_evaluate(Tree& t, int kernel, const float* f, const float* g, float* ou
 
     // downward pass (stream B forks here: started together with the upward pass it only
     // competed with the other FP32-bound kernels, measured no faster)
+    if (conc) EB_CUDA(cudaEventRecord(t.ev_fork, sa));
     fork_b();
     if (!conc) s2l(sa);
     mark(phase++);

@@ -99,7 +99,10 @@ constexpr int PL_UNROLL = EBEM_PL_UNROLL;
 
 // the same, for TPT targets per thread: the source loop is outermost so that each record is
 // read from shared memory once for all TPT targets (one LDS.128 per pair at TPT = 4)
-template <bool SL, bool DL, bool STRESS, int TPT>
+// SAFE = false where no staged source can coincide with a target (check surfaces, boxes
+// other than the target's own leaf: coincident points share a Morton key and hence a leaf),
+// dropping the r = 0 select from the pair (2 of ~43 instructions for U+P).
+template <bool SL, bool DL, bool STRESS, int TPT, bool SAFE = true>
 __device__ __forceinline__ void pair_loop_multi(const float4* __restrict__ srec, int cnt, const float* x,
                                                 const float* y, const float* z, const KConst& kc, float (*acc)[STRESS ? 6 : 3]) {
     constexpr int R = STRESS ? REC_STRESS : REC_DISP;
@@ -119,7 +122,7 @@ __device__ __forceinline__ void pair_loop_multi(const float4* __restrict__ srec,
         for (int k = 0; k < TPT; ++k) {
             float dx = x[k] - p.x, dy = y[k] - p.y, dz = z[k] - p.z;
             float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
-            float ri = safe_rinv(r2);
+            float ri = SAFE ? safe_rinv(r2) : rsqrtf(r2);
             if (!STRESS) {
                 if (SL && DL) acc_UP(dx, dy, dz, ri, f.x, f.y, f.z, g.x, g.y, g.z, n.x, n.y, n.z, p.w, kc.a1, kc.a3, acc[k]);
                 else if (SL) acc_U(dx, dy, dz, ri, f.x, f.y, f.z, kc.a1, acc[k]);
@@ -136,7 +139,7 @@ __device__ __forceinline__ void pair_loop_multi(const float4* __restrict__ srec,
 
 // the same for a lane group: records j = g, g + G, ... of the staged tile (stride RS float4),
 // TPT targets per thread
-template <bool SL, bool DL, bool STRESS, int TPT, int RS>
+template <bool SL, bool DL, bool STRESS, int TPT, int RS, bool SAFE = true>
 __device__ __forceinline__ void pair_loop_strided(const float4* __restrict__ srec, int cnt, int g, int G,
                                                   const float* x, const float* y, const float* z, const KConst& kc,
                                                   float (*acc)[STRESS ? 6 : 3]) {
@@ -156,7 +159,7 @@ __device__ __forceinline__ void pair_loop_strided(const float4* __restrict__ sre
         for (int k = 0; k < TPT; ++k) {
             float dx = x[k] - p.x, dy = y[k] - p.y, dz = z[k] - p.z;
             float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
-            float ri = safe_rinv(r2);
+            float ri = SAFE ? safe_rinv(r2) : rsqrtf(r2);
             if (!STRESS) {
                 if (SL && DL) acc_UP(dx, dy, dz, ri, f.x, f.y, f.z, gg.x, gg.y, gg.z, n.x, n.y, n.z, p.w, kc.a1, kc.a3, acc[k]);
                 else if (SL) acc_U(dx, dy, dz, ri, f.x, f.y, f.z, kc.a1, acc[k]);
