@@ -17,8 +17,10 @@
 // A x = b (Eq. num2), applied matrix-free as L(u, p) = P u - U p.
 #include <cmath>
 
+#include <cstdio>
 #include <cstdlib>
 
+#include "bem_near.cuh"
 #include "fmm.cuh"
 #include "p2p.cuh"
 
@@ -58,6 +60,7 @@ struct Bem {
     DBuf<float> CU, CP;     // [n x 9] local correction blocks (row-major 3x3)
     DBuf<double> DU, DP;    // [n x 9] diagonal blocks U_self, 1/2 I + P_self (preconditioner)
     DBuf<float> f, g, y;    // expanded densities [n nq x 3], FMM output [n x 3]
+    NearMat nm;             // near-field operator of the last solve's boundary conditions
     ~Bem() { delete tree; }
 };
 
@@ -244,7 +247,20 @@ static void apply_L(Bem& B, int mode, double sign, const int32_t* bc, const floa
     const int64_t n = B.n;
     expand_kernel<<<ceil_div(n * B.nq, 256), 256, 0, s>>>(mode, bc, x, n, B.nq, B.f.p, B.g.p);
     EB_CHECK_LAUNCH();
+    static const bool prof = std::getenv("EBEM_BEM_PROFILE") != nullptr;   // diagnostics: phase times to stderr
+    if (prof) B.tree->profile = true;
     fmm_evaluate(*B.tree, K_UP, B.f.p, B.g.p, B.y.p, s);
+    if (prof) {
+        EB_CUDA(cudaStreamSynchronize(s));
+        ebem_phase_stat st[Tree::NPHASE];
+        const int np = phase_stats(*B.tree, K_UP, st, Tree::NPHASE);
+        double tot = 0;
+        for (int i = 0; i < np; ++i) {
+            std::fprintf(stderr, "%s %.2f  ", st[i].name, st[i].ms);
+            tot += st[i].ms;
+        }
+        std::fprintf(stderr, "| total %.2f ms\n", tot);
+    }
     local_kernel<T><<<ceil_div(n, 256), 256, 0, s>>>(mode, sign, bc, x, n, B.CU.p, B.CP.p, B.y.p, out);
     EB_CHECK_LAUNCH();
 }
@@ -458,10 +474,18 @@ int bem_gmres(Bem& B, const int32_t* bc, const float* val, float* x, int m, int 
     const double bn = dnorm(b.p, n3, hd.p, part.p, s);
     to_f64_kernel<<<ceil_div(n3, 256), 256, 0, s>>>(x, xd.p, n3);
     EB_CHECK_LAUNCH();
+    // near field from the operator held in HBM (bem_near.cu) when it fits
+    const bool use_nm = near_matrix_enabled() && near_matrix_build(*B.tree, B.nq, B.n, bc, B.mat, B.nm, s);
+    struct HookGuard {
+        Tree& t;
+        ~HookGuard() { t.near_hook = nullptr; }
+    } hook_guard{*B.tree};
     auto matvec = [&](const double* v, double* out) {   // out = A v
         to_f32_kernel<<<ceil_div(n3, 256), 256, 0, s>>>(v, xf.p, n3);
         EB_CHECK_LAUNCH();
+        if (use_nm) B.tree->near_hook = [&](cudaStream_t st) { near_matrix_apply(*B.tree, B.nm, xf.p, st); };
         apply_L<double>(B, 0, 1.0, bc, xf.p, out, s);
+        B.tree->near_hook = nullptr;
     };
     auto pmatvec = [&](const double* v, double* out) {  // out = A M^-1 v (right preconditioning)
         if (!precond) return matvec(v, out);

@@ -1126,6 +1126,10 @@ void fmm_evaluate(Tree& t, int kernel, const float* f, const float* g, float* ou
         else launch_check<false, true>(t, t.s2l_box.p, t.n_s2l, t.x_src_off.p, t.x_src_idx.p, RAD_DC, t.Qd.p, qb, qs, st);
     };
     auto near = [&](cudaStream_t st) {
+        if (t.near_hook) {
+            t.near_hook(st);
+            return;
+        }
         switch (kernel) {
             case K_U: launch_near<true, false, false>(t, st); break;
             case K_P: launch_near<false, true, false>(t, st); break;

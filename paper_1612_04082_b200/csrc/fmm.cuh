@@ -16,6 +16,7 @@
 #pragma once
 #include <cuda.h>
 
+#include <functional>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -151,6 +152,7 @@ struct Tree {
     DBuf<double> PHID, PHIU;             // [n_phid x me], [n_phiu x me] (fp64 far field)
     DBuf<float4> PHIDF, PHIUF;           // [n_phid x ne], [n_phiu x ne] (fp32 far field, scaled)
     DBuf<float> near_sorted;             // [ntrg x 6] near field, sorted target order
+    std::function<void(cudaStream_t)> near_hook;   // replaces the near-field kernel (BEM near operator)
     DBuf<int> near_off, near_idx;        // per box: source boxes summed directly (U + direct X/W)
     DBuf<int> m2t_off, m2t_idx;          // per box: W-list boxes evaluated from their equivalent density
     // two-stream schedule (fmm_evaluate): created on first use
