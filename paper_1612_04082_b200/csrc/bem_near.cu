@@ -16,8 +16,8 @@
 // directly summed X/W/V entries, r = 0 excluded).
 //
 // Layout: per target leaf i (eval order) the unique panels of its near sources, sorted, are
-// its columns; N_i is stored [9][rows][ncol] (component-major, so a warp reading 32 columns
-// of one row and component is one 128-B transaction).
+// its columns; N_i is stored [9][rows][ncol padded to 4] (component-major, so a warp reading
+// 128 columns of one row and component is one 512-B run of 16-B loads).
 #include <cstdio>
 #include <vector>
 
@@ -108,12 +108,17 @@ nm_assemble(int n_eval, const int* __restrict__ eval_box, const int* __restrict_
     const int i = blockIdx.x;
     if (i >= n_eval) return;
     const int b = eval_box[i];
-    const int rows = tend[b] - tbeg[b], nc = ncol[i];
+    const int rows = tend[b] - tbeg[b], nc = ncol[i], ncp = (nc + 3) & ~3;
     if (nc == 0 || rows == 0) return;
     float* base = M + moff[i];
-    const int64_t plane = (int64_t)rows * nc;
+    const int64_t plane = (int64_t)rows * ncp;
     for (int64_t idx = threadIdx.x; idx < plane; idx += blockDim.x) {
-        const int r = (int)(idx / nc), c = (int)(idx - (int64_t)r * nc);
+        const int r = (int)(idx / ncp), c = (int)(idx - (int64_t)r * ncp);
+        if (c >= nc) {                                  // padding columns (x is staged as 0 there)
+#pragma unroll
+            for (int q = 0; q < 9; ++q) base[q * plane + idx] = 0.f;
+            continue;
+        }
         const int sg = col_first[i] + c;
         const bool dir = bc[col_panel[sg]] == 0;
         const int t = tbeg[b] + r;
@@ -153,44 +158,52 @@ nm_assemble(int n_eval, const int* __restrict__ eval_box, const int* __restrict_
 constexpr int NM_T = 256, NM_CH = 1024;
 
 // near(t) = N_i x_gathered: one CTA per target leaf, the leaf's panel densities staged in
-// shared memory NM_CH columns at a time, a warp per target row (lanes over columns)
+// shared memory NM_CH columns at a time, a warp per target row, each lane 4 columns per
+// step (rows padded to a multiple of 4 columns: nine 16-B streaming loads per lane)
 __global__ void __launch_bounds__(NM_T)
 nm_apply(int n_eval, const int* __restrict__ eval_box, const int* __restrict__ tbeg, const int* __restrict__ tend,
          const int* __restrict__ col_first, const int* __restrict__ ncol, const long long* __restrict__ moff,
          const int* __restrict__ col_panel, const float* __restrict__ M, const float* __restrict__ x,
          float* __restrict__ near) {
-    __shared__ float xs[3][NM_CH];
+    __shared__ __align__(16) float xs[3][NM_CH];
     const int i = blockIdx.x;
     if (i >= n_eval) return;
     const int b = eval_box[i];
-    const int rows = tend[b] - tbeg[b], nc = ncol[i], t0 = tbeg[b];
+    const int rows = tend[b] - tbeg[b], nc = ncol[i], ncp = (nc + 3) & ~3, t0 = tbeg[b];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (nc == 0) {
         for (int q = threadIdx.x; q < 3 * rows; q += NM_T) near[3 * (int64_t)t0 + q] = 0.f;
         return;
     }
     const float* base = M + moff[i];
-    const int64_t plane = (int64_t)rows * nc;
-    for (int c0 = 0; c0 < nc; c0 += NM_CH) {
-        const int cnt = min(NM_CH, nc - c0);
+    const int64_t plane = (int64_t)rows * ncp;
+    for (int c0 = 0; c0 < ncp; c0 += NM_CH) {
+        const int cnt = min(NM_CH, ncp - c0);
         __syncthreads();
         for (int c = threadIdx.x; c < cnt; c += NM_T) {
-            const int p = col_panel[col_first[i] + c0 + c];
-            xs[0][c] = x[3 * p];
-            xs[1][c] = x[3 * p + 1];
-            xs[2][c] = x[3 * p + 2];
+            const bool in = c0 + c < nc;
+            const int p = in ? col_panel[col_first[i] + c0 + c] : 0;
+            xs[0][c] = in ? x[3 * p] : 0.f;
+            xs[1][c] = in ? x[3 * p + 1] : 0.f;
+            xs[2][c] = in ? x[3 * p + 2] : 0.f;
         }
         __syncthreads();
         for (int r = warp; r < rows; r += NM_T / 32) {
-            const float* m = base + (int64_t)r * nc + c0;
+            const float* m = base + (int64_t)r * ncp + c0;
             float acc[3] = {0.f, 0.f, 0.f};
-            for (int c = lane; c < cnt; c += 32) {
-                const float x0 = xs[0][c], x1 = xs[1][c], x2 = xs[2][c];
+            for (int c = 4 * lane; c < cnt; c += 128) {
+                const float4 x0 = *reinterpret_cast<const float4*>(&xs[0][c]);
+                const float4 x1 = *reinterpret_cast<const float4*>(&xs[1][c]);
+                const float4 x2 = *reinterpret_cast<const float4*>(&xs[2][c]);
+                float4 v[9];
+#pragma unroll
+                for (int q = 0; q < 9; ++q) v[q] = __ldcs(reinterpret_cast<const float4*>(m + q * plane + c));
 #pragma unroll
                 for (int p = 0; p < 3; ++p) {
-                    acc[p] = fmaf(__ldcs(m + (3 * p) * plane + c), x0, acc[p]);
-                    acc[p] = fmaf(__ldcs(m + (3 * p + 1) * plane + c), x1, acc[p]);
-                    acc[p] = fmaf(__ldcs(m + (3 * p + 2) * plane + c), x2, acc[p]);
+                    const float4 a = v[3 * p], bq = v[3 * p + 1], cq = v[3 * p + 2];
+                    acc[p] = fmaf(a.x, x0.x, fmaf(a.y, x0.y, fmaf(a.z, x0.z, fmaf(a.w, x0.w, acc[p]))));
+                    acc[p] = fmaf(bq.x, x1.x, fmaf(bq.y, x1.y, fmaf(bq.z, x1.z, fmaf(bq.w, x1.w, acc[p]))));
+                    acc[p] = fmaf(cq.x, x2.x, fmaf(cq.y, x2.y, fmaf(cq.z, x2.z, fmaf(cq.w, x2.w, acc[p]))));
                 }
             }
 #pragma unroll
@@ -283,7 +296,7 @@ bool near_matrix_build(const Tree& t, int nq, int64_t npanels, const int32_t* bc
     long long tot = 0;
     for (int i = 0; i < ne; ++i) {
         mo[i] = tot;
-        tot += 9LL * hr[i] * hn[i];
+        tot += 9LL * hr[i] * ((hn[i] + 3) & ~3);   // rows padded to 4 columns (16-B aligned)
     }
     size_t fr = 0, tt = 0;
     EB_CUDA(cudaMemGetInfo(&fr, &tt));

@@ -1079,7 +1079,8 @@ void fmm_evaluate(Tree& t, int kernel, const float* f, const float* g, float* ou
     const int src_kernel = stress ? kernel - 3 : kernel;    // D->U, S->P, DS->UP
     EB_REQUIRE(!dl || t.has_normals, "double-layer kernel needs normals at fmm_build_tree");
     if (t.ntrg == 0) return;
-    const bool conc = !t.profile;
+    static const bool serial = std::getenv("EBEM_SERIAL") != nullptr;   // diagnostics: one stream
+    const bool conc = !t.profile && !serial;
     if (conc && !t.sA) {
         int least = 0, greatest = 0;
         EB_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
