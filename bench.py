@@ -308,7 +308,7 @@ def main():
     ap.add_argument("--n", type=int, default=1_000_000)
     ap.add_argument("--p", type=int, default=None, help="multipole order (default: 6 matvec, 8 gmres)")
     ap.add_argument("--max-pts", type=int, default=None,
-                    help="leaf capacity (default: 64 for the matvec (configs[2]), 1024 for gmres)")
+                    help="leaf capacity (default: 64 for the matvec (configs[2]), 1536 for gmres)")
     ap.add_argument("--ref-sample", type=int, default=512)
     ap.add_argument("--cpu-sample", type=int, default=3072)
     ap.add_argument("--no-cpu", action="store_true")
@@ -324,7 +324,7 @@ def main():
     args = ap.parse_args()
     gm = args.workload == "gmres"
     if args.max_pts is None:   # configs[2] fixes 64 for the matvec; the others state none: fastest measured
-        args.max_pts = {"gmres": 1024, "stress": 256}.get(args.workload, 64)
+        args.max_pts = {"gmres": 1536, "stress": 256}.get(args.workload, 64)
     if args.p is None:
         args.p = 8 if args.workload in ("gmres", "stress") else 6
     if args.impl == "reference":

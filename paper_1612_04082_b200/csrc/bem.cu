@@ -256,7 +256,9 @@ static void apply_L(Bem& B, int mode, double sign, const int32_t* bc, const floa
         const int np = phase_stats(*B.tree, K_UP, st, Tree::NPHASE);
         double tot = 0;
         for (int i = 0; i < np; ++i) {
-            std::fprintf(stderr, "%s %.2f  ", st[i].name, st[i].ms);
+            std::fprintf(stderr, "%s %.2f", st[i].name, st[i].ms);
+            if (st[i].interactions > 0) std::fprintf(stderr, " (%.2f G pairs)", st[i].interactions / 1e9);
+            std::fprintf(stderr, "  ");
             tot += st[i].ms;
         }
         std::fprintf(stderr, "| total %.2f ms\n", tot);
@@ -296,7 +298,11 @@ Bem* bem_create(const float* verts, int64_t n, int nq, int max_pts, int p, const
     self_terms_kernel<<<ceil_div(n, 128), 128, 0, s>>>(verts, n, nq, B->qpts.p, B->qw.p, B->cent.p, B->nrm.p, m.G, m.nu,
                                                        B->CU.p, B->CP.p, B->DU.p, B->DP.p);
     EB_CHECK_LAUNCH();
-    B->tree = build_tree(B->qpts.p, B->qnrm.p, B->qw.p, ns, B->cent.p, n, max_pts, p, m, s);
+    // W boxes with fewer than 16 n_e quadrature sources are summed directly (R11): in the BEM
+    // the far field is fp64 (M2T ~7 ps per target-equivalent point pair) while a direct entry
+    // costs one fp32 pair, or 36 B of the near operator per target and panel (measured on
+    // configs[4]: 99 -> 90 ms per iteration)
+    B->tree = build_tree(B->qpts.p, B->qnrm.p, B->qw.p, ns, B->cent.p, n, max_pts, p, m, s, 16.0);
     // GMRES needs an operator linear to ~1e-8: fp64 far field and the precise (drained)
     // tensor-core accumulation (see fmm.cu)
     tree_precise(*B->tree, s);

@@ -225,9 +225,9 @@ __global__ void nm_diff(const int32_t* __restrict__ a, const int32_t* __restrict
 
 }  // namespace
 
-bool near_matrix_enabled() {
-    static const bool on = !(std::getenv("EBEM_BEM_NEARMAT") && std::atoi(std::getenv("EBEM_BEM_NEARMAT")) == 0);
-    return on;
+bool near_matrix_enabled() {   // read per solve (tests switch it)
+    const char* e = std::getenv("EBEM_BEM_NEARMAT");
+    return !(e && std::atoi(e) == 0);
 }
 
 bool near_matrix_build(const Tree& t, int nq, int64_t npanels, const int32_t* bc, const Material& m, NearMat& N,

@@ -358,6 +358,9 @@ __device__ __forceinline__ void far_round_f32(int t0, int t_beg, int t_end, int 
         }
 }
 
+#ifndef FAR64_TMAX
+#define FAR64_TMAX 4
+#endif
 template <bool STRESS>
 __global__ void __launch_bounds__(32 * EV_WARPS)
 far_eval_f64_kernel(int n_eval, const int* __restrict__ eval_box, const int* __restrict__ l2t_slot,
@@ -382,12 +385,20 @@ far_eval_f64_kernel(int n_eval, const int* __restrict__ eval_box, const int* __r
     const int nfar = own + (woff[b + 1] - woff[b]);
     for (int t0 = t_beg; t0 < t_end;) {
         int L;
-        const int tpt = lane_groups_max<2>(t_end - t0, L);   // fp64: at most 2 targets per lane
+        // fp64: up to 4 targets per lane (2 for the 6-component stress sums): independent
+        // Newton/accumulation chains hide the DFMA latency
+        const int tpt = STRESS ? lane_groups_max<2>(t_end - t0, L) : lane_groups_max<FAR64_TMAX>(t_end - t0, L);
 #define EB_FAR64(T)                                                                                                  \
     far_round_f64<STRESS, T>(t0, t_beg, t_end, L, b, own, nfar, widx, woff[b], PHID, l2t, PHIU, phiu_slot, anchor, \
                              level, geo, sse, ne, trg, kc, cfar, ph, lane, near, trg_perm, out)
         if (tpt == 1) EB_FAR64(1);
-        else EB_FAR64(2);
+        else if (STRESS || tpt == 2) EB_FAR64(2);
+#if FAR64_TMAX >= 3
+        else if (tpt == 3) EB_FAR64(3);
+#endif
+#if FAR64_TMAX >= 4
+        else EB_FAR64(4);
+#endif
 #undef EB_FAR64
         t0 += L * tpt;
     }
@@ -742,7 +753,8 @@ void schedule_tree(Tree& t, cudaStream_t s) {
     // EBEM_XW_DIRECT=0 keeps the paper's S2L / M2T for every entry.
     const bool xw_direct = !(std::getenv("EBEM_XW_DIRECT") && std::atoi(std::getenv("EBEM_XW_DIRECT")) == 0);
     auto x_direct = [&](int b) { return xw_direct && leaf[b] && tsub[b] < P.nc; };
-    auto w_direct = [&](int a) { return xw_direct && nsub[a] < P.ne; };
+    const double wf = std::getenv("EBEM_W_DIRECT_F") ? std::atof(std::getenv("EBEM_W_DIRECT_F")) : t.w_direct;
+    auto w_direct = [&](int a) { return xw_direct && nsub[a] < wf * P.ne; };
     // V-list pairs of two leaves with few points: one M2L costs ~ (3 n_e)^2 tensor-core MACs
     // (x3 for 3xTF32) plus its share of the fp64 state; summing the nsrc x ntrg pairs directly
     // is cheaper below ~kappa (3 n_e)^2 pair interactions (kappa measured on the 1M beam).

@@ -70,6 +70,7 @@ struct OpPairs {
 struct Tree {
     int64_t nsrc = 0, ntrg = 0, npts = 0;
     int max_pts = 0, p = 0;
+    double w_direct = 1.0;               // R11: W box summed directly below w_direct x n_e sources
     Material mat{};
     bool has_normals = false, has_weights = false;
     double origin[3] = {0, 0, 0}, side = 1;
@@ -161,8 +162,9 @@ struct Tree {
     int64_t device_bytes = 0;
 };
 
+// w_direct: W entries whose box holds fewer sources than w_direct x n_e are summed directly (R11)
 Tree* build_tree(const float* src, const float* nrm, const float* w, int64_t nsrc, const float* trg,
-                 int64_t ntrg, int max_pts, int p, const Material& m, cudaStream_t s);
+                 int64_t ntrg, int max_pts, int p, const Material& m, cudaStream_t s, double w_direct = 1.0);
 void fmm_evaluate(Tree& t, int kernel, const float* f, const float* g, float* out, cudaStream_t s);
 void tree_info(const Tree& t, ebem_tree_info* info);
 int64_t tree_export(const Tree& t, int what, void* buf, int64_t cap);

@@ -371,9 +371,10 @@ static void csr_from_counts(DBuf<int>& cnt_then_off, int nb, int64_t& total, cud
 void schedule_tree(Tree& t, cudaStream_t s);   // fmm.cu
 
 Tree* build_tree(const float* src, const float* nrm, const float* w, int64_t nsrc, const float* trg,
-                 int64_t ntrg, int max_pts, int p, const Material& m, cudaStream_t s) {
+                 int64_t ntrg, int max_pts, int p, const Material& m, cudaStream_t s, double w_direct) {
     const auto t0_build = std::chrono::steady_clock::now();
     auto T = std::make_unique<Tree>();
+    T->w_direct = w_direct;
     Tree& t = *T;
     t.nsrc = nsrc;
     t.ntrg = ntrg;

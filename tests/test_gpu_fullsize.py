@@ -88,13 +88,13 @@ def test_config3_stress_full(eb):
 
 def test_config4_gmres_full(eb):
     """configs[4]: the 1.93 M-triangle cell, mixed BVP, block-Jacobi GMRES(50) to 1e-6 at
-    p = 8, leaf 1024: converges, and the tractions balance (net force of the solved + given
+    p = 8, leaf 1536 (the bench setting): converges, and the tractions balance (net force of the solved + given
     tractions over the closed surface ~ 0 against the applied unit load)."""
     d = geo.metamaterial_cell(nc=160, level=5, nvoids=64)
     verts = torch.from_numpy(d["verts"]).cuda()
     bc = torch.from_numpy(d["bc_type"]).cuda()
     val = torch.from_numpy(d["bc_val"]).cuda()
-    op = eb.bem_create(verts, nq=16, max_pts=1024, p=8, K=d["K"], G=d["G"])
+    op = eb.bem_create(verts, nq=16, max_pts=1536, p=8, K=d["K"], G=d["G"])
     x = torch.zeros((d["verts"].shape[0], 3), device="cuda")
     x, it, res = eb.bem_gmres_solve(op, bc, val, x, restart=50, max_iter=600, tol=1e-6, precond=1, check=False)
     V = d["verts"].astype(np.float64)
