@@ -117,31 +117,39 @@ __device__ __forceinline__ int64_t lower_bound_ll(const long long* __restrict__ 
     return lo;
 }
 
-// one level: decide splits and child ranges
+// one level: decide splits and child ranges.  Eight lanes per box, lane c finding where
+// child c ends (independent binary searches: the top levels' searches over the whole key
+// array were a 7-deep chain of dependent ~20-step searches in one thread).
 __global__ void split_count(int nb, int level, const int* __restrict__ beg, const int* __restrict__ end,
                             const long long* __restrict__ bkey, const long long* __restrict__ keys,
                             const int* __restrict__ cs, const int* __restrict__ ct, int max_pts,
                             int* __restrict__ cb, int* __restrict__ nchild) {
-    const int b = blockIdx.x * blockDim.x + threadIdx.x;
-    if (b >= nb) return;
-    const int B = beg[b], E = end[b];
-    const int ns = cs[E] - cs[B], nt = ct[E] - ct[B];
-    int cnt = 0;
-    if (level < MAXLEVEL && max(ns, nt) > max_pts) {
+    const int64_t gid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int c = (int)(gid & 7);
+    const int64_t b = gid >> 3;
+    const bool valid = b < nb;
+    const int B = valid ? beg[b] : 0, E = valid ? end[b] : 0;
+    const bool split = valid && level < MAXLEVEL && max(cs[E] - cs[B], ct[E] - ct[B]) > max_pts;
+    int64_t e = E;
+    if (split && c < 7) {
         const int shift = 3 * (MAXLEVEL - level - 1);
-        int64_t prev = B;
-        for (int c = 0; c < 8; ++c) {
-            long long hi = ((bkey[b] << 3) + c + 1) << shift;
-            int64_t e = (c == 7) ? E : lower_bound_ll(keys, prev, E, hi);
-            cb[9 * b + c] = (int)prev;
-            if (e > prev) ++cnt;
-            prev = e;
-        }
-        cb[9 * b + 8] = E;
-    } else {
-        for (int c = 0; c < 9; ++c) cb[9 * b + c] = -1;
+        const long long hi = ((bkey[b] << 3) + c + 1) << shift;
+        e = lower_bound_ll(keys, B, E, hi);
     }
-    nchild[b] = cnt;
+    // child c spans [end of child c-1, e)
+    const unsigned mask = 0xffffffffu;
+    int64_t prev = __shfl_up_sync(mask, e, 1, 8);
+    if (c == 0) prev = B;
+    const unsigned nonempty = __ballot_sync(mask, split && e > prev);
+    if (!valid) return;
+    if (split) {
+        cb[9 * b + c] = (int)prev;
+        if (c == 7) cb[9 * b + 8] = E;
+    } else {
+        cb[9 * b + c] = -1;
+        if (c == 7) cb[9 * b + 8] = -1;
+    }
+    if (c == 0) nchild[b] = __popc((nonempty >> (threadIdx.x & 24)) & 0xffu);
 }
 
 __global__ void make_children(int nb, int base_this, int base_next, const int* __restrict__ cb,
@@ -474,8 +482,8 @@ Tree* build_tree(const float* src, const float* nrm, const float* w, int64_t nsr
         const int nb = cur.n;
         DBuf<int> cb(9 * nb), nch(nb + 1);
         EB_CUDA(cudaMemsetAsync(nch.p, 0, sizeof(int) * (nb + 1), s));
-        split_count<<<ceil_div(nb, 128), 128, 0, s>>>(nb, l, cur.beg.p, cur.end.p, cur.key.p, t.keys.p, cs.p, ct.p,
-                                                      max_pts, cb.p, nch.p);
+        split_count<<<ceil_div((int64_t)nb * 8, 128), 128, 0, s>>>(nb, l, cur.beg.p, cur.end.p, cur.key.p, t.keys.p,
+                                                                  cs.p, ct.p, max_pts, cb.p, nch.p);
         EB_CHECK_LAUNCH();
         const int nnext = (int)exclusive_scan_i32(nch.p, nch.p, nb + 1, s);
         cur.child.alloc(8 * nb);
