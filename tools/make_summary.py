@@ -60,6 +60,21 @@ def tree_table(path):
 
 
 tree = tree_table(os.path.join(d, "tree_build_launches.csv"))
+bem = run("tools/ncu_summary.py", os.path.join(d, "bem_raw.csv")) if os.path.exists(os.path.join(d, "bem_raw.csv")) else ""
+bem_note = ""
+if bem:
+    import csv
+    rows = [r for r in csv.reader(open(os.path.join(d, "bem_raw.csv")))]
+    hdr = rows[0]
+    for r in rows[2:]:
+        if len(r) == len(hdr) and "nm_apply" in r[hdr.index("Kernel Name")]:
+            t_ms = float(r[hdr.index("gpu__time_duration.sum")].replace(",", ""))
+            t_ms *= {"ms": 1, "us": 1e-3, "usecond": 1e-3, "msecond": 1}.get(rows[1][hdr.index("gpu__time_duration.sum")], 1)
+            rd = float(r[hdr.index("dram__bytes_read.sum")].replace(",", ""))
+            rd *= {"Gbyte": 1e9, "Mbyte": 1e6, "byte": 1}.get(rows[1][hdr.index("dram__bytes_read.sum")], 1)
+            bem_note = (f"`nm_apply` (one application of the BEM near operator held in HBM): "
+                        f"{rd / 1e9:.1f} GB read in {t_ms:.2f} ms = {rd / t_ms / 1e6:.0f} GB/s "
+                        f"({100 * rd / t_ms / 1e6 / 6462.7:.0f}% of the measured 6462.7 GB/s HBM peak).")
 txt = f"""# Round 1 profiles (B200, sm_100a, `--clock-control none`)
 
 All captures were taken after the same command had exited 0 without ncu (under gpurun).
@@ -80,6 +95,8 @@ Regenerate this file with `python tools/make_summary.py {d}`.
 * `tree_build_launches.csv` — launch list (time, DRAM bytes) of three 1M-point tree builds
   (the first one includes the one-time operator precompute).
 * `traffic.json` — DRAM bytes of one M2L launch, read by bench.py for `roofline.traffic`.
+* `bem_raw.csv` — the BEM near-operator apply and the fp64 far-field kernel (configs[4]).
+* All of the above are produced by `bash tools/profile_round.sh r01` under gpurun.
 * `early/` — captures of the first versions (31.6 ms → 8.45 ms), kept for the record.
 
 Other workloads:
@@ -97,12 +114,16 @@ the {b["value"]:.2f} ms step.
 {shares}
 ## Full captures of the hot kernels
 {hot}
+## BEM operator kernels (configs[4], `bem_raw.csv`: `ncu --set full -k regex:"nm_apply|far_eval_f64" -c 2 python tools/prof_bem.py`)
+{bem}
+{bem_note}
+
 ## Tree and list passes (1M points; HBM bandwidth per kernel)
 {tree}
 
 The tree passes are short launches on 1M keys, bound by launch latency and the per-level
-loop rather than by HBM (6.5 TB/s); the build's wall time is dominated by the host-side
-scheduling of the interaction lists into operator pair tables.
+loop rather than by HBM (6.5 TB/s); the build's wall time (~23 ms per 1M points) is
+dominated by the host-side scheduling of the leaf lists and tile tables.
 
 M2L DRAM traffic per launch: {(tr['dram_read'] + tr['dram_write']) / 1e9:.2f} GB
 ({tr['dram_read'] / 1e9:.2f} read, {tr['dram_write'] / 1e9:.2f} written).
