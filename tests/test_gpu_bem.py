@@ -105,3 +105,22 @@ def test_near_operator_matches_near_kernel(eb, monkeypatch):
         print("near operator", k, "iterations", it, itr, "residual", res, resr)
         assert res <= 1e-6 and abs(it - itr) <= 3
         assert KN.rel_l2(x, xr) < 1e-4      # both stop at residual 1e-6; a wrong block is O(1)
+
+
+def test_near_operator_memory_fallback_and_nq1(eb, monkeypatch):
+    """When the near operator does not fit its memory budget the solve runs the near-field
+    kernel instead (same answer); with one quadrature point per panel (nq = 1) the stored
+    operator holds one point per block and matches the kernel path too."""
+    verts, c, n, a, bc, val, uex, tex, V = _problem(4)
+    bcd, vald = torch.from_numpy(bc).cuda(), torch.from_numpy(val.astype(np.float32)).cuda()
+    for nq in (16, 1):
+        sols = []
+        for frac in ("0.6", "1e-12"):          # 1e-12: nothing fits, the kernel path runs
+            monkeypatch.setenv("EBEM_BEM_NEARMAT_FRAC", frac)
+            op2 = eb.bem_create(torch.from_numpy(verts).cuda(), nq=nq, max_pts=32, p=8, K=KB, G=G)
+            x = torch.zeros((len(bc), 3), device="cuda")
+            x, it, res = eb.bem_gmres_solve(op2, bcd, vald, x, restart=50, max_iter=300, tol=1e-6)
+            assert res <= 1e-6
+            sols.append(x.cpu().numpy().reshape(-1))
+        print("nq", nq, "near operator vs kernel:", KN.rel_l2(sols[0], sols[1]))
+        assert KN.rel_l2(sols[0], sols[1]) < 1e-4
