@@ -1101,6 +1101,11 @@ void fmm_evaluate(Tree& t, int kernel, const float* f, const float* g, float* ou
         for (cudaEvent_t* e : {&t.ev_fork, &t.ev_s2l, &t.ev_near, &t.ev_joinA})
             EB_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
     }
+    // diagnostics (EBEM_TRACE=1): stream timeline of the overlapped section, printed per call
+    static const bool trace = std::getenv("EBEM_TRACE") != nullptr;
+    static cudaEvent_t tev[8] = {};
+    if (trace && !tev[0])
+        for (auto& e : tev) EB_CUDA(cudaEventCreate(&e));
     cudaStream_t sa = s, sb = s;
     if (conc) {
         sa = t.sA;
@@ -1158,7 +1163,9 @@ void fmm_evaluate(Tree& t, int kernel, const float* f, const float* g, float* ou
         EB_CUDA(cudaStreamWaitEvent(sb, t.ev_fork, 0));
         s2l(sb);
         EB_CUDA(cudaEventRecord(t.ev_s2l, sb));
+        if (trace) EB_CUDA(cudaEventRecord(tev[1], sb));
         near(sb);
+        if (trace) EB_CUDA(cudaEventRecord(tev[2], sb));
         EB_CUDA(cudaEventRecord(t.ev_near, sb));
     };
 
@@ -1210,11 +1217,13 @@ void fmm_evaluate(Tree& t, int kernel, const float* f, const float* g, float* ou
     };
     if (!conc) q2z_dn();
     mark(phase++);
+    if (trace) EB_CUDA(cudaEventRecord(tev[3], sa));
     if (t.use_tc && t.tc_fast) tc_pairs_gemm_fast(t.m2l, P.mM2L_b, P.mM2L_s, t.Zb.p, t.Zs.p, lde, me, me, t.W.p, lde, false, sa);
     else if (t.use_tc && m2l_drain_fast())   // precise accumulation, two-slice fast-kernel data flow
         tc_pairs_gemm_fast(t.m2l, P.mM2L_b, P.mM2L_s, t.Zb.p, t.Zs.p, lde, me, me, t.W.p, lde, true, sa);
     else if (t.use_tc) tc_pairs_gemm(t.m2l, P.mM2L_b, P.mM2L_s, t.mZb, t.mZs, me, me, t.W.p, lde, sa);
     else gemm_pairs_f32(t.m2l, P.M2L.p, me, me, lde, t.Z.p, lde, t.W.p, lde, sa);
+    if (trace) EB_CUDA(cudaEventRecord(tev[4], sa));
     if (conc) {
         EB_CUDA(cudaStreamWaitEvent(sa, t.ev_s2l, 0));
         q2z_dn();
@@ -1243,8 +1252,10 @@ void fmm_evaluate(Tree& t, int kernel, const float* f, const float* g, float* ou
                               sa);
     }
     mark(phase++);
+    if (trace) EB_CUDA(cudaEventRecord(tev[5], sa));
     if (conc) EB_CUDA(cudaStreamWaitEvent(sa, t.ev_near, 0));
     else near(sa);
+    if (trace) EB_CUDA(cudaEventRecord(tev[6], sa));
     mark(phase++);
     if (stress) launch_far<true>(t, out, sa);
     else launch_far<false>(t, out, sa);
@@ -1254,6 +1265,15 @@ void fmm_evaluate(Tree& t, int kernel, const float* f, const float* g, float* ou
     }
     mark(phase++);
     t.ev_valid = t.profile;
+    if (trace && conc) {
+        EB_CUDA(cudaEventRecord(tev[7], sa));
+        EB_CUDA(cudaEventSynchronize(tev[7]));
+        float ms[8] = {};
+        for (int k = 1; k < 8; ++k) EB_CUDA(cudaEventElapsedTime(&ms[k], tev[3], tev[k]));
+        std::fprintf(stderr,
+                     "[trace, ms from M2L start] near %.3f..%.3f  M2L ..%.3f  L2L+PHI ..%.3f  wait near ..%.3f  "
+                     "end %.3f\n", ms[1], ms[2], ms[4], ms[5], ms[6], ms[7]);
+    }
 }
 
 // flops per pair interaction of the fp32 pair loop, counted in the SASS of the compiled
