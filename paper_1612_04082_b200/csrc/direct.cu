@@ -12,7 +12,7 @@
 
 namespace ebem {
 
-__global__ void prepare_kernel(int kernel, float cU, float cP, float cD, float cS, float a,
+__global__ void prepare_kernel(int kernel, float cU, float cP, float cD, float cS, float a, float b4,
                                const float* __restrict__ y, const float* __restrict__ nrm,
                                const float* __restrict__ w, const float* __restrict__ f,
                                const float* __restrict__ g, const int* __restrict__ gperm,
@@ -34,6 +34,16 @@ __global__ void prepare_kernel(int kernel, float cU, float cP, float cD, float c
         nx = nrm[3 * o]; ny = nrm[3 * o + 1]; nz = nrm[3 * o + 2];
     }
     float ng = nx * gx + ny * gy + nz * gz;
+    if (st && sl && dl) {    // acc_DS record (elastic.cuh): a-scaled f, the per-source constants
+        float4* r = rec + i * REC_STRESS;
+        r[0] = make_float4(px, py, pz, 1.5f * a * ng);
+        r[1] = make_float4(a * fx, a * fy, a * fz, -0.5f * b4 * ng);
+        r[2] = make_float4(gx, gy, gz, 0.f);
+        r[3] = make_float4(nx, ny, nz, 0.f);
+        r[4] = make_float4(a * nx * gx, a * ny * gy, a * nz * gz, a * (nx * gy + ny * gx));
+        r[5] = make_float4(a * (ny * gz + nz * gy), a * (nx * gz + nz * gx), 0.f, 0.f);
+        return;
+    }
     if (!st) {
         float4* r = rec + i * REC_DISP;
         r[0] = make_float4(px, py, pz, a * ng);
@@ -56,7 +66,7 @@ void prepare_sources(int kernel, const Material& m, const float* y, const float*
                      const int* dperm, int64_t n, float4* rec, cudaStream_t s) {
     if (n == 0) return;
     prepare_kernel<<<ceil_div(n, 256), 256, 0, s>>>(kernel, (float)m.cU, (float)m.cP, (float)m.cD,
-                                                    (float)m.cS, (float)m.a, y, nrm, w, f, g, gperm,
+                                                    (float)m.cS, (float)m.a, (float)m.b4, y, nrm, w, f, g, gperm,
                                                     dperm, n, rec);
     EB_CHECK_LAUNCH();
 }
@@ -110,6 +120,11 @@ direct_kernel(const float4* __restrict__ rec, int64_t nsrc, int64_t ntiles, cons
         }
         const int slot = (int)(c - first_cta(tb * ntiles, U, G));
         float* o = partial + ((int64_t)tb * kslots + slot) * DIRECT_TB * NC;
+        if (STRESS && SL && DL)   // acc_DS accumulates half of the diagonal
+#pragma unroll
+            for (int k = 0; k < DIRECT_TPT; ++k)
+#pragma unroll
+                for (int q = 0; q < 3; ++q) acc[k][q] *= 2.f;
 #pragma unroll
         for (int k = 0; k < DIRECT_TPT; ++k)
 #pragma unroll

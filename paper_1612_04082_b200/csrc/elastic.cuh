@@ -140,33 +140,38 @@ __device__ __forceinline__ void acc_S(T dx, T dy, T dz, T ri, T gx, T gy, T gz, 
     s[5] = fmat(ux, dz, fmat(uz, dx, fmat(ri3, NG[5], s[5])));
 }
 
-// both stress kernels at once (D + S): one symmetric update with w = v (D) + u (S) and one
-// diagonal coefficient (Cdelta - A (d.f)) instead of two
-template <class T>
-__device__ __forceinline__ void acc_DS(T dx, T dy, T dz, T ri, T fx, T fy, T fz, T gx, T gy, T gz, T nx, T ny,
-                                       T nz, T ng, const T* NG, T a, T nu, T b4, T* s) {
+// both stress kernels at once (D + S), re-associated for the FP32 pipe (63 instead of ~71
+// instructions per pair).  Per source the record carries (prepare_kernel, K_DS):
+//   f' = a cD w f,  q1 = 1.5 a (n.g),  q2n = -0.5 (1 - 4 nu)(n.g),  g = cS w g,  n,
+//   NGh = a (n_i g_i) on the diagonal (half of NG_ii), a (n_i g_j + n_j g_i) off it,
+// and the DIAGONAL accumulators s[0..2] hold HALF the stress (the caller doubles them):
+//   w   = (hCdd + hB) d + rinv^3 f' + 3 nu rinv^5 [(d.n) g + (d.g) n]
+//   hCdd + hB = rinv^5 [q1 - 7.5 (d.n)(d.g) rinv^2 + (1.5 / a)(d.f')]
+//   s_ii/2 += w_i d_i + rinv^3 NGh_ii + Cdelta / 2,  Cdelta / 2 = 1.5 a (d.n)(d.g) rinv^5
+//             + rinv^3 (q2n - 0.5 d.f')
+//   s_ij   += w_i d_j + w_j d_i + rinv^3 NG_ij
+// which is D (v = A f + (B/2) d, diagonal -A (d.f), A = a rinv^3, B = 3 (d.f) rinv^5) plus
+// S (acc_S above) term by term.
+template <class T, class KC>
+__device__ __forceinline__ void acc_DS(T dx, T dy, T dz, T ri, T fx, T fy, T fz, T q2n, T gx, T gy, T gz, T nx,
+                                       T ny, T nz, T q1, const T* NG, const KC& kc, T* s) {
     T ri2 = ri * ri;
     T ri3 = ri2 * ri;
     T ri5 = ri3 * ri2;
-    // D part: v = A f + (B/2) d with A = a rinv^3, B = 3 (d.f) rinv^5; diagonal -A (d.f)
-    T df = fmat(dz, fz, fmat(dy, fy, dx * fx));
-    T A = a * ri3;
-    T hB = T(1.5) * df * ri5;
-    // S part
+    T df = fmat(dz, fz, fmat(dy, fy, dx * fx));          // d.f' = a d.f
     T dn = fmat(dz, nz, fmat(dy, ny, dx * nx));
     T dg = fmat(dz, gz, fmat(dy, gy, dx * gx));
     T dndg = dn * dg;
-    T hCdd = T(0.5) * ri5 * (T(3) * a * ng - T(15) * dndg * ri2);
-    T Cgd = T(3) * nu * dn * ri5;
-    T Cnd = T(3) * nu * dg * ri5;
-    T Cdl = T(3) * a * dndg * ri5 - b4 * ng * ri3 - A * df;
-    const T hd = hCdd + hB;
-    T wx = fmat(Cnd, nx, fmat(Cgd, gx, fmat(A, fx, hd * dx)));
-    T wy = fmat(Cnd, ny, fmat(Cgd, gy, fmat(A, fy, hd * dy)));
-    T wz = fmat(Cnd, nz, fmat(Cgd, gz, fmat(A, fz, hd * dz)));
-    s[0] = fmat(T(2) * wx, dx, fmat(ri3, NG[0], s[0] + Cdl));
-    s[1] = fmat(T(2) * wy, dy, fmat(ri3, NG[1], s[1] + Cdl));
-    s[2] = fmat(T(2) * wz, dz, fmat(ri3, NG[2], s[2] + Cdl));
+    T hd = ri5 * fmat(kc.ds_k2, df, fmat(T(-7.5), dndg * ri2, q1));
+    T c3 = kc.ds_k4 * ri5;
+    T Cgd = dn * c3, Cnd = dg * c3;
+    T hCdl = fmat(kc.ds_k5, dndg * ri5, ri3 * fmat(T(-0.5), df, q2n));
+    T wx = fmat(Cnd, nx, fmat(Cgd, gx, fmat(ri3, fx, hd * dx)));
+    T wy = fmat(Cnd, ny, fmat(Cgd, gy, fmat(ri3, fy, hd * dy)));
+    T wz = fmat(Cnd, nz, fmat(Cgd, gz, fmat(ri3, fz, hd * dz)));
+    s[0] = fmat(wx, dx, fmat(ri3, NG[0], s[0] + hCdl));
+    s[1] = fmat(wy, dy, fmat(ri3, NG[1], s[1] + hCdl));
+    s[2] = fmat(wz, dz, fmat(ri3, NG[2], s[2] + hCdl));
     s[3] = fmat(wx, dy, fmat(wy, dx, fmat(ri3, NG[3], s[3])));
     s[4] = fmat(wy, dz, fmat(wz, dy, fmat(ri3, NG[4], s[4])));
     s[5] = fmat(wx, dz, fmat(wz, dx, fmat(ri3, NG[5], s[5])));

@@ -493,7 +493,8 @@ __device__ __forceinline__ void near_round(int t0, int t_beg, int t_end, int L, 
             const int t = t0 + l + L * j;
             if (t < t_end)
 #pragma unroll
-                for (int c = 0; c < NC; ++c) near[(int64_t)t * NC + c] = acc[j][c];
+                for (int c = 0; c < NC; ++c)   // acc_DS accumulates half of the diagonal
+                    near[(int64_t)t * NC + c] = (STRESS && SL && DL && c < 3) ? 2.f * acc[j][c] : acc[j][c];
         }
 }
 
@@ -1286,7 +1287,7 @@ static double flops_per_pair(int kernel) {
         case K_UP: return 59;
         case K_D: return 54;
         case K_S: return 87;
-        default: return 104;
+        default: return 97;
     }
 }
 

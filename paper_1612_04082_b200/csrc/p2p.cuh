@@ -23,12 +23,14 @@ constexpr int REC_STRESS = 6;
 
 struct KConst {
     float a1, a, a3, nu, b4;
+    float ds_k2, ds_k4, ds_k5;   // D+S pair: 1.5 / a, 3 nu, 1.5 a (acc_DS)
     double a1d, ad, nud, b4d;
 };
 
 inline KConst make_kconst(const Material& m) {
     KConst k;
     k.a1 = (float)m.a1; k.a = (float)m.a; k.a3 = (float)(m.a / 3.0); k.nu = (float)m.nu; k.b4 = (float)m.b4;
+    k.ds_k2 = (float)(1.5 / m.a); k.ds_k4 = (float)(3.0 * m.nu); k.ds_k5 = (float)(1.5 * m.a);
     k.a1d = m.a1; k.ad = m.a; k.nud = m.nu; k.b4d = m.b4;
     return k;
 }
@@ -41,57 +43,7 @@ void prepare_sources(int kernel, const Material& m, const float* y, const float*
                      const float* w, const int* gperm, const float* f, const float* g,
                      const int* dperm, int64_t n, float4* rec, cudaStream_t s);
 
-// ------------------------------------------------------------------ pair loop
-// Accumulate the interactions of `cnt` prepared sources staged in shared memory
-// (srec, stride R float4) into one target's accumulator acc[3 or 6].
-template <bool SL, bool DL, bool STRESS>
-__device__ __forceinline__ void pair_loop(const float4* __restrict__ srec, int cnt, float x, float y,
-                                          float z, const KConst& kc, float* acc) {
-    constexpr int R = STRESS ? REC_STRESS : REC_DISP;
-#pragma unroll 4
-    for (int j = 0; j < cnt; ++j) {
-        const float4 p = srec[j * R + 0];
-        float dx = x - p.x, dy = y - p.y, dz = z - p.z;
-        float r2 = dx * dx + dy * dy + dz * dz;
-        float ri = safe_rinv(r2);
-        if (!STRESS) {
-            if (SL && DL) {
-                const float4 f = srec[j * R + 1];
-                const float4 g = srec[j * R + 2];
-                const float4 n = srec[j * R + 3];
-                acc_UP(dx, dy, dz, ri, f.x, f.y, f.z, g.x, g.y, g.z, n.x, n.y, n.z, p.w, kc.a1, kc.a3, acc);
-            } else if (SL) {
-                const float4 f = srec[j * R + 1];
-                acc_U(dx, dy, dz, ri, f.x, f.y, f.z, kc.a1, acc);
-            } else {
-                const float4 g = srec[j * R + 2];
-                const float4 n = srec[j * R + 3];
-                acc_P(dx, dy, dz, ri, g.x, g.y, g.z, n.x, n.y, n.z, p.w, kc.a3, acc);
-            }
-        } else {
-            if (SL && DL) {
-                const float4 f = srec[j * R + 1];
-                const float4 g = srec[j * R + 2];
-                const float4 n = srec[j * R + 3];
-                const float4 t0 = srec[j * R + 4];
-                const float4 t1 = srec[j * R + 5];
-                const float NG[6] = {t0.x, t0.y, t0.z, t0.w, t1.x, t1.y};
-                acc_DS(dx, dy, dz, ri, f.x, f.y, f.z, g.x, g.y, g.z, n.x, n.y, n.z, p.w, NG, kc.a, kc.nu, kc.b4, acc);
-            } else if (SL) {
-                const float4 f = srec[j * R + 1];
-                acc_D(dx, dy, dz, ri, f.x, f.y, f.z, kc.a, acc);
-            } else {
-                const float4 g = srec[j * R + 2];
-                const float4 n = srec[j * R + 3];
-                const float4 t0 = srec[j * R + 4];
-                const float4 t1 = srec[j * R + 5];
-                const float NG[6] = {t0.x, t0.y, t0.z, t0.w, t1.x, t1.y};
-                acc_S(dx, dy, dz, ri, g.x, g.y, g.z, n.x, n.y, n.z, p.w, NG, kc.a, kc.nu, kc.b4, acc);
-            }
-        }
-    }
-}
-
+// ------------------------------------------------------------------ pair loops
 #ifndef EBEM_PL_UNROLL
 #define EBEM_PL_UNROLL 4
 #endif
@@ -128,7 +80,7 @@ __device__ __forceinline__ void pair_loop_multi(const float4* __restrict__ srec,
                 else if (SL) acc_U(dx, dy, dz, ri, f.x, f.y, f.z, kc.a1, acc[k]);
                 else acc_P(dx, dy, dz, ri, g.x, g.y, g.z, n.x, n.y, n.z, p.w, kc.a3, acc[k]);
             } else {
-                if (SL && DL) acc_DS(dx, dy, dz, ri, f.x, f.y, f.z, g.x, g.y, g.z, n.x, n.y, n.z, p.w, NG, kc.a, kc.nu, kc.b4, acc[k]);
+                if (SL && DL) acc_DS(dx, dy, dz, ri, f.x, f.y, f.z, f.w, g.x, g.y, g.z, n.x, n.y, n.z, p.w, NG, kc, acc[k]);
                 else if (SL) acc_D(dx, dy, dz, ri, f.x, f.y, f.z, kc.a, acc[k]);
                 else acc_S(dx, dy, dz, ri, g.x, g.y, g.z, n.x, n.y, n.z, p.w, NG, kc.a, kc.nu, kc.b4, acc[k]);
             }
@@ -165,7 +117,7 @@ __device__ __forceinline__ void pair_loop_strided(const float4* __restrict__ sre
                 else if (SL) acc_U(dx, dy, dz, ri, f.x, f.y, f.z, kc.a1, acc[k]);
                 else acc_P(dx, dy, dz, ri, gg.x, gg.y, gg.z, n.x, n.y, n.z, p.w, kc.a3, acc[k]);
             } else {
-                if (SL && DL) acc_DS(dx, dy, dz, ri, f.x, f.y, f.z, gg.x, gg.y, gg.z, n.x, n.y, n.z, p.w, NG, kc.a, kc.nu, kc.b4, acc[k]);
+                if (SL && DL) acc_DS(dx, dy, dz, ri, f.x, f.y, f.z, f.w, gg.x, gg.y, gg.z, n.x, n.y, n.z, p.w, NG, kc, acc[k]);
                 else if (SL) acc_D(dx, dy, dz, ri, f.x, f.y, f.z, kc.a, acc[k]);
                 else acc_S(dx, dy, dz, ri, gg.x, gg.y, gg.z, n.x, n.y, n.z, p.w, NG, kc.a, kc.nu, kc.b4, acc[k]);
             }
