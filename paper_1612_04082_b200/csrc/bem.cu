@@ -475,8 +475,18 @@ int bem_gmres(Bem& B, const int32_t* bc, const float* val, float* x, int m, int 
         prec_setup<<<ceil_div(B.n, 256), 256, 0, s>>>(bc, B.DU.p, B.DP.p, B.n, Minv.p);
         EB_CHECK_LAUNCH();
     }
-    // right-hand side b = -L(known values)
+    // sources grouped per leaf by panel type: each then carries one layer only, and the check
+    // potentials run one-kernel pair loops (EBEM_BEM_SPLIT=0: the combined U+P loop)
+    struct SplitGuard {
+        Tree& t;
+        ~SplitGuard() { t.split_mode = 0; }
+    } split_guard{*B.tree};
+    const bool split = !(std::getenv("EBEM_BEM_SPLIT") && std::atoi(std::getenv("EBEM_BEM_SPLIT")) == 0);
+    if (split) tree_partition_sources(*B.tree, bc, B.nq, s);
+    // right-hand side b = -L(known values): Dirichlet panels carry u (double layer)
+    B.tree->split_mode = split ? 2 : 0;
     apply_L<double>(B, 1, -1.0, bc, val, b.p, s);
+    B.tree->split_mode = split ? 1 : 0;   // A x: Dirichlet panels carry p (single layer)
     const double bn = dnorm(b.p, n3, hd.p, part.p, s);
     to_f64_kernel<<<ceil_div(n3, 256), 256, 0, s>>>(x, xd.p, n3);
     EB_CHECK_LAUNCH();

@@ -14,6 +14,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <type_traits>
 
 #include "fmm.cuh"
 #include "p2p.cuh"
@@ -56,7 +57,7 @@ check_potential_kernel(const int* __restrict__ tbox, const int* __restrict__ sof
                        const int* __restrict__ sbeg, const int* __restrict__ send, const int* __restrict__ anchor,
                        const int* __restrict__ level, BoxGeo geo, double rad, const float* __restrict__ sc, int nc,
                        const float4* __restrict__ rec, KConst kc, float* __restrict__ Q, float* __restrict__ Qb,
-                       float* __restrict__ Qs, int ldq) {
+                       float* __restrict__ Qs, int ldq, const int* __restrict__ ssplit, int smode) {
     __shared__ float4 srec[CP_TILE * REC_DISP];
     const int i = blockIdx.x;
     const int b = tbox[i];
@@ -91,7 +92,22 @@ check_potential_kernel(const int* __restrict__ tbox, const int* __restrict__ sof
                 srec[q] = v;
             }
             __syncthreads();
-            pair_loop_multi<SL, DL, false, KPT, false>(srec, cnt, x, y, z, kc, acc);   // check points never coincide
+            // (check points never coincide with sources: SAFE = false)
+            if (SL && DL && smode) {
+                // BEM sources grouped by panel type (tree_partition_sources): each source
+                // carries only one layer, so each part runs the one-kernel loop
+                const int cs = min(max(ssplit[a] - s0, 0), cnt);
+                const float4* s2 = srec + cs * REC_DISP;
+                if (smode == 1) {
+                    pair_loop_multi<true, false, false, KPT, false>(srec, cs, x, y, z, kc, acc);
+                    pair_loop_multi<false, true, false, KPT, false>(s2, cnt - cs, x, y, z, kc, acc);
+                } else {
+                    pair_loop_multi<false, true, false, KPT, false>(srec, cs, x, y, z, kc, acc);
+                    pair_loop_multi<true, false, false, KPT, false>(s2, cnt - cs, x, y, z, kc, acc);
+                }
+            } else {
+                pair_loop_multi<SL, DL, false, KPT, false>(srec, cnt, x, y, z, kc, acc);
+            }
         }
     }
 #pragma unroll
@@ -993,7 +1009,7 @@ static void launch_check(const Tree& t, const int* tbox, int n, const int* soff,
     EB_CUDA(cudaFuncSetAttribute(check_potential_kernel<SL, DL, K>, cudaFuncAttributePreferredSharedMemoryCarveout, 100)); \
     check_potential_kernel<SL, DL, K><<<n, nthr, 0, s>>>(tbox, soff, sidx, t.sbeg.p, t.send.p, t.anchor.p,         \
                                                          t.level.p, geo, rad, P.s_c.p, P.nc, t.rec_disp.p, kc,    \
-                                                         Q, Qb, Qs, P.ldc)
+                                                         Q, Qb, Qs, P.ldc, t.ssplit.p, t.ssplit.p ? t.split_mode : 0)
     switch (kpt) {
         case 1: EB_CHECK_LAUNCH_KPT(1); break;
         case 2: EB_CHECK_LAUNCH_KPT(2); break;
@@ -1002,6 +1018,94 @@ static void launch_check(const Tree& t, const int* tbox, int n, const int* soff,
     }
 #undef EB_CHECK_LAUNCH_KPT
     EB_CHECK_LAUNCH();
+}
+
+// BEM: the sources of every leaf grouped by the boundary-condition type of their panel
+// (Dirichlet first, stable), so that inside a solve each group carries one layer only
+// (mode 0: Dirichlet -> single layer, Neumann -> double layer; mode 1 the reverse) and the
+// check potentials run the one-kernel pair loops.  A permutation inside each leaf: every
+// box range stays valid.  ssplit[leaf] = first source of the second group.
+__global__ void partition_kernel(int nb, const int* __restrict__ is_leaf, const int* __restrict__ sbeg,
+                                 const int* __restrict__ send, const int* __restrict__ src_perm, int nq,
+                                 const int32_t* __restrict__ bc, int* __restrict__ dest, int* __restrict__ ssplit) {
+    __shared__ int n0s, w0[32], w1[32];
+    const int b = blockIdx.x;
+    if (b >= nb || !is_leaf[b]) return;
+    const int B = sbeg[b], E = send[b];
+    if (E <= B) return;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    if (threadIdx.x == 0) n0s = 0;
+    __syncthreads();
+    int c0 = 0;
+    for (int s = B + threadIdx.x; s < E; s += blockDim.x) c0 += bc[src_perm[s] / nq] == 0;
+    atomicAdd(&n0s, c0);
+    __syncthreads();
+    const int n0 = n0s;
+    const unsigned lt = (1u << lane) - 1u;
+    int base0 = 0, base1 = 0;
+    for (int s0 = B; s0 < E; s0 += blockDim.x) {
+        const int s = s0 + threadIdx.x;
+        const bool valid = s < E;
+        const bool f = valid && bc[src_perm[s] / nq] == 0;
+        const unsigned b0 = __ballot_sync(0xffffffffu, f), b1 = __ballot_sync(0xffffffffu, valid && !f);
+        if (lane == 0) {
+            w0[warp] = __popc(b0);
+            w1[warp] = __popc(b1);
+        }
+        __syncthreads();
+        int p0 = 0, p1 = 0, t0 = 0, t1 = 0;
+        for (int w = 0; w < nw; ++w) {
+            if (w < warp) {
+                p0 += w0[w];
+                p1 += w1[w];
+            }
+            t0 += w0[w];
+            t1 += w1[w];
+        }
+        if (valid) dest[s] = f ? B + base0 + p0 + __popc(b0 & lt) : B + n0 + base1 + p1 + __popc(b1 & lt);
+        base0 += t0;
+        base1 += t1;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) ssplit[b] = B + n0;
+}
+
+__global__ void iota_kernel(int* __restrict__ a, int64_t n) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) a[i] = (int)i;
+}
+
+template <class T>
+__global__ void scatter_rows(const T* __restrict__ in, const int* __restrict__ dest, int64_t n, int w,
+                             T* __restrict__ out) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    for (int c = 0; c < w; ++c) out[(int64_t)dest[i] * w + c] = in[i * w + c];
+}
+
+void tree_partition_sources(Tree& t, const int32_t* bc, int nq, cudaStream_t s) {
+    const int64_t n = t.nsrc;
+    if (n == 0 || t.nboxes == 0) return;
+    DBuf<int> dest(n);
+    iota_kernel<<<ceil_div(n, 256), 256, 0, s>>>(dest.p, n);
+    EB_CHECK_LAUNCH();
+    if (t.ssplit.n != (size_t)t.nboxes) t.ssplit.alloc(t.nboxes);
+    partition_kernel<<<t.nboxes, 256, 0, s>>>(t.nboxes, t.is_leaf.p, t.sbeg.p, t.send.p, t.src_perm.p, nq, bc, dest.p,
+                                              t.ssplit.p);
+    EB_CHECK_LAUNCH();
+    auto permute = [&](auto& buf, int w) {
+        using T = typename std::remove_reference<decltype(*buf.p)>::type;
+        if (!buf.p) return;
+        DBuf<T> tmp(buf.n);
+        scatter_rows<T><<<ceil_div(n, 256), 256, 0, s>>>(buf.p, dest.p, n, w, tmp.p);
+        EB_CHECK_LAUNCH();
+        buf = std::move(tmp);
+    };
+    permute(t.src_perm, 1);
+    permute(t.src_xyz, 3);
+    if (t.has_normals) permute(t.src_nrm, 3);
+    if (t.has_weights) permute(t.src_w, 1);
+    EB_CUDA(cudaStreamSynchronize(s));
 }
 
 // switch a built tree to the precise configuration (fp64 far field, drained tensor-core

@@ -154,6 +154,8 @@ struct Tree {
     DBuf<float4> PHIDF, PHIUF;           // [n_phid x ne], [n_phiu x ne] (fp32 far field, scaled)
     DBuf<float> near_sorted;             // [ntrg x 6] near field, sorted target order
     std::function<void(cudaStream_t)> near_hook;   // replaces the near-field kernel (BEM near operator)
+    DBuf<int> ssplit;                    // BEM: per leaf, first source of the second boundary-condition group
+    int split_mode = 0;                  // 0 off; 1: [sbeg, ssplit) single layer, rest double layer; 2 reverse
     DBuf<int> near_off, near_idx;        // per box: source boxes summed directly (U + direct X/W)
     DBuf<int> m2t_off, m2t_idx;          // per box: W-list boxes evaluated from their equivalent density
     // two-stream schedule (fmm_evaluate): created on first use
@@ -198,6 +200,7 @@ template <class XT>
 void tc_split_rows(const XT* X, int ld, int64_t row0, int64_t nrows, int K, float* Xb, float* Xs,
                    cudaStream_t s);
 void tree_precise(Tree& t, cudaStream_t s);
+void tree_partition_sources(Tree& t, const int32_t* bc, int nq, cudaStream_t s);
 void tree_m2l_fast(Tree& t, bool fast, cudaStream_t s);
 void tc_build_tiles(OpPairs& P, int M, int K, bool fast);
 void tc_pairs_gemm_fast(const OpPairs& P, const CUtensorMap& Ab, const CUtensorMap& As, const float* Bb,

@@ -77,9 +77,11 @@ def test_gmres_matches_dense_solve_and_patch_test(eb):
 
 def test_near_operator_matches_near_kernel(eb, monkeypatch):
     """The BEM near field held in HBM (bem_near.cu: per-leaf 3x3 blocks of the summed
-    quadrature-point kernels) against the pair-by-pair near-field kernel: same solve to fp32
-    rounding, on a cell with voids (leaves straddling panels, direct X/W entries); the stored
-    operator is reused for the same boundary conditions and rebuilt when they change."""
+    quadrature-point kernels) and the per-leaf grouping of sources by panel type (one-layer
+    check-potential loops) against the pair-by-pair near-field kernel and the combined loop:
+    same solve to fp32 rounding, on a cell with voids (leaves straddling panels, direct X/W
+    entries); the stored operator is reused for the same boundary conditions and rebuilt
+    when they change (the grouping then changes too)."""
     d = geo.metamaterial_cell(nc=24, level=2, nvoids=4, seed=3)
     verts = torch.from_numpy(d["verts"]).cuda()
     val = torch.from_numpy(d["bc_val"]).cuda()
@@ -96,9 +98,11 @@ def test_near_operator_matches_near_kernel(eb, monkeypatch):
     bc1[: len(bc1) // 7] = 0          # more Dirichlet panels: the blocks change kind
     ref = []
     monkeypatch.setenv("EBEM_BEM_NEARMAT", "0")
+    monkeypatch.setenv("EBEM_BEM_SPLIT", "0")       # and the combined U+P check-potential loop
     for bc in (bc0, bc1):
         ref.append(solve(bc))
     monkeypatch.setenv("EBEM_BEM_NEARMAT", "1")
+    monkeypatch.setenv("EBEM_BEM_SPLIT", "1")       # sources grouped by panel type per leaf
     for k, bc in enumerate((bc0, bc0, bc1)):      # build, reuse, rebuild
         x, it, res = solve(bc)
         xr, itr, resr = ref[0 if k < 2 else 1]
