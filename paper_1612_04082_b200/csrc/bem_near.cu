@@ -325,7 +325,8 @@ bool near_matrix_build(const Tree& t, int nq, int64_t npanels, const int32_t* bc
 
 void near_matrix_apply(const Tree& t, const NearMat& N, const float* x, cudaStream_t s) {
     if (t.n_eval == 0) return;
-    nm_apply<<<t.n_eval, NM_T, 0, s>>>(t.n_eval, t.eval_box.p, t.tbeg.p, t.tend.p, N.col_first.p, N.ncol.p,
+    static const int pad = beside_translation_pad((const void*)nm_apply);
+    nm_apply<<<t.n_eval, NM_T, pad, s>>>(t.n_eval, t.eval_box.p, t.tbeg.p, t.tend.p, N.col_first.p, N.ncol.p,
                                        N.moff.p, N.col_panel.p, N.M.p, x, t.near_sorted.p);
     EB_CHECK_LAUNCH();
 }

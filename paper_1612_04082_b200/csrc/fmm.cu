@@ -1135,6 +1135,24 @@ void tree_m2l_fast(Tree& t, bool fast, cudaStream_t s) {
 }
 
 // near field (U-list P2P) into the sorted near buffer
+// Dynamic shared memory a stream-B kernel requests so that at most two of its CTAs fit beside
+// one persistent translation CTA (tc_pairs_fast_kernel) and they fill its leftover shared
+// memory.  Measured on the 1M-point matvec (with the M2L timestamp below): 4.64 ms with three
+// near-field CTAs beside each M2L CTA (no padding), 4.45-4.48 with two, 4.60 with one — the
+// third takes issue slots the M2L producer warps need.  EBEM_NEAR_PAD=bytes overrides.
+int beside_translation_pad(const void* kernel) {
+    if (const char* e = std::getenv("EBEM_NEAR_PAD")) return std::atoi(e);
+    cudaFuncAttributes fa;
+    EB_CUDA(cudaFuncGetAttributes(&fa, kernel));
+    int dev = 0, smem_sm = 0, resv = 0;
+    EB_CUDA(cudaGetDevice(&dev));
+    EB_CUDA(cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev));
+    EB_CUDA(cudaDeviceGetAttribute(&resv, cudaDevAttrReservedSharedMemoryPerBlock, dev));
+    const int free_sm = smem_sm - (tc_fast_smem_bytes() + resv);
+    const int pad = (free_sm / 2 - resv - (int)fa.sharedSizeBytes - 128) & ~127;
+    return pad > 0 ? pad : 0;
+}
+
 template <bool SL, bool DL, bool STRESS>
 static void launch_near(const Tree& t, cudaStream_t s) {
     if (t.n_eval == 0) return;
@@ -1145,7 +1163,8 @@ static void launch_near(const Tree& t, cudaStream_t s) {
                                      100));
         carve = true;
     }
-    near_eval_kernel<SL, DL, STRESS><<<ceil_div(t.n_eval, EV_WARPS), 32 * EV_WARPS, 0, s>>>(
+    static const int pad = beside_translation_pad((const void*)near_eval_kernel<SL, DL, STRESS>);
+    near_eval_kernel<SL, DL, STRESS><<<ceil_div(t.n_eval, EV_WARPS), 32 * EV_WARPS, pad, s>>>(
         t.n_eval, t.eval_box.p, t.near_off.p, t.near_idx.p, t.sbeg.p, t.send.p, t.tbeg.p, t.tend.p, t.trg_xyz.p,
         STRESS ? t.rec_stress.p : t.rec_disp.p, kc, t.near_sorted.p);
     EB_CHECK_LAUNCH();
@@ -1206,6 +1225,7 @@ void fmm_evaluate(Tree& t, int kernel, const float* f, const float* g, float* ou
         EB_CUDA(cudaStreamCreateWithPriority(&t.sB, cudaStreamNonBlocking, least));
         for (cudaEvent_t* e : {&t.ev_fork, &t.ev_s2l, &t.ev_near, &t.ev_joinA})
             EB_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+        EB_CUDA(cudaEventCreate(&t.ev_m2l));
     }
     // diagnostics (EBEM_TRACE=1): stream timeline of the overlapped section, printed per call
     static const bool trace = std::getenv("EBEM_TRACE") != nullptr;
@@ -1324,6 +1344,10 @@ void fmm_evaluate(Tree& t, int kernel, const float* f, const float* g, float* ou
     if (!conc) q2z_dn();
     mark(phase++);
     if (trace) EB_CUDA(cudaEventRecord(tev[3], sa));
+    // a timestamp on stream A just before M2L: measured to let the near-field CTAs (padded to
+    // two per SM beside a translation CTA, beside_translation_pad) take their slots first,
+    // 4.67 -> 4.48 ms per matvec; a timing-disabled event does not have the effect
+    if (conc) EB_CUDA(cudaEventRecord(t.ev_m2l, sa));
     if (t.use_tc && t.tc_fast) tc_pairs_gemm_fast(t.m2l, P.mM2L_b, P.mM2L_s, t.Zb.p, t.Zs.p, lde, me, me, t.W.p, lde, false, sa);
     else if (t.use_tc && m2l_drain_fast())   // precise accumulation, two-slice fast-kernel data flow
         tc_pairs_gemm_fast(t.m2l, P.mM2L_b, P.mM2L_s, t.Zb.p, t.Zs.p, lde, me, me, t.W.p, lde, true, sa);

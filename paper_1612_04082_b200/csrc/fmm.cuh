@@ -137,7 +137,7 @@ struct Tree {
     ~Tree() {
         for (auto& e : ev)
             if (e) cudaEventDestroy(e);
-        for (cudaEvent_t e : {ev_fork, ev_s2l, ev_near, ev_joinA})
+        for (cudaEvent_t e : {ev_fork, ev_s2l, ev_near, ev_joinA, ev_m2l})
             if (e) cudaEventDestroy(e);
         if (sA) cudaStreamDestroy(sA);
         if (sB) cudaStreamDestroy(sB);
@@ -160,7 +160,7 @@ struct Tree {
     DBuf<int> m2t_off, m2t_idx;          // per box: W-list boxes evaluated from their equivalent density
     // two-stream schedule (fmm_evaluate): created on first use
     cudaStream_t sA = nullptr, sB = nullptr;
-    cudaEvent_t ev_fork = nullptr, ev_s2l = nullptr, ev_near = nullptr, ev_joinA = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_s2l = nullptr, ev_near = nullptr, ev_joinA = nullptr, ev_m2l = nullptr;
     int64_t device_bytes = 0;
 };
 
@@ -203,6 +203,8 @@ void tree_precise(Tree& t, cudaStream_t s);
 void tree_partition_sources(Tree& t, const int32_t* bc, int nq, cudaStream_t s);
 void tree_m2l_fast(Tree& t, bool fast, cudaStream_t s);
 void tc_build_tiles(OpPairs& P, int M, int K, bool fast);
+int tc_fast_smem_bytes();                     // dynamic shared memory of one fast translation CTA
+int beside_translation_pad(const void* kernel);   // fmm.cu: stream-B co-residency padding
 void tc_pairs_gemm_fast(const OpPairs& P, const CUtensorMap& Ab, const CUtensorMap& As, const float* Bb,
                         const float* Bs, int ldb, int M, int K, double* Y, int ldy, bool drain, cudaStream_t s);
 void tc_pairs_gemm(const OpPairs& P, const CUtensorMap& Ab, const CUtensorMap& As, const CUtensorMap& Bb,

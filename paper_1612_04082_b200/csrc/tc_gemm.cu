@@ -664,6 +664,8 @@ void tc_build_tiles(OpPairs& P, int M, int K, bool fast) {
     if (!t.empty()) EB_CUDA(cudaMemcpy(P.tiles.p, t.data(), t.size() * sizeof(tc::Tile), cudaMemcpyHostToDevice));
 }
 
+int tc_fast_smem_bytes() { return tc::fast::SMEM_BYTES; }
+
 void tc_pairs_gemm_fast(const OpPairs& P, const CUtensorMap& Ab, const CUtensorMap& As, const float* Bb,
                         const float* Bs, int ldb, int M, int K, double* Y, int ldy, bool drain, cudaStream_t s) {
     if (P.ntiles == 0) return;
