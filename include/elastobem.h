@@ -214,6 +214,13 @@ int64_t fmm_tree_export(const ebem_tree *tree, int what, void *buf, int64_t cap)
  *   iters_out / resid_out (host, may be NULL): iterations and final relative residual.
  *   restart in [1, 63] (EBEM_ERR_ARG otherwise): the Krylov basis is (restart + 1) fp64
  *   vectors of npanels*3 on the device.
+ *   Inside the solve the operator is the same map re-associated for the B200 (results equal
+ *   to fp32 rounding): the near field is held in device memory as one 3x3 block per target
+ *   and near panel (built at the first solve, rebuilt when bc_type changes, kept by the
+ *   handle until bem_free; it may take up to 60% of the free device memory, and the
+ *   pair-kernel near field is used when it does not fit), and the sources of every leaf are
+ *   grouped by the bc_type of their panel (a permutation inside each leaf).  The handle must
+ *   not be used from two streams at once.
  * Array arguments of bem_apply / bem_rhs / bem_gmres_solve must be device pointers.
  */
 typedef struct ebem_bem ebem_bem;
