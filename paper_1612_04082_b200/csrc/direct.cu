@@ -73,7 +73,10 @@ void prepare_sources(int kernel, const Material& m, const float* y, const float*
 
 constexpr int DIRECT_THREADS = 128;
 constexpr int DIRECT_TPT = 4;          // targets per thread (measured best of 3..8)
-constexpr int DIRECT_TILE = 128;       // sources per shared-memory tile
+#ifndef EBEM_DIRECT_TILE
+#define EBEM_DIRECT_TILE 64      // 64: configs[1] 50.3% of FP32 peak, 128: 49.9%, 256: 48.2%
+#endif
+constexpr int DIRECT_TILE = EBEM_DIRECT_TILE;   // sources per shared-memory tile
 constexpr int DIRECT_TB = DIRECT_THREADS * DIRECT_TPT;   // targets per target block
 
 // Work = (target block, source tile) units, target-block major.  The grid is exactly the
