@@ -47,7 +47,10 @@ __device__ __forceinline__ float tf32_rna(float x) {
 // sources of boxes sidx[soff[i] .. soff[i+1]) (or of tbox[i] itself when soff is null).
 // Output Q[i][3 nc] (fp32).  PAPER.md line 147: the approximation sum_i phi_i K(x_i, y)
 // is fitted to the sources' field on a check surface.
-constexpr int CP_T = 256, CP_TILE = 64;
+#ifndef EBEM_CP_TILE
+#define EBEM_CP_TILE 64
+#endif
+constexpr int CP_T = 256, CP_TILE = EBEM_CP_TILE;
 
 // one thread per check point (KPT points per thread when the surface has more than CP_T),
 // accumulators in registers, sources streamed through shared memory
