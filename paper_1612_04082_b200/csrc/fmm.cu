@@ -1226,7 +1226,7 @@ void fmm_evaluate(Tree& t, int kernel, const float* f, const float* g, float* ou
         EB_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
         EB_CUDA(cudaStreamCreateWithPriority(&t.sA, cudaStreamNonBlocking, greatest));
         EB_CUDA(cudaStreamCreateWithPriority(&t.sB, cudaStreamNonBlocking, least));
-        for (cudaEvent_t* e : {&t.ev_fork, &t.ev_s2l, &t.ev_near, &t.ev_joinA})
+        for (cudaEvent_t* e : {&t.ev_fork, &t.ev_s2l, &t.ev_near, &t.ev_joinA, &t.ev_zz, &t.ev_wz})
             EB_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
         EB_CUDA(cudaEventCreate(&t.ev_m2l));
     }
@@ -1260,8 +1260,16 @@ void fmm_evaluate(Tree& t, int kernel, const float* f, const float* g, float* ou
     if (stress)
         prepare_sources(kernel, t.mat, t.src_xyz.p, t.src_nrm.p, t.src_w.p, nullptr, f, g, t.src_perm.p, t.nsrc,
                         t.rec_stress.p, sa);
-    t.Z.zero(sa);
-    t.W.zero(sa);
+    if (conc) {   // the accumulators are cleared on stream B beside the prep and S2M kernels
+        EB_CUDA(cudaStreamWaitEvent(sb, t.ev_fork, 0));
+        t.Z.zero(sb);
+        EB_CUDA(cudaEventRecord(t.ev_zz, sb));
+        t.W.zero(sb);
+        EB_CUDA(cudaEventRecord(t.ev_wz, sb));
+    } else {
+        t.Z.zero(sa);
+        t.W.zero(sa);
+    }
     mark(phase++);
 
     auto s2l = [&](cudaStream_t st) {
@@ -1310,6 +1318,7 @@ void fmm_evaluate(Tree& t, int kernel, const float* f, const float* g, float* ou
     const int lde = P.lde, ldc = P.ldc;
     auto zrows = [&](int l) { return (int64_t)t.up_lstart[l + 1] - t.up_lstart[l]; };
     auto wrows = [&](int l) { return (int64_t)t.dn_lstart[l + 1] - t.dn_lstart[l]; };
+    if (conc) EB_CUDA(cudaStreamWaitEvent(sa, t.ev_zz, 0));
     if (t.use_tc) {
         if (t.ml_fast) tc_pairs_gemm_fast(t.q2z_up, P.mQu1T_b, P.mQu1T_s, t.Qb.p, t.Qs.p, ldc, me, mc, t.Z.p, lde, false, sa);
         else tc_pairs_gemm(t.q2z_up, P.mQu1T_b, P.mQu1T_s, t.mQb, t.mQs, me, mc, t.Z.p, lde, sa);
@@ -1350,7 +1359,10 @@ void fmm_evaluate(Tree& t, int kernel, const float* f, const float* g, float* ou
     // a timestamp on stream A just before M2L: measured to let the near-field CTAs (padded to
     // two per SM beside a translation CTA, beside_translation_pad) take their slots first,
     // 4.67 -> 4.48 ms per matvec; a timing-disabled event does not have the effect
-    if (conc) EB_CUDA(cudaEventRecord(t.ev_m2l, sa));
+    if (conc) {
+        EB_CUDA(cudaStreamWaitEvent(sa, t.ev_wz, 0));
+        EB_CUDA(cudaEventRecord(t.ev_m2l, sa));
+    }
     if (t.use_tc && t.tc_fast) tc_pairs_gemm_fast(t.m2l, P.mM2L_b, P.mM2L_s, t.Zb.p, t.Zs.p, lde, me, me, t.W.p, lde, false, sa);
     else if (t.use_tc && m2l_drain_fast())   // precise accumulation, two-slice fast-kernel data flow
         tc_pairs_gemm_fast(t.m2l, P.mM2L_b, P.mM2L_s, t.Zb.p, t.Zs.p, lde, me, me, t.W.p, lde, true, sa);

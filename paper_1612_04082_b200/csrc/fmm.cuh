@@ -137,7 +137,7 @@ struct Tree {
     ~Tree() {
         for (auto& e : ev)
             if (e) cudaEventDestroy(e);
-        for (cudaEvent_t e : {ev_fork, ev_s2l, ev_near, ev_joinA, ev_m2l})
+        for (cudaEvent_t e : {ev_fork, ev_s2l, ev_near, ev_joinA, ev_m2l, ev_zz, ev_wz})
             if (e) cudaEventDestroy(e);
         if (sA) cudaStreamDestroy(sA);
         if (sB) cudaStreamDestroy(sB);
@@ -160,7 +160,8 @@ struct Tree {
     DBuf<int> m2t_off, m2t_idx;          // per box: W-list boxes evaluated from their equivalent density
     // two-stream schedule (fmm_evaluate): created on first use
     cudaStream_t sA = nullptr, sB = nullptr;
-    cudaEvent_t ev_fork = nullptr, ev_s2l = nullptr, ev_near = nullptr, ev_joinA = nullptr, ev_m2l = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_s2l = nullptr, ev_near = nullptr, ev_joinA = nullptr, ev_m2l = nullptr,
+                ev_zz = nullptr, ev_wz = nullptr;
     int64_t device_bytes = 0;
 };
 
