@@ -918,9 +918,6 @@ void schedule_tree(Tree& t, cudaStream_t s) {
     }
     t.n_eval = (int)ev.size();
     t.n_phid = (int)phid_box.size();
-    t.phid_lvl.assign(t.nlevels + 1, t.n_phid);   // phid rows are in box (level-major) order
-    for (int k = t.n_phid - 1; k >= 0; --k) t.phid_lvl[level[phid_box[k]]] = k;
-    for (int l = t.nlevels - 1; l >= 0; --l) t.phid_lvl[l] = std::min(t.phid_lvl[l], t.phid_lvl[l + 1]);
     t.n_phiu = (int)phiu_box.size();
     t.eval_box.alloc(std::max<size_t>(ev.size(), 1));
     h2d(t.eval_box.p, ev.data(), ev.size(), s);
