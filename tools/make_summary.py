@@ -60,6 +60,13 @@ def tree_table(path):
 
 
 tree = tree_table(os.path.join(d, "tree_build_launches.csv"))
+extra_caps = ""
+for name, label in (("p10_raw.csv", "p = 10 matvec (1M beam): the drained M2L kernel, "
+                                   "`ncu --set full -k regex:tc_pairs_fast_kernel -c 20 python tools/prof_fmm.py --p 10`"),
+                    ("stress_raw.csv", "configs[3] stress: near field (D+S) and M2L, "
+                                       "`ncu --set full -k regex:\"near_eval|tc_pairs_fast\" -c 12` on the stress driver")):
+    if os.path.exists(os.path.join(d, name)):
+        extra_caps += f"\n### {label} (`{name}`)\n" + run("tools/ncu_summary.py", os.path.join(d, name))
 bem = run("tools/ncu_summary.py", os.path.join(d, "bem_raw.csv")) if os.path.exists(os.path.join(d, "bem_raw.csv")) else ""
 bem_note = ""
 if bem:
@@ -114,6 +121,8 @@ the {b["value"]:.2f} ms step.
 {shares}
 ## Full captures of the hot kernels
 {hot}
+## Other captures
+{extra_caps}
 ## BEM operator kernels (configs[4], `bem_raw.csv`: `ncu --set full -k regex:"nm_apply|far_eval_f64" -c 2 python tools/prof_bem.py`)
 {bem}
 {bem_note}
