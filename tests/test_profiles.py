@@ -24,8 +24,8 @@ def test_bench_line_has_the_contract_keys():
 
 
 def test_summary_regenerates_from_the_raw_captures(tmp_path):
-    out = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "make_summary.py"), PROF], cwd=ROOT,
-                         capture_output=True, text=True)
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "make_summary.py"), PROF,
+                          str(tmp_path / "SUMMARY.md")], cwd=ROOT, capture_output=True, text=True)
     assert out.returncode == 0, out.stderr
     assert "Kernel shares of one matvec" in out.stdout and "M2L DRAM traffic per launch" in out.stdout
     # the file on disk is what the generator writes

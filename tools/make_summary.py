@@ -137,5 +137,5 @@ dominated by the host-side scheduling of the leaf lists and tile tables.
 M2L DRAM traffic per launch: {(tr['dram_read'] + tr['dram_write']) / 1e9:.2f} GB
 ({tr['dram_read'] / 1e9:.2f} read, {tr['dram_write'] / 1e9:.2f} written).
 """
-open(os.path.join(d, "SUMMARY.md"), "w").write(txt)
+open(sys.argv[2] if len(sys.argv) > 2 else os.path.join(d, "SUMMARY.md"), "w").write(txt)
 print(txt)
