@@ -518,10 +518,16 @@ int bem_gmres(Bem& B, const int32_t* bc, const float* val, float* x, int m, int 
         return EBEM_OK;
     }
     std::vector<double> H((size_t)(m + 1) * m), cs(m), sn(m), g(m + 1), h(m + 1), h2(m + 1);
+    bool x_zero = dnorm(xd.p, n3, hd.p, part.p, s) == 0.0;   // r0 = b without a matvec
     while (true) {
-        matvec(xd.p, w.p);
-        sub_kernel<<<ceil_div(n3, 256), 256, 0, s>>>(b.p, w.p, n3);   // w = b - A x
-        EB_CHECK_LAUNCH();
+        if (x_zero) {
+            EB_CUDA(cudaMemcpyAsync(w.p, b.p, sizeof(double) * n3, cudaMemcpyDeviceToDevice, s));
+            x_zero = false;
+        } else {
+            matvec(xd.p, w.p);
+            sub_kernel<<<ceil_div(n3, 256), 256, 0, s>>>(b.p, w.p, n3);   // w = b - A x
+            EB_CHECK_LAUNCH();
+        }
         const double beta = dnorm(w.p, n3, hd.p, part.p, s);
         rel = beta / bn;
         if (rel <= tol || it >= max_iter) break;
