@@ -30,7 +30,8 @@
  *     line 37); the kernels use nu = (3K - 2G) / (2 (3K + G)).
  *   - Memory: unless stated otherwise, array arguments of one call must be either
  *     all device pointers (the call is asynchronous on `stream`) or all host pointers
- *     (the call stages them through device memory and returns after completion).
+ *     (the call stages them through device memory and returns after completion); a
+ *     call that mixes the two kinds returns EBEM_ERR_ARG before touching any array.
  *     The library never takes ownership of caller arrays.
  *   - stream: a cudaStream_t passed as void* (NULL = legacy default stream).
  *   - Errors: every int-returning call returns 0 on success and a negative code on
@@ -130,16 +131,20 @@ int fmm_eval_stress(ebem_tree *tree, int kernel, const float *f, const float *g,
 int fmm_tree_free(ebem_tree *tree);
 
 /*
- * Native phase profiler.  fmm_set_profiling(tree, 1) makes every later evaluation
- * record CUDA events on its stream between the phases below; fmm_phase_stats fills
- * up to `cap` entries (returns the number of phases) with, per phase and for the
- * given kernel id: kernel launches per evaluation, ALGORITHMIC work per evaluation
- * (flops: pair interactions x flops per interaction of the kernel as written in
- * elastic.cuh, or 2 M K per GEMM column; bytes: operands read once + results
- * written once), its arithmetic precision and the device time of the last profiled
- * evaluation (ms, -1 if none; synchronises on that evaluation's last event).
+ * Native phase profiler.  fmm_set_profiling(tree, mode): 0 off; 1 "solo" -- every later
+ * evaluation runs its phases one after another on the caller's stream, each bracketed by
+ * CUDA events; 2 "in situ" -- the normal overlapped two-stream schedule, each phase
+ * bracketed by CUDA events on the (internal) stream it is launched on, so a phase's time
+ * includes the slowdown from whatever runs beside it.  Switching the mode resets the record.
+ * fmm_phase_stats fills up to `cap` entries (returns the number of phases) with, per phase
+ * and for the given kernel id: kernel launches per evaluation, ALGORITHMIC work per
+ * evaluation (flops: pair interactions x flops per interaction of the kernel as written in
+ * elastic.cuh, or 2 M K per GEMM column; bytes: operands read once + results written
+ * once), its arithmetic precision and the MEAN device time over the evaluations profiled
+ * since the mode was set (at most the last 64; ms, -1 if none; synchronises the device).
  * Phases: prep, S2M, Q2Z_up, M2M, S2L, Q2Z_dn, M2L, L2L, PHI, NEAR, FAR (near field:
  * U list and the directly summed X/W/V entries; far field: L2T + M2T and the scatter).
+ * Returns EBEM_ERR_ARG for a mode outside 0..2.
  */
 typedef struct ebem_phase_stat {
     char name[16];
@@ -221,7 +226,8 @@ int64_t fmm_tree_export(const ebem_tree *tree, int what, void *buf, int64_t cap)
  *   pair-kernel near field is used when it does not fit), and the sources of every leaf are
  *   grouped by the bc_type of their panel (a permutation inside each leaf).  The handle must
  *   not be used from two streams at once.
- * Array arguments of bem_apply / bem_rhs / bem_gmres_solve must be device pointers.
+ * Array arguments of bem_apply / bem_rhs / bem_gmres_solve must be device pointers
+ * (EBEM_ERR_ARG otherwise, checked for every array argument).
  */
 typedef struct ebem_bem ebem_bem;
 
@@ -232,6 +238,16 @@ int bem_rhs(ebem_bem *bem, const int32_t *bc_type, const float *bc_val, float *b
 int bem_gmres_solve(ebem_bem *bem, const int32_t *bc_type, const float *bc_val, float *x,
                     int restart, int max_iter, double tol, int precond, int32_t *iters_out,
                     double *resid_out, void *stream);
+/*
+ * bem_gmres_history -- residual history of the last bem_gmres_solve on this handle (host).
+ *   what 0: the Arnoldi estimate |g_{j+1}| / |b| after every iteration (one entry per
+ *           iteration: the GMRES least-squares residual);
+ *   what 1: the true relative residual |b - A x| / |b| at the start of every restart cycle
+ *           and after the last one (computed by one extra operator application).
+ *   The gap between the two measures the inexactness of the fp32 operator (R12).
+ *   Copies min(n, cap) doubles to buf and returns n (>= 0), or a negative error.
+ */
+int bem_gmres_history(const ebem_bem *bem, int what, double *buf, int cap);
 int bem_free(ebem_bem *bem);
 
 #ifdef __cplusplus

@@ -44,6 +44,7 @@ _lib.bem_rhs.argtypes = [_VP, _VP, _VP, _VP, _VP]
 _lib.bem_gmres_solve.argtypes = [_VP, _VP, _VP, _VP, ctypes.c_int, ctypes.c_int, ctypes.c_double, ctypes.c_int,
                                  ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_double), _VP]
 _lib.bem_free.argtypes = [_VP]
+_lib.bem_gmres_history.argtypes = [_VP, ctypes.c_int, ctypes.POINTER(ctypes.c_double), ctypes.c_int]
 
 
 class TreeInfo(ctypes.Structure):
@@ -82,18 +83,42 @@ def _is_cuda(a):
     return a is not None and hasattr(a, "is_cuda") and a.is_cuda
 
 
-def _ptr(a, keep):
-    """device or host pointer of a float32/int32 contiguous array (None -> NULL)."""
+def _ptr(a, keep, writes=False):
+    """device or host pointer of a float32/int32 contiguous array (None -> NULL).  Inputs may
+    be non-contiguous (a contiguous copy is passed); an array the library WRITES (an output,
+    or GMRES's in-place x) must be contiguous, or the result would land in a temporary."""
     if a is None:
         return None
     if hasattr(a, "data_ptr"):                      # torch tensor
         if not a.is_contiguous():
+            if writes:
+                raise ValueError("output / in-place array must be contiguous")
             a = a.contiguous()
         keep.append(a)
         return a.data_ptr()
+    if writes:
+        if not (isinstance(a, np.ndarray) and a.flags["C_CONTIGUOUS"] and a.dtype == np.float32):
+            raise ValueError("output array must be a C-contiguous float32 numpy array or tensor")
+        return a.ctypes.data
     arr = np.ascontiguousarray(a)
     keep.append(arr)
     return arr.ctypes.data
+
+
+def _bc(bc_type):
+    """boundary-condition types as int32 (the C ABI reads int32_t): integer arrays of another
+    width are converted explicitly; anything else is an error."""
+    if hasattr(bc_type, "dtype") and hasattr(bc_type, "data_ptr"):
+        import torch
+        if bc_type.dtype == torch.int32:
+            return bc_type
+        if bc_type.dtype.is_floating_point or bc_type.dtype == torch.bool:
+            raise TypeError("bc_type must be an integer tensor")
+        return bc_type.to(torch.int32)
+    arr = np.asarray(bc_type)
+    if not np.issubdtype(arr.dtype, np.integer):
+        raise TypeError("bc_type must be an integer array")
+    return np.ascontiguousarray(arr, dtype=np.int32)
 
 
 def _stream(*arrs):
@@ -130,7 +155,7 @@ def bem_kernel_direct(kernel, trg, src, nrm=None, w=None, f=None, g=None, K=1.0,
     keep = []
     _check(_lib.bem_kernel_direct(kernel, _ptr(trg, keep), ntrg, _ptr(src, keep), _ptr(nrm, keep),
                                   _ptr(w, keep), _ptr(f, keep), _ptr(g, keep), nsrc, float(K),
-                                  float(G), _ptr(out, keep), _stream(trg, out)))
+                                  float(G), _ptr(out, keep, True), _stream(trg, out)))
     return out
 
 
@@ -173,7 +198,7 @@ def _fmm_eval(fn, tree, kernel, f, g, out, nc):
     if out is None:
         out = _out_like(ref, (tree.ntrg, nc))
     keep = []
-    _check(fn(tree.handle, kernel, _ptr(f, keep), _ptr(g, keep), _ptr(out, keep), _stream(f, g, out)))
+    _check(fn(tree.handle, kernel, _ptr(f, keep), _ptr(g, keep), _ptr(out, keep, True), _stream(f, g, out)))
     return out
 
 
@@ -222,8 +247,10 @@ def fmm_tree_export(tree, what):
 
 
 def fmm_set_profiling(tree, on=True):
-    """record CUDA events between the KIFMM phases of every later evaluation (native profiler)."""
-    _check(_lib.fmm_set_profiling(tree.handle, 1 if on else 0))
+    """native phase profiler: on = False/0 off, True/1 "solo" (phases one after another),
+    2 or "insitu" (the normal overlapped schedule, events on each phase's own stream)."""
+    mode = 2 if on == "insitu" else int(on)
+    _check(_lib.fmm_set_profiling(tree.handle, mode))
 
 
 def fmm_phase_stats(tree, kernel):
@@ -273,7 +300,8 @@ def bem_apply(bem, bc_type, x, out=None):
     import torch
     out = torch.empty_like(x) if out is None else out
     keep = []
-    _check(_lib.bem_apply(bem.handle, _ptr(bc_type, keep), _ptr(x, keep), _ptr(out, keep), _stream(x)))
+    _check(_lib.bem_apply(bem.handle, _ptr(_bc(bc_type), keep), _ptr(_f32(x), keep), _ptr(out, keep, True),
+                          _stream(x)))
     return out
 
 
@@ -281,7 +309,8 @@ def bem_rhs(bem, bc_type, bc_val, out=None):
     import torch
     out = torch.empty_like(bc_val) if out is None else out
     keep = []
-    _check(_lib.bem_rhs(bem.handle, _ptr(bc_type, keep), _ptr(bc_val, keep), _ptr(out, keep), _stream(bc_val)))
+    _check(_lib.bem_rhs(bem.handle, _ptr(_bc(bc_type), keep), _ptr(_f32(bc_val), keep), _ptr(out, keep, True),
+                        _stream(bc_val)))
     return out
 
 
@@ -291,7 +320,8 @@ def bem_gmres_solve(bem, bc_type, bc_val, x, restart=50, max_iter=1000, tol=1e-6
     keep = []
     it = ctypes.c_int32(0)
     res = ctypes.c_double(0)
-    rc = _lib.bem_gmres_solve(bem.handle, _ptr(bc_type, keep), _ptr(bc_val, keep), _ptr(x, keep), int(restart),
+    rc = _lib.bem_gmres_solve(bem.handle, _ptr(_bc(bc_type), keep), _ptr(_f32(bc_val), keep), _ptr(_f32(x), keep, True),
+                              int(restart),
                               int(max_iter), float(tol), int(precond), ctypes.byref(it), ctypes.byref(res),
                               _stream(x))
     if check or rc not in (0, -4):
@@ -299,7 +329,21 @@ def bem_gmres_solve(bem, bc_type, bc_val, x, restart=50, max_iter=1000, tol=1e-6
     return x, int(it.value), float(res.value)
 
 
+def bem_gmres_history(bem):
+    """residual history of the last bem_gmres_solve: (Arnoldi estimate per iteration, true
+    relative residual at every restart and at the end), as numpy float64 arrays."""
+    out = []
+    for what in (0, 1):
+        n = _lib.bem_gmres_history(bem.handle, what, None, 0)
+        if n < 0:
+            _check(n)
+        buf = (ctypes.c_double * max(n, 1))()
+        _lib.bem_gmres_history(bem.handle, what, buf, n)
+        out.append(np.array(buf[:n], dtype=np.float64))
+    return tuple(out)
+
+
 __all__ = ["bem_kernel_direct", "fmm_build_tree", "fmm_matvec", "fmm_eval_stress", "fmm_tree_info",
-           "fmm_tree_export", "bem_create", "bem_apply", "bem_rhs", "bem_gmres_solve", "BemOperator", "fmm_set_profiling", "fmm_phase_stats",
+           "fmm_tree_export", "bem_create", "bem_apply", "bem_rhs", "bem_gmres_solve", "bem_gmres_history", "BemOperator", "fmm_set_profiling", "fmm_phase_stats",
            "ebem_launch_count", "FmmTree", "EbemError", "LIB_PATH",
            "KERNEL_U", "KERNEL_P", "KERNEL_UP", "KERNEL_D", "KERNEL_S", "KERNEL_DS"]

@@ -19,6 +19,7 @@
 
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 
 #include "bem_near.cuh"
 #include "fmm.cuh"
@@ -60,7 +61,11 @@ struct Bem {
     DBuf<float> CU, CP;     // [n x 9] local correction blocks (row-major 3x3)
     DBuf<double> DU, DP;    // [n x 9] diagonal blocks U_self, 1/2 I + P_self (preconditioner)
     DBuf<float> f, g, y;    // expanded densities [n nq x 3], FMM output [n x 3]
+    DBuf<double> yd;        // FMM output in fp64 (the operator inside GMRES)
     NearMat nm;             // near-field operator of the last solve's boundary conditions
+    // residual history of the last bem_gmres_solve (bem_gmres_history): the Arnoldi estimate
+    // |g_{j+1}| / |b| after every iteration, and the true |b - A x| / |b| at every restart
+    std::vector<double> hist_est, hist_true;
     ~Bem() { delete tree; }
 };
 
@@ -205,50 +210,66 @@ __global__ void self_terms_kernel(const float* __restrict__ V, int64_t n, int nq
 // ------------------------------------------------------------------ operator L(u, p) = P u - U p
 // mode 0 (A x): p = x on Dirichlet panels, u = x on Neumann panels
 // mode 1 (rhs): u = value on Dirichlet panels, p = value on Neumann panels
-__device__ __forceinline__ void split_up(int mode, int bc, const float* xv, float* u, float* p) {
+template <class XT>
+__device__ __forceinline__ void split_up(int mode, int bc, const XT* xv, XT* u, XT* p) {
     const bool dir = bc == 0;
     const bool is_p = mode == 0 ? dir : !dir;
     for (int c = 0; c < 3; ++c) {
-        u[c] = is_p ? 0.f : xv[c];
-        p[c] = is_p ? xv[c] : 0.f;
+        u[c] = is_p ? XT(0) : xv[c];
+        p[c] = is_p ? xv[c] : XT(0);
     }
 }
 
-__global__ void expand_kernel(int mode, const int32_t* __restrict__ bc, const float* __restrict__ x, int64_t n, int nq,
+// FMM source densities of the quadrature points (fp32: the FMM's input precision)
+template <class XT>
+__global__ void expand_kernel(int mode, const int32_t* __restrict__ bc, const XT* __restrict__ x, int64_t n, int nq,
                               float* __restrict__ f, float* __restrict__ g) {
     const int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (o >= n * nq) return;
     const int64_t j = o / nq;
-    float u[3], p[3];
+    XT u[3], p[3];
     split_up(mode, bc[j], x + 3 * j, u, p);
     for (int c = 0; c < 3; ++c) {
-        f[3 * o + c] = -p[c];      // single layer enters as - U p
-        g[3 * o + c] = u[c];       // double layer as + P u
+        f[3 * o + c] = (float)-p[c];      // single layer enters as - U p
+        g[3 * o + c] = (float)u[c];       // double layer as + P u
     }
 }
 
-template <class T>
-__global__ void local_kernel(int mode, double sign, const int32_t* __restrict__ bc, const float* __restrict__ x,
+// out = sign (y + CP u - CU p): the local pass of l. 189 in fp64 (x and y fp32 outside GMRES,
+// fp64 inside)
+template <class XT, class YT, class T>
+__global__ void local_kernel(int mode, double sign, const int32_t* __restrict__ bc, const XT* __restrict__ x,
                              int64_t n, const float* __restrict__ CU, const float* __restrict__ CP,
-                             const float* __restrict__ y, T* __restrict__ out) {
+                             const YT* __restrict__ y, T* __restrict__ out) {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= n) return;
-    float u[3], p[3];
+    XT u[3], p[3];
     split_up(mode, bc[i], x + 3 * i, u, p);
     for (int r = 0; r < 3; ++r) {
         double s = y[3 * i + r];
-        for (int c = 0; c < 3; ++c) s += (double)CP[9 * i + 3 * r + c] * u[c] - (double)CU[9 * i + 3 * r + c] * p[c];
+        for (int c = 0; c < 3; ++c)
+            s += (double)CP[9 * i + 3 * r + c] * (double)u[c] - (double)CU[9 * i + 3 * r + c] * (double)p[c];
         out[3 * i + r] = (T)(sign * s);
     }
 }
 
-template <class T>
-static void apply_L(Bem& B, int mode, double sign, const int32_t* bc, const float* x, T* out, cudaStream_t s) {
+// L(u, p) of the panel vector x.  y64: the FMM result in fp64 (B.yd; GMRES), else fp32 (B.y)
+template <class XT, class T>
+static void apply_L(Bem& B, int mode, double sign, const int32_t* bc, const XT* x, T* out, cudaStream_t s,
+                    bool y64 = false) {
     const int64_t n = B.n;
-    expand_kernel<<<ceil_div(n * B.nq, 256), 256, 0, s>>>(mode, bc, x, n, B.nq, B.f.p, B.g.p);
+    expand_kernel<XT><<<ceil_div(n * B.nq, 256), 256, 0, s>>>(mode, bc, x, n, B.nq, B.f.p, B.g.p);
     EB_CHECK_LAUNCH();
     static const bool prof = std::getenv("EBEM_BEM_PROFILE") != nullptr;   // diagnostics: phase times to stderr
-    if (prof) B.tree->profile = true;
+    if (prof) set_profiling(*B.tree, 1);
+    if (y64) {
+        if (!B.yd.p) B.yd.alloc(3 * n);
+        B.tree->out_d = B.yd.p;
+    }
+    struct OutGuard {
+        Tree& t;
+        ~OutGuard() { t.out_d = nullptr; }
+    } out_guard{*B.tree};
     fmm_evaluate(*B.tree, K_UP, B.f.p, B.g.p, B.y.p, s);
     if (prof) {
         EB_CUDA(cudaStreamSynchronize(s));
@@ -263,7 +284,8 @@ static void apply_L(Bem& B, int mode, double sign, const int32_t* bc, const floa
         }
         std::fprintf(stderr, "| total %.2f ms\n", tot);
     }
-    local_kernel<T><<<ceil_div(n, 256), 256, 0, s>>>(mode, sign, bc, x, n, B.CU.p, B.CP.p, B.y.p, out);
+    if (y64) local_kernel<XT, double, T><<<ceil_div(n, 256), 256, 0, s>>>(mode, sign, bc, x, n, B.CU.p, B.CP.p, B.yd.p, out);
+    else local_kernel<XT, float, T><<<ceil_div(n, 256), 256, 0, s>>>(mode, sign, bc, x, n, B.CU.p, B.CP.p, B.y.p, out);
     EB_CHECK_LAUNCH();
 }
 
@@ -316,11 +338,11 @@ Bem* bem_create(const float* verts, int64_t n, int nq, int max_pts, int p, const
 void bem_free(Bem* B) { delete B; }
 
 void bem_apply(Bem& B, const int32_t* bc, const float* x, float* y, cudaStream_t s) {
-    apply_L<float>(B, 0, 1.0, bc, x, y, s);
+    apply_L<float, float>(B, 0, 1.0, bc, x, y, s);
 }
 
 void bem_rhs(Bem& B, const int32_t* bc, const float* val, float* b, cudaStream_t s) {
-    apply_L<float>(B, 1, -1.0, bc, val, b, s);
+    apply_L<float, float>(B, 1, -1.0, bc, val, b, s);
 }
 
 // ------------------------------------------------------------------ GMRES (fp64 Krylov basis)
@@ -409,6 +431,17 @@ __global__ void add_kernel(const double* __restrict__ a, double* __restrict__ b,
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i < n) b[i] += a[i];
 }
+// diagnostics: a deterministic pseudo-random vector in [-1, 1) (EBEM_GMRES_PROBE)
+__global__ void hash_fill(double* __restrict__ a, int64_t n, double sc) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    uint64_t z = (uint64_t)i * 0x9E3779B97F4A7C15ull + 0x632BE59BD9B4E019ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    z ^= z >> 31;
+    a[i] = sc * ((double)(z >> 11) * (1.0 / 9007199254740992.0) * 2.0 - 1.0);
+}
+
 __global__ void sub_kernel(const double* __restrict__ a, double* __restrict__ b, int64_t n) {   // b = a - b
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i < n) b[i] = a[i] - b[i];
@@ -458,17 +491,43 @@ static double dnorm(const double* v, int64_t n, double* tmp, double* part, cudaS
 int bem_gmres(Bem& B, const int32_t* bc, const float* val, float* x, int m, int max_iter, double tol, int32_t* iters,
               double* resid, int precond, cudaStream_t s) {
     const int64_t n3 = 3 * B.n;
-    // M2L accumulation for this solve: the full-chain (fast) kernel when the tolerance is no
-    // tighter than 1e-6 (configs[4]: the same 233 iterations, 5% faster), the drained one
-    // otherwise; bem_apply outside a solve stays on the drained kernel.
+    B.hist_est.clear();
+    B.hist_true.clear();
+    static const bool trace = std::getenv("EBEM_GMRES_TRACE") != nullptr;   // diagnostics: history to stderr
+    // M2L accumulation for this solve: the full-chain (fast) kernel only for the block-Jacobi
+    // preconditioned solve with a tolerance no tighter than 1e-6 (configs[4]: the same 233
+    // iterations, 5% faster); the drained kernel for the paper's unpreconditioned solver, whose
+    // attainable residual is set by the operator's rounding noise (reading R12), for
+    // tighter tolerances, and for bem_apply outside a solve.
     struct M2LMode {
         Tree& t;
         cudaStream_t s;
         ~M2LMode() { tree_m2l_fast(t, false, s); }
     } mode{*B.tree, s};
-    tree_m2l_fast(*B.tree, tol >= 1e-6 && !std::getenv("EBEM_BEM_PRECISE_M2L"), s);
+    // (EBEM_BEM_M2L=fast|precise overrides; EBEM_BEM_PRECISE_M2L=1 = precise)
+    bool m2l_fast = precond && tol >= 1e-6 && !std::getenv("EBEM_BEM_PRECISE_M2L");
+    if (const char* e = std::getenv("EBEM_BEM_M2L")) m2l_fast = std::strcmp(e, "fast") == 0;
+    tree_m2l_fast(*B.tree, m2l_fast, s);
     DBuf<double> V((size_t)(m + 1) * n3), w(n3), b(n3), xd(n3), hd(m + 2), Minv, tp, part((size_t)DOT_BLOCKS * 64);
-    DBuf<float> xf(n3), yf(n3);
+    struct SplitGuard {
+        Tree& t;
+        ~SplitGuard() { t.split_mode = 0; }
+    } split_guard{*B.tree};
+    // right-hand side b = -L(known values), with the combined single + double layer loops (the
+    // per-leaf grouping below is only set up once a solve is needed)
+    B.tree->split_mode = 0;
+    apply_L<float, double>(B, 1, -1.0, bc, val, b.p, s, true);
+    const double bn = dnorm(b.p, n3, hd.p, part.p, s);
+    if (bn == 0.0) {   // x = 0 solves it; nothing else (near operator, grouping) is set up
+        EB_CUDA(cudaMemsetAsync(x, 0, sizeof(float) * n3, s));
+        EB_CUDA(cudaStreamSynchronize(s));
+        if (iters) *iters = 0;
+        if (resid) *resid = 0;
+        return EBEM_OK;
+    }
+    to_f64_kernel<<<ceil_div(n3, 256), 256, 0, s>>>(x, xd.p, n3);
+    EB_CHECK_LAUNCH();
+    bool x_zero = dnorm(xd.p, n3, hd.p, part.p, s) == 0.0;   // r0 = b without a matvec
     if (precond) {
         Minv.alloc(9 * B.n);
         tp.alloc(n3);
@@ -477,31 +536,32 @@ int bem_gmres(Bem& B, const int32_t* bc, const float* val, float* x, int m, int 
     }
     // sources grouped per leaf by panel type: each then carries one layer only, and the check
     // potentials run one-kernel pair loops (EBEM_BEM_SPLIT=0: the combined U+P loop)
-    struct SplitGuard {
-        Tree& t;
-        ~SplitGuard() { t.split_mode = 0; }
-    } split_guard{*B.tree};
     const bool split = !(std::getenv("EBEM_BEM_SPLIT") && std::atoi(std::getenv("EBEM_BEM_SPLIT")) == 0);
     if (split) tree_partition_sources(*B.tree, bc, B.nq, s);
-    // right-hand side b = -L(known values): Dirichlet panels carry u (double layer)
-    B.tree->split_mode = split ? 2 : 0;
-    apply_L<double>(B, 1, -1.0, bc, val, b.p, s);
     B.tree->split_mode = split ? 1 : 0;   // A x: Dirichlet panels carry p (single layer)
-    const double bn = dnorm(b.p, n3, hd.p, part.p, s);
-    to_f64_kernel<<<ceil_div(n3, 256), 256, 0, s>>>(x, xd.p, n3);
-    EB_CHECK_LAUNCH();
     // near field from the operator held in HBM (bem_near.cu) when it fits
     const bool use_nm = near_matrix_enabled() && near_matrix_build(*B.tree, B.nq, B.n, bc, B.mat, B.nm, s);
     struct HookGuard {
         Tree& t;
-        ~HookGuard() { t.near_hook = nullptr; }
+        ~HookGuard() {
+            t.near_hook = nullptr;
+            t.near_f64 = false;
+        }
     } hook_guard{*B.tree};
-    auto matvec = [&](const double* v, double* out) {   // out = A v
-        to_f32_kernel<<<ceil_div(n3, 256), 256, 0, s>>>(v, xf.p, n3);
-        EB_CHECK_LAUNCH();
-        if (use_nm) B.tree->near_hook = [&](cudaStream_t st) { near_matrix_apply(*B.tree, B.nm, xf.p, st); };
-        apply_L<double>(B, 0, 1.0, bc, xf.p, out, s);
+    if (use_nm && B.tree->near_sorted_d.n < (size_t)3 * B.tree->ntrg) B.tree->near_sorted_d.alloc(3 * B.tree->ntrg);
+    // out = A v, fp64 in and out: the near operator reads v in fp64 and accumulates in fp64,
+    // the local pass is fp64 and the FMM returns its sum in fp64; only the far field's
+    // sources (the quadrature-point densities) are fp32 (the FMM's own precision)
+    auto matvec = [&](const double* v, double* out) {
+        if (use_nm) {
+            B.tree->near_hook = [&, v](cudaStream_t st) {
+                near_matrix_apply(*B.tree, B.nm, v, B.tree->near_sorted_d.p, st);
+            };
+            B.tree->near_f64 = true;
+        }
+        apply_L<double, double>(B, 0, 1.0, bc, v, out, s, true);
         B.tree->near_hook = nullptr;
+        B.tree->near_f64 = false;
     };
     auto pmatvec = [&](const double* v, double* out) {  // out = A M^-1 v (right preconditioning)
         if (!precond) return matvec(v, out);
@@ -511,14 +571,7 @@ int bem_gmres(Bem& B, const int32_t* bc, const float* val, float* x, int m, int 
     };
     int it = 0;
     double rel = 1.0;
-    if (bn == 0.0) {
-        EB_CUDA(cudaMemsetAsync(x, 0, sizeof(float) * n3, s));
-        if (iters) *iters = 0;
-        if (resid) *resid = 0;
-        return EBEM_OK;
-    }
     std::vector<double> H((size_t)(m + 1) * m), cs(m), sn(m), g(m + 1), h(m + 1), h2(m + 1);
-    bool x_zero = dnorm(xd.p, n3, hd.p, part.p, s) == 0.0;   // r0 = b without a matvec
     while (true) {
         if (x_zero) {
             EB_CUDA(cudaMemcpyAsync(w.p, b.p, sizeof(double) * n3, cudaMemcpyDeviceToDevice, s));
@@ -530,6 +583,8 @@ int bem_gmres(Bem& B, const int32_t* bc, const float* val, float* x, int m, int 
         }
         const double beta = dnorm(w.p, n3, hd.p, part.p, s);
         rel = beta / bn;
+        B.hist_true.push_back(rel);
+        if (trace) std::fprintf(stderr, "[gmres] it %d true residual %.3e\n", it, rel);
         if (rel <= tol || it >= max_iter) break;
         scale_copy<<<ceil_div(n3, 256), 256, 0, s>>>(w.p, 1.0 / beta, V.p, n3);
         EB_CHECK_LAUNCH();
@@ -568,6 +623,8 @@ int bem_gmres(Bem& B, const int32_t* bc, const float* val, float* x, int m, int 
             ++it;
             k = j + 1;
             rel = std::fabs(g[j + 1]) / bn;
+            B.hist_est.push_back(rel);
+            if (trace) std::fprintf(stderr, "[gmres] it %d estimate %.3e\n", it, rel);
             if (rel <= tol || it >= max_iter || hn == 0) break;
         }
         // y = H^-1 g (upper triangular), x += V y
@@ -593,8 +650,30 @@ int bem_gmres(Bem& B, const int32_t* bc, const float* val, float* x, int m, int 
             sub_kernel<<<ceil_div(n3, 256), 256, 0, s>>>(b.p, w.p, n3);
             EB_CHECK_LAUNCH();
             rel = dnorm(w.p, n3, hd.p, part.p, s) / bn;
+            B.hist_true.push_back(rel);
+            if (trace) std::fprintf(stderr, "[gmres] it %d true residual %.3e (final)\n", it, rel);
             break;
         }
+    }
+    if (std::getenv("EBEM_GMRES_PROBE")) {
+        // linearity of the operator as GMRES applies it: |A(x + y) - A x - A y| / |A (x + y)|
+        // for the solution x and a pseudo-random y of the same norm (rounding noise that
+        // bounds the attainable residual)
+        DBuf<double> y(n3), xy(n3), Ax(n3), Ay(n3), Axy(n3);
+        const double xn = dnorm(xd.p, n3, hd.p, part.p, s);
+        hash_fill<<<ceil_div(n3, 256), 256, 0, s>>>(y.p, n3, 1.0);
+        const double yn = dnorm(y.p, n3, hd.p, part.p, s);
+        hash_fill<<<ceil_div(n3, 256), 256, 0, s>>>(y.p, n3, xn / yn);
+        EB_CUDA(cudaMemcpyAsync(xy.p, xd.p, sizeof(double) * n3, cudaMemcpyDeviceToDevice, s));
+        add_kernel<<<ceil_div(n3, 256), 256, 0, s>>>(y.p, xy.p, n3);
+        matvec(xd.p, Ax.p);
+        matvec(y.p, Ay.p);
+        matvec(xy.p, Axy.p);
+        add_kernel<<<ceil_div(n3, 256), 256, 0, s>>>(Ay.p, Ax.p, n3);      // Ax += Ay
+        const double den = dnorm(Axy.p, n3, hd.p, part.p, s);
+        sub_kernel<<<ceil_div(n3, 256), 256, 0, s>>>(Axy.p, Ax.p, n3);     // Ax = Axy - (Ax + Ay)
+        const double num = dnorm(Ax.p, n3, hd.p, part.p, s);
+        std::fprintf(stderr, "[gmres probe] eps_linearity %.3e  |x| %.4e  |b| %.4e\n", num / den, xn, bn);
     }
     to_f32_kernel<<<ceil_div(n3, 256), 256, 0, s>>>(xd.p, x, n3);
     EB_CHECK_LAUNCH();
@@ -602,6 +681,13 @@ int bem_gmres(Bem& B, const int32_t* bc, const float* val, float* x, int m, int 
     if (iters) *iters = it;
     if (resid) *resid = rel;
     return rel <= tol ? EBEM_OK : EBEM_ERR_NOCONV;
+}
+
+int bem_history(const Bem& B, int what, double* buf, int cap) {
+    const std::vector<double>& h = what == 0 ? B.hist_est : B.hist_true;
+    const int n = (int)h.size();
+    for (int i = 0; i < std::min(n, cap); ++i) buf[i] = h[i];
+    return n;
 }
 
 }  // namespace ebem

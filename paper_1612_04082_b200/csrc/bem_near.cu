@@ -163,16 +163,18 @@ constexpr int NM_T = 256, NM_CH = 1024;
 __global__ void __launch_bounds__(NM_T)
 nm_apply(int n_eval, const int* __restrict__ eval_box, const int* __restrict__ tbeg, const int* __restrict__ tend,
          const int* __restrict__ col_first, const int* __restrict__ ncol, const long long* __restrict__ moff,
-         const int* __restrict__ col_panel, const float* __restrict__ M, const float* __restrict__ x,
-         float* __restrict__ near) {
-    __shared__ __align__(16) float xs[3][NM_CH];
+         const int* __restrict__ col_panel, const float* __restrict__ M, const double* __restrict__ x,
+         double* __restrict__ near) {
+    // fp64 densities and fp64 accumulation of the fp32 operator entries: the near field is
+    // then linear in x to fp64 rounding (the kernel is HBM-bound, the FP64 pipe has room)
+    __shared__ __align__(16) double xs[3][NM_CH];
     const int i = blockIdx.x;
     if (i >= n_eval) return;
     const int b = eval_box[i];
     const int rows = tend[b] - tbeg[b], nc = ncol[i], ncp = (nc + 3) & ~3, t0 = tbeg[b];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (nc == 0) {
-        for (int q = threadIdx.x; q < 3 * rows; q += NM_T) near[3 * (int64_t)t0 + q] = 0.f;
+        for (int q = threadIdx.x; q < 3 * rows; q += NM_T) near[3 * (int64_t)t0 + q] = 0.0;
         return;
     }
     const float* base = M + moff[i];
@@ -183,27 +185,27 @@ nm_apply(int n_eval, const int* __restrict__ eval_box, const int* __restrict__ t
         for (int c = threadIdx.x; c < cnt; c += NM_T) {
             const bool in = c0 + c < nc;
             const int p = in ? col_panel[col_first[i] + c0 + c] : 0;
-            xs[0][c] = in ? x[3 * p] : 0.f;
-            xs[1][c] = in ? x[3 * p + 1] : 0.f;
-            xs[2][c] = in ? x[3 * p + 2] : 0.f;
+            xs[0][c] = in ? x[3 * p] : 0.0;
+            xs[1][c] = in ? x[3 * p + 1] : 0.0;
+            xs[2][c] = in ? x[3 * p + 2] : 0.0;
         }
         __syncthreads();
         for (int r = warp; r < rows; r += NM_T / 32) {
             const float* m = base + (int64_t)r * ncp + c0;
-            float acc[3] = {0.f, 0.f, 0.f};
+            double acc[3] = {0.0, 0.0, 0.0};
             for (int c = 4 * lane; c < cnt; c += 128) {
-                const float4 x0 = *reinterpret_cast<const float4*>(&xs[0][c]);
-                const float4 x1 = *reinterpret_cast<const float4*>(&xs[1][c]);
-                const float4 x2 = *reinterpret_cast<const float4*>(&xs[2][c]);
+                const double* x0 = &xs[0][c];
+                const double* x1 = &xs[1][c];
+                const double* x2 = &xs[2][c];
                 float4 v[9];
 #pragma unroll
                 for (int q = 0; q < 9; ++q) v[q] = __ldcs(reinterpret_cast<const float4*>(m + q * plane + c));
 #pragma unroll
                 for (int p = 0; p < 3; ++p) {
                     const float4 a = v[3 * p], bq = v[3 * p + 1], cq = v[3 * p + 2];
-                    acc[p] = fmaf(a.x, x0.x, fmaf(a.y, x0.y, fmaf(a.z, x0.z, fmaf(a.w, x0.w, acc[p]))));
-                    acc[p] = fmaf(bq.x, x1.x, fmaf(bq.y, x1.y, fmaf(bq.z, x1.z, fmaf(bq.w, x1.w, acc[p]))));
-                    acc[p] = fmaf(cq.x, x2.x, fmaf(cq.y, x2.y, fmaf(cq.z, x2.z, fmaf(cq.w, x2.w, acc[p]))));
+                    acc[p] = fma((double)a.x, x0[0], fma((double)a.y, x0[1], fma((double)a.z, x0[2], fma((double)a.w, x0[3], acc[p]))));
+                    acc[p] = fma((double)bq.x, x1[0], fma((double)bq.y, x1[1], fma((double)bq.z, x1[2], fma((double)bq.w, x1[3], acc[p]))));
+                    acc[p] = fma((double)cq.x, x2[0], fma((double)cq.y, x2[1], fma((double)cq.z, x2[2], fma((double)cq.w, x2[3], acc[p]))));
                 }
             }
 #pragma unroll
@@ -211,7 +213,7 @@ nm_apply(int n_eval, const int* __restrict__ eval_box, const int* __restrict__ t
 #pragma unroll
                 for (int o = 16; o > 0; o >>= 1) acc[p] += __shfl_xor_sync(0xffffffffu, acc[p], o);
             if (lane == 0) {
-                float* o = near + 3 * (int64_t)(t0 + r);
+                double* o = near + 3 * (int64_t)(t0 + r);
                 for (int p = 0; p < 3; ++p) o[p] = c0 == 0 ? acc[p] : o[p] + acc[p];
             }
         }
@@ -323,11 +325,11 @@ bool near_matrix_build(const Tree& t, int nq, int64_t npanels, const int32_t* bc
     return true;
 }
 
-void near_matrix_apply(const Tree& t, const NearMat& N, const float* x, cudaStream_t s) {
+void near_matrix_apply(const Tree& t, const NearMat& N, const double* x, double* near, cudaStream_t s) {
     if (t.n_eval == 0) return;
     static const int pad = beside_translation_pad((const void*)nm_apply);
     nm_apply<<<t.n_eval, NM_T, pad, s>>>(t.n_eval, t.eval_box.p, t.tbeg.p, t.tend.p, N.col_first.p, N.ncol.p,
-                                       N.moff.p, N.col_panel.p, N.M.p, x, t.near_sorted.p);
+                                       N.moff.p, N.col_panel.p, N.M.p, x, near);
     EB_CHECK_LAUNCH();
 }
 

@@ -28,7 +28,7 @@ bool near_matrix_enabled();
 // does not fit the memory budget (the near-field kernel is used then)
 bool near_matrix_build(const Tree& t, int nq, int64_t npanels, const int32_t* bc, const Material& m, NearMat& N,
                        cudaStream_t s);
-// t.near_sorted = N x (x: panel vector [npanels x 3], caller order)
-void near_matrix_apply(const Tree& t, const NearMat& N, const float* x, cudaStream_t s);
+// near[sorted target][3] = N x (x: panel vector [npanels x 3], caller order), fp64
+void near_matrix_apply(const Tree& t, const NearMat& N, const double* x, double* near, cudaStream_t s);
 
 }  // namespace ebem

@@ -1,6 +1,7 @@
 // extern "C" boundary of the library (include/elastobem.h).  Argument checking, host
 // staging of host-pointer calls, exception -> error-code translation.  No compute here.
 #include <cstring>
+#include <initializer_list>
 
 #include "../../include/elastobem.h"
 #include "fmm.cuh"
@@ -82,6 +83,17 @@ struct Staged {
     }
 };
 
+// Every non-NULL array argument of one call must be of one kind (include/elastobem.h,
+// "Memory"): a host pointer handed to a kernel would fault and poison the CUDA context, so a
+// mix is rejected up front.  Returns true for device pointers.
+static bool device_args(std::initializer_list<const void*> ptrs) {
+    int ndev = 0, nhost = 0;
+    for (const void* p : ptrs)
+        if (p) ++(is_device_ptr(p) ? ndev : nhost);
+    EB_REQUIRE(ndev == 0 || nhost == 0, "array arguments mix host and device pointers");
+    return ndev > 0;
+}
+
 static void check_material(double K, double G) {
     EB_REQUIRE(K > 0 && G > 0, "material: K and G must be positive");
 }
@@ -131,8 +143,9 @@ extern "C" int bem_kernel_direct(int kernel, const float* trg, int64_t ntrg, con
     cudaStream_t s = (cudaStream_t)stream;
     Material m = make_material(K, G);
     const int nc = kernel_ncomp(kernel);
+    const bool dev = device_args({trg, src, nrm, w, f, g, out});
     if (ntrg == 0) return EBEM_OK;
-    if (is_device_ptr(trg) || is_device_ptr(out)) {
+    if (dev) {
         direct_sum_device(kernel, m, trg, ntrg, src, nrm, w, f, g, nsrc, out, s);
     } else {
         Staged st(s);
@@ -164,7 +177,7 @@ extern "C" int fmm_build_tree(const float* src, const float* nrm, const float* w
     EB_REQUIRE(p >= 3 && p <= 12, "p must be in [3, 12]");
     check_material(K, G);
     cudaStream_t s = (cudaStream_t)stream;
-    const bool dev = is_device_ptr(src) || is_device_ptr(trg);
+    const bool dev = device_args({src, nrm, w, trg});
     Staged st(s);
     const float* dsrc = dev ? src : st.in(src, nsrc * 3);
     const float* dnrm = dev ? nrm : st.in(nrm, nsrc * 3);
@@ -190,7 +203,7 @@ static int fmm_eval_common(ebem_tree* tree, int kernel, const float* f, const fl
     EB_REQUIRE(out != nullptr || t->ntrg == 0, "out required");
     cudaStream_t s = (cudaStream_t)stream;
     const int nc = kernel_ncomp(kernel);
-    if (is_device_ptr(out) || is_device_ptr(f) || is_device_ptr(g)) {
+    if (device_args({f, g, out})) {
         fmm_evaluate(*t, kernel, f, g, out, s);
     } else {
         Staged st(s);
@@ -227,7 +240,7 @@ extern "C" int64_t ebem_launch_count(void) { return launch_count(); }
 extern "C" int fmm_set_profiling(ebem_tree* tree, int on) {
     EB_API_BEGIN
     EB_REQUIRE(tree, "NULL tree");
-    reinterpret_cast<Tree*>(tree)->profile = on != 0;
+    set_profiling(*reinterpret_cast<Tree*>(tree), on);
     return EBEM_OK;
     EB_API_END
 }
@@ -274,7 +287,7 @@ extern "C" int bem_create(const float* vertices, int64_t npanels, int nq, int ma
 extern "C" int bem_apply(ebem_bem* bem, const int32_t* bc_type, const float* x, float* y, void* stream) {
     EB_API_BEGIN
     EB_REQUIRE(bem && bc_type && x && y, "NULL argument");
-    EB_REQUIRE(is_device_ptr(x) && is_device_ptr(y) && is_device_ptr(bc_type), "bem_apply needs device pointers");
+    EB_REQUIRE(device_args({bc_type, x, y}), "bem_apply needs device pointers");
     ebem::bem_apply(*reinterpret_cast<Bem*>(bem), bc_type, x, y, (cudaStream_t)stream);
     return EBEM_OK;
     EB_API_END
@@ -283,7 +296,7 @@ extern "C" int bem_apply(ebem_bem* bem, const int32_t* bc_type, const float* x, 
 extern "C" int bem_rhs(ebem_bem* bem, const int32_t* bc_type, const float* bc_val, float* b, void* stream) {
     EB_API_BEGIN
     EB_REQUIRE(bem && bc_type && bc_val && b, "NULL argument");
-    EB_REQUIRE(is_device_ptr(bc_val) && is_device_ptr(b) && is_device_ptr(bc_type), "bem_rhs needs device pointers");
+    EB_REQUIRE(device_args({bc_type, bc_val, b}), "bem_rhs needs device pointers");
     ebem::bem_rhs(*reinterpret_cast<Bem*>(bem), bc_type, bc_val, b, (cudaStream_t)stream);
     return EBEM_OK;
     EB_API_END
@@ -296,12 +309,18 @@ extern "C" int bem_gmres_solve(ebem_bem* bem, const int32_t* bc_type, const floa
     set_last_error("");
     EB_REQUIRE(bem && bc_type && bc_val && x, "NULL argument");
     EB_REQUIRE(restart >= 1 && restart <= 63 && max_iter >= 1 && tol > 0, "bad GMRES parameters");
-    EB_REQUIRE(is_device_ptr(x) && is_device_ptr(bc_val) && is_device_ptr(bc_type),
-               "bem_gmres_solve needs device pointers");
+    EB_REQUIRE(device_args({bc_type, bc_val, x}), "bem_gmres_solve needs device pointers");
     const int rc = ebem::bem_gmres(*reinterpret_cast<Bem*>(bem), bc_type, bc_val, x, restart, max_iter, tol, iters_out,
                                    resid_out, precond, (cudaStream_t)stream);
     if (rc != EBEM_OK) set_last_error("GMRES did not reach the tolerance");
     return rc;
+    EB_API_END
+}
+
+extern "C" int bem_gmres_history(const ebem_bem* bem, int what, double* buf, int cap) {
+    EB_API_BEGIN
+    EB_REQUIRE(bem && (buf || cap == 0) && cap >= 0 && (what == 0 || what == 1), "bad argument");
+    return bem_history(*reinterpret_cast<const Bem*>(bem), what, buf, cap);
     EB_API_END
 }
 

@@ -166,7 +166,7 @@ __device__ __forceinline__ double far_rinv<double>(double r2) {
 // fp64 far field (p >= 9 and GMRES): the unit equivalent surface is held once per CTA in
 // fp64 shared memory and scaled per box in the inner loop, so a warp stages only its box's
 // densities (3 ne doubles); lane groups as in the fp32 kernel.
-template <bool STRESS, int TPT>
+template <bool STRESS, int TPT, class NT, class OT>
 __device__ __forceinline__ void far_round_f64(int t0, int t_beg, int t_end, int L, int b, int own, int nfar,
                                               const int* __restrict__ widx, int wbeg, const double* __restrict__ PHID,
                                               int l2t, const double* __restrict__ PHIU,
@@ -174,8 +174,8 @@ __device__ __forceinline__ void far_round_f64(int t0, int t_beg, int t_end, int 
                                               const int* __restrict__ level, const BoxGeo& geo,
                                               const double* __restrict__ sse, int ne, const float* __restrict__ trg,
                                               const KConst& kc, double cfar, double* ph, int lane,
-                                              const float* __restrict__ near, const int* __restrict__ trg_perm,
-                                              float* __restrict__ out) {
+                                              const NT* __restrict__ near, const int* __restrict__ trg_perm,
+                                              OT* __restrict__ out) {
     constexpr int NC = STRESS ? 6 : 3;
     const int G = 32 / L, grp = lane / L, l = lane % L;
     int tc[TPT];
@@ -233,9 +233,9 @@ __device__ __forceinline__ void far_round_f64(int t0, int t_beg, int t_end, int 
         for (int j = 0; j < TPT; ++j) {
             const int t = t0 + l + L * j;
             if (t < t_end) {
-                float* o = out + (int64_t)trg_perm[t] * NC;
+                OT* o = out + (int64_t)trg_perm[t] * NC;
 #pragma unroll
-                for (int c = 0; c < NC; ++c) o[c] = (float)(acc[j][c] + (double)near[(int64_t)t * NC + c]);
+                for (int c = 0; c < NC; ++c) o[c] = (OT)(acc[j][c] + (double)near[(int64_t)t * NC + c]);
             }
         }
 }
@@ -381,15 +381,15 @@ __device__ __forceinline__ void far_round_f32(int t0, int t_beg, int t_end, int 
 #ifndef FAR64_TMAX
 #define FAR64_TMAX 4
 #endif
-template <bool STRESS>
+template <bool STRESS, class NT, class OT>
 __global__ void __launch_bounds__(32 * EV_WARPS)
 far_eval_f64_kernel(int n_eval, const int* __restrict__ eval_box, const int* __restrict__ l2t_slot,
                     const double* __restrict__ PHID, const double* __restrict__ PHIU,
                     const int* __restrict__ phiu_slot, const int* __restrict__ woff, const int* __restrict__ widx,
                     const int* __restrict__ tbeg, const int* __restrict__ tend, const int* __restrict__ anchor,
                     const int* __restrict__ level, BoxGeo geo, const double* __restrict__ se, int ne,
-                    const float* __restrict__ trg, KConst kc, double cfar, const float* __restrict__ near,
-                    const int* __restrict__ trg_perm, float* __restrict__ out) {
+                    const float* __restrict__ trg, KConst kc, double cfar, const NT* __restrict__ near,
+                    const int* __restrict__ trg_perm, OT* __restrict__ out) {
     extern __shared__ double dsm[];
     double* sse = dsm;                                      // [3 ne] unit surface (CTA)
     for (int k = threadIdx.x; k < 3 * ne; k += blockDim.x) sse[k] = se[k];
@@ -409,7 +409,8 @@ far_eval_f64_kernel(int n_eval, const int* __restrict__ eval_box, const int* __r
         // Newton/accumulation chains hide the DFMA latency
         const int tpt = STRESS ? lane_groups_max<2>(t_end - t0, L) : lane_groups_max<FAR64_TMAX>(t_end - t0, L);
 #define EB_FAR64(T)                                                                                                  \
-    far_round_f64<STRESS, T>(t0, t_beg, t_end, L, b, own, nfar, widx, woff[b], PHID, l2t, PHIU, phiu_slot, anchor, \
+    far_round_f64<STRESS, T, NT, OT>(t0, t_beg, t_end, L, b, own, nfar, widx, woff[b], PHID, l2t, PHIU, phiu_slot,   \
+                                     anchor, \
                              level, geo, sse, ne, trg, kc, cfar, ph, lane, near, trg_perm, out)
         if (tpt == 1) EB_FAR64(1);
         else if (STRESS || tpt == 2) EB_FAR64(2);
@@ -1184,12 +1185,18 @@ static void launch_far(const Tree& t, float* out, cudaStream_t s) {
     const int grid = ceil_div(t.n_eval, EV_WARPS);
     if (t.far64) {
         const size_t sm = sizeof(double) * 3 * P.ne * (EV_WARPS + 1);
-        auto ffn = far_eval_f64_kernel<STRESS>;
-        if (sm > 48 * 1024) EB_CUDA(cudaFuncSetAttribute(ffn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-        ffn<<<grid, 32 * EV_WARPS, sm, s>>>(t.n_eval, t.eval_box.p, t.eval_l2t_slot.p, t.PHID.p, t.PHIU.p,
-                                            t.phiu_slot.p, t.m2t_off.p, t.m2t_idx.p, t.tbeg.p, t.tend.p,
-                                            t.anchor.p, t.level.p, geo, P.s_e64.p, P.ne, t.trg_xyz.p, kc, cfar,
-                                            t.near_sorted.p, t.trg_perm.p, out);
+        auto go = [&](auto ffn, const auto* near, auto* o) {
+            if (sm > 48 * 1024)
+                EB_CUDA(cudaFuncSetAttribute(ffn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+            ffn<<<grid, 32 * EV_WARPS, sm, s>>>(t.n_eval, t.eval_box.p, t.eval_l2t_slot.p, t.PHID.p, t.PHIU.p,
+                                                t.phiu_slot.p, t.m2t_off.p, t.m2t_idx.p, t.tbeg.p, t.tend.p,
+                                                t.anchor.p, t.level.p, geo, P.s_e64.p, P.ne, t.trg_xyz.p, kc, cfar,
+                                                near, t.trg_perm.p, o);
+        };
+        // (the BEM operator inside GMRES: fp64 near field in, fp64 result out)
+        if (t.out_d && t.near_f64) go(far_eval_f64_kernel<STRESS, double, double>, t.near_sorted_d.p, t.out_d);
+        else if (t.out_d) go(far_eval_f64_kernel<STRESS, float, double>, t.near_sorted.p, t.out_d);
+        else go(far_eval_f64_kernel<STRESS, float, float>, t.near_sorted.p, out);
     } else {
         const size_t sm = sizeof(float4) * 2 * P.ne * EV_WARPS;
         auto ffn = far_eval_f32_kernel<STRESS>;
@@ -1220,7 +1227,7 @@ void fmm_evaluate(Tree& t, int kernel, const float* f, const float* g, float* ou
     EB_REQUIRE(!dl || t.has_normals, "double-layer kernel needs normals at fmm_build_tree");
     if (t.ntrg == 0) return;
     static const bool serial = std::getenv("EBEM_SERIAL") != nullptr;   // diagnostics: one stream
-    const bool conc = !t.profile && !serial;
+    const bool conc = t.profile != 1 && !serial;
     if (conc && !t.sA) {
         int least = 0, greatest = 0;
         EB_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
@@ -1242,17 +1249,48 @@ void fmm_evaluate(Tree& t, int kernel, const float* f, const float* g, float* ou
         EB_CUDA(cudaEventRecord(t.ev_fork, s));
         EB_CUDA(cudaStreamWaitEvent(sa, t.ev_fork, 0));
     }
-    int phase = 0;
-    int64_t l0 = 0;
-    auto mark = [&](int ph) {   // phase boundary: event + launch count of the finished phase
-        const int64_t l = launch_count();
-        if (ph > 0) t.phase_launches[ph - 1] = (int)(l - l0);
-        l0 = l;
-        if (t.profile) EB_CUDA(cudaEventRecord(t.ev[ph], s));
+    // phase brackets: begin / end timing events on the stream a phase is launched on (when
+    // profiling) and the number of kernels its enqueue issued
+    enum { PH_PREP, PH_S2M, PH_Q2Z_UP, PH_M2M, PH_S2L, PH_Q2Z_DN, PH_M2L, PH_L2L, PH_PHI, PH_NEAR, PH_FAR };
+    Tree::ProfSet* ps = nullptr;
+    if (t.profile) {
+        if (t.prof_ring.empty()) {
+            t.prof_ring.resize(Tree::PROF_RING);
+            for (auto& r : t.prof_ring)
+                for (int i = 0; i < Tree::NPHASE; ++i) {
+                    EB_CUDA(cudaEventCreate(&r.b[i]));
+                    EB_CUDA(cudaEventCreate(&r.e[i]));
+                }
+        }
+        ps = &t.prof_ring[t.prof_count % Tree::PROF_RING];
+        for (bool& u : ps->used) u = false;
+        ++t.prof_count;
+    }
+    int64_t lbeg[Tree::NPHASE] = {};
+    for (int& x : t.phase_launches) x = 0;
+    auto pb = [&](int ph, cudaStream_t st) {
+        lbeg[ph] = launch_count();
+        if (ps) {
+            EB_CUDA(cudaEventRecord(ps->b[ph], st));
+            ps->from[ph] = ps->b[ph];
+        }
     };
-    if (t.profile && !t.ev[0])
-        for (auto& e : t.ev) EB_CUDA(cudaEventCreate(&e));
-    mark(phase++);
+    // stream-B phases in situ: a timing event recorded on B ahead of the near-field kernel
+    // delays its start enough that M2L takes the SMs first (measured: matvec 4.4 -> 4.7 ms),
+    // so B records END events only and each B phase is timed from the end of what precedes
+    // it (S2L from the fork point = the end of M2M on stream A, NEAR from the end of S2L)
+    auto pb_after = [&](int ph, int prev) {
+        lbeg[ph] = launch_count();
+        if (ps) ps->from[ph] = ps->e[prev];
+    };
+    auto pe = [&](int ph, cudaStream_t st) {
+        t.phase_launches[ph] += (int)(launch_count() - lbeg[ph]);
+        if (ps) {
+            EB_CUDA(cudaEventRecord(ps->e[ph], st));
+            ps->used[ph] = true;
+        }
+    };
+    pb(PH_PREP, sa);
 
     // prepared sources in tree order (geometry sorted, densities via src_perm)
     prepare_sources(src_kernel, t.mat, t.src_xyz.p, t.src_nrm.p, t.src_w.p, nullptr, f, g, t.src_perm.p, t.nsrc,
@@ -1270,7 +1308,7 @@ void fmm_evaluate(Tree& t, int kernel, const float* f, const float* g, float* ou
         t.Z.zero(sa);
         t.W.zero(sa);
     }
-    mark(phase++);
+    pe(PH_PREP, sa);
 
     auto s2l = [&](cudaStream_t st) {
         if (!t.n_s2l) return;
@@ -1298,15 +1336,20 @@ void fmm_evaluate(Tree& t, int kernel, const float* f, const float* g, float* ou
     auto fork_b = [&]() {
         if (!conc) return;
         EB_CUDA(cudaStreamWaitEvent(sb, t.ev_fork, 0));
+        pb_after(PH_S2L, PH_M2M);
         s2l(sb);
+        pe(PH_S2L, sb);
         EB_CUDA(cudaEventRecord(t.ev_s2l, sb));
         if (trace) EB_CUDA(cudaEventRecord(tev[1], sb));
+        pb_after(PH_NEAR, PH_S2L);
         near(sb);
+        pe(PH_NEAR, sb);
         if (trace) EB_CUDA(cudaEventRecord(tev[2], sb));
         EB_CUDA(cudaEventRecord(t.ev_near, sb));
     };
 
     // upward pass
+    pb(PH_S2M, sa);
     {
         float* qb = t.use_tc ? t.Qb.p : nullptr;
         float* qs = t.use_tc ? t.Qs.p : nullptr;
@@ -1314,18 +1357,20 @@ void fmm_evaluate(Tree& t, int kernel, const float* f, const float* g, float* ou
         else if (sl) launch_check<true, false>(t, t.s2m_box.p, t.n_s2m, nullptr, nullptr, RAD_UC, t.Q.p, qb, qs, sa);
         else launch_check<false, true>(t, t.s2m_box.p, t.n_s2m, nullptr, nullptr, RAD_UC, t.Q.p, qb, qs, sa);
     }
-    mark(phase++);
+    pe(PH_S2M, sa);
     const int lde = P.lde, ldc = P.ldc;
     auto zrows = [&](int l) { return (int64_t)t.up_lstart[l + 1] - t.up_lstart[l]; };
     auto wrows = [&](int l) { return (int64_t)t.dn_lstart[l + 1] - t.dn_lstart[l]; };
     if (conc) EB_CUDA(cudaStreamWaitEvent(sa, t.ev_zz, 0));
+    pb(PH_Q2Z_UP, sa);
     if (t.use_tc) {
         if (t.ml_fast) tc_pairs_gemm_fast(t.q2z_up, P.mQu1T_b, P.mQu1T_s, t.Qb.p, t.Qs.p, ldc, me, mc, t.Z.p, lde, false, sa);
         else tc_pairs_gemm(t.q2z_up, P.mQu1T_b, P.mQu1T_s, t.mQb, t.mQs, me, mc, t.Z.p, lde, sa);
     } else {
         gemm_pairs_f32(t.q2z_up, P.Qu1T.p, me, mc, ldc, t.Q.p, ldc, t.Z.p, lde, sa);
     }
-    mark(phase++);
+    pe(PH_Q2Z_UP, sa);
+    pb(PH_M2M, sa);
     for (int l = t.nlevels - 2; l >= 2; --l) {
         if (t.use_tc) {
             tc_split_rows(t.Z.p, lde, t.up_lstart[l + 1], zrows(l + 1), me, t.Zb.p, t.Zs.p, sa);
@@ -1336,14 +1381,17 @@ void fmm_evaluate(Tree& t, int kernel, const float* f, const float* g, float* ou
         }
     }
     if (t.use_tc && t.nlevels > 2) tc_split_rows(t.Z.p, lde, t.up_lstart[2], zrows(2), me, t.Zb.p, t.Zs.p, sa);
-    mark(phase++);
+    pe(PH_M2M, sa);
 
     // downward pass (stream B forks here: started together with the upward pass it only
     // competed with the other FP32-bound kernels, measured no faster)
     if (conc) EB_CUDA(cudaEventRecord(t.ev_fork, sa));
     fork_b();
-    if (!conc) s2l(sa);
-    mark(phase++);
+    if (!conc) {
+        pb(PH_S2L, sa);
+        s2l(sa);
+        pe(PH_S2L, sa);
+    }
     auto q2z_dn = [&]() {
         if (!t.n_s2l) return;
         if (t.use_tc) {
@@ -1353,27 +1401,35 @@ void fmm_evaluate(Tree& t, int kernel, const float* f, const float* g, float* ou
             gemm_pairs_f32(t.q2z_dn, P.Qd1T.p, me, mc, ldc, t.Qd.p, ldc, t.W.p, lde, sa);
         }
     };
-    if (!conc) q2z_dn();
-    mark(phase++);
+    if (!conc) {
+        pb(PH_Q2Z_DN, sa);
+        q2z_dn();
+        pe(PH_Q2Z_DN, sa);
+    }
     if (trace) EB_CUDA(cudaEventRecord(tev[3], sa));
     // a timestamp on stream A just before M2L: measured to let the near-field CTAs (padded to
     // two per SM beside a translation CTA, beside_translation_pad) take their slots first,
-    // 4.67 -> 4.48 ms per matvec; a timing-disabled event does not have the effect
+    // 4.67 -> 4.48 ms per matvec; a timing-disabled event does not have the effect (when
+    // profiling, the phase's own begin event is that timestamp)
     if (conc) {
         EB_CUDA(cudaStreamWaitEvent(sa, t.ev_wz, 0));
-        EB_CUDA(cudaEventRecord(t.ev_m2l, sa));
+        if (!ps) EB_CUDA(cudaEventRecord(t.ev_m2l, sa));
     }
+    pb(PH_M2L, sa);
     if (t.use_tc && t.tc_fast) tc_pairs_gemm_fast(t.m2l, P.mM2L_b, P.mM2L_s, t.Zb.p, t.Zs.p, lde, me, me, t.W.p, lde, false, sa);
     else if (t.use_tc && m2l_drain_fast())   // precise accumulation, two-slice fast-kernel data flow
         tc_pairs_gemm_fast(t.m2l, P.mM2L_b, P.mM2L_s, t.Zb.p, t.Zs.p, lde, me, me, t.W.p, lde, true, sa);
     else if (t.use_tc) tc_pairs_gemm(t.m2l, P.mM2L_b, P.mM2L_s, t.mZb, t.mZs, me, me, t.W.p, lde, sa);
     else gemm_pairs_f32(t.m2l, P.M2L.p, me, me, lde, t.Z.p, lde, t.W.p, lde, sa);
+    pe(PH_M2L, sa);
     if (trace) EB_CUDA(cudaEventRecord(tev[4], sa));
     if (conc) {
         EB_CUDA(cudaStreamWaitEvent(sa, t.ev_s2l, 0));
+        pb(PH_Q2Z_DN, sa);
         q2z_dn();
+        pe(PH_Q2Z_DN, sa);
     }
-    mark(phase++);
+    pb(PH_L2L, sa);
     for (int l = 3; l < t.nlevels; ++l) {
         if (t.use_tc) {
             tc_split_rows(t.W.p, lde, t.dn_lstart[l - 1], wrows(l - 1), me, t.Wb.p, t.Ws.p, sa);
@@ -1383,7 +1439,8 @@ void fmm_evaluate(Tree& t, int kernel, const float* f, const float* g, float* ou
             gemm_pairs_f32(t.l2l[l], P.L2L.p, me, me, lde, t.W.p, lde, t.W.p, lde, sa);
         }
     }
-    mark(phase++);
+    pe(PH_L2L, sa);
+    pb(PH_PHI, sa);
 
     // equivalent densities (fp64) and leaf evaluation
     if (t.far64) {
@@ -1396,20 +1453,24 @@ void fmm_evaluate(Tree& t, int kernel, const float* f, const float* g, float* ou
         gemm_pairs_f64_to_f32(t.phiu_pairs, P.Ruinv.p, me, me, t.Z.p, lde, t.phiu_scale.p, cfar, t.PHIUF.p, P.ne,
                               sa);
     }
-    mark(phase++);
+    pe(PH_PHI, sa);
     if (trace) EB_CUDA(cudaEventRecord(tev[5], sa));
-    if (conc) EB_CUDA(cudaStreamWaitEvent(sa, t.ev_near, 0));
-    else near(sa);
+    if (conc) {
+        EB_CUDA(cudaStreamWaitEvent(sa, t.ev_near, 0));
+    } else {
+        pb(PH_NEAR, sa);
+        near(sa);
+        pe(PH_NEAR, sa);
+    }
     if (trace) EB_CUDA(cudaEventRecord(tev[6], sa));
-    mark(phase++);
+    pb(PH_FAR, sa);
     if (stress) launch_far<true>(t, out, sa);
     else launch_far<false>(t, out, sa);
+    pe(PH_FAR, sa);
     if (conc) {
         EB_CUDA(cudaEventRecord(t.ev_joinA, sa));
         EB_CUDA(cudaStreamWaitEvent(s, t.ev_joinA, 0));
     }
-    mark(phase++);
-    t.ev_valid = t.profile;
     if (trace && conc) {
         EB_CUDA(cudaEventRecord(tev[7], sa));
         EB_CUDA(cudaEventSynchronize(tev[7]));
@@ -1479,12 +1540,22 @@ int phase_stats(Tree& t, int kernel, ebem_phase_stat* out, int cap) {
     st[10].flops = (t.w_l2t_inter + t.w_m2t_inter) * flops_per_pair(stress ? K_D : K_U);
     st[10].flops_fp64 = t.far64 ? st[10].flops : 0;
     st[10].bytes = t.ntrg * (12.0 + 4.0 * (stress ? 6 : 3) * 2) + (t.far64 ? 8.0 : 16.0 / 3.0) * me * (t.n_phid + t.n_phiu);
-    if (t.ev_valid) {
-        EB_CUDA(cudaEventSynchronize(t.ev[Tree::NPHASE]));
+    // mean device time over the evaluations recorded since profiling was switched on
+    const int nrec = std::min(t.prof_count, (int)Tree::PROF_RING);
+    if (nrec > 0) {
+        EB_CUDA(cudaDeviceSynchronize());
         for (int i = 0; i < Tree::NPHASE; ++i) {
-            float ms = 0;
-            EB_CUDA(cudaEventElapsedTime(&ms, t.ev[i], t.ev[i + 1]));
-            st[i].ms = ms;
+            double sum = 0;
+            int n = 0;
+            for (int k = 0; k < nrec; ++k) {
+                const Tree::ProfSet& r = t.prof_ring[k];
+                if (!r.used[i]) continue;
+                float ms = 0;
+                EB_CUDA(cudaEventElapsedTime(&ms, r.from[i], r.e[i]));
+                sum += ms;
+                ++n;
+            }
+            st[i].ms = n ? sum / n : 0.0;
         }
     }
     const int n = std::min(cap, (int)Tree::NPHASE);
@@ -1492,5 +1563,11 @@ int phase_stats(Tree& t, int kernel, ebem_phase_stat* out, int cap) {
     return Tree::NPHASE;
 }
 
+
+void set_profiling(Tree& t, int mode) {
+    EB_REQUIRE(mode >= 0 && mode <= 2, "profiling mode must be 0, 1 or 2");
+    t.profile = mode;
+    t.prof_count = 0;
+}
 
 }  // namespace ebem

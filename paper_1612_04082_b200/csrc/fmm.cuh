@@ -123,11 +123,20 @@ struct Tree {
     bool tc_fast = false;                // p <= 8 plain matvec: two-slice full-K tensor-core kernel
     bool ml_fast = false;                // Q2Z / M2M / L2L on the fast kernel too
 
-    // profiling (fmm_set_profiling / fmm_phase_stats)
-    static constexpr int NPHASE = 11;
-    bool profile = false;
-    cudaEvent_t ev[NPHASE + 1] = {};
-    bool ev_valid = false;
+    // profiling (fmm_set_profiling / fmm_phase_stats): 0 off; 1 phases one after another on
+    // the caller's stream (solo times); 2 in situ: the normal two-stream schedule, each phase
+    // bracketed by timing events on the stream it is launched on.  Every profiled evaluation
+    // records into the next of PROF_RING event sets; fmm_phase_stats averages the sets
+    // recorded since profiling was switched on (at most the last PROF_RING).
+    static constexpr int NPHASE = 11, PROF_RING = 64;
+    int profile = 0;
+    struct ProfSet {
+        cudaEvent_t b[NPHASE] = {}, e[NPHASE] = {};
+        cudaEvent_t from[NPHASE] = {};   // the event a phase's time is measured from
+        bool used[NPHASE] = {};
+    };
+    std::vector<ProfSet> prof_ring;
+    int prof_count = 0;                  // evaluations recorded since fmm_set_profiling
     int phase_launches[NPHASE] = {};
     // algorithmic work counts (schedule time)
     double w_s2m_inter = 0, w_s2l_inter = 0, w_p2p_inter = 0, w_l2t_inter = 0, w_m2t_inter = 0;
@@ -135,8 +144,11 @@ struct Tree {
     int64_t w_m2m_pairs = 0, w_l2l_pairs = 0;
     int w_m2l_ops = 0;
     ~Tree() {
-        for (auto& e : ev)
-            if (e) cudaEventDestroy(e);
+        for (auto& ps : prof_ring)
+            for (int i = 0; i < NPHASE; ++i) {
+                if (ps.b[i]) cudaEventDestroy(ps.b[i]);
+                if (ps.e[i]) cudaEventDestroy(ps.e[i]);
+            }
         for (cudaEvent_t e : {ev_fork, ev_s2l, ev_near, ev_joinA, ev_m2l, ev_zz, ev_wz})
             if (e) cudaEventDestroy(e);
         if (sA) cudaStreamDestroy(sA);
@@ -153,6 +165,12 @@ struct Tree {
     DBuf<double> PHID, PHIU;             // [n_phid x me], [n_phiu x me] (fp64 far field)
     DBuf<float4> PHIDF, PHIUF;           // [n_phid x ne], [n_phiu x ne] (fp32 far field, scaled)
     DBuf<float> near_sorted;             // [ntrg x 6] near field, sorted target order
+    // BEM operator inside GMRES (bem.cu): the near hook writes the near field in fp64 to
+    // near_sorted_d (near_f64), and the fp64 far field writes its sum to out_d instead of the
+    // float output, so the Krylov vectors meet no fp32 rounding outside the FMM's far field
+    DBuf<double> near_sorted_d;
+    bool near_f64 = false;
+    double* out_d = nullptr;
     std::function<void(cudaStream_t)> near_hook;   // replaces the near-field kernel (BEM near operator)
     DBuf<int> ssplit;                    // BEM: per leaf, first source of the second boundary-condition group
     int split_mode = 0;                  // 0 off; 1: [sbeg, ssplit) single layer, rest double layer; 2 reverse
@@ -172,6 +190,7 @@ void fmm_evaluate(Tree& t, int kernel, const float* f, const float* g, float* ou
 void tree_info(const Tree& t, ebem_tree_info* info);
 int64_t tree_export(const Tree& t, int what, void* buf, int64_t cap);
 int phase_stats(Tree& t, int kernel, ebem_phase_stat* out, int cap);
+void set_profiling(Tree& t, int mode);
 struct Bem;
 Bem* bem_create(const float* verts, int64_t n, int nq, int max_pts, int p, const Material& m, cudaStream_t s);
 void bem_free(Bem* B);
@@ -179,6 +198,7 @@ void bem_apply(Bem& B, const int32_t* bc, const float* x, float* y, cudaStream_t
 void bem_rhs(Bem& B, const int32_t* bc, const float* val, float* b, cudaStream_t s);
 int bem_gmres(Bem& B, const int32_t* bc, const float* val, float* x, int m, int max_iter, double tol,
               int32_t* iters, double* resid, int precond, cudaStream_t s);
+int bem_history(const Bem& B, int what, double* buf, int cap);
 
 // ------------------------------------------------------------------ primitives (linalg.cu)
 // exclusive scan of n ints (out may alias in); returns the total on the host (syncs)

@@ -9,6 +9,7 @@
 // [K; a I] = Q R (classical Gram-Schmidt with one full re-orthogonalisation, fp64), so
 // the Tikhonov pseudo-inverse is R^-1 Q_1^T (Q_1 = first 3 n_c rows of Q).
 #include <cmath>
+#include <cstdlib>
 
 #include "elastic.cuh"
 #include "fmm.cuh"
@@ -247,6 +248,7 @@ static std::shared_ptr<Plan> make_plan(int p, const Material& m, cudaStream_t s)
     P->pc = p + 1;
     P->mat = m;
     P->rcond = std::max(1e-9, std::pow(10.0, -(p + 1)));
+    if (const char* e = std::getenv("EBEM_RCOND")) P->rcond = std::atof(e);   // diagnostics (A/B of reading R6)
     std::vector<double> se = surface_grid(p), sc = surface_grid(P->pc);
     P->ne = (int)se.size() / 3;
     P->nc = (int)sc.size() / 3;

@@ -49,7 +49,10 @@ def test_operator_and_rhs_match_dense_oracle(eb, nq):
     assert KN.rel_l2(bg, b) < 1e-5
 
 
-def test_gmres_matches_dense_solve_and_patch_test(eb):
+@pytest.mark.parametrize("precond", [0, 1])
+def test_gmres_matches_dense_solve_and_patch_test(eb, precond):
+    """the paper's GMRES (precond = 0) and the block-Jacobi right-preconditioned one
+    (precond = 1, the same residual |b - A x| / |b|) against dense LU of the oracle system."""
     verts, c, n, a, bc, val, uex, tex, V = _problem(4)
     V0, V1, V2 = (verts[:, k].astype(np.float64) for k in range(3))
     c64, n64, a64 = geo.panels(V0, V1, V2)
@@ -59,8 +62,10 @@ def test_gmres_matches_dense_solve_and_patch_test(eb):
     op = eb.bem_create(torch.from_numpy(verts).cuda(), nq=16, max_pts=32, p=8, K=KB, G=G)
     x = torch.zeros((len(bc), 3), device="cuda")
     x, it, res = eb.bem_gmres_solve(op, torch.from_numpy(bc).cuda(), torch.from_numpy(val.astype(np.float32)).cuda(),
-                                    x, restart=50, max_iter=300, tol=1e-6)
-    print("GMRES iterations", it, "residual", res)
+                                    x, restart=50, max_iter=300, tol=1e-6, precond=precond)
+    print("GMRES precond", precond, "iterations", it, "residual", res)
+    est, true = eb.bem_gmres_history(op)
+    assert len(est) == it and est[-1] <= 1e-6 and true[0] == 1.0
     assert res <= 1e-6 and 0 < it < 300
     xs = x.cpu().numpy().astype(np.float64)
     assert KN.rel_l2(xs.reshape(-1), xref) < 1e-4
@@ -71,8 +76,54 @@ def test_gmres_matches_dense_solve_and_patch_test(eb):
     x2 = torch.zeros_like(x)
     x2, it2, res2 = eb.bem_gmres_solve(op, torch.from_numpy(bc).cuda(),
                                        torch.from_numpy(val.astype(np.float32)).cuda(), x2, restart=5, max_iter=3,
-                                       tol=1e-6, check=False)
+                                       tol=1e-6, precond=precond, check=False)
     assert it2 == 3 and res2 > 1e-6
+    # a warm start (nonzero initial guess: the dense solution perturbed by 1%) takes the
+    # r0 = b - A x0 branch and reaches the same solution
+    rng = np.random.default_rng(3)
+    x0 = (xref.reshape(-1, 3) * (1 + 0.01 * rng.standard_normal((len(bc), 3)))).astype(np.float32)
+    x3 = torch.from_numpy(x0).cuda()
+    x3, it3, res3 = eb.bem_gmres_solve(op, torch.from_numpy(bc).cuda(),
+                                       torch.from_numpy(val.astype(np.float32)).cuda(), x3, restart=50,
+                                       max_iter=300, tol=1e-6, precond=precond)
+    est3, true3 = eb.bem_gmres_history(op)
+    print("warm start: iterations", it3, "first true residual", true3[0])
+    assert res3 <= 1e-6 and 1e-6 < true3[0] < 1.0
+    assert KN.rel_l2(x3.cpu().numpy().reshape(-1).astype(np.float64), xref) < 1e-4
+
+
+def test_gmres_solver_setting_of_configs4_matches_dense_oracle(eb):
+    """configs[4]'s solver setting -- block-Jacobi right preconditioner, tol 1e-6 (so the
+    full-chain tensor-core M2L), the near operator held in HBM, sources grouped per leaf by
+    panel type, p = 8 -- on a small voided cell (unit cube 6 x 6 cells per face + two
+    icosphere voids: 1024 panels, 16384 quadrature sources) with 64 sources per leaf, so the
+    tree has several levels and every list kind, against dense LU of the oracle's system
+    (PAPER.md Eqs. num, num2; l. 181 GMRES, l. 187 16-point quadrature)."""
+    d = geo.metamaterial_cell(nc=6, level=1, nvoids=2, seed=5)
+    verts = d["verts"]
+    V0, V1, V2 = (verts[:, k].astype(np.float64) for k in range(3))
+    c64, n64, a64 = geo.panels(V0, V1, V2)
+    U, P = OB.assemble(c64, n64, a64, V0, V1, V2, d["K"], d["G"], nq=16)
+    A, b = OB.mixed_system(U, P, d["bc_type"], d["bc_val"])
+    xref = np.linalg.solve(A, b)
+    op = eb.bem_create(torch.from_numpy(verts).cuda(), nq=16, max_pts=64, p=8, K=d["K"], G=d["G"])
+    bc, val = torch.from_numpy(d["bc_type"]).cuda(), torch.from_numpy(d["bc_val"]).cuda()
+    # the operator itself (bem_apply) and the right-hand side against the dense system
+    rng = np.random.default_rng(2)
+    xr = rng.standard_normal(A.shape[0]).astype(np.float32)
+    y = eb.bem_apply(op, bc, torch.from_numpy(xr).cuda().view(-1, 3)).cpu().numpy().reshape(-1)
+    assert KN.rel_l2(y, A @ xr.astype(np.float64)) < 1e-5
+    bg = eb.bem_rhs(op, bc, val).cpu().numpy().reshape(-1)
+    assert KN.rel_l2(bg, b) < 1e-5
+    x = torch.zeros((verts.shape[0], 3), device="cuda")
+    x, it, res = eb.bem_gmres_solve(op, bc, val, x, restart=50, max_iter=400, tol=1e-6, precond=1)
+    err = KN.rel_l2(x.cpu().numpy().reshape(-1).astype(np.float64), xref)
+    print("voided cell: iterations", it, "residual", res, "solution rel-L2 vs dense LU", err,
+          "cond", np.linalg.cond(A))
+    assert res <= 1e-6 and err < 1e-4
+    # true residual of the returned solution against the oracle's own matrix
+    xs = x.cpu().numpy().reshape(-1).astype(np.float64)
+    assert np.linalg.norm(b - A @ xs) / np.linalg.norm(b) < 1e-4
 
 
 def test_near_operator_matches_near_kernel(eb, monkeypatch):

@@ -8,7 +8,7 @@ from oracle import cdirect
 from oracle import kernels as KN
 from oracle import tree as OT
 from workloads import geometry as geo
-from tests.gpu_util import csr_lists, need_gpu, torch
+from tests.gpu_util import assert_fmm_close, csr_lists, need_gpu, torch
 
 pytestmark = pytest.mark.gpu
 
@@ -33,7 +33,7 @@ def _fmm_vs_direct(eb, src, trg, nrm, w, f, g, kern, p=6, s=16, tol=1e-4):
     if np.linalg.norm(ref) == 0:
         assert np.abs(out).max() == 0
     else:
-        assert KN.rel_l2(out, ref) < tol
+        assert_fmm_close(out, ref, tol)
     return tree
 
 

@@ -8,7 +8,7 @@ from oracle import kernels as KN
 from oracle import kifmm as OF
 from oracle import tree as OT
 from workloads import geometry as geo
-from tests.gpu_util import csr_lists, need_gpu, to_dev, torch
+from tests.gpu_util import assert_fmm_close, csr_lists, need_gpu, per_target_error, to_dev, torch
 
 pytestmark = pytest.mark.gpu
 
@@ -63,15 +63,16 @@ def beam20k():
 def test_fmm_matvec_converges_in_p(eb, beam20k):
     d, ref = beam20k
     t = to_dev(d)
-    errs = {}
+    errs, worst = {}, {}
     for p in (4, 6, 8, 10):
         tree = eb.fmm_build_tree(t["src"], t["nrm"], t["w"], max_pts=64, p=p, K=d["K"], G=d["G"])
         out = eb.fmm_matvec(tree, eb.KERNEL_UP, t["f"], t["g"])
-        errs[p] = KN.rel_l2(out.cpu().numpy().astype(np.float64), ref)
-    print("fmm rel-L2 by p:", errs)
+        errs[p], worst[p] = per_target_error(out.cpu().numpy(), ref)
+    print("fmm rel-L2 by p:", errs, "worst target:", worst)
     assert errs[4] > errs[6] > errs[8] > errs[10]
-    assert errs[6] <= 1e-4
-    assert errs[10] <= 1e-6
+    assert worst[4] > worst[6] > worst[8] > worst[10]
+    assert errs[6] <= 1e-4 and worst[6] <= 1e-3
+    assert errs[10] <= 1e-6 and worst[10] <= 1e-5
 
 
 def test_fmm_matches_reference_tree_code(eb, monkeypatch):
@@ -87,11 +88,14 @@ def test_fmm_matches_reference_tree_code(eb, monkeypatch):
     monkeypatch.setenv("EBEM_XW_DIRECT", "0")
     tree = eb.fmm_build_tree(t["src"], t["nrm"], t["w"], max_pts=32, p=6, K=d["K"], G=d["G"])
     out = eb.fmm_matvec(tree, eb.KERNEL_UP, t["f"], t["g"]).cpu().numpy().astype(np.float64)
-    assert KN.rel_l2(out, ref) <= 1e-5
+    assert_fmm_close(out, ref, 1e-5, label="GPU vs oracle KIFMM p=6")
     monkeypatch.delenv("EBEM_XW_DIRECT")
     tree = eb.fmm_build_tree(t["src"], t["nrm"], t["w"], max_pts=32, p=6, K=d["K"], G=d["G"])
     out2 = eb.fmm_matvec(tree, eb.KERNEL_UP, t["f"], t["g"]).cpu().numpy().astype(np.float64)
-    assert KN.rel_l2(out2, exact) <= 1.05 * KN.rel_l2(ref, exact)
+    rel_o, worst_o = per_target_error(ref, exact)
+    rel_g, worst_g = per_target_error(out2, exact)
+    print("vs exact: oracle KIFMM", rel_o, worst_o, " GPU (direct X/W/V)", rel_g, worst_g)
+    assert rel_g <= 1.05 * rel_o and worst_g <= 1.5 * worst_o
 
 
 @pytest.mark.parametrize("kern", [0, 1, 3, 4, 5])
@@ -102,9 +106,7 @@ def test_fmm_kernels_and_separate_targets(eb, kern):
     fn = eb.fmm_eval_stress if kern >= 3 else eb.fmm_matvec
     out = fn(tree, kern, t["f"], t["g"]).cpu().numpy().astype(np.float64)
     ref = cdirect.direct_sum(kern, d["trg"], d["src"], d["K"], d["G"], w=d["w"], f=d["f"], g=d["g"], nrm=d["nrm"])
-    err = KN.rel_l2(out, ref)
-    print("kernel", kern, "rel-L2", err)
-    assert err <= 1e-5
+    assert_fmm_close(out, ref, 1e-5, label=f"kernel {kern} p=8")
 
 
 def test_fmm_deterministic(eb, beam20k):

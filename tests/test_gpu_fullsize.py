@@ -9,7 +9,7 @@ from oracle import cdirect
 from oracle import kernels as KN
 from oracle import tree as OT
 from workloads import geometry as geo
-from tests.gpu_util import csr_lists, need_gpu, to_dev, torch
+from tests.gpu_util import csr_lists, need_gpu, per_target_error, to_dev, torch
 
 pytestmark = pytest.mark.gpu
 
@@ -27,7 +27,7 @@ def _sampled_err(eb, d, tree, kern, idx, stress=False):
     out = fn(tree, kern, t["f"], t["g"]).cpu().numpy().astype(np.float64)
     trg = d.get("trg", d["src"])
     ref = cdirect.direct_sum(kern, trg[idx], d["src"], d["K"], d["G"], w=d["w"], f=d["f"], g=d["g"], nrm=d["nrm"])
-    return KN.rel_l2(out[idx], ref)
+    return per_target_error(out[idx], ref)      # (rel-L2, worst sampled target)
 
 
 @pytest.fixture(scope="module")
@@ -58,10 +58,10 @@ def test_config2_p6_and_p10(eb, beam200k):
     for p in (6, 10):
         tree = eb.fmm_build_tree(t["src"], t["nrm"], t["w"], max_pts=64, p=p, K=d["K"], G=d["G"])
         errs[p] = _sampled_err(eb, d, tree, KN.KERNEL_UP, idx)
-    print("configs[2] sampled rel-L2:", errs)
-    assert errs[6] <= 1e-4
-    assert errs[10] <= 1e-6
-    assert errs[10] < errs[6]
+    print("configs[2] sampled (rel-L2, worst target):", errs)
+    assert errs[6][0] <= 1e-4 and errs[6][1] <= 1e-3
+    assert errs[10][0] <= 1e-6 and errs[10][1] <= 1e-5
+    assert errs[10][0] < errs[6][0]
 
 
 def test_bench_workload_1m(eb):
@@ -70,9 +70,9 @@ def test_bench_workload_1m(eb):
     t = to_dev(d)
     tree = eb.fmm_build_tree(t["src"], t["nrm"], t["w"], max_pts=64, p=6, K=d["K"], G=d["G"])
     idx = np.sort(np.random.default_rng(22).choice(d["src"].shape[0], 800, replace=False))
-    err = _sampled_err(eb, d, tree, KN.KERNEL_UP, idx)
-    print("1M beam p=6 sampled rel-L2:", err)
-    assert err <= 1e-4
+    err, worst = _sampled_err(eb, d, tree, KN.KERNEL_UP, idx)
+    print("1M beam p=6 sampled rel-L2:", err, "worst target:", worst)
+    assert err <= 1e-4 and worst <= 1e-3
 
 
 def test_config3_stress_full(eb):
@@ -81,9 +81,9 @@ def test_config3_stress_full(eb):
     t = to_dev(d)
     tree = eb.fmm_build_tree(t["src"], t["nrm"], t["w"], trg=t["trg"], max_pts=256, p=8, K=d["K"], G=d["G"])
     idx = np.sort(np.random.default_rng(23).choice(d["trg"].shape[0], 400, replace=False))
-    err = _sampled_err(eb, d, tree, KN.KERNEL_DS, idx, stress=True)
-    print("configs[3] sampled rel-L2:", err)
-    assert err <= 1e-5
+    err, worst = _sampled_err(eb, d, tree, KN.KERNEL_DS, idx, stress=True)
+    print("configs[3] sampled rel-L2:", err, "worst target:", worst)
+    assert err <= 1e-5 and worst <= 1e-4
 
 
 def test_config4_gmres_full(eb):
