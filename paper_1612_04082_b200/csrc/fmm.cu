@@ -573,6 +573,139 @@ near_eval_kernel(int n_eval, const int* __restrict__ eval_box, const int* __rest
     }
 }
 
+// near field, version 2: the leaf's near sources as MERGED contiguous ranges of the sorted
+// source array (neighbouring boxes are mostly adjacent in Morton order, so ~27 boxes of ~24
+// sources collapse into a few long runs and the 32-source tiles are full), staged per warp by
+// cp.async into a double buffer: the next tile is in flight while the current one is summed.
+// A range flagged `safe` contains the target leaf's own sources (the only place where r = 0
+// can occur, reading R8) and uses the r = 0-excluding pair loop.
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
+                 "l"(src)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+template <bool SL, bool DL, bool STRESS, int TPT>
+__device__ __forceinline__ void near_round2(int t0, int t_beg, int t_end, int L, int e0, int e1,
+                                            const int2* __restrict__ rng, const float* __restrict__ trg,
+                                            const float4* __restrict__ rec, const KConst& kc,
+                                            float* __restrict__ near, float4* buf, int lane) {
+    constexpr int NC = STRESS ? 6 : 3;
+    constexpr int R = STRESS ? REC_STRESS : REC_DISP;
+    constexpr int RS = R + 1;
+    constexpr int TILE = NEAR_TILE;
+    const int G = 32 / L, grp = lane / L, l = lane % L;
+    float x[TPT], y[TPT], z[TPT], acc[TPT][NC];
+#pragma unroll
+    for (int j = 0; j < TPT; ++j) {
+        const int t = t0 + l + L * j;
+        const int tc = t < t_end ? t : t_beg;
+        x[j] = trg[3 * tc];
+        y[j] = trg[3 * tc + 1];
+        z[j] = trg[3 * tc + 2];
+#pragma unroll
+        for (int c = 0; c < NC; ++c) acc[j][c] = 0.f;
+    }
+    auto issue = [&](float4* dst, int s, int cnt) {
+        const float4* src = rec + (int64_t)s * R;
+        for (int q = lane; q < cnt * R; q += 32) cp_async16(dst + (q / R) * RS + q % R, src + q);
+        cp_async_commit();
+    };
+    int e = e0, s = 0, rend = 0;
+    bool safe = false;
+    if (e < e1) {
+        const int2 r = rng[e];
+        s = r.x;
+        rend = r.y & 0x7fffffff;
+        safe = r.y < 0;
+    }
+    int cnt = e < e1 ? min(TILE, rend - s) : 0;
+    int b = 0;
+    if (cnt) issue(buf, s, cnt);
+    while (cnt > 0) {
+        int ns = s + cnt, ncnt = 0;
+        bool nsafe = safe;
+        if (ns >= rend) {
+            if (++e < e1) {
+                const int2 r = rng[e];
+                ns = r.x;
+                rend = r.y & 0x7fffffff;
+                nsafe = r.y < 0;
+                ncnt = min(TILE, rend - ns);
+            }
+        } else {
+            ncnt = min(TILE, rend - ns);
+        }
+        if (ncnt) {
+            issue(buf + (b ^ 1) * TILE * RS, ns, ncnt);
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
+        }
+        __syncwarp();
+        const float4* cur = buf + b * TILE * RS;
+        if (safe) pair_loop_strided<SL, DL, STRESS, TPT, RS, true>(cur, cnt, grp, G, x, y, z, kc, acc);
+        else pair_loop_strided<SL, DL, STRESS, TPT, RS, false>(cur, cnt, grp, G, x, y, z, kc, acc);
+        __syncwarp();                  // the buffer is refilled two tiles later
+        s = ns;
+        safe = nsafe;
+        cnt = ncnt;
+        b ^= 1;
+    }
+    reduce_groups<NC, TPT>(acc, L);
+    if (grp == 0)
+#pragma unroll
+        for (int j = 0; j < TPT; ++j) {
+            const int t = t0 + l + L * j;
+            if (t < t_end)
+#pragma unroll
+                for (int c = 0; c < NC; ++c)   // acc_DS accumulates half of the diagonal
+                    near[(int64_t)t * NC + c] = (STRESS && SL && DL && c < 3) ? 2.f * acc[j][c] : acc[j][c];
+        }
+}
+
+template <bool SL, bool DL, bool STRESS>
+__global__ void __launch_bounds__(32 * EV_WARPS)
+near_eval2_kernel(int n_eval, const int* __restrict__ eval_box, const int* __restrict__ roff,
+                  const int2* __restrict__ rng, const int* __restrict__ tbeg, const int* __restrict__ tend,
+                  const float* __restrict__ trg, const float4* __restrict__ rec, KConst kc, float* __restrict__ near) {
+    constexpr int R = STRESS ? REC_STRESS : REC_DISP;
+    __shared__ __align__(16) float4 buf_all[EV_WARPS][2 * NEAR_TILE * (R + 1)];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int i = blockIdx.x * EV_WARPS + warp;
+    if (i >= n_eval) return;
+    float4* buf = buf_all[warp];
+    const int b = eval_box[i];
+    const int t_beg = tbeg[b], t_end = tend[b];
+    const int e0 = roff[b], e1 = roff[b + 1];
+    for (int t0 = t_beg; t0 < t_end;) {
+        int L;
+#define EB_NEAR2(T) near_round2<SL, DL, STRESS, T>(t0, t_beg, t_end, L, e0, e1, rng, trg, rec, kc, near, buf, lane)
+        if constexpr (STRESS) {
+            const int tpt = lane_groups_max<NEAR_TMAX_STRESS>(t_end - t0, L);
+            if (tpt == 1) EB_NEAR2(1);
+#if NEAR_TMAX_STRESS >= 3
+            else if (tpt == 3) EB_NEAR2(3);
+#endif
+            else EB_NEAR2(2);
+            t0 += L * tpt;
+        } else {
+            const int tpt = lane_groups(t_end - t0, L);
+            switch (tpt) {
+                case 1: EB_NEAR2(1); break;
+                case 2: EB_NEAR2(2); break;
+                case 3: EB_NEAR2(3); break;
+                default: EB_NEAR2(4); break;
+            }
+            t0 += L * tpt;
+        }
+#undef EB_NEAR2
+    }
+}
+
 // precise M2L (p >= 9, GMRES) on the two-slice fast-kernel data flow with drained groups;
 // EBEM_M2L_DRAIN=0 selects the one-slice precise kernel instead
 static bool m2l_drain_fast() {
@@ -701,7 +834,7 @@ void schedule_tree(Tree& t, cudaStream_t s) {
     };
     std::vector<int> level = dl(t.level, nb), parent = dl(t.parent, nb), child = dl(t.child, 8 * (size_t)nb),
                      leaf = dl(t.is_leaf, nb), nsub = dl(t.nsrc_sub, nb), tsub = dl(t.ntrg_sub, nb),
-                     anchor = dl(t.anchor, 3 * (size_t)nb);
+                     anchor = dl(t.anchor, 3 * (size_t)nb), hsb = dl(t.sbeg, nb), hse = dl(t.send, nb);
     std::vector<int> off[4], idx[4];
     for (int k = 0; k < 4; ++k) {
         off[k] = dl(t.lst_off[k], nb + 1);
@@ -865,6 +998,31 @@ void schedule_tree(Tree& t, cudaStream_t s) {
     h2d(t.near_off.p, noff.data(), nb + 1, s);
     t.near_idx.alloc(std::max<size_t>(nidx.size(), 1));
     h2d(t.near_idx.p, nidx.data(), nidx.size(), s);
+    // merged source ranges of every near list (near_eval2_kernel)
+    {
+        std::vector<int> roff(nb + 1, 0);
+        std::vector<int2> rng, tmp;
+        for (int b = 0; b < nb; ++b) {
+            tmp.clear();
+            for (int e = noff[b]; e < noff[b + 1]; ++e) {
+                const int a = nidx[e];
+                if (hse[a] > hsb[a]) tmp.push_back(make_int2(hsb[a], hse[a]));
+            }
+            std::sort(tmp.begin(), tmp.end(), [](int2 u, int2 v) { return u.x < v.x; });
+            const size_t first = rng.size();
+            for (const int2& r : tmp) {
+                if (rng.size() > first && rng.back().y == r.x) rng.back().y = r.y;
+                else rng.push_back(r);
+            }
+            for (size_t k = first; k < rng.size(); ++k)
+                if (hse[b] > hsb[b] && rng[k].x <= hsb[b] && hsb[b] < rng[k].y) rng[k].y |= (int)0x80000000u;
+            roff[b + 1] = (int)rng.size();
+        }
+        t.near_roff.alloc(nb + 1);
+        h2d(t.near_roff.p, roff.data(), nb + 1, s);
+        t.near_rng.alloc(std::max<size_t>(rng.size(), 1));
+        h2d(t.near_rng.p, rng.data(), rng.size(), s);
+    }
     t.m2t_off.alloc(nb + 1);
     h2d(t.m2t_off.p, moff.data(), nb + 1, s);
     t.m2t_idx.alloc(std::max<size_t>(midx.size(), 1));
@@ -1167,10 +1325,26 @@ static void launch_near(const Tree& t, cudaStream_t s) {
                                      100));
         carve = true;
     }
-    static const int pad = beside_translation_pad((const void*)near_eval_kernel<SL, DL, STRESS>);
-    near_eval_kernel<SL, DL, STRESS><<<ceil_div(t.n_eval, EV_WARPS), 32 * EV_WARPS, pad, s>>>(
-        t.n_eval, t.eval_box.p, t.near_off.p, t.near_idx.p, t.sbeg.p, t.send.p, t.tbeg.p, t.tend.p, t.trg_xyz.p,
-        STRESS ? t.rec_stress.p : t.rec_disp.p, kc, t.near_sorted.p);
+    // near_eval2_kernel (merged ranges, cp.async double buffer) is 3.5% faster alone but made
+    // the overlapped matvec slower (4.41 -> 4.56 ms): the default stays the per-box kernel
+    static const bool v1 = !(std::getenv("EBEM_NEAR_V2") && std::atoi(std::getenv("EBEM_NEAR_V2")));
+    if (v1) {
+        static const int pad = beside_translation_pad((const void*)near_eval_kernel<SL, DL, STRESS>);
+        near_eval_kernel<SL, DL, STRESS><<<ceil_div(t.n_eval, EV_WARPS), 32 * EV_WARPS, pad, s>>>(
+            t.n_eval, t.eval_box.p, t.near_off.p, t.near_idx.p, t.sbeg.p, t.send.p, t.tbeg.p, t.tend.p, t.trg_xyz.p,
+            STRESS ? t.rec_stress.p : t.rec_disp.p, kc, t.near_sorted.p);
+    } else {
+        static bool carve2 = false;
+        if (!carve2) {
+            EB_CUDA(cudaFuncSetAttribute(near_eval2_kernel<SL, DL, STRESS>,
+                                         cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+            carve2 = true;
+        }
+        static const int pad = beside_translation_pad((const void*)near_eval2_kernel<SL, DL, STRESS>);
+        near_eval2_kernel<SL, DL, STRESS><<<ceil_div(t.n_eval, EV_WARPS), 32 * EV_WARPS, pad, s>>>(
+            t.n_eval, t.eval_box.p, t.near_roff.p, t.near_rng.p, t.tbeg.p, t.tend.p, t.trg_xyz.p,
+            STRESS ? t.rec_stress.p : t.rec_disp.p, kc, t.near_sorted.p);
+    }
     EB_CHECK_LAUNCH();
 }
 
@@ -1268,24 +1442,27 @@ void fmm_evaluate(Tree& t, int kernel, const float* f, const float* g, float* ou
     }
     int64_t lbeg[Tree::NPHASE] = {};
     for (int& x : t.phase_launches) x = 0;
+    // In situ (mode 2) only M2L and the near field are timed, with events placed exactly where
+    // the unprofiled schedule has them: M2L's begin event is the timestamp the schedule records
+    // before M2L anyway (see below), its end event follows it on stream A, and the near
+    // field's end event follows it on stream B.  Any further timing event ahead of the fork
+    // shifted which of the two kernels takes the SMs first (measured: 4.41 -> 4.73 ms).
+    const bool insitu = ps && conc;
+    auto timed = [&](int ph) { return ps && (!insitu || ph == PH_M2L || ph == PH_NEAR); };
     auto pb = [&](int ph, cudaStream_t st) {
         lbeg[ph] = launch_count();
-        if (ps) {
+        if (timed(ph)) {
             EB_CUDA(cudaEventRecord(ps->b[ph], st));
             ps->from[ph] = ps->b[ph];
         }
     };
-    // stream-B phases in situ: a timing event recorded on B ahead of the near-field kernel
-    // delays its start enough that M2L takes the SMs first (measured: matvec 4.4 -> 4.7 ms),
-    // so B records END events only and each B phase is timed from the end of what precedes
-    // it (S2L from the fork point = the end of M2M on stream A, NEAR from the end of S2L)
-    auto pb_after = [&](int ph, int prev) {
-        lbeg[ph] = launch_count();
-        if (ps) ps->from[ph] = ps->e[prev];
-    };
+    // stream-B phases in situ: no event ahead of the near-field kernel; NEAR is timed from
+    // M2L's begin event (both start at the fork) to its own end event and includes S2L
+    auto pb_after = [&](int ph) { lbeg[ph] = launch_count(); };
+    auto pe_count = [&](int ph) { t.phase_launches[ph] += (int)(launch_count() - lbeg[ph]); };
     auto pe = [&](int ph, cudaStream_t st) {
         t.phase_launches[ph] += (int)(launch_count() - lbeg[ph]);
-        if (ps) {
+        if (timed(ph)) {
             EB_CUDA(cudaEventRecord(ps->e[ph], st));
             ps->used[ph] = true;
         }
@@ -1336,12 +1513,13 @@ void fmm_evaluate(Tree& t, int kernel, const float* f, const float* g, float* ou
     auto fork_b = [&]() {
         if (!conc) return;
         EB_CUDA(cudaStreamWaitEvent(sb, t.ev_fork, 0));
-        pb_after(PH_S2L, PH_M2M);
+        pb_after(PH_S2L);
         s2l(sb);
-        pe(PH_S2L, sb);
+        pe_count(PH_S2L);
         EB_CUDA(cudaEventRecord(t.ev_s2l, sb));
         if (trace) EB_CUDA(cudaEventRecord(tev[1], sb));
-        pb_after(PH_NEAR, PH_S2L);
+        pb_after(PH_NEAR);
+        if (ps) ps->from[PH_NEAR] = ps->b[PH_M2L];   // recorded on A right after the fork
         near(sb);
         pe(PH_NEAR, sb);
         if (trace) EB_CUDA(cudaEventRecord(tev[2], sb));
@@ -1555,7 +1733,7 @@ int phase_stats(Tree& t, int kernel, ebem_phase_stat* out, int cap) {
                 sum += ms;
                 ++n;
             }
-            st[i].ms = n ? sum / n : 0.0;
+            st[i].ms = n ? sum / n : -1.0;     // -1: not timed (S2L in situ: inside NEAR)
         }
     }
     const int n = std::min(cap, (int)Tree::NPHASE);

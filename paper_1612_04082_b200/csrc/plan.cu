@@ -11,6 +11,8 @@
 #include <cmath>
 #include <cstdlib>
 
+#include <cooperative_groups.h>
+
 #include "elastic.cuh"
 #include "fmm.cuh"
 
@@ -64,111 +66,155 @@ static void kmat(const Plan& P, const DBuf<double>& sx, int nx, double xs, const
 }
 
 // ------------------------------------------------------------------ CGS2 QR
-__global__ void cgs_dots(const double* __restrict__ Q, int m, const double* __restrict__ v, double* __restrict__ r) {
-    const int k = blockIdx.x;
-    __shared__ double sh[256];
-    double s = 0.0;
-    for (int i = threadIdx.x; i < m; i += 256) s += Q[(int64_t)k * m + i] * v[i];
-    sh[threadIdx.x] = s;
+// One cooperative kernel for the whole factorisation (grid-wide barriers between the steps of
+// each column): a launch per step and column took ~3 n launches (≈ 1500 at p = 4, 4400 at
+// p = 10) -- one-time work, but it filled every launch list with plan kernels.
+// Column j: v = a_j; two passes of r = Q_{<j}^T v, v -= Q_{<j} r, R_{<j, j} += r (classical
+// Gram-Schmidt with one full re-orthogonalisation); R_jj = |v|, q_j = v / R_jj.  Every
+// reduction has a fixed order (deterministic).
+namespace cg = cooperative_groups;
+
+constexpr int PT = 256;
+
+__device__ __forceinline__ double block_sum(double x, double* sh) {
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
     __syncthreads();
-    for (int o = 128; o > 0; o >>= 1) {
-        if (threadIdx.x < o) sh[threadIdx.x] += sh[threadIdx.x + o];
-        __syncthreads();
-    }
-    if (threadIdx.x == 0) r[k] = sh[0];
+    if (l == 0) sh[w] = x;
+    __syncthreads();
+    double t = 0.0;
+    for (int k = 0; k < PT / 32; ++k) t += sh[k];
+    return t;
 }
 
-__global__ void cgs_update(const double* __restrict__ Q, int m, int j, const double* __restrict__ r,
-                           double* __restrict__ v, double* __restrict__ Rcol) {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < m) {
-        double s = 0.0;
-        for (int k = 0; k < j; ++k) s += Q[(int64_t)k * m + i] * r[k];
-        v[i] -= s;
+__global__ void __launch_bounds__(PT)
+cgs2_coop(double* __restrict__ Q, int m, int n, double* __restrict__ R, double* __restrict__ v,
+          double* __restrict__ r, double* __restrict__ part) {
+    cg::grid_group grid = cg::this_grid();
+    __shared__ double sh[PT / 32];
+    const int64_t gt = (int64_t)blockIdx.x * PT + threadIdx.x, gs = (int64_t)gridDim.x * PT;
+    for (int j = 0; j < n; ++j) {
+        for (int64_t i = gt; i < m; i += gs) v[i] = Q[(int64_t)j * m + i];
+        grid.sync();
+        for (int pass = 0; pass < 2 && j > 0; ++pass) {
+            for (int k = blockIdx.x; k < j; k += gridDim.x) {          // r_k = q_k . v
+                double x = 0.0;
+                for (int i = threadIdx.x; i < m; i += PT) x += Q[(int64_t)k * m + i] * v[i];
+                x = block_sum(x, sh);
+                if (threadIdx.x == 0) r[k] = x;
+            }
+            grid.sync();
+            for (int64_t i = gt; i < m; i += gs) {                    // v -= Q r
+                double x = 0.0;
+                for (int k = 0; k < j; ++k) x += Q[(int64_t)k * m + i] * r[k];
+                v[i] -= x;
+            }
+            for (int64_t k = gt; k < j; k += gs) R[(int64_t)j * n + k] += r[k];
+            grid.sync();
+        }
+        double x = 0.0;                                                // |v|^2, block partials
+        for (int64_t i = gt; i < m; i += gs) x += v[i] * v[i];
+        x = block_sum(x, sh);
+        if (threadIdx.x == 0) part[blockIdx.x] = x;
+        grid.sync();
+        double nn = 0.0;
+        for (int b = 0; b < (int)gridDim.x; ++b) nn += part[b];
+        const double nrm = sqrt(nn);
+        for (int64_t i = gt; i < m; i += gs) Q[(int64_t)j * m + i] = v[i] / nrm;
+        if (gt == 0) R[(int64_t)j * n + j] = nrm;
+        grid.sync();
     }
-    if (i < j) Rcol[i] += r[i];
 }
 
-__global__ void cgs_finish(double* __restrict__ Q, int m, int j, const double* __restrict__ v,
-                           double* __restrict__ Rjj) {
-    __shared__ double sh[256];
-    double s = 0.0;
-    for (int i = threadIdx.x; i < m; i += 256) s += v[i] * v[i];
-    sh[threadIdx.x] = s;
-    __syncthreads();
-    for (int o = 128; o > 0; o >>= 1) {
-        if (threadIdx.x < o) sh[threadIdx.x] += sh[threadIdx.x + o];
-        __syncthreads();
-    }
-    const double nrm = sqrt(sh[0]);
-    for (int i = threadIdx.x; i < m; i += 256) Q[(int64_t)j * m + i] = v[i] / nrm;
-    if (threadIdx.x == 0) *Rjj = nrm;
+static int coop_grid(const void* fn) {
+    int per = 0;
+    EB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, PT, 0));
+    return std::max(1, std::min(per, 2)) * num_sms();
 }
 
 // A (m x n) column-major in Q on entry; on exit Q has orthonormal columns and R (n x n,
 // column-major, upper) satisfies A = Q R.
 static void cgs2_qr(double* Q, int m, int n, double* R, cudaStream_t s) {
-    DBuf<double> v(m), r(n);
+    const int grid = coop_grid((const void*)cgs2_coop);
+    DBuf<double> v(m), r(n), part(grid);
     EB_CUDA(cudaMemsetAsync(R, 0, sizeof(double) * n * n, s));
-    for (int j = 0; j < n; ++j) {
-        d2d(v.p, Q + (int64_t)j * m, m, s);
-        for (int pass = 0; pass < 2 && j > 0; ++pass) {
-            cgs_dots<<<j, 256, 0, s>>>(Q, m, v.p, r.p);
-            cgs_update<<<ceil_div(std::max(m, j), 256), 256, 0, s>>>(Q, m, j, r.p, v.p, R + (int64_t)j * n);
-        }
-        cgs_finish<<<1, 256, 0, s>>>(Q, m, j, v.p, R + (int64_t)j * n + j);
-    }
+    void* args[] = {&Q, &m, &n, &R, &v.p, &r.p, &part.p};
+    EB_CUDA(cudaLaunchCooperativeKernel((const void*)cgs2_coop, grid, PT, args, 0, s));
     EB_CHECK_LAUNCH();
+    EB_CUDA(cudaStreamSynchronize(s));
 }
 
-// X = R^-1 (both n x n; R column-major upper, X row-major upper), row i from the bottom:
-// X[i, :] = (e_i - sum_{k>i} R[i,k] X[k, :]) / R[i,i]
-__global__ void trinv_row(const double* __restrict__ R, int n, int i, double* __restrict__ X) {
-    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+// X = R^-1 (both n x n; R column-major upper, X row-major upper): a warp per column j of X,
+// back substitution X[i, j] = (delta_ij - sum_{i<k<=j} R[i,k] X[k, j]) / R[i,i] from i = j
+// down to 0, the column kept in shared memory (one launch for all columns)
+constexpr int TI_W = 4;
+__global__ void __launch_bounds__(32 * TI_W)
+trinv_cols(const double* __restrict__ R, int n, double* __restrict__ X) {
+    extern __shared__ double col_all[];
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    const int j = blockIdx.x * TI_W + w;
     if (j >= n) return;
-    double s = (i == j) ? 1.0 : 0.0;
-    for (int k = i + 1; k <= j; ++k) s -= R[(int64_t)k * n + i] * X[(int64_t)k * n + j];
-    X[(int64_t)i * n + j] = (j < i) ? 0.0 : s / R[(int64_t)i * n + i];
+    double* col = col_all + (size_t)w * n;
+    for (int i = j; i >= 0; --i) {
+        double x = 0.0;
+        for (int k = i + 1 + l; k <= j; k += 32) x += R[(int64_t)k * n + i] * col[k];
+        for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+        if (l == 0) col[i] = ((i == j ? 1.0 : 0.0) - x) / R[(int64_t)i * n + i];
+        __syncwarp();
+    }
+    for (int i = l; i < n; i += 32) X[(int64_t)i * n + j] = i <= j ? col[i] : 0.0;
 }
 
-__global__ void power_step(const double* __restrict__ K, int m, int n, const double* __restrict__ v,
-                           double* __restrict__ t) {
-    // t = K v  (K row-major m x n)
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= m) return;
-    double s = 0.0;
-    for (int j = 0; j < n; ++j) s += K[(int64_t)i * n + j] * v[j];
-    t[i] = s;
-}
-__global__ void power_stepT(const double* __restrict__ K, int m, int n, const double* __restrict__ t,
-                            double* __restrict__ v) {
-    const int j = blockIdx.x * blockDim.x + threadIdx.x;
-    if (j >= n) return;
-    double s = 0.0;
-    for (int i = 0; i < m; ++i) s += K[(int64_t)i * n + j] * t[i];
-    v[j] = s;
-}
-
-// largest singular value of K (row-major m x n) by 60 power iterations on K^T K
-static double sigma_max(const double* K, int m, int n, cudaStream_t s) {
-    DBuf<double> v(n), t(m);
-    std::vector<double> hv(n, 1.0 / std::sqrt((double)n));
-    h2d(v.p, hv.data(), n, s);
-    double sig = 0;
+// largest singular value of K (row-major m x n): 60 power iterations on K^T K in one
+// cooperative launch (v <- K^T K v / |K^T K v|, sigma = sqrt|K^T K v| at the end)
+__global__ void __launch_bounds__(PT)
+power_coop(const double* __restrict__ K, int m, int n, double* __restrict__ v, double* __restrict__ t,
+           double* __restrict__ part, double* __restrict__ sig) {
+    cg::grid_group grid = cg::this_grid();
+    __shared__ double sh[PT / 32];
+    const int64_t gt = (int64_t)blockIdx.x * PT + threadIdx.x, gs = (int64_t)gridDim.x * PT;
+    for (int64_t j = gt; j < n; j += gs) v[j] = 1.0 / sqrt((double)n);
+    grid.sync();
+    double nrm = 1.0;
     for (int it = 0; it < 60; ++it) {
-        power_step<<<ceil_div(m, 256), 256, 0, s>>>(K, m, n, v.p, t.p);
-        power_stepT<<<ceil_div(n, 256), 256, 0, s>>>(K, m, n, t.p, v.p);
-        d2h(hv.data(), v.p, n, s);
-        EB_CUDA(cudaStreamSynchronize(s));
-        double nn = 0;
-        for (double x : hv) nn += x * x;
-        nn = std::sqrt(nn);
-        sig = std::sqrt(nn);
-        for (double& x : hv) x /= nn;
-        h2d(v.p, hv.data(), n, s);
+        for (int64_t i = gt; i < m; i += gs) {            // t = K v
+            double x = 0.0;
+            for (int j = 0; j < n; ++j) x += K[i * n + j] * v[j];
+            t[i] = x;
+        }
+        grid.sync();
+        double ss = 0.0;
+        for (int64_t j = gt; j < n; j += gs) {            // w = K^T t (into v after the norm)
+            double x = 0.0;
+            for (int i = 0; i < m; ++i) x += K[(int64_t)i * n + j] * t[i];
+            ss += x * x;
+        }
+        ss = block_sum(ss, sh);
+        if (threadIdx.x == 0) part[blockIdx.x] = ss;
+        grid.sync();
+        double nn = 0.0;
+        for (int b = 0; b < (int)gridDim.x; ++b) nn += part[b];
+        nrm = sqrt(nn);
+        for (int64_t j = gt; j < n; j += gs) {
+            double x = 0.0;
+            for (int i = 0; i < m; ++i) x += K[(int64_t)i * n + j] * t[i];
+            v[j] = x / nrm;
+        }
+        grid.sync();
     }
+    if (gt == 0) *sig = sqrt(nrm);
+}
+
+static double sigma_max(const double* K, int m, int n, cudaStream_t s) {
+    const int grid = coop_grid((const void*)power_coop);
+    DBuf<double> v(n), t(m), part(grid), sig(1);
+    void* args[] = {&K, &m, &n, &v.p, &t.p, &part.p, &sig.p};
+    EB_CUDA(cudaLaunchCooperativeKernel((const void*)power_coop, grid, PT, args, 0, s));
     EB_CHECK_LAUNCH();
-    return sig;
+    double h = 0;
+    d2h(&h, sig.p, 1, s);
+    EB_CUDA(cudaStreamSynchronize(s));
+    return h;
 }
 
 __global__ void build_aug(const double* __restrict__ K, int mc, int me, double alpha, double* __restrict__ A) {
@@ -214,7 +260,9 @@ static void factor_solve(const Plan& P, const DBuf<double>& sc, double rc, const
     EB_CHECK_LAUNCH();
     cgs2_qr(Q.p, m, me, R.p, s);
     Rinv.alloc((size_t)me * me);
-    for (int i = me - 1; i >= 0; --i) trinv_row<<<ceil_div(me, 256), 256, 0, s>>>(R.p, me, i, Rinv.p);
+    const size_t tsm = sizeof(double) * me * TI_W;
+    if (tsm > 48 * 1024) EB_CUDA(cudaFuncSetAttribute(trinv_cols, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm));
+    trinv_cols<<<ceil_div(me, TI_W), 32 * TI_W, tsm, s>>>(R.p, me, Rinv.p);
     EB_CHECK_LAUNCH();
     Q1T.alloc((size_t)me * mc);
     extract_q1t<<<ceil_div((int64_t)me * mc, 256), 256, 0, s>>>(Q.p, m, mc, me, Q1T.p);
@@ -228,7 +276,10 @@ static void composites(const Plan& P, const DBuf<double>& Q1T, const DBuf<double
                        const std::vector<double>& yo, double scale, float* out, cudaStream_t s) {
     const int mc = P.mc, me = P.me;
     const int nb = (int)xo.size() / 3;
-    const int chunk = 16;
+    // operators per batch: as many as ~2 GB of fp64 scratch allows (all 316 M2L operators in one
+    // batch up to p = 7, a handful of batches at p = 10)
+    const double per = 8.0 * (2.0 * mc * me + (double)me * me);
+    const int chunk = std::max(1, std::min(nb, (int)(2e9 / per)));
     DBuf<double> K((size_t)chunk * mc * me), T((size_t)chunk * mc * me), C((size_t)chunk * me * me);
     for (int b0 = 0; b0 < nb; b0 += chunk) {
         const int nbc = std::min(chunk, nb - b0);

@@ -109,6 +109,23 @@ def test_fmm_kernels_and_separate_targets(eb, kern):
     assert_fmm_close(out, ref, 1e-5, label=f"kernel {kern} p=8")
 
 
+def test_build_launch_count(eb):
+    """a first build at a new order (translation operators computed: cooperative QR, power
+    iteration and triangular inverse, batched composites) plus the tree and its lists stays
+    within a few hundred kernel launches, so the hot kernels of a following evaluation appear
+    early in any launch list."""
+    d = geo.config2(n=4000, seed=5)
+    t = to_dev(d)
+    l0 = eb.ebem_launch_count()
+    tree = eb.fmm_build_tree(t["src"], t["nrm"], t["w"], max_pts=64, p=5, K=1.3, G=0.6)
+    n = eb.ebem_launch_count() - l0
+    print("launches for a first p = 5 build:", n)
+    assert n < 300
+    l0 = eb.ebem_launch_count()
+    eb.fmm_matvec(tree, eb.KERNEL_UP, t["f"], t["g"])
+    assert eb.ebem_launch_count() - l0 < 60
+
+
 def test_fmm_deterministic(eb, beam20k):
     """fp64 accumulation of the translation outputs makes repeated evaluations identical
     (GMRES needs a consistent operator)."""
