@@ -63,6 +63,7 @@ struct Bem {
     DBuf<float> f, g, y;    // expanded densities [n nq x 3], FMM output [n x 3]
     DBuf<double> yd;        // FMM output in fp64 (the operator inside GMRES)
     NearMat nm;             // near-field operator of the last solve's boundary conditions
+    PanelOp s2m_op, s2l_op; // check-potential operators (S2M of the source leaves, S2L of the X lists)
     // residual history of the last bem_gmres_solve (bem_gmres_history): the Arnoldi estimate
     // |g_{j+1}| / |b| after every iteration, and the true |b - A x| / |b| at every restart
     std::vector<double> hist_est, hist_true;
@@ -256,10 +257,12 @@ __global__ void local_kernel(int mode, double sign, const int32_t* __restrict__ 
 // L(u, p) of the panel vector x.  y64: the FMM result in fp64 (B.yd; GMRES), else fp32 (B.y)
 template <class XT, class T>
 static void apply_L(Bem& B, int mode, double sign, const int32_t* bc, const XT* x, T* out, cudaStream_t s,
-                    bool y64 = false) {
+                    bool y64 = false, bool expand = true) {
     const int64_t n = B.n;
-    expand_kernel<XT><<<ceil_div(n * B.nq, 256), 256, 0, s>>>(mode, bc, x, n, B.nq, B.f.p, B.g.p);
-    EB_CHECK_LAUNCH();
+    if (expand) {   // (not needed when stored operators replace every pass over the quadrature points)
+        expand_kernel<XT><<<ceil_div(n * B.nq, 256), 256, 0, s>>>(mode, bc, x, n, B.nq, B.f.p, B.g.p);
+        EB_CHECK_LAUNCH();
+    }
     static const bool prof = std::getenv("EBEM_BEM_PROFILE") != nullptr;   // diagnostics: phase times to stderr
     if (prof) set_profiling(*B.tree, 1);
     if (y64) {
@@ -539,29 +542,44 @@ int bem_gmres(Bem& B, const int32_t* bc, const float* val, float* x, int m, int 
     const bool split = !(std::getenv("EBEM_BEM_SPLIT") && std::atoi(std::getenv("EBEM_BEM_SPLIT")) == 0);
     if (split) tree_partition_sources(*B.tree, bc, B.nq, s);
     B.tree->split_mode = split ? 1 : 0;   // A x: Dirichlet panels carry p (single layer)
-    // near field from the operator held in HBM (bem_near.cu) when it fits
-    const bool use_nm = near_matrix_enabled() && near_matrix_build(*B.tree, B.nq, B.n, bc, B.mat, B.nm, s);
+    // near field, and the S2M / S2L check potentials, from operators held in HBM (bem_near.cu)
+    // when they fit (built in that order: the near operator saves the most per byte)
+    Tree& T = *B.tree;
+    const bool use_nm = near_matrix_enabled() && near_matrix_build(T, B.nq, B.n, bc, B.mat, B.nm, s);
+    const bool use_cm = use_nm && T.use_tc && check_matrix_enabled() &&
+                        panel_op_build(T, PanelOp::S2M, B.nq, B.n, bc, B.mat, B.s2m_op, s);
+    const bool use_cl = use_cm && (T.n_s2l == 0 || panel_op_build(T, PanelOp::S2L, B.nq, B.n, bc, B.mat, B.s2l_op, s));
     struct HookGuard {
         Tree& t;
         ~HookGuard() {
-            t.near_hook = nullptr;
+            t.near_hook = t.s2m_hook = t.s2l_hook = nullptr;
             t.near_f64 = false;
+            t.force_serial = false;
         }
-    } hook_guard{*B.tree};
+    } hook_guard{T};
+    // one stream inside the solve: the HBM-bound near operator beside the tensor-core M2L was
+    // slower than the two back to back (configs[4]: 82 vs 77.5 ms per iteration)
+    T.force_serial = !(std::getenv("EBEM_BEM_CONC") && std::atoi(std::getenv("EBEM_BEM_CONC")));
     if (use_nm && B.tree->near_sorted_d.n < (size_t)3 * B.tree->ntrg) B.tree->near_sorted_d.alloc(3 * B.tree->ntrg);
     // out = A v, fp64 in and out: the near operator reads v in fp64 and accumulates in fp64,
     // the local pass is fp64 and the FMM returns its sum in fp64; only the far field's
     // sources (the quadrature-point densities) are fp32 (the FMM's own precision)
     auto matvec = [&](const double* v, double* out) {
         if (use_nm) {
-            B.tree->near_hook = [&, v](cudaStream_t st) {
-                near_matrix_apply(*B.tree, B.nm, v, B.tree->near_sorted_d.p, st);
-            };
-            B.tree->near_f64 = true;
+            T.near_hook = [&, v](cudaStream_t st) { near_matrix_apply(T, B.nm, v, T.near_sorted_d.p, st); };
+            T.near_f64 = true;
         }
-        apply_L<double, double>(B, 0, 1.0, bc, v, out, s, true);
-        B.tree->near_hook = nullptr;
-        B.tree->near_f64 = false;
+        if (use_cm)
+            T.s2m_hook = [&, v](cudaStream_t st) {
+                panel_op_apply(T, B.s2m_op, v, nullptr, T.Qb.p, T.Qs.p, T.plan->ldc, st);
+            };
+        if (use_cl && T.n_s2l)
+            T.s2l_hook = [&, v](cudaStream_t st) {
+                panel_op_apply(T, B.s2l_op, v, nullptr, T.Qdb.p, T.Qds.p, T.plan->ldc, st);
+            };
+        apply_L<double, double>(B, 0, 1.0, bc, v, out, s, true, !(use_nm && use_cl));
+        T.near_hook = T.s2m_hook = T.s2l_hook = nullptr;
+        T.near_f64 = false;
     };
     auto pmatvec = [&](const double* v, double* out) {  // out = A M^-1 v (right preconditioning)
         if (!precond) return matvec(v, out);

@@ -1125,11 +1125,14 @@ void schedule_tree(Tree& t, cudaStream_t s) {
         // 0.17 ms faster, error 2.907e-5 -> 2.912e-5; at p = 8 the error grew 1.9e-6 -> 2.7e-6)
         static const int ml_fast_pmax = std::getenv("EBEM_ML_FAST") ? std::atoi(std::getenv("EBEM_ML_FAST")) : 6;
         t.ml_fast = t.tc_fast && P.p <= ml_fast_pmax;
-        tc_build_tiles(t.q2z_up, me, mc, t.ml_fast);
-        tc_build_tiles(t.q2z_dn, me, mc, t.ml_fast);
-        tc_build_tiles(t.m2l, me, me, t.tc_fast || m2l_drain_fast());
-        for (auto& x : t.m2m) tc_build_tiles(x, me, me, t.ml_fast);
-        for (auto& x : t.l2l) tc_build_tiles(x, me, me, t.ml_fast);
+        // tile shapes: the full-chain kernels take wide tiles (tc_fast_tile_mode), the drained
+        // M2L two-slice tiles, the one-slice precise kernel 128 x 128
+        const int fm = tc_fast_tile_mode();
+        tc_build_tiles(t.q2z_up, me, mc, t.ml_fast ? fm : 0);
+        tc_build_tiles(t.q2z_dn, me, mc, t.ml_fast ? fm : 0);
+        tc_build_tiles(t.m2l, me, me, t.tc_fast ? fm : (m2l_drain_fast() ? 1 : 0));
+        for (auto& x : t.m2m) tc_build_tiles(x, me, me, t.ml_fast ? fm : 0);
+        for (auto& x : t.l2l) tc_build_tiles(x, me, me, t.ml_fast ? fm : 0);
     }
     if (t.far64) {
         t.PHID.alloc((size_t)std::max(1, t.n_phid) * me);
@@ -1292,7 +1295,7 @@ void tree_m2l_fast(Tree& t, bool fast, cudaStream_t s) {
     fast = fast && t.use_tc && P.p < FAR_FP64_MIN_P;
     if (fast == t.tc_fast) return;
     t.tc_fast = fast;
-    tc_build_tiles(t.m2l, P.me, P.me, fast || m2l_drain_fast());
+    tc_build_tiles(t.m2l, P.me, P.me, fast ? tc_fast_tile_mode() : (m2l_drain_fast() ? 1 : 0));
     EB_CUDA(cudaStreamSynchronize(s));
 }
 
@@ -1401,7 +1404,7 @@ void fmm_evaluate(Tree& t, int kernel, const float* f, const float* g, float* ou
     EB_REQUIRE(!dl || t.has_normals, "double-layer kernel needs normals at fmm_build_tree");
     if (t.ntrg == 0) return;
     static const bool serial = std::getenv("EBEM_SERIAL") != nullptr;   // diagnostics: one stream
-    const bool conc = t.profile != 1 && !serial;
+    const bool conc = t.profile != 1 && !serial && !t.force_serial;
     if (conc && !t.sA) {
         int least = 0, greatest = 0;
         EB_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
@@ -1469,9 +1472,12 @@ void fmm_evaluate(Tree& t, int kernel, const float* f, const float* g, float* ou
     };
     pb(PH_PREP, sa);
 
-    // prepared sources in tree order (geometry sorted, densities via src_perm)
-    prepare_sources(src_kernel, t.mat, t.src_xyz.p, t.src_nrm.p, t.src_w.p, nullptr, f, g, t.src_perm.p, t.nsrc,
-                    t.rec_disp.p, sa);
+    // prepared sources in tree order (geometry sorted, densities via src_perm); not needed when
+    // every pass that reads them is replaced by a stored operator (the BEM inside GMRES)
+    const bool need_rec = !(t.near_hook && t.s2m_hook && (t.s2l_hook || t.n_s2l == 0));
+    if (need_rec)
+        prepare_sources(src_kernel, t.mat, t.src_xyz.p, t.src_nrm.p, t.src_w.p, nullptr, f, g, t.src_perm.p, t.nsrc,
+                        t.rec_disp.p, sa);
     if (stress)
         prepare_sources(kernel, t.mat, t.src_xyz.p, t.src_nrm.p, t.src_w.p, nullptr, f, g, t.src_perm.p, t.nsrc,
                         t.rec_stress.p, sa);
@@ -1489,6 +1495,10 @@ void fmm_evaluate(Tree& t, int kernel, const float* f, const float* g, float* ou
 
     auto s2l = [&](cudaStream_t st) {
         if (!t.n_s2l) return;
+        if (t.s2l_hook) {
+            t.s2l_hook(st);
+            return;
+        }
         float* qb = t.use_tc ? t.Qdb.p : nullptr;
         float* qs = t.use_tc ? t.Qds.p : nullptr;
         if (sl && dl) launch_check<true, true>(t, t.s2l_box.p, t.n_s2l, t.x_src_off.p, t.x_src_idx.p, RAD_DC, t.Qd.p, qb, qs, st);
@@ -1528,7 +1538,9 @@ void fmm_evaluate(Tree& t, int kernel, const float* f, const float* g, float* ou
 
     // upward pass
     pb(PH_S2M, sa);
-    {
+    if (t.s2m_hook) {
+        t.s2m_hook(sa);
+    } else {
         float* qb = t.use_tc ? t.Qb.p : nullptr;
         float* qs = t.use_tc ? t.Qs.p : nullptr;
         if (sl && dl) launch_check<true, true>(t, t.s2m_box.p, t.n_s2m, nullptr, nullptr, RAD_UC, t.Q.p, qb, qs, sa);

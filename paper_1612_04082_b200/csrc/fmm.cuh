@@ -63,6 +63,8 @@ struct OpPairs {
     std::vector<int> op_ptr_h;   // host copy (launch sizing)
     int max_per_op = 0;
     int ntiles = 0;              // tensor-core tiles (op, first pair, #pairs, row block)
+    int tile_mode = 0;           // tile shape: 0 128 rows x 128 pairs (precise), 1 256 x 128 (fast /
+                                 // drained two-slice), 2 128 x 256 (wide, full-chain)
     DBuf<int> tiles;
 };
 
@@ -172,6 +174,9 @@ struct Tree {
     bool near_f64 = false;
     double* out_d = nullptr;
     std::function<void(cudaStream_t)> near_hook;   // replaces the near-field kernel (BEM near operator)
+    std::function<void(cudaStream_t)> s2m_hook;    // replaces the S2M check potentials (BEM S2M operator)
+    std::function<void(cudaStream_t)> s2l_hook;    // replaces the S2L check potentials (BEM S2L operator)
+    bool force_serial = false;                     // one stream (the BEM inside GMRES, measured faster)
     DBuf<int> ssplit;                    // BEM: per leaf, first source of the second boundary-condition group
     int split_mode = 0;                  // 0 off; 1: [sbeg, ssplit) single layer, rest double layer; 2 reverse
     DBuf<int> near_off, near_idx;        // per box: source boxes summed directly (U + direct X/W)
@@ -226,7 +231,8 @@ void tc_split_rows(const XT* X, int ld, int64_t row0, int64_t nrows, int K, floa
 void tree_precise(Tree& t, cudaStream_t s);
 void tree_partition_sources(Tree& t, const int32_t* bc, int nq, cudaStream_t s);
 void tree_m2l_fast(Tree& t, bool fast, cudaStream_t s);
-void tc_build_tiles(OpPairs& P, int M, int K, bool fast);
+void tc_build_tiles(OpPairs& P, int M, int K, int mode);
+int tc_fast_tile_mode();                       // 2 (wide kernel) unless EBEM_M2L_WIDE=0, then 1
 int tc_fast_smem_bytes();                     // dynamic shared memory of one fast translation CTA
 int beside_translation_pad(const void* kernel);   // fmm.cu: stream-B co-residency padding
 void tc_pairs_gemm_fast(const OpPairs& P, const CUtensorMap& Ab, const CUtensorMap& As, const float* Bb,

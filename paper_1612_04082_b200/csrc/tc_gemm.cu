@@ -558,6 +558,178 @@ tc_pairs_fast_kernel(const __grid_constant__ CUtensorMap mapAb, const __grid_con
     if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
 }
 
+// ------------------------------------------------------------------ wide variant (full chain)
+// The same contraction with one 128-row operator slice x 256 pairs per tile (MMA N = 256).
+// A tf32 M128 x N x K8 MMA takes 128 N / 256 cycles and reads (128 + N) x 32 B of shared
+// memory (both operands from smem): at N = 128 that is 128 B / cycle, the whole shared-memory
+// bandwidth, before the TMA / cp.async fills of the next stage (another ~62 B / cycle) -- the
+// two-slice kernel's tensor pipe could not exceed ~2/3.  At N = 256 the operand reads are
+// 96 B / cycle for the same bytes filled per MMA cycle.  TMEM: 2 tiles x 256 columns.
+namespace wide {
+constexpr int BNW = 256;
+constexpr int STAGES = 2;
+constexpr int A_BYTES = BM * BK * 4;                    // 16 KB (128 rows x 32 K)
+constexpr int B_BYTES = BNW * BK * 4;                   // 32 KB (256 rows x 32 K)
+constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;  // A_b, A_s, B_b, B_s = 96 KB
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256;
+constexpr int TMEM_COLS = 512;
+constexpr int NPROD = 3;
+constexpr int THREADS = 256;
+constexpr int NG = (BNW / 4 + NPROD - 1) / NPROD;       // four-row groups per producer warp
+}  // namespace wide
+
+__global__ void __launch_bounds__(wide::THREADS, 1)
+tc_pairs_wide_kernel(const __grid_constant__ CUtensorMap mapAb, const __grid_constant__ CUtensorMap mapAs,
+                     const float* __restrict__ Bb, const float* __restrict__ Bs, int ldb,
+                     const Tile* __restrict__ tiles, int ntiles, const int2* __restrict__ pairs, int M, int K,
+                     double* __restrict__ Y, int ldy) {
+    constexpr int STAGES = wide::STAGES, STAGE_BYTES = wide::STAGE_BYTES, A_BYTES = wide::A_BYTES,
+                  B_BYTES = wide::B_BYTES, TMEM_COLS = wide::TMEM_COLS, NPROD = wide::NPROD, NG = wide::NG,
+                  BNW = wide::BNW;
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    uint64_t* bars = (uint64_t*)(smem + STAGES * STAGE_BYTES);
+    uint64_t* full_b = bars;                     // [STAGES]
+    uint64_t* empty_b = bars + STAGES;           // [STAGES]
+    uint64_t* accf_b = bars + 2 * STAGES;        // [2]
+    uint64_t* acce_b = bars + 2 * STAGES + 2;    // [2]
+    uint32_t* tmem_slot = (uint32_t*)(bars + 2 * STAGES + 4);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(smem_u32(&full_b[s]), 1 + 32 * NPROD);   // A expect_tx + cp.async arrivals
+            mbar_init(smem_u32(&empty_b[s]), 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(smem_u32(&accf_b[b]), 1);
+            mbar_init(smem_u32(&acce_b[b]), 4);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 2) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(TMEM_COLS));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0 || warp == 2 || warp == 3) {
+        // ---------------- producers: warp 0 lane 0 the A tiles (TMA); warps 0, 2, 3 the B rows
+        const int pi = warp == 0 ? 0 : warp - 1;
+        const int piece = lane & 7, rsub = lane >> 3;
+        int c = 0;
+        for (int ti = blockIdx.x; ti < ntiles; ti += gridDim.x) {
+            const Tile tl = tiles[ti];
+            int64_t srow[NG];
+#pragma unroll
+            for (int g = 0; g < NG; ++g) {
+                const int r = rsub + 4 * (pi + NPROD * g);
+                srow[g] = (int64_t)__ldg(&pairs[tl.p0 + min(r, tl.np - 1)].y) * ldb;
+            }
+            const int ngrp = ((tl.np + 15) & ~15) / 4;     // row groups the MMA reads (N)
+            for (int kc = tl.kc0; kc < tl.kc1; ++kc, ++c) {
+                const int s = c % STAGES;
+                mbar_wait(smem_u32(&empty_b[s]), ((c / STAGES) & 1) ^ 1);
+                uint8_t* st = smem + s * STAGE_BYTES;
+                const uint32_t full = smem_u32(&full_b[s]);
+                if (pi == 0 && lane == 0) {
+                    mbar_expect_tx(full, 2 * A_BYTES);
+                    tma_load_3d(smem_u32(st), &mapAb, kc * BK, tl.m0, tl.op, full);
+                    tma_load_3d(smem_u32(st + A_BYTES), &mapAs, kc * BK, tl.m0, tl.op, full);
+                }
+                const int col = kc * BK + 4 * piece;
+                const uint32_t nb = col < ldb ? 16u : 0u;      // zero-fill past the row
+                const uint32_t b0 = smem_u32(st + 2 * A_BYTES);
+                const uint32_t b1 = b0 + B_BYTES;
+#pragma unroll
+                for (int g = 0; g < NG; ++g) {
+                    const int grp = pi + NPROD * g;
+                    if (grp < ngrp) {
+                        const int r = rsub + 4 * grp;
+                        const int64_t off = srow[g] + col;
+                        const uint32_t so = (uint32_t)(r * 128 + ((piece ^ (r & 7)) * 16));
+                        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(b0 + so),
+                                     "l"(nb ? Bb + off : Bb), "r"(nb)
+                                     : "memory");
+                        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(b1 + so),
+                                     "l"(nb ? Bs + off : Bs), "r"(nb)
+                                     : "memory");
+                    }
+                }
+                asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(full) : "memory");
+            }
+        }
+    } else if (warp == 1) {
+        // ---------------- MMA issuer
+        int c = 0, it = 0;
+        for (int ti = blockIdx.x; ti < ntiles; ti += gridDim.x, ++it) {
+            const int ab = it & 1;
+            const uint32_t nmma = (uint32_t)((tiles[ti].np + 15) & ~15);
+            const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((nmma >> 3) << 17) |
+                                   ((uint32_t)(BM >> 4) << 24);
+            mbar_wait(smem_u32(&acce_b[ab]), ((it >> 1) & 1) ^ 1);
+            asm volatile("tcgen05.fence::after_thread_sync;");
+            const int kc0 = tiles[ti].kc0, kc1 = tiles[ti].kc1;
+            for (int kc = kc0; kc < kc1; ++kc, ++c) {
+                const int s = c % STAGES;
+                mbar_wait(smem_u32(&full_b[s]), (c / STAGES) & 1);
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // cp.async data -> tensor core
+                asm volatile("tcgen05.fence::after_thread_sync;");
+                if (lane == 0) {
+                    const uint32_t st = smem_u32(smem + s * STAGE_BYTES);
+                    const uint64_t a_b = smem_desc(st), a_s = smem_desc(st + A_BYTES);
+                    const uint64_t bb = smem_desc(st + 2 * A_BYTES), bs = smem_desc(st + 2 * A_BYTES + B_BYTES);
+                    const uint32_t d = tmem + (uint32_t)(ab * BNW);
+                    const int ksteps = min(BK, K - kc * BK + 7) / 8;
+                    for (int k = 0; k < ksteps; ++k) {
+                        const uint64_t off = (uint64_t)(2 * k);
+                        mma_tf32(d, a_b + off, bb + off, idesc, kc != kc0 || k != 0);
+                        mma_tf32(d, a_b + off, bs + off, idesc, 1);
+                        mma_tf32(d, a_s + off, bb + off, idesc, 1);
+                    }
+                    mma_commit(smem_u32(&empty_b[s]));
+                    if (kc == kc1 - 1) mma_commit(smem_u32(&accf_b[ab]));
+                }
+                __syncwarp();
+            }
+        }
+    } else if (warp >= EPI_WARP0) {
+        // ---------------- epilogue: TMEM -> fp64 atomics, 32 columns at a time
+        const int wq = warp - EPI_WARP0;
+        int it = 0;
+        for (int ti = blockIdx.x; ti < ntiles; ti += gridDim.x, ++it) {
+            const Tile tl = tiles[ti];
+            const int ab = it & 1;
+            mbar_wait(smem_u32(&accf_b[ab]), (it >> 1) & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;");
+            const int2* pp = pairs + tl.p0;
+            const int row = tl.m0 + 32 * wq + lane;
+#pragma unroll 1
+            for (int c0 = 0; c0 < tl.np; c0 += 32) {
+                uint32_t v[32];
+                tmem_ld32(tmem + ((uint32_t)(32 * wq) << 16) + (uint32_t)(ab * BNW + c0), v);
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                if (row < M) {
+#pragma unroll
+                    for (int j = 0; j < 32; ++j)
+                        if (c0 + j < tl.np)
+                            atomicAdd(Y + (int64_t)__ldg(&pp[c0 + j].x) * ldy + row, (double)__uint_as_float(v[j]));
+                }
+            }
+            asm volatile("tcgen05.fence::before_thread_sync;");
+            __syncwarp();
+            if (lane == 0) mbar_arrive(smem_u32(&acce_b[ab]));
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
+}
+
 // round-to-nearest TF32 (low 13 mantissa bits zero): both halves of the split are exact TF32
 // values, so the tensor core's own fp32->tf32 handling (truncation) never applies, and the
 // two rounding errors are unbiased (truncated remainders are one-signed and their dropped
@@ -639,14 +811,23 @@ template void tc_split_rows<double>(const double*, int, int64_t, int64_t, int, f
 // and Z rows in L2 across operators but re-read the operators per chunk: no faster).  Launches with fewer tiles than SMs (the coarse M2M/L2L
 // levels) split K over several CTAs: a lone tile streams its 15 K chunks through one SM in
 // ~20 us, while its partial sums are added by the fp64 atomics of the epilogue anyway.
-void tc_build_tiles(OpPairs& P, int M, int K, bool fast) {
+int tc_fast_tile_mode() {
+    static const int m = (std::getenv("EBEM_M2L_WIDE") && std::atoi(std::getenv("EBEM_M2L_WIDE")) == 0) ? 1 : 2;
+    return m;
+}
+
+void tc_build_tiles(OpPairs& P, int M, int K, int mode) {
     std::vector<tc::Tile> t;
-    const int mstep = fast ? tc::fast::MT * tc::BM : tc::BM;
+    const int mstep = mode == 1 ? tc::fast::MT * tc::BM : tc::BM;
+    const int bn = mode == 2 ? tc::wide::BNW : tc::BN;
     const int nk = (K + tc::BK - 1) / tc::BK;
+    P.tile_mode = mode;
+    // op-major; the row blocks of one pair group are consecutive (run side by side on
+    // neighbouring CTAs, so the second load of the same gathered B rows hits L2)
     for (int o = 0; o < P.nops; ++o)
-        for (int p0 = P.op_ptr_h[o]; p0 < P.op_ptr_h[o + 1]; p0 += tc::BN)
+        for (int p0 = P.op_ptr_h[o]; p0 < P.op_ptr_h[o + 1]; p0 += bn)
             for (int m0 = 0; m0 < M; m0 += mstep)
-                t.push_back({o, p0, std::min(tc::BN, P.op_ptr_h[o + 1] - p0), m0, 0, nk});
+                t.push_back({o, p0, std::min(bn, P.op_ptr_h[o + 1] - p0), m0, 0, nk});
     const int nsplit = t.empty() ? 1 : std::max(1, std::min(nk / 3, num_sms() / (int)t.size()));
     if (nsplit > 1) {
         std::vector<tc::Tile> u;
@@ -669,6 +850,21 @@ int tc_fast_smem_bytes() { return tc::fast::SMEM_BYTES; }
 void tc_pairs_gemm_fast(const OpPairs& P, const CUtensorMap& Ab, const CUtensorMap& As, const float* Bb,
                         const float* Bs, int ldb, int M, int K, double* Y, int ldy, bool drain, cudaStream_t s) {
     if (P.ntiles == 0) return;
+    if (P.tile_mode == 2) {
+        EB_REQUIRE(!drain, "internal: wide tiles with the drained kernel");
+        static bool wattr = false;
+        if (!wattr) {
+            EB_CUDA(cudaFuncSetAttribute(tc::tc_pairs_wide_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         tc::wide::SMEM_BYTES));
+            wattr = true;
+        }
+        const int grid = std::min(P.ntiles, num_sms());
+        tc::tc_pairs_wide_kernel<<<grid, tc::wide::THREADS, tc::wide::SMEM_BYTES, s>>>(
+            Ab, As, Bb, Bs, ldb, reinterpret_cast<const tc::Tile*>(P.tiles.p), P.ntiles, P.pairs.p, M, K, Y, ldy);
+        EB_CHECK_LAUNCH();
+        return;
+    }
+    EB_REQUIRE(P.tile_mode == 1, "internal: fast kernel needs two-slice tiles");
     static bool attr[2] = {false, false};
     auto fn = drain ? tc::tc_pairs_fast_kernel<true> : tc::tc_pairs_fast_kernel<false>;
     if (!attr[drain]) {

@@ -128,8 +128,9 @@ def test_gmres_solver_setting_of_configs4_matches_dense_oracle(eb):
 
 def test_near_operator_matches_near_kernel(eb, monkeypatch):
     """The BEM near field held in HBM (bem_near.cu: per-leaf 3x3 blocks of the summed
-    quadrature-point kernels) and the per-leaf grouping of sources by panel type (one-layer
-    check-potential loops) against the pair-by-pair near-field kernel and the combined loop:
+    quadrature-point kernels), the S2M / S2L check-potential operators built the same way, and
+    the per-leaf grouping of sources by panel type (one-layer check-potential loops) against
+    the pair-by-pair near-field and check-potential kernels and the combined loop:
     same solve to fp32 rounding, on a cell with voids (leaves straddling panels, direct X/W
     entries); the stored operator is reused for the same boundary conditions and rebuilt
     when they change (the grouping then changes too)."""
@@ -154,12 +155,14 @@ def test_near_operator_matches_near_kernel(eb, monkeypatch):
         ref.append(solve(bc))
     monkeypatch.setenv("EBEM_BEM_NEARMAT", "1")
     monkeypatch.setenv("EBEM_BEM_SPLIT", "1")       # sources grouped by panel type per leaf
-    for k, bc in enumerate((bc0, bc0, bc1)):      # build, reuse, rebuild
-        x, it, res = solve(bc)
-        xr, itr, resr = ref[0 if k < 2 else 1]
-        print("near operator", k, "iterations", it, itr, "residual", res, resr)
-        assert res <= 1e-6 and abs(it - itr) <= 3
-        assert KN.rel_l2(x, xr) < 1e-4      # both stop at residual 1e-6; a wrong block is O(1)
+    for checkmat in ("0", "1"):                     # near operator alone; + S2M / S2L operators
+        monkeypatch.setenv("EBEM_BEM_CHECKMAT", checkmat)
+        for k, bc in enumerate((bc0, bc0, bc1)):      # build, reuse, rebuild
+            x, it, res = solve(bc)
+            xr, itr, resr = ref[0 if k < 2 else 1]
+            print("near operator, check operators", checkmat, k, "iterations", it, itr, "residual", res, resr)
+            assert res <= 1e-6 and abs(it - itr) <= 3
+            assert KN.rel_l2(x, xr) < 1e-4      # both stop at residual 1e-6; a wrong block is O(1)
 
 
 def test_near_operator_memory_fallback_and_nq1(eb, monkeypatch):
