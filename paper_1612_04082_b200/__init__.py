@@ -17,6 +17,8 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "lib", "libelastobem.so")
+if os.environ.get("EBEM_LIB_VARIANT"):       # A/B measurement builds (_build.py variant ...)
+    LIB_PATH = os.path.join(_HERE, "lib", "variants", os.environ["EBEM_LIB_VARIANT"] + ".so")
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"{LIB_PATH} not built; run `python -c 'import __graft_entry__ as g; g.build()'`")

@@ -24,9 +24,24 @@ def _needs(obj: str, deps) -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, defs=(), variant: str = "") -> str:
+    """Compile every csrc/*.cu and link lib/libelastobem.so.  `defs` (-D flags) with a
+    `variant` name build an A/B variant instead: lib/variants/<variant>.so, selected at import
+    by EBEM_LIB_VARIANT=<variant> (measurement only; the product library is the default)."""
+    global OBJ, LIB
+    obj_dir, lib_path = OBJ, LIB
+    if variant:
+        OBJ = os.path.join(PKG, "build", "variants", variant)
+        LIB = os.path.join(LIBDIR, "variants", variant + ".so")
+    try:
+        return _build(force, verbose, [f"-D{d}" for d in defs])
+    finally:
+        OBJ, LIB = obj_dir, lib_path
+
+
+def _build(force, verbose, dflags) -> str:
     os.makedirs(OBJ, exist_ok=True)
-    os.makedirs(LIBDIR, exist_ok=True)
+    os.makedirs(os.path.dirname(LIB), exist_ok=True)
     srcs = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
     headers = glob.glob(os.path.join(CSRC, "*.cuh")) + [os.path.join(PKG, "..", "include", "elastobem.h")]
     jobs = []
@@ -37,7 +52,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
     def compile_one(job):
         src, obj = job
-        cmd = [NVCC, *ARCH, *FLAGS, "-c", src, "-o", obj]
+        cmd = [NVCC, *ARCH, *FLAGS, *dflags, "-c", src, "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"nvcc failed for {src}:\n{r.stderr}")
@@ -58,4 +73,6 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
 if __name__ == "__main__":
     import sys
-    print(build(force="--force" in sys.argv, verbose=True))
+    a = [x for x in sys.argv[1:] if x != "--force"]
+    # python _build.py [--force] [variant DEF=1 DEF2=3 ...]
+    print(build(force="--force" in sys.argv, verbose=True, variant=a[0] if a else "", defs=a[1:]))

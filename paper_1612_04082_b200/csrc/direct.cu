@@ -90,15 +90,23 @@ __device__ __forceinline__ int64_t first_cta(int64_t u, int64_t U, int64_t G) {
     return ((u + 1) * G + U - 1) / U - 1;          // CTA whose range contains unit u
 }
 
+#ifndef EBEM_PACKED
+#define EBEM_PACKED 1        // packed FFMA2 pair loop (two targets per instruction)
+#endif
+
 template <bool SL, bool DL, bool STRESS>
 __global__ void __launch_bounds__(DIRECT_THREADS)
 direct_kernel(const float4* __restrict__ rec, int64_t nsrc, int64_t ntiles, const float* __restrict__ trg,
               int64_t ntrg, int64_t U, int kslots, KConst kc, float* __restrict__ partial) {
     constexpr int R = STRESS ? REC_STRESS : REC_DISP;
     constexpr int NC = STRESS ? 6 : 3;
+    constexpr int NP = DIRECT_TPT / 2;
     __shared__ float4 srec[DIRECT_TILE * R];
     const int64_t G = gridDim.x, c = blockIdx.x;
     const int64_t u_beg = c * U / G, u_end = (c + 1) * U / G;
+#if EBEM_PACKED
+    const KConst2 kc2(kc);
+#endif
     int64_t u = u_beg;
     while (u < u_end) {
         const int64_t tb = u / ntiles;
@@ -113,14 +121,38 @@ direct_kernel(const float4* __restrict__ rec, int64_t nsrc, int64_t ntiles, cons
 #pragma unroll
             for (int q = 0; q < NC; ++q) acc[k][q] = 0.f;
         }
+#if EBEM_PACKED
+        F2 x2[NP], y2[NP], z2[NP], acc2[NP][NC];
+#pragma unroll
+        for (int k = 0; k < NP; ++k) {
+            x2[k] = F2(x[2 * k], x[2 * k + 1]);
+            y2[k] = F2(y[2 * k], y[2 * k + 1]);
+            z2[k] = F2(z[2 * k], z[2 * k + 1]);
+#pragma unroll
+            for (int q = 0; q < NC; ++q) acc2[k][q] = F2(0.f);
+        }
+#endif
         for (; u < u_stop; ++u) {
             const int64_t s0 = (u - tb * ntiles) * DIRECT_TILE;
             const int cnt = (int)min((int64_t)DIRECT_TILE, nsrc - s0);
             __syncthreads();
             for (int i = threadIdx.x; i < cnt * R; i += DIRECT_THREADS) srec[i] = rec[s0 * R + i];
             __syncthreads();
+#if EBEM_PACKED
+            pair_loop_packed<SL, DL, STRESS, NP, R, true, PL_UNROLL>(srec, cnt, 0, 1, x2, y2, z2, kc2, acc2);
+#else
             pair_loop_multi<SL, DL, STRESS, DIRECT_TPT>(srec, cnt, x, y, z, kc, acc);
+#endif
         }
+#if EBEM_PACKED
+#pragma unroll
+        for (int k = 0; k < NP; ++k)
+#pragma unroll
+            for (int q = 0; q < NC; ++q) {
+                acc[2 * k][q] = acc2[k][q].v.x;
+                acc[2 * k + 1][q] = acc2[k][q].v.y;
+            }
+#endif
         const int slot = (int)(c - first_cta(tb * ntiles, U, G));
         float* o = partial + ((int64_t)tb * kslots + slot) * DIRECT_TB * NC;
         if (STRESS && SL && DL)   // acc_DS accumulates half of the diagonal

@@ -573,6 +573,124 @@ near_eval_kernel(int n_eval, const int* __restrict__ eval_box, const int* __rest
     }
 }
 
+// Packed lane groups (FFMA2 pair loops, packed.cuh): groups of L lanes, each lane NP PAIRS of
+// targets (t0 + l + L j, j = 0 .. 2 NP - 1; pack k = targets 2k, 2k + 1), L * 2 NP >= nt as
+// tight as possible; on ties the smaller group (more targets per lane: each staged source
+// record is read once for more targets).  Returns NP (NPMAX and L = 32 when nt exceeds
+// 64 NPMAX: rounds are repeated).
+template <int NPMAX>
+__device__ __forceinline__ int lane_groups_packed(int nt, int& L) {
+    if (nt > 64 * NPMAX) {
+        L = 32;
+        return NPMAX;
+    }
+    int best = 1 << 30, np = NPMAX;
+    L = 32;
+    for (int l = 32; l >= 4; l >>= 1) {
+        const int t = (nt + 2 * l - 1) / (2 * l);
+        if (t <= NPMAX && 2 * l * t <= best) {
+            best = 2 * l * t;
+            L = l;
+            np = t;
+        }
+    }
+    return np;
+}
+
+template <int NC, int NP>
+__device__ __forceinline__ void reduce_groups_packed(F2 (*acc)[NC], int L) {
+    for (int off = L; off < 32; off <<= 1)
+#pragma unroll
+        for (int k = 0; k < NP; ++k)
+#pragma unroll
+            for (int c = 0; c < NC; ++c) {
+                acc[k][c].v.x += __shfl_xor_sync(0xffffffffu, acc[k][c].v.x, off);
+                acc[k][c].v.y += __shfl_xor_sync(0xffffffffu, acc[k][c].v.y, off);
+            }
+}
+
+// near field with the packed pair loop: as near_round, two targets per FP32 instruction
+template <bool SL, bool DL, bool STRESS, int NP>
+__device__ __forceinline__ void near_round_p(int t0, int t_beg, int t_end, int L, int b, const int* __restrict__ uoff,
+                                             const int* __restrict__ uidx, const int* __restrict__ sbeg,
+                                             const int* __restrict__ send, const float* __restrict__ trg,
+                                             const float4* __restrict__ rec, const KConst2& kc,
+                                             float* __restrict__ near, float4* srec, int lane) {
+    constexpr int NC = STRESS ? 6 : 3;
+    constexpr int R = STRESS ? REC_STRESS : REC_DISP;
+    constexpr int RS = R + 1;
+    const int G = 32 / L, grp = lane / L, l = lane % L;
+    F2 x[NP], y[NP], z[NP], acc[NP][NC];
+#pragma unroll
+    for (int k = 0; k < NP; ++k) {
+        const int ta = t0 + l + L * (2 * k), tb = ta + L;
+        const int ca = ta < t_end ? ta : t_beg, cb = tb < t_end ? tb : t_beg;
+        x[k] = F2(trg[3 * ca], trg[3 * cb]);
+        y[k] = F2(trg[3 * ca + 1], trg[3 * cb + 1]);
+        z[k] = F2(trg[3 * ca + 2], trg[3 * cb + 2]);
+#pragma unroll
+        for (int c = 0; c < NC; ++c) acc[k][c] = F2(0.f);
+    }
+    for (int e = uoff[b]; e < uoff[b + 1]; ++e) {
+        const int a = uidx[e];
+        for (int s0 = sbeg[a]; s0 < send[a]; s0 += NEAR_TILE) {
+            const int cnt = min(NEAR_TILE, send[a] - s0);
+            __syncwarp();
+            for (int q = lane; q < cnt * R; q += 32) srec[(q / R) * RS + q % R] = rec[(int64_t)s0 * R + q];
+            __syncwarp();
+            if (a == b) pair_loop_packed<SL, DL, STRESS, NP, RS, true>(srec, cnt, grp, G, x, y, z, kc, acc);
+            else pair_loop_packed<SL, DL, STRESS, NP, RS, false>(srec, cnt, grp, G, x, y, z, kc, acc);
+        }
+    }
+    reduce_groups_packed<NC, NP>(acc, L);
+    if (grp == 0)
+#pragma unroll
+        for (int k = 0; k < NP; ++k)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int t = t0 + l + L * (2 * k + h);
+                if (t < t_end)
+#pragma unroll
+                    for (int c = 0; c < NC; ++c) {   // acc_DS accumulates half of the diagonal
+                        const float v = h ? acc[k][c].v.y : acc[k][c].v.x;
+                        near[(int64_t)t * NC + c] = (STRESS && SL && DL && c < 3) ? 2.f * v : v;
+                    }
+            }
+}
+
+#ifndef NEAR_NPMAX
+#define NEAR_NPMAX 4
+#endif
+template <bool SL, bool DL, bool STRESS>
+__global__ void __launch_bounds__(32 * EV_WARPS)
+near_eval_p_kernel(int n_eval, const int* __restrict__ eval_box, const int* __restrict__ uoff,
+                   const int* __restrict__ uidx, const int* __restrict__ sbeg, const int* __restrict__ send,
+                   const int* __restrict__ tbeg, const int* __restrict__ tend, const float* __restrict__ trg,
+                   const float4* __restrict__ rec, KConst kc1, float* __restrict__ near) {
+    constexpr int R = STRESS ? REC_STRESS : REC_DISP;
+    constexpr int NPM = STRESS ? 2 : NEAR_NPMAX;       // 6-component sums: fewer pairs per lane
+    __shared__ float4 srec_all[EV_WARPS][NEAR_TILE * (R + 1)];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int i = blockIdx.x * EV_WARPS + warp;
+    if (i >= n_eval) return;
+    const KConst2 kc(kc1);
+    float4* srec = srec_all[warp];
+    const int b = eval_box[i];
+    const int t_beg = tbeg[b], t_end = tend[b];
+    for (int t0 = t_beg; t0 < t_end;) {
+        int L;
+        const int np = lane_groups_packed<NPM>(t_end - t0, L);
+#define EB_NEARP(N) \
+    near_round_p<SL, DL, STRESS, N>(t0, t_beg, t_end, L, b, uoff, uidx, sbeg, send, trg, rec, kc, near, srec, lane)
+        if (np == 1) EB_NEARP(1);
+        else if (np == 2 || NPM == 2) EB_NEARP(2);
+        else if (np == 3) EB_NEARP(3);
+        else EB_NEARP(NPM);
+#undef EB_NEARP
+        t0 += 2 * L * np;
+    }
+}
+
 // near field, version 2: the leaf's near sources as MERGED contiguous ranges of the sorted
 // source array (neighbouring boxes are mostly adjacent in Morton order, so ~27 boxes of ~24
 // sources collapse into a few long runs and the 32-source tiles are full), staged per warp by
@@ -1133,6 +1251,26 @@ void schedule_tree(Tree& t, cudaStream_t s) {
         tc_build_tiles(t.m2l, me, me, t.tc_fast ? fm : (m2l_drain_fast() ? 1 : 0));
         for (auto& x : t.m2m) tc_build_tiles(x, me, me, t.ml_fast ? fm : 0);
         for (auto& x : t.l2l) tc_build_tiles(x, me, me, t.ml_fast ? fm : 0);
+        // M2M and L2L chains as one cooperative launch each (tc_chain_kernel); EBEM_ML_CHAIN=0:
+        // a split launch plus a translation launch per level
+        static const bool chain_on = !(std::getenv("EBEM_ML_CHAIN") && std::atoi(std::getenv("EBEM_ML_CHAIN")) == 0);
+        t.ml_chain = t.ml_fast && chain_on;
+        if (t.ml_chain) {
+            std::vector<const OpPairs*> up, dn;
+            std::vector<int64_t> ur0, urn, dr0, drn;
+            for (int l = t.nlevels - 2; l >= 2; --l) {      // M2M at l reads the Z rows of level l + 1
+                up.push_back(&t.m2m[l]);
+                ur0.push_back(t.up_lstart[l + 1]);
+                urn.push_back(t.up_lstart[l + 2] - t.up_lstart[l + 1]);
+            }
+            for (int l = 3; l < t.nlevels; ++l) {           // L2L at l reads the W rows of level l - 1
+                dn.push_back(&t.l2l[l]);
+                dr0.push_back(t.dn_lstart[l - 1]);
+                drn.push_back(t.dn_lstart[l] - t.dn_lstart[l - 1]);
+            }
+            tc_build_chain(t.m2m_chain, up, ur0, urn, me, me, s);
+            tc_build_chain(t.l2l_chain, dn, dr0, drn, me, me, s);
+        }
     }
     if (t.far64) {
         t.PHID.alloc((size_t)std::max(1, t.n_phid) * me);
@@ -1331,7 +1469,22 @@ static void launch_near(const Tree& t, cudaStream_t s) {
     // near_eval2_kernel (merged ranges, cp.async double buffer) is 3.5% faster alone but made
     // the overlapped matvec slower (4.41 -> 4.56 ms): the default stays the per-box kernel
     static const bool v1 = !(std::getenv("EBEM_NEAR_V2") && std::atoi(std::getenv("EBEM_NEAR_V2")));
-    if (v1) {
+    // EBEM_NEAR_PACKED=1: packed FFMA2 pair loop (two targets per FP32 instruction)
+    // (1.348 vs 1.36 ms alone, but the overlapped matvec 4.70 vs 4.45 ms: its 127 registers
+    // leave room for fewer near-field CTAs beside the translation CTAs; off by default)
+    static const bool packed = std::getenv("EBEM_NEAR_PACKED") && std::atoi(std::getenv("EBEM_NEAR_PACKED")) == 1;
+    if (v1 && packed) {
+        static bool carve_p = false;
+        if (!carve_p) {
+            EB_CUDA(cudaFuncSetAttribute(near_eval_p_kernel<SL, DL, STRESS>,
+                                         cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+            carve_p = true;
+        }
+        static const int pad = beside_translation_pad((const void*)near_eval_p_kernel<SL, DL, STRESS>);
+        near_eval_p_kernel<SL, DL, STRESS><<<ceil_div(t.n_eval, EV_WARPS), 32 * EV_WARPS, pad, s>>>(
+            t.n_eval, t.eval_box.p, t.near_off.p, t.near_idx.p, t.sbeg.p, t.send.p, t.tbeg.p, t.tend.p, t.trg_xyz.p,
+            STRESS ? t.rec_stress.p : t.rec_disp.p, kc, t.near_sorted.p);
+    } else if (v1) {
         static const int pad = beside_translation_pad((const void*)near_eval_kernel<SL, DL, STRESS>);
         near_eval_kernel<SL, DL, STRESS><<<ceil_div(t.n_eval, EV_WARPS), 32 * EV_WARPS, pad, s>>>(
             t.n_eval, t.eval_box.p, t.near_off.p, t.near_idx.p, t.sbeg.p, t.send.p, t.tbeg.p, t.tend.p, t.trg_xyz.p,
@@ -1561,6 +1714,11 @@ void fmm_evaluate(Tree& t, int kernel, const float* f, const float* g, float* ou
     }
     pe(PH_Q2Z_UP, sa);
     pb(PH_M2M, sa);
+    if (t.use_tc && t.ml_chain) {
+        if (t.nlevels > 2)
+            tc_chain_run(t.m2m_chain, P.mM2M_b, P.mM2M_s, t.Z.p, lde, t.Zb.p, t.Zs.p, me, me, t.Z.p, lde,
+                         t.up_lstart[2], zrows(2), sa);
+    } else {
     for (int l = t.nlevels - 2; l >= 2; --l) {
         if (t.use_tc) {
             tc_split_rows(t.Z.p, lde, t.up_lstart[l + 1], zrows(l + 1), me, t.Zb.p, t.Zs.p, sa);
@@ -1571,6 +1729,7 @@ void fmm_evaluate(Tree& t, int kernel, const float* f, const float* g, float* ou
         }
     }
     if (t.use_tc && t.nlevels > 2) tc_split_rows(t.Z.p, lde, t.up_lstart[2], zrows(2), me, t.Zb.p, t.Zs.p, sa);
+    }
     pe(PH_M2M, sa);
 
     // downward pass (stream B forks here: started together with the upward pass it only
@@ -1620,6 +1779,9 @@ void fmm_evaluate(Tree& t, int kernel, const float* f, const float* g, float* ou
         pe(PH_Q2Z_DN, sa);
     }
     pb(PH_L2L, sa);
+    if (t.use_tc && t.ml_chain) {
+        tc_chain_run(t.l2l_chain, P.mL2L_b, P.mL2L_s, t.W.p, lde, t.Wb.p, t.Ws.p, me, me, t.W.p, lde, 0, 0, sa);
+    } else {
     for (int l = 3; l < t.nlevels; ++l) {
         if (t.use_tc) {
             tc_split_rows(t.W.p, lde, t.dn_lstart[l - 1], wrows(l - 1), me, t.Wb.p, t.Ws.p, sa);
@@ -1628,6 +1790,7 @@ void fmm_evaluate(Tree& t, int kernel, const float* f, const float* g, float* ou
         } else {
             gemm_pairs_f32(t.l2l[l], P.L2L.p, me, me, lde, t.W.p, lde, t.W.p, lde, sa);
         }
+    }
     }
     pe(PH_L2L, sa);
     pb(PH_PHI, sa);

@@ -68,6 +68,22 @@ struct OpPairs {
     DBuf<int> tiles;
 };
 
+// a level chain (M2M or L2L) run as one cooperative launch (tc_gemm.cu, tc_chain_kernel)
+struct ChainArgs {
+    int nlev;
+    int lvl_tile[MAXLEVEL + 1];          // tiles of chain level i: [lvl_tile[i], lvl_tile[i + 1])
+    long long row0[MAXLEVEL], nrows[MAXLEVEL];   // source rows split before level i
+    long long tail_row0, tail_rows;      // rows split after the last level (upward chain)
+};
+struct Chain {
+    int nlev = 0;
+    std::vector<int> lvl_tile;
+    std::vector<int64_t> row0, nrows;
+    DBuf<int> tiles;
+    DBuf<int2> pairs;
+    DBuf<unsigned> bar;                  // grid-barrier counter (cleared before each launch), level times
+};
+
 // ------------------------------------------------------------------ tree
 struct Tree {
     int64_t nsrc = 0, ntrg = 0, npts = 0;
@@ -109,6 +125,8 @@ struct Tree {
     std::vector<OpPairs> m2m;            // per level (parents at that level), 8 ops
     OpPairs m2l;                         // all levels, 316 ops
     std::vector<OpPairs> l2l;            // per level (children at that level), 8 ops
+    Chain m2m_chain, l2l_chain;          // the same, one cooperative launch per pass (ml_chain)
+    bool ml_chain = false;
     // leaf evaluation
     int n_eval = 0;                      // leaves with targets
     DBuf<int> eval_box;                  // [n_eval]
@@ -232,7 +250,13 @@ void tree_precise(Tree& t, cudaStream_t s);
 void tree_partition_sources(Tree& t, const int32_t* bc, int nq, cudaStream_t s);
 void tree_m2l_fast(Tree& t, bool fast, cudaStream_t s);
 void tc_build_tiles(OpPairs& P, int M, int K, int mode);
-int tc_fast_tile_mode();                       // 2 (wide kernel) unless EBEM_M2L_WIDE=0, then 1
+void tc_build_chain(Chain& ch, const std::vector<const OpPairs*>& levels, const std::vector<int64_t>& row0,
+                    const std::vector<int64_t>& nrows, int M, int K, cudaStream_t s);
+// X: fp64 state rows (ldx), split into Xb / Xs level by level ([row0, row0 + nrows) before
+// each level, [tail_row0, tail_row0 + tail_rows) after the last); Y += translations
+void tc_chain_run(const Chain& ch, const CUtensorMap& Ab, const CUtensorMap& As, const double* X, int ldx, float* Xb,
+                  float* Xs, int M, int K, double* Y, int ldy, int64_t tail_row0, int64_t tail_rows, cudaStream_t s);
+int tc_fast_tile_mode();                       // 1 (two-slice tiles) unless EBEM_M2L_WIDE=1, then 2
 int tc_fast_smem_bytes();                     // dynamic shared memory of one fast translation CTA
 int beside_translation_pad(const void* kernel);   // fmm.cu: stream-B co-residency padding
 void tc_pairs_gemm_fast(const OpPairs& P, const CUtensorMap& Ab, const CUtensorMap& As, const float* Bb,

@@ -4,6 +4,7 @@
 #pragma once
 #include "common.cuh"
 #include "elastic.cuh"
+#include "packed.cuh"
 
 namespace ebem {
 
@@ -88,6 +89,51 @@ __device__ __forceinline__ void pair_loop_multi(const float4* __restrict__ srec,
     }
 }
 
+
+// Packed variant: NP pairs of targets per thread, each pair evaluated by FFMA2/FMUL2/FADD2
+// against the broadcast source record (packed.cuh: half the FP32 issue slots per pair).
+// Records j = g, g + G, ... of the tile at stride RS float4 (g = 0, G = 1, RS = R: all).
+struct KConst2 {
+    F2 a1, a, a3, nu, b4, ds_k2, ds_k4, ds_k5;
+    __device__ __forceinline__ explicit KConst2(const KConst& k)
+        : a1(k.a1), a(k.a), a3(k.a3), nu(k.nu), b4(k.b4), ds_k2(k.ds_k2), ds_k4(k.ds_k4), ds_k5(k.ds_k5) {}
+};
+
+template <bool SL, bool DL, bool STRESS, int NP, int RS, bool SAFE, int UNROLL = 2>
+__device__ __forceinline__ void pair_loop_packed(const float4* __restrict__ srec, int cnt, int g, int G, const F2* x,
+                                                 const F2* y, const F2* z, const KConst2& kc,
+                                                 F2 (*acc)[STRESS ? 6 : 3]) {
+#pragma unroll UNROLL
+    for (int j = g; j < cnt; j += G) {
+        const float4 p = srec[j * RS + 0];
+        const float4 f = SL ? srec[j * RS + 1] : make_float4(0, 0, 0, 0);
+        const float4 gg = DL ? srec[j * RS + 2] : make_float4(0, 0, 0, 0);
+        const float4 n = DL ? srec[j * RS + 3] : make_float4(0, 0, 0, 0);
+        F2 NG[6] = {F2(0.f), F2(0.f), F2(0.f), F2(0.f), F2(0.f), F2(0.f)};
+        if (STRESS && DL) {
+            const float4 t0 = srec[j * RS + 4];
+            const float4 t1 = srec[j * RS + 5];
+            NG[0] = F2(t0.x); NG[1] = F2(t0.y); NG[2] = F2(t0.z); NG[3] = F2(t0.w); NG[4] = F2(t1.x); NG[5] = F2(t1.y);
+        }
+        const F2 px(p.x), py(p.y), pz(p.z), pw(p.w);
+        const F2 fx(f.x), fy(f.y), fz(f.z), fw(f.w), gx(gg.x), gy(gg.y), gz(gg.z), nx(n.x), ny(n.y), nz(n.z);
+#pragma unroll
+        for (int k = 0; k < NP; ++k) {
+            const F2 dx = x[k] - px, dy = y[k] - py, dz = z[k] - pz;
+            const F2 r2 = fmat(dz, dz, fmat(dy, dy, dx * dx));
+            const F2 ri = SAFE ? safe_rinv2(r2) : rsqrt2(r2);
+            if (!STRESS) {
+                if (SL && DL) acc_UP(dx, dy, dz, ri, fx, fy, fz, gx, gy, gz, nx, ny, nz, pw, kc.a1, kc.a3, acc[k]);
+                else if (SL) acc_U(dx, dy, dz, ri, fx, fy, fz, kc.a1, acc[k]);
+                else acc_P(dx, dy, dz, ri, gx, gy, gz, nx, ny, nz, pw, kc.a3, acc[k]);
+            } else {
+                if (SL && DL) acc_DS(dx, dy, dz, ri, fx, fy, fz, fw, gx, gy, gz, nx, ny, nz, pw, NG, kc, acc[k]);
+                else if (SL) acc_D(dx, dy, dz, ri, fx, fy, fz, kc.a, acc[k]);
+                else acc_S(dx, dy, dz, ri, gx, gy, gz, nx, ny, nz, pw, NG, kc.a, kc.nu, kc.b4, acc[k]);
+            }
+        }
+    }
+}
 
 // the same for a lane group: records j = g, g + G, ... of the staged tile (stride RS float4),
 // TPT targets per thread

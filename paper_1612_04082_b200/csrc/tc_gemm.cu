@@ -17,6 +17,8 @@
 #include <cuda.h>
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 
 #include "fmm.cuh"
 
@@ -755,6 +757,251 @@ __global__ void split_rows_kernel(const XT* __restrict__ X, int ld, int64_t row0
     Xs[r * ld + c] = to_tf32(x - (XT)b);
 }
 
+// ------------------------------------------------------------------ level chain (M2M, L2L)
+// The upward (M2M, fine to coarse) and downward (L2L, coarse to fine) passes are chains of
+// small dependent contractions, one per tree level.  Launched level by
+// level they cost a split launch (fp64 state -> TF32 head / remainder) plus a translation
+// launch per level, and the coarse levels are all latency (kernel prologue, pipeline fill,
+// epilogue, teardown).  This persistent kernel runs a whole chain in one cooperative launch:
+// per level, all threads of the grid split that level's source rows (grid-stride sweep), a
+// grid-wide barrier, the level's translation tiles (data flow of tc_pairs_fast_kernel<false>:
+// two 128-row operator slices x up to 128 pairs, TMA A, cp.async B, full-K TMEM accumulation,
+// fp64 atomic epilogue), another grid barrier.  The upward chain's last sweep also splits the
+// coarsest rows, which the M2L reads.
+// (A variant whose producers read the fp64 rows and split them while staging was measured 4x
+// slower per level: register-staged loads cannot run ahead of the ring like cp.async.)
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// grid-wide barrier number `k` (0, 1, ...): the CTA's prior writes are released, every CTA's
+// writes before its arrival are acquired (the acquire also invalidates this SM's L1)
+__device__ __forceinline__ void grid_barrier(unsigned* gbar, unsigned k) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(gbar) : "memory");
+        const unsigned target = (k + 1) * gridDim.x;
+        while (ld_acquire_u32(gbar) < target) __nanosleep(32);
+    }
+    __syncthreads();
+}
+
+// rows [row0, row0 + nrows) of X split into Xb / Xs: a warp per row, each lane up to 8
+// independent 16-B loads in flight (a grid-stride element loop was latency bound: ~0.3 TB/s)
+__device__ __forceinline__ void split_sweep(const double* X, int ldx, int64_t row0, int64_t nrows, int K,
+                                            float* __restrict__ Xb, float* __restrict__ Xs) {
+    const int lane = threadIdx.x & 31;
+    const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int K2 = K >> 1;                       // K is even (3 n_e, n_e even)
+    for (int64_t r = row0 + gw; r < row0 + nrows; r += nw) {
+        const double2* src = reinterpret_cast<const double2*>(X + r * ldx);
+        float2* db = reinterpret_cast<float2*>(Xb + r * ldx);
+        float2* ds = reinterpret_cast<float2*>(Xs + r * ldx);
+        for (int j0 = 0; j0 < K2; j0 += 8 * 32) {
+            double2 v[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const int j = j0 + q * 32 + lane;
+                v[q] = j < K2 ? src[j] : make_double2(0.0, 0.0);
+            }
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const int j = j0 + q * 32 + lane;
+                if (j < K2) {
+                    const float h0 = to_tf32(v[q].x), h1 = to_tf32(v[q].y);
+                    db[j] = make_float2(h0, h1);
+                    ds[j] = make_float2(to_tf32(v[q].x - (double)h0), to_tf32(v[q].y - (double)h1));
+                }
+            }
+        }
+    }
+}
+
+__global__ void __launch_bounds__(fast::THREADS, 1)
+tc_chain_kernel(const __grid_constant__ CUtensorMap mapAb, const __grid_constant__ CUtensorMap mapAs,
+                const double* X, int ldx, float* Xb, float* Xs, const Tile* __restrict__ tiles,
+                const int2* __restrict__ pairs, int M, int K, double* Y, int ldy, const __grid_constant__ ChainArgs ca,
+                unsigned* __restrict__ gbar) {
+    constexpr int MT = fast::MT, STAGES = fast::STAGES, STAGE_BYTES = fast::STAGE_BYTES, TMEM_COLS = fast::TMEM_COLS;
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    uint64_t* bars = (uint64_t*)(smem + STAGES * STAGE_BYTES);
+    uint64_t* full_b = bars;                     // [STAGES]
+    uint64_t* empty_b = bars + STAGES;           // [STAGES]
+    uint64_t* accf_b = bars + 2 * STAGES;        // [2]
+    uint64_t* acce_b = bars + 2 * STAGES + 2;    // [2]
+    uint32_t* tmem_slot = (uint32_t*)(bars + 2 * STAGES + 4);
+    unsigned long long* trace = reinterpret_cast<unsigned long long*>(gbar + 2);
+    auto stamp = [&](int i) {                    // diagnostics (EBEM_CHAIN_TRACE): level end times
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+            unsigned long long t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            trace[i] = t;
+        }
+    };
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(smem_u32(&full_b[s]), 1 + 32 * fast::NPROD);   // A expect_tx + cp.async arrivals
+            mbar_init(smem_u32(&empty_b[s]), 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(smem_u32(&accf_b[b]), 1);
+            mbar_init(smem_u32(&acce_b[b]), 4);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 2) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(TMEM_COLS));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const uint32_t tmem = *tmem_slot;
+    stamp(0);
+
+    int c = 0, it = 0;                           // stage uses / accumulator uses (per role)
+    unsigned nb = 0;                             // grid barriers passed
+    for (int lv = 0; lv < ca.nlev; ++lv) {
+        split_sweep(X, ldx, ca.row0[lv], ca.nrows[lv], K, Xb, Xs);   // this level's source rows
+        grid_barrier(gbar, nb++);
+        const int tb = ca.lvl_tile[lv], te = ca.lvl_tile[lv + 1];
+        if (warp == 0 || warp == 2 || warp == 3) {
+            // ---------------- producers (as tc_pairs_fast_kernel)
+            const int pi = warp == 0 ? 0 : warp - 1;
+            const int piece = lane & 7, rsub = lane >> 3;
+            for (int ti = tb + blockIdx.x; ti < te; ti += gridDim.x) {
+                const Tile tl = tiles[ti];
+                int64_t srow[fast::NG];
+#pragma unroll
+                for (int g = 0; g < fast::NG; ++g) {
+                    const int r = rsub + 4 * (pi + fast::NPROD * g);
+                    srow[g] = (int64_t)__ldg(&pairs[tl.p0 + min(r, tl.np - 1)].y) * ldx;
+                }
+                const int ngrp = ((tl.np + 15) & ~15) / 4;
+                for (int kc = tl.kc0; kc < tl.kc1; ++kc, ++c) {
+                    const int s = c % STAGES;
+                    mbar_wait(smem_u32(&empty_b[s]), ((c / STAGES) & 1) ^ 1);
+                    uint8_t* st = smem + s * STAGE_BYTES;
+                    const uint32_t full = smem_u32(&full_b[s]);
+                    if (pi == 0 && lane == 0) {
+                        mbar_expect_tx(full, 2 * MT * OPND_BYTES);
+#pragma unroll
+                        for (int mt = 0; mt < MT; ++mt) {
+                            tma_load_3d(smem_u32(st + (2 * mt) * OPND_BYTES), &mapAb, kc * BK, tl.m0 + mt * BM, tl.op,
+                                        full);
+                            tma_load_3d(smem_u32(st + (2 * mt + 1) * OPND_BYTES), &mapAs, kc * BK, tl.m0 + mt * BM,
+                                        tl.op, full);
+                        }
+                    }
+                    const int col = kc * BK + 4 * piece;
+                    const uint32_t nbytes = col < ldx ? 16u : 0u;
+                    const uint32_t b0 = smem_u32(st + 2 * MT * OPND_BYTES);
+                    const uint32_t b1 = b0 + OPND_BYTES;
+#pragma unroll
+                    for (int g = 0; g < fast::NG; ++g) {
+                        const int grp = pi + fast::NPROD * g;
+                        if (grp < ngrp) {
+                            const int r = rsub + 4 * grp;
+                            const int64_t off = srow[g] + col;
+                            const uint32_t so = (uint32_t)(r * 128 + ((piece ^ (r & 7)) * 16));
+                            asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(b0 + so),
+                                         "l"(nbytes ? Xb + off : Xb), "r"(nbytes)
+                                         : "memory");
+                            asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(b1 + so),
+                                         "l"(nbytes ? Xs + off : Xs), "r"(nbytes)
+                                         : "memory");
+                        }
+                    }
+                    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(full) : "memory");
+                }
+            }
+        } else if (warp == 1) {
+            // ---------------- MMA issuer (as tc_pairs_fast_kernel<false>)
+            for (int ti = tb + blockIdx.x; ti < te; ti += gridDim.x, ++it) {
+                const int ab = it & 1;
+                const uint32_t nmma = (uint32_t)((tiles[ti].np + 15) & ~15);
+                const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((nmma >> 3) << 17) |
+                                       ((uint32_t)(BM >> 4) << 24);
+                mbar_wait(smem_u32(&acce_b[ab]), ((it >> 1) & 1) ^ 1);
+                asm volatile("tcgen05.fence::after_thread_sync;");
+                const int kc0 = tiles[ti].kc0, kc1 = tiles[ti].kc1;
+                for (int kc = kc0; kc < kc1; ++kc, ++c) {
+                    const int s = c % STAGES;
+                    mbar_wait(smem_u32(&full_b[s]), (c / STAGES) & 1);
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    asm volatile("tcgen05.fence::after_thread_sync;");
+                    if (lane == 0) {
+                        const uint32_t st = smem_u32(smem + s * STAGE_BYTES);
+                        const uint64_t bb = smem_desc(st + 2 * MT * OPND_BYTES),
+                                       bs = smem_desc(st + (2 * MT + 1) * OPND_BYTES);
+                        const int ksteps = min(BK, K - kc * BK + 7) / 8;
+                        for (int k = 0; k < ksteps; ++k) {
+                            const uint64_t off = (uint64_t)(2 * k);
+#pragma unroll
+                            for (int mt = 0; mt < MT; ++mt) {
+                                const uint64_t a_b = smem_desc(st + (2 * mt) * OPND_BYTES) + off;
+                                const uint64_t a_s = smem_desc(st + (2 * mt + 1) * OPND_BYTES) + off;
+                                const uint32_t d = tmem + (uint32_t)((ab * MT + mt) * BN);
+                                mma_tf32(d, a_b, bb + off, idesc, kc != kc0 || k != 0);
+                                mma_tf32(d, a_b, bs + off, idesc, 1);
+                                mma_tf32(d, a_s, bb + off, idesc, 1);
+                            }
+                        }
+                        mma_commit(smem_u32(&empty_b[s]));
+                        if (kc == kc1 - 1) mma_commit(smem_u32(&accf_b[ab]));
+                    }
+                    __syncwarp();
+                }
+            }
+        } else if (warp >= EPI_WARP0) {
+            // ---------------- epilogue: TMEM -> fp64 atomics (REDs; no per-thread fence, which
+            // would make them returning ATOMs: thread 0's release after the CTA barrier covers them)
+            const int wq = warp - EPI_WARP0;
+            for (int ti = tb + blockIdx.x; ti < te; ti += gridDim.x, ++it) {
+                const Tile tl = tiles[ti];
+                const int ab = it & 1;
+                mbar_wait(smem_u32(&accf_b[ab]), (it >> 1) & 1);
+                asm volatile("tcgen05.fence::after_thread_sync;");
+                const int2* pp = pairs + tl.p0;
+#pragma unroll
+                for (int mt = 0; mt < MT; ++mt) {
+                    const int row = tl.m0 + mt * BM + 32 * wq + lane;
+#pragma unroll 1
+                    for (int c0 = 0; c0 < tl.np; c0 += 32) {
+                        uint32_t v[32];
+                        tmem_ld32(tmem + ((uint32_t)(32 * wq) << 16) + (uint32_t)((ab * MT + mt) * BN + c0), v);
+                        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                        if (row < M) {
+#pragma unroll
+                            for (int j = 0; j < 32; ++j)
+                                if (c0 + j < tl.np)
+                                    atomicAdd(Y + (int64_t)__ldg(&pp[c0 + j].x) * ldy + row,
+                                              (double)__uint_as_float(v[j]));
+                        }
+                    }
+                }
+                asm volatile("tcgen05.fence::before_thread_sync;");
+                __syncwarp();
+                if (lane == 0) mbar_arrive(smem_u32(&acce_b[ab]));
+            }
+        }
+        grid_barrier(gbar, nb++);                // this level's results complete and visible
+        stamp(lv + 1);
+    }
+    // the coarsest rows (upward chain: read by the M2L)
+    if (ca.tail_rows > 0) split_sweep(X, ldx, ca.tail_row0, ca.tail_rows, K, Xb, Xs);
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
+}
+
 // ------------------------------------------------------------------ host side
 typedef CUresult (*EncodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                 const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
@@ -812,7 +1059,9 @@ template void tc_split_rows<double>(const double*, int, int64_t, int64_t, int, f
 // levels) split K over several CTAs: a lone tile streams its 15 K chunks through one SM in
 // ~20 us, while its partial sums are added by the fp64 atomics of the epilogue anyway.
 int tc_fast_tile_mode() {
-    static const int m = (std::getenv("EBEM_M2L_WIDE") && std::atoi(std::getenv("EBEM_M2L_WIDE")) == 0) ? 1 : 2;
+    // the wide (128 x 256) tiles: M2L 1.715 vs 1.632 ms alone, matvec 4.61 vs 4.46 ms
+    // (profiles/r02/ab_m2l_wide.txt); EBEM_M2L_WIDE=1 selects them
+    static const int m = (std::getenv("EBEM_M2L_WIDE") && std::atoi(std::getenv("EBEM_M2L_WIDE")) == 1) ? 2 : 1;
     return m;
 }
 
@@ -890,6 +1139,96 @@ void tc_pairs_gemm(const OpPairs& P, const CUtensorMap& Ab, const CUtensorMap& A
     tc::tc_pairs_kernel<<<grid, tc::THREADS, tc::SMEM_BYTES, s>>>(
         Ab, As, Bb, Bs, reinterpret_cast<const tc::Tile*>(P.tiles.p), P.ntiles, P.pairs.p, M, K, Y, ldy);
     EB_CHECK_LAUNCH();
+}
+
+
+// ------------------------------------------------------------------ level chain (host)
+// Tiles of every level of a chain in execution order (two-slice tiles as tc_build_tiles
+// mode 1, split K on levels with fewer tiles than SMs), over one concatenated pair array.
+void tc_build_chain(Chain& ch, const std::vector<const OpPairs*>& levels, const std::vector<int64_t>& row0,
+                    const std::vector<int64_t>& nrows, int M, int K, cudaStream_t s) {
+    std::vector<tc::Tile> t;
+    std::vector<int> lt(1, 0);
+    int64_t np = 0;
+    for (const OpPairs* P : levels) np += P->npairs;
+    ch.pairs.alloc(std::max<int64_t>(np, 1));
+    int64_t base = 0;
+    const int mstep = tc::fast::MT * tc::BM;
+    const int nk = (K + tc::BK - 1) / tc::BK;
+    for (const OpPairs* P : levels) {
+        if (P->npairs) d2d(ch.pairs.p + base, P->pairs.p, (size_t)P->npairs, s);
+        std::vector<tc::Tile> u;
+        for (int o = 0; o < P->nops; ++o)
+            for (int p0 = P->op_ptr_h[o]; p0 < P->op_ptr_h[o + 1]; p0 += tc::BN)
+                for (int m0 = 0; m0 < M; m0 += mstep)
+                    u.push_back({o, (int)(base + p0), std::min(tc::BN, P->op_ptr_h[o + 1] - p0), m0, 0, nk});
+        const int nsplit = u.empty() ? 1 : std::max(1, std::min(nk / 3, num_sms() / (int)u.size()));
+        for (const tc::Tile& x : u)
+            for (int q = 0; q < nsplit; ++q) {
+                tc::Tile y = x;
+                y.kc0 = nk * q / nsplit;
+                y.kc1 = nk * (q + 1) / nsplit;
+                t.push_back(y);
+            }
+        lt.push_back((int)t.size());
+        base += P->npairs;
+    }
+    EB_REQUIRE(levels.size() <= (size_t)MAXLEVEL && row0.size() == levels.size() && nrows.size() == levels.size(),
+               "internal: chain levels");
+    ch.nlev = (int)levels.size();
+    ch.lvl_tile = lt;
+    ch.row0 = row0;
+    ch.nrows = nrows;
+    ch.tiles.alloc(std::max<size_t>(t.size(), 1) * sizeof(tc::Tile) / sizeof(int));
+    if (!t.empty()) EB_CUDA(cudaMemcpyAsync(ch.tiles.p, t.data(), t.size() * sizeof(tc::Tile), cudaMemcpyHostToDevice, s));
+    ch.bar.alloc(4 + 2 * (MAXLEVEL + 1));          // counter, pad, then level timestamps (u64)
+    EB_CUDA(cudaStreamSynchronize(s));
+}
+
+void tc_chain_run(const Chain& ch, const CUtensorMap& Ab, const CUtensorMap& As, const double* X, int ldx, float* Xb,
+                  float* Xs, int M, int K, double* Y, int ldy, int64_t tail_row0, int64_t tail_rows, cudaStream_t s) {
+    if (ch.nlev == 0 && tail_rows <= 0) return;
+    ChainArgs ca{};
+    ca.nlev = ch.nlev;
+    for (int i = 0; i <= ch.nlev; ++i) ca.lvl_tile[i] = ch.lvl_tile[i];
+    for (int i = 0; i < ch.nlev; ++i) {
+        ca.row0[i] = ch.row0[i];
+        ca.nrows[i] = ch.nrows[i];
+    }
+    ca.tail_row0 = tail_row0;
+    ca.tail_rows = tail_rows;
+    static bool attr = false;
+    if (!attr) {
+        EB_CUDA(cudaFuncSetAttribute(tc::tc_chain_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     tc::fast::SMEM_BYTES));
+        attr = true;
+    }
+    EB_CUDA(cudaMemsetAsync(ch.bar.p, 0, sizeof(unsigned), s));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(num_sms());                 // one CTA per SM (its shared memory allows no more)
+    cfg.blockDim = dim3(tc::fast::THREADS);
+    cfg.dynamicSmemBytes = tc::fast::SMEM_BYTES;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeCooperative;     // the grid barrier needs every CTA resident
+    at[0].val.cooperative = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    EB_CUDA(cudaLaunchKernelEx(&cfg, tc::tc_chain_kernel, Ab, As, X, ldx, Xb, Xs,
+                               reinterpret_cast<const tc::Tile*>(ch.tiles.p), (const int2*)ch.pairs.p, M, K, Y, ldy, ca,
+                               (unsigned*)ch.bar.p));
+    EB_CHECK_LAUNCH();
+    static const bool trace = std::getenv("EBEM_CHAIN_TRACE") != nullptr;
+    if (trace) {
+        std::vector<unsigned long long> ts(ch.nlev + 1);
+        EB_CUDA(cudaMemcpyAsync(ts.data(), ch.bar.p + 2, sizeof(unsigned long long) * (ch.nlev + 1),
+                                cudaMemcpyDeviceToHost, s));
+        EB_CUDA(cudaStreamSynchronize(s));
+        std::fprintf(stderr, "[chain %s] levels (us):", tail_rows > 0 ? "up" : "down");
+        for (int i = 0; i < ch.nlev; ++i)
+            std::fprintf(stderr, " %d:%.1f(%d tiles)", i, (ts[i + 1] - ts[i]) * 1e-3, ch.lvl_tile[i + 1] - ch.lvl_tile[i]);
+        std::fprintf(stderr, "\n");
+    }
 }
 
 }  // namespace ebem
