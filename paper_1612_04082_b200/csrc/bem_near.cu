@@ -505,6 +505,7 @@ bool panel_op_build(const Tree& t, PanelOp::Kind kind, int nq, int64_t npanels, 
         tot += 9LL * hr[i] * ((hn[i] + 3) & ~3);   // rows padded to 4 columns (16-B aligned)
     }
     size_t fr = 0, tt = 0;
+    cache_trim();                              // cached blocks count as free memory here
     EB_CUDA(cudaMemGetInfo(&fr, &tt));
     const double frac = std::getenv("EBEM_BEM_NEARMAT_FRAC") ? std::atof(std::getenv("EBEM_BEM_NEARMAT_FRAC")) : 0.6;
     if ((double)tot * 4.0 > frac * (double)fr) {

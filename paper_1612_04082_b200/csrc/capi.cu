@@ -1,7 +1,10 @@
 // extern "C" boundary of the library (include/elastobem.h).  Argument checking, host
 // staging of host-pointer calls, exception -> error-code translation.  No compute here.
+#include <cstdlib>
 #include <cstring>
 #include <initializer_list>
+#include <map>
+#include <mutex>
 
 #include "../../include/elastobem.h"
 #include "fmm.cuh"
@@ -25,6 +28,74 @@ bool is_device_ptr(const void* p) {
         return false;
     }
     return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+// ------------------------------------------------------------------ block cache (DBuf)
+namespace {
+struct BlockCache {
+    std::mutex mu;
+    std::multimap<size_t, void*> free_blocks;   // rounded size -> block
+    size_t cached = 0, cap = 0;
+    BlockCache() {
+        const char* e = std::getenv("EBEM_CACHE_MB");
+        cap = (size_t)(e ? std::atoll(e) : 16384) << 20;
+    }
+};
+BlockCache& block_cache() {
+    static BlockCache* c = new BlockCache;      // never destroyed: DBufs may outlive statics
+    return *c;
+}
+constexpr size_t CACHE_MIN = 1 << 20, CACHE_GRAIN = 2 << 20;
+size_t cache_round(size_t b) { return (b + CACHE_GRAIN - 1) / CACHE_GRAIN * CACHE_GRAIN; }
+}  // namespace
+
+void* cache_alloc(size_t bytes) {
+    void* p = nullptr;
+    if (bytes >= CACHE_MIN) {
+        BlockCache& c = block_cache();
+        const size_t r = cache_round(bytes);
+        {
+            std::lock_guard<std::mutex> g(c.mu);
+            auto it = c.free_blocks.find(r);
+            if (it != c.free_blocks.end()) {
+                p = it->second;
+                c.free_blocks.erase(it);
+                c.cached -= r;
+                return p;
+            }
+        }
+        if (cudaMalloc(&p, r) != cudaSuccess) {   // out of memory: return the cache, retry once
+            cudaGetLastError();
+            cache_trim();
+            EB_CUDA(cudaMalloc(&p, r));
+        }
+        return p;
+    }
+    EB_CUDA(cudaMalloc(&p, bytes));
+    return p;
+}
+
+void cache_free(void* p, size_t bytes) {
+    if (!p) return;
+    if (bytes >= CACHE_MIN) {
+        BlockCache& c = block_cache();
+        const size_t r = cache_round(bytes);
+        std::lock_guard<std::mutex> g(c.mu);
+        if (c.cached + r <= c.cap) {
+            c.free_blocks.emplace(r, p);
+            c.cached += r;
+            return;
+        }
+    }
+    cudaFree(p);
+}
+
+void cache_trim() {
+    BlockCache& c = block_cache();
+    std::lock_guard<std::mutex> g(c.mu);
+    for (auto& kv : c.free_blocks) cudaFree(kv.second);
+    c.free_blocks.clear();
+    c.cached = 0;
 }
 
 int num_sms() {

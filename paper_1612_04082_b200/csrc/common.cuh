@@ -41,8 +41,17 @@ void count_launch();
     } while (0)
 
 // ------------------------------------------------------------------ device buffers
-// Owning device allocation (cudaMalloc; the library's only allocator for long-lived
-// state, stream-ordered cudaMallocAsync for per-call scratch).
+// Block cache behind DBuf: released blocks of >= 1 MB are kept (up to a total of
+// EBEM_CACHE_MB, default 16 GB) and handed out again to an allocation of the same rounded
+// size, so rebuilding a tree of the same problem allocates nothing (cudaMalloc + cudaFree of
+// the ~1 GB workspace cost 4-5 ms of a 1M-point build).  cache_trim() returns everything to
+// the driver (before free-memory queries).
+void* cache_alloc(size_t bytes);
+void cache_free(void* p, size_t bytes);
+void cache_trim();
+
+// Owning device allocation (the block cache above; the library's only allocator for
+// long-lived state, stream-ordered cudaMallocAsync for per-call scratch).
 template <class T>
 struct DBuf {
     T* p = nullptr;
@@ -60,10 +69,10 @@ struct DBuf {
     void alloc(size_t n_) {
         release();
         n = n_;
-        if (n) EB_CUDA(cudaMalloc(&p, n * sizeof(T)));
+        if (n) p = (T*)cache_alloc(n * sizeof(T));
     }
     void release() {
-        if (p) cudaFree(p);
+        if (p) cache_free(p, n * sizeof(T));
         p = nullptr;
         n = 0;
     }

@@ -691,139 +691,6 @@ near_eval_p_kernel(int n_eval, const int* __restrict__ eval_box, const int* __re
     }
 }
 
-// near field, version 2: the leaf's near sources as MERGED contiguous ranges of the sorted
-// source array (neighbouring boxes are mostly adjacent in Morton order, so ~27 boxes of ~24
-// sources collapse into a few long runs and the 32-source tiles are full), staged per warp by
-// cp.async into a double buffer: the next tile is in flight while the current one is summed.
-// A range flagged `safe` contains the target leaf's own sources (the only place where r = 0
-// can occur, reading R8) and uses the r = 0-excluding pair loop.
-__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
-                 "l"(src)
-                 : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
-
-template <bool SL, bool DL, bool STRESS, int TPT>
-__device__ __forceinline__ void near_round2(int t0, int t_beg, int t_end, int L, int e0, int e1,
-                                            const int2* __restrict__ rng, const float* __restrict__ trg,
-                                            const float4* __restrict__ rec, const KConst& kc,
-                                            float* __restrict__ near, float4* buf, int lane) {
-    constexpr int NC = STRESS ? 6 : 3;
-    constexpr int R = STRESS ? REC_STRESS : REC_DISP;
-    constexpr int RS = R + 1;
-    constexpr int TILE = NEAR_TILE;
-    const int G = 32 / L, grp = lane / L, l = lane % L;
-    float x[TPT], y[TPT], z[TPT], acc[TPT][NC];
-#pragma unroll
-    for (int j = 0; j < TPT; ++j) {
-        const int t = t0 + l + L * j;
-        const int tc = t < t_end ? t : t_beg;
-        x[j] = trg[3 * tc];
-        y[j] = trg[3 * tc + 1];
-        z[j] = trg[3 * tc + 2];
-#pragma unroll
-        for (int c = 0; c < NC; ++c) acc[j][c] = 0.f;
-    }
-    auto issue = [&](float4* dst, int s, int cnt) {
-        const float4* src = rec + (int64_t)s * R;
-        for (int q = lane; q < cnt * R; q += 32) cp_async16(dst + (q / R) * RS + q % R, src + q);
-        cp_async_commit();
-    };
-    int e = e0, s = 0, rend = 0;
-    bool safe = false;
-    if (e < e1) {
-        const int2 r = rng[e];
-        s = r.x;
-        rend = r.y & 0x7fffffff;
-        safe = r.y < 0;
-    }
-    int cnt = e < e1 ? min(TILE, rend - s) : 0;
-    int b = 0;
-    if (cnt) issue(buf, s, cnt);
-    while (cnt > 0) {
-        int ns = s + cnt, ncnt = 0;
-        bool nsafe = safe;
-        if (ns >= rend) {
-            if (++e < e1) {
-                const int2 r = rng[e];
-                ns = r.x;
-                rend = r.y & 0x7fffffff;
-                nsafe = r.y < 0;
-                ncnt = min(TILE, rend - ns);
-            }
-        } else {
-            ncnt = min(TILE, rend - ns);
-        }
-        if (ncnt) {
-            issue(buf + (b ^ 1) * TILE * RS, ns, ncnt);
-            cp_async_wait<1>();
-        } else {
-            cp_async_wait<0>();
-        }
-        __syncwarp();
-        const float4* cur = buf + b * TILE * RS;
-        if (safe) pair_loop_strided<SL, DL, STRESS, TPT, RS, true>(cur, cnt, grp, G, x, y, z, kc, acc);
-        else pair_loop_strided<SL, DL, STRESS, TPT, RS, false>(cur, cnt, grp, G, x, y, z, kc, acc);
-        __syncwarp();                  // the buffer is refilled two tiles later
-        s = ns;
-        safe = nsafe;
-        cnt = ncnt;
-        b ^= 1;
-    }
-    reduce_groups<NC, TPT>(acc, L);
-    if (grp == 0)
-#pragma unroll
-        for (int j = 0; j < TPT; ++j) {
-            const int t = t0 + l + L * j;
-            if (t < t_end)
-#pragma unroll
-                for (int c = 0; c < NC; ++c)   // acc_DS accumulates half of the diagonal
-                    near[(int64_t)t * NC + c] = (STRESS && SL && DL && c < 3) ? 2.f * acc[j][c] : acc[j][c];
-        }
-}
-
-template <bool SL, bool DL, bool STRESS>
-__global__ void __launch_bounds__(32 * EV_WARPS)
-near_eval2_kernel(int n_eval, const int* __restrict__ eval_box, const int* __restrict__ roff,
-                  const int2* __restrict__ rng, const int* __restrict__ tbeg, const int* __restrict__ tend,
-                  const float* __restrict__ trg, const float4* __restrict__ rec, KConst kc, float* __restrict__ near) {
-    constexpr int R = STRESS ? REC_STRESS : REC_DISP;
-    __shared__ __align__(16) float4 buf_all[EV_WARPS][2 * NEAR_TILE * (R + 1)];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int i = blockIdx.x * EV_WARPS + warp;
-    if (i >= n_eval) return;
-    float4* buf = buf_all[warp];
-    const int b = eval_box[i];
-    const int t_beg = tbeg[b], t_end = tend[b];
-    const int e0 = roff[b], e1 = roff[b + 1];
-    for (int t0 = t_beg; t0 < t_end;) {
-        int L;
-#define EB_NEAR2(T) near_round2<SL, DL, STRESS, T>(t0, t_beg, t_end, L, e0, e1, rng, trg, rec, kc, near, buf, lane)
-        if constexpr (STRESS) {
-            const int tpt = lane_groups_max<NEAR_TMAX_STRESS>(t_end - t0, L);
-            if (tpt == 1) EB_NEAR2(1);
-#if NEAR_TMAX_STRESS >= 3
-            else if (tpt == 3) EB_NEAR2(3);
-#endif
-            else EB_NEAR2(2);
-            t0 += L * tpt;
-        } else {
-            const int tpt = lane_groups(t_end - t0, L);
-            switch (tpt) {
-                case 1: EB_NEAR2(1); break;
-                case 2: EB_NEAR2(2); break;
-                case 3: EB_NEAR2(3); break;
-                default: EB_NEAR2(4); break;
-            }
-            t0 += L * tpt;
-        }
-#undef EB_NEAR2
-    }
-}
-
 // precise M2L (p >= 9, GMRES) on the two-slice fast-kernel data flow with drained groups;
 // EBEM_M2L_DRAIN=0 selects the one-slice precise kernel instead
 static bool m2l_drain_fast() {
@@ -931,6 +798,64 @@ static void build_m2l_pairs(Tree& t, int nb, double vdir, cudaStream_t s) {
     EB_CUDA(cudaStreamSynchronize(s));
 }
 
+// ------------------------------------------------------------------ leaf lists (device)
+// Per target leaf b: the near list (sources summed directly: the U list, the V entries cheaper
+// direct (reading R11), the X entries when b is cheaper direct, the W entries whose box holds
+// few sources) and the M2T list (the other W entries), in that order -- the order the near
+// field sums them.  Pass 1 counts (and the near sources per leaf for the work counts), pass 2
+// fills at the scanned offsets.
+struct NearRule {
+    int xw_direct, v_dir_on, nc;
+    double w_thresh, v_thresh;   // w_direct: nsub < w_thresh; v_direct: nsub * tsub < v_thresh
+};
+
+template <bool FILL>
+__global__ void leaf_lists_kernel(int nb, const int* __restrict__ leaf, const int* __restrict__ nsub,
+                                  const int* __restrict__ tsub, const int* __restrict__ uoff,
+                                  const int* __restrict__ uidx, const int* __restrict__ voff,
+                                  const int* __restrict__ vidx, const int* __restrict__ woff,
+                                  const int* __restrict__ widx, const int* __restrict__ xoff,
+                                  const int* __restrict__ xidx, NearRule r, int* __restrict__ ncnt,
+                                  int* __restrict__ mcnt, int* __restrict__ nsrc, const int* __restrict__ npos,
+                                  const int* __restrict__ mpos, int* __restrict__ nidx, int* __restrict__ midx) {
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= nb) {                               // the last CSR entry: counts 0 before the scan
+        if (!FILL && b == nb) ncnt[b] = mcnt[b] = 0;
+        return;
+    }
+    int n = 0, m = 0, ns = 0;
+    const int np0 = FILL ? npos[b] : 0, mp0 = FILL ? mpos[b] : 0;
+    auto put_n = [&](int a) {
+        if (FILL) nidx[np0 + n] = a;
+        ++n;
+        ns += nsub[a];
+    };
+    if (leaf[b] && tsub[b] > 0) {
+        for (int e = uoff[b]; e < uoff[b + 1]; ++e) put_n(uidx[e]);
+        for (int e = voff[b]; e < voff[b + 1]; ++e) {
+            const int a = vidx[e];
+            if (nsub[a] > 0 && r.v_dir_on && leaf[a] && (double)nsub[a] * tsub[b] < r.v_thresh) put_n(a);
+        }
+        if (r.xw_direct && tsub[b] < r.nc)
+            for (int e = xoff[b]; e < xoff[b + 1]; ++e)
+                if (nsub[xidx[e]] > 0) put_n(xidx[e]);
+        for (int e = woff[b]; e < woff[b + 1]; ++e) {
+            const int a = widx[e];
+            if (nsub[a] == 0) continue;
+            if (r.xw_direct && nsub[a] < r.w_thresh) put_n(a);
+            else {
+                if (FILL) midx[mp0 + m] = a;
+                ++m;
+            }
+        }
+    }
+    if (!FILL) {
+        ncnt[b] = n;
+        mcnt[b] = m;
+        nsrc[b] = ns;
+    }
+}
+
 // ------------------------------------------------------------------ schedule (host)
 void schedule_tree(Tree& t, cudaStream_t s) {
     const Plan& P = *t.plan;
@@ -952,9 +877,9 @@ void schedule_tree(Tree& t, cudaStream_t s) {
     };
     std::vector<int> level = dl(t.level, nb), parent = dl(t.parent, nb), child = dl(t.child, 8 * (size_t)nb),
                      leaf = dl(t.is_leaf, nb), nsub = dl(t.nsrc_sub, nb), tsub = dl(t.ntrg_sub, nb),
-                     anchor = dl(t.anchor, 3 * (size_t)nb), hsb = dl(t.sbeg, nb), hse = dl(t.send, nb);
+                     anchor = dl(t.anchor, 3 * (size_t)nb);
     std::vector<int> off[4], idx[4];
-    for (int k = 0; k < 4; ++k) {
+    for (int k = 2; k < 4; ++k) {            // W, X (the U and V lists stay on the device)
         off[k] = dl(t.lst_off[k], nb + 1);
         idx[k] = dl(t.lst_idx[k], t.lst_n[k]);
     }
@@ -1027,17 +952,16 @@ void schedule_tree(Tree& t, cudaStream_t s) {
     const bool xw_direct = !(std::getenv("EBEM_XW_DIRECT") && std::atoi(std::getenv("EBEM_XW_DIRECT")) == 0);
     auto x_direct = [&](int b) { return xw_direct && leaf[b] && tsub[b] < P.nc; };
     const double wf = std::getenv("EBEM_W_DIRECT_F") ? std::atof(std::getenv("EBEM_W_DIRECT_F")) : t.w_direct;
-    auto w_direct = [&](int a) { return xw_direct && nsub[a] < wf * P.ne; };
+    // (w_direct(a): xw_direct && nsub[a] < wf n_e -- applied by leaf_lists_kernel)
     // V-list pairs of two leaves with few points: one M2L costs ~ (3 n_e)^2 tensor-core MACs
     // (x3 for 3xTF32) plus its share of the fp64 state; summing the nsrc x ntrg pairs directly
     // is cheaper below ~kappa (3 n_e)^2 pair interactions (kappa measured on the 1M beam).
     static const double kappa = std::getenv("EBEM_V_DIRECT") ? std::atof(std::getenv("EBEM_V_DIRECT")) : 0.006;
     // (only with the fp32 far field, p <= 8: at p >= 9 the fp32 direct sums would exceed the
     // fp64 far field's error, measured 1.5e-6 vs 5.5e-7 at p = 10)
+    // (v_direct(b, a): both leaves, nsub[a] tsub[b] < kappa (3 n_e)^2 -- leaf_lists_kernel and
+    // the M2L pair table)
     const bool v_dir_on = xw_direct && P.p < FAR_FP64_MIN_P;
-    auto v_direct = [&](int b, int a) {
-        return v_dir_on && leaf[b] && leaf[a] && (double)nsub[a] * tsub[b] < kappa * (double)P.me * P.me;
-    };
 
     // S2L: boxes with X-list leaves that hold sources
     std::vector<int> s2l, xoff(1, 0), xidx;
@@ -1091,60 +1015,37 @@ void schedule_tree(Tree& t, cudaStream_t s) {
     }
 
     lap("l2l");
-    // leaf evaluation: near list (U + direct X + direct W) and M2T list (the other W entries)
+    // leaf evaluation: near list (U + direct V / X / W) and M2T list (the other W entries), on
+    // the device; the host keeps the M2T list (PHI_U slots) and the near sources per leaf
     std::vector<int> ev, l2t, phid_box, phiu_box, phiu(nb, -1);
-    std::vector<int> noff(nb + 1, 0), nidx, moff(nb + 1, 0), midx;
-    for (int b = 0; b < nb; ++b) {
-        if (leaf[b] && tsub[b] > 0) {
-            for (int e = off[0][b]; e < off[0][b + 1]; ++e) nidx.push_back(idx[0][e]);
-            for (int e = off[1][b]; e < off[1][b + 1]; ++e)
-                if (nsub[idx[1][e]] > 0 && v_direct(b, idx[1][e])) nidx.push_back(idx[1][e]);
-            if (x_direct(b))
-                for (int e = off[3][b]; e < off[3][b + 1]; ++e)
-                    if (nsub[idx[3][e]] > 0) nidx.push_back(idx[3][e]);
-            for (int e = off[2][b]; e < off[2][b + 1]; ++e) {
-                const int a = idx[2][e];
-                if (nsub[a] == 0) continue;
-                if (w_direct(a)) nidx.push_back(a);
-                else midx.push_back(a);
-            }
-        }
-        noff[b + 1] = (int)nidx.size();
-        moff[b + 1] = (int)midx.size();
-    }
-    t.near_off.alloc(nb + 1);
-    h2d(t.near_off.p, noff.data(), nb + 1, s);
-    t.near_idx.alloc(std::max<size_t>(nidx.size(), 1));
-    h2d(t.near_idx.p, nidx.data(), nidx.size(), s);
-    // merged source ranges of every near list (near_eval2_kernel)
+    std::vector<int> moff(nb + 1, 0), midx, near_ns(nb);
     {
-        std::vector<int> roff(nb + 1, 0);
-        std::vector<int2> rng, tmp;
-        for (int b = 0; b < nb; ++b) {
-            tmp.clear();
-            for (int e = noff[b]; e < noff[b + 1]; ++e) {
-                const int a = nidx[e];
-                if (hse[a] > hsb[a]) tmp.push_back(make_int2(hsb[a], hse[a]));
-            }
-            std::sort(tmp.begin(), tmp.end(), [](int2 u, int2 v) { return u.x < v.x; });
-            const size_t first = rng.size();
-            for (const int2& r : tmp) {
-                if (rng.size() > first && rng.back().y == r.x) rng.back().y = r.y;
-                else rng.push_back(r);
-            }
-            for (size_t k = first; k < rng.size(); ++k)
-                if (hse[b] > hsb[b] && rng[k].x <= hsb[b] && hsb[b] < rng[k].y) rng[k].y |= (int)0x80000000u;
-            roff[b + 1] = (int)rng.size();
-        }
-        t.near_roff.alloc(nb + 1);
-        h2d(t.near_roff.p, roff.data(), nb + 1, s);
-        t.near_rng.alloc(std::max<size_t>(rng.size(), 1));
-        h2d(t.near_rng.p, rng.data(), rng.size(), s);
+        const NearRule rule{xw_direct ? 1 : 0, v_dir_on ? 1 : 0, P.nc, wf * P.ne,
+                            v_dir_on ? kappa * (double)P.me * P.me : 0.0};
+        DBuf<int> ncnt(nb + 1), mcnt(nb + 1), nsrc(nb);
+        leaf_lists_kernel<false><<<ceil_div(nb + 1, 128), 128, 0, s>>>(
+            nb, t.is_leaf.p, t.nsrc_sub.p, t.ntrg_sub.p, t.lst_off[0].p, t.lst_idx[0].p, t.lst_off[1].p, t.lst_idx[1].p,
+            t.lst_off[2].p, t.lst_idx[2].p, t.lst_off[3].p, t.lst_idx[3].p, rule, ncnt.p, mcnt.p, nsrc.p, nullptr,
+            nullptr, nullptr, nullptr);
+        EB_CHECK_LAUNCH();
+        t.near_off.alloc(nb + 1);
+        t.m2t_off.alloc(nb + 1);
+        const int64_t nn = exclusive_scan_i32(ncnt.p, t.near_off.p, nb + 1, s);
+        const int64_t nm = exclusive_scan_i32(mcnt.p, t.m2t_off.p, nb + 1, s);
+        t.near_idx.alloc(std::max<int64_t>(nn, 1));
+        t.m2t_idx.alloc(std::max<int64_t>(nm, 1));
+        leaf_lists_kernel<true><<<ceil_div(nb, 128), 128, 0, s>>>(
+            nb, t.is_leaf.p, t.nsrc_sub.p, t.ntrg_sub.p, t.lst_off[0].p, t.lst_idx[0].p, t.lst_off[1].p, t.lst_idx[1].p,
+            t.lst_off[2].p, t.lst_idx[2].p, t.lst_off[3].p, t.lst_idx[3].p, rule, nullptr, nullptr, nullptr,
+            t.near_off.p, t.m2t_off.p, t.near_idx.p, t.m2t_idx.p);
+        EB_CHECK_LAUNCH();
+        midx.resize(nm);
+        d2h(moff.data(), t.m2t_off.p, nb + 1, s);
+        d2h(midx.data(), t.m2t_idx.p, nm, s);
+        d2h(near_ns.data(), nsrc.p, nb, s);
+        EB_CUDA(cudaStreamSynchronize(s));
     }
-    t.m2t_off.alloc(nb + 1);
-    h2d(t.m2t_off.p, moff.data(), nb + 1, s);
-    t.m2t_idx.alloc(std::max<size_t>(midx.size(), 1));
-    h2d(t.m2t_idx.p, midx.data(), midx.size(), s);
+    lap("  near/m2t lists");
     std::vector<double> phid_scale, phiu_scale;
     std::vector<int2> prd, pru;
     auto half = [&](int b) { return t.side / (double)(1 << level[b]) * 0.5; };
@@ -1169,6 +1070,7 @@ void schedule_tree(Tree& t, cudaStream_t s) {
             }
         }
     }
+    lap("  eval/phi slots");
     // algorithmic work counts for the phase profiler
     {
         const double nc = P.nc, ne = P.ne;
@@ -1179,8 +1081,7 @@ void schedule_tree(Tree& t, cudaStream_t s) {
             for (int e = xoff[i]; e < xoff[i + 1]; ++e) { t.w_s2l_src += nsub[xidx[e]]; t.w_s2l_inter += nsub[xidx[e]] * nc; }
         for (size_t i = 0; i < ev.size(); ++i) {
             const int b = ev[i];
-            double ns = 0;
-            for (int e = noff[b]; e < noff[b + 1]; ++e) ns += nsub[nidx[e]];
+            const double ns = near_ns[b];
             t.w_p2p_src += ns;
             t.w_p2p_inter += ns * tsub[b];
             if (l2t[i] >= 0) t.w_l2t_inter += ne * tsub[b];
@@ -1193,6 +1094,7 @@ void schedule_tree(Tree& t, cudaStream_t s) {
         t.w_m2l_ops = 0;
         for (int o = 0; o < t.m2l.nops; ++o) t.w_m2l_ops += t.m2l.op_ptr_h[o + 1] > t.m2l.op_ptr_h[o];
     }
+    lap("  work counts");
     t.n_eval = (int)ev.size();
     t.n_phid = (int)phid_box.size();
     t.n_phiu = (int)phiu_box.size();
@@ -1466,14 +1368,13 @@ static void launch_near(const Tree& t, cudaStream_t s) {
                                      100));
         carve = true;
     }
-    // near_eval2_kernel (merged ranges, cp.async double buffer) is 3.5% faster alone but made
-    // the overlapped matvec slower (4.41 -> 4.56 ms): the default stays the per-box kernel
-    static const bool v1 = !(std::getenv("EBEM_NEAR_V2") && std::atoi(std::getenv("EBEM_NEAR_V2")));
+    // (a variant staging each leaf's near sources as merged contiguous ranges with a cp.async
+    // double buffer was 3.5% faster alone but made the overlapped matvec slower, 4.41 -> 4.56 ms)
     // EBEM_NEAR_PACKED=1: packed FFMA2 pair loop (two targets per FP32 instruction)
     // (1.348 vs 1.36 ms alone, but the overlapped matvec 4.70 vs 4.45 ms: its 127 registers
     // leave room for fewer near-field CTAs beside the translation CTAs; off by default)
     static const bool packed = std::getenv("EBEM_NEAR_PACKED") && std::atoi(std::getenv("EBEM_NEAR_PACKED")) == 1;
-    if (v1 && packed) {
+    if (packed) {
         static bool carve_p = false;
         if (!carve_p) {
             EB_CUDA(cudaFuncSetAttribute(near_eval_p_kernel<SL, DL, STRESS>,
@@ -1484,21 +1385,10 @@ static void launch_near(const Tree& t, cudaStream_t s) {
         near_eval_p_kernel<SL, DL, STRESS><<<ceil_div(t.n_eval, EV_WARPS), 32 * EV_WARPS, pad, s>>>(
             t.n_eval, t.eval_box.p, t.near_off.p, t.near_idx.p, t.sbeg.p, t.send.p, t.tbeg.p, t.tend.p, t.trg_xyz.p,
             STRESS ? t.rec_stress.p : t.rec_disp.p, kc, t.near_sorted.p);
-    } else if (v1) {
+    } else {
         static const int pad = beside_translation_pad((const void*)near_eval_kernel<SL, DL, STRESS>);
         near_eval_kernel<SL, DL, STRESS><<<ceil_div(t.n_eval, EV_WARPS), 32 * EV_WARPS, pad, s>>>(
             t.n_eval, t.eval_box.p, t.near_off.p, t.near_idx.p, t.sbeg.p, t.send.p, t.tbeg.p, t.tend.p, t.trg_xyz.p,
-            STRESS ? t.rec_stress.p : t.rec_disp.p, kc, t.near_sorted.p);
-    } else {
-        static bool carve2 = false;
-        if (!carve2) {
-            EB_CUDA(cudaFuncSetAttribute(near_eval2_kernel<SL, DL, STRESS>,
-                                         cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-            carve2 = true;
-        }
-        static const int pad = beside_translation_pad((const void*)near_eval2_kernel<SL, DL, STRESS>);
-        near_eval2_kernel<SL, DL, STRESS><<<ceil_div(t.n_eval, EV_WARPS), 32 * EV_WARPS, pad, s>>>(
-            t.n_eval, t.eval_box.p, t.near_roff.p, t.near_rng.p, t.tbeg.p, t.tend.p, t.trg_xyz.p,
             STRESS ? t.rec_stress.p : t.rec_disp.p, kc, t.near_sorted.p);
     }
     EB_CHECK_LAUNCH();

@@ -198,9 +198,6 @@ struct Tree {
     DBuf<int> ssplit;                    // BEM: per leaf, first source of the second boundary-condition group
     int split_mode = 0;                  // 0 off; 1: [sbeg, ssplit) single layer, rest double layer; 2 reverse
     DBuf<int> near_off, near_idx;        // per box: source boxes summed directly (U + direct X/W)
-    DBuf<int> near_roff;                 // per box: CSR offsets into near_rng
-    DBuf<int2> near_rng;                 // the same sources as merged contiguous ranges of the sorted
-                                         // source array: (begin, end | 2^31 if it holds the box's own sources)
     DBuf<int> m2t_off, m2t_idx;          // per box: W-list boxes evaluated from their equivalent density
     // two-stream schedule (fmm_evaluate): created on first use
     cudaStream_t sA = nullptr, sB = nullptr;
