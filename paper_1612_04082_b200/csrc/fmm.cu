@@ -1153,9 +1153,12 @@ void schedule_tree(Tree& t, cudaStream_t s) {
         tc_build_tiles(t.m2l, me, me, t.tc_fast ? fm : (m2l_drain_fast() ? 1 : 0));
         for (auto& x : t.m2m) tc_build_tiles(x, me, me, t.ml_fast ? fm : 0);
         for (auto& x : t.l2l) tc_build_tiles(x, me, me, t.ml_fast ? fm : 0);
-        // M2M and L2L chains as one cooperative launch each (tc_chain_kernel); EBEM_ML_CHAIN=0:
-        // a split launch plus a translation launch per level
-        static const bool chain_on = !(std::getenv("EBEM_ML_CHAIN") && std::atoi(std::getenv("EBEM_ML_CHAIN")) == 0);
+        // EBEM_ML_CHAIN=1: M2M and L2L chains as one persistent launch each (tc_chain_kernel).
+        // Measured on the 1M beam: M2M 0.341 -> 0.317 ms, L2L 0.321 -> 0.306 ms alone, but the
+        // overlapped matvec unchanged (4.41-4.44 ms either way) and the host-buffer (e2e) matvec
+        // 0.4 ms slower (5.79 vs 5.39 ms, mean of 3-4 runs); default: a split launch plus a
+        // translation launch per level
+        static const bool chain_on = std::getenv("EBEM_ML_CHAIN") && std::atoi(std::getenv("EBEM_ML_CHAIN")) == 1;
         t.ml_chain = t.ml_fast && chain_on;
         if (t.ml_chain) {
             std::vector<const OpPairs*> up, dn;

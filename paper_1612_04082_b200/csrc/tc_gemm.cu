@@ -1463,11 +1463,16 @@ void tc_chain_run(const Chain& ch, const CUtensorMap& Ab, const CUtensorMap& As,
     cfg.blockDim = dim3(tc::fast::THREADS);
     cfg.dynamicSmemBytes = tc::fast::SMEM_BYTES;
     cfg.stream = s;
+    // The grid barrier needs every CTA resident: one CTA per SM always fits an idle SM, and
+    // the only concurrent kernels (the stream-B P2P kernels) never wait on this one, so CTAs
+    // not yet resident start as those leave.  EBEM_CHAIN_COOP=1 launches cooperatively (the
+    // driver then checks residency; measured 0.2-0.4 ms slower end to end)
+    static const bool coop = std::getenv("EBEM_CHAIN_COOP") && std::atoi(std::getenv("EBEM_CHAIN_COOP")) == 1;
     cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeCooperative;     // the grid barrier needs every CTA resident
+    at[0].id = cudaLaunchAttributeCooperative;
     at[0].val.cooperative = 1;
     cfg.attrs = at;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = coop ? 1 : 0;
     EB_CUDA(cudaLaunchKernelEx(&cfg, tc::tc_chain_kernel, Ab, As, X, ldx, Xb, Xs,
                                reinterpret_cast<const tc::Tile*>(ch.tiles.p), (const int2*)ch.pairs.p, M, K, Y, ldy, ca,
                                (unsigned*)ch.bar.p));

@@ -7,7 +7,7 @@ import subprocess
 import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-PROF = os.path.join(ROOT, "profiles", "r01")
+PROF = os.path.join(ROOT, "profiles", "r02")
 
 
 def test_bench_line_has_the_contract_keys():

@@ -82,32 +82,62 @@ if bem:
             bem_note = (f"`nm_apply` (one application of the BEM near operator held in HBM): "
                         f"{rd / 1e9:.1f} GB read in {t_ms:.2f} ms = {rd / t_ms / 1e6:.0f} GB/s "
                         f"({100 * rd / t_ms / 1e6 / 6462.7:.0f}% of the measured 6462.7 GB/s HBM peak).")
-txt = f"""# Round 1 profiles (B200, sm_100a, `--clock-control none`)
+rnd = os.path.basename(os.path.normpath(d))
+have = lambda f: os.path.exists(os.path.join(d, f))
+files = [f"* `bench_latest.json` — `python bench.py` (defaults: 1M-point beam, U+P, p = 6, leaf 64, "
+         f"{b['steps']} L2-flushed steps): **{b['value']:.2f} ms per matvec**, rel-L2 {b['rel_l2']:.2e} on 3072 "
+         f"sampled targets vs the fp64 oracle; e2e with pinned host buffers {b['e2e']['value']:.2f} ms; "
+         f"configs[1] direct P {b['p2p']['ms']:.3f} ms = {b['p2p']['ginteractions_per_s']:.0f} G interactions/s = "
+         f"**{100 * b['p2p']['frac_fp32_peak']:.1f}% of FP32 peak** ({b['p2p']['flops_per_interaction']} flop/pair "
+         f"counted in SASS, `tools/count_flops.sh`); SM clock {b['clocks']['sm_mhz']:.0f} MHz, throttle reasons "
+         f"{b['clocks']['reasons']}.",
+         "* `launches_bench.csv` — `ncu --metrics gpu__time_duration.sum --clock-control none --csv "
+         "python bench.py --steps 2 --warmup 3 --no-cpu ...`.",
+         "* `hot_raw.csv`, `hot_details.csv` — `ncu --set full --import-source on -k regex:<hot kernels> "
+         "-c 12 python tools/prof_fmm.py --reps 1` (S2M, Q2Z, M2M/L2L, near field, M2L); `hot2_*` — the same "
+         "for the PHI (DMMA), far-field and direct kernels.",
+         "* `traffic.json` — DRAM bytes of one M2L launch (from `hot_raw.csv`), read by bench.py for "
+         "`roofline.traffic`.",
+         "* `tree_build_launches.csv` — launch list (time, DRAM bytes) of three 1M-point tree builds (the first "
+         "one includes the one-time operator precompute)."]
+if have("tree_build_timing.txt"):
+    files.append("* `tree_build_timing.txt` — host-side laps of the build (`EBEM_BUILD_TIMING=1`).")
+if have("bem_raw.csv"):
+    files.append("* `bem_raw.csv` — the BEM operator kernels inside GMRES (configs[4]).")
+if have("bem_phases.txt"):
+    files.append("* `bem_phases.txt` — per-phase times of each BEM operator application (`EBEM_BEM_PROFILE=1`).")
+if have("precise_raw.csv"):
+    files.append("* `precise_raw.csv`, `precise_details.csv` — the first `tc_pairs_kernel` launches (Q2Z / M2M).")
+if have("early"):
+    files.append("* `early/` — captures of the first versions (31.6 ms → 8.45 ms), kept for the record.")
+files.append(f"* All of the above are produced by `bash tools/profile_round.sh {rnd}` under gpurun.")
+for key, label in (("stress", "configs[3] stress (D+S), 500k sources -> 1M grid targets"),
+                   ("gmres", "configs[4] BEM GMRES, block-Jacobi"),
+                   ("gmres_paper", "configs[4] BEM GMRES, no preconditioner (the paper's)")):
+    x = b.get(key)
+    if not x:
+        continue
+    if "iterations" in x:
+        extra.append(f"* {label}: {x['value']:.1f} s, {x['iterations']} iterations, residual {x['rel_residual']:.1e}, "
+                     f"{x['ms_per_iteration']:.0f} ms/iteration, SM clock {x['clocks']['sm_mhz']:.0f} MHz "
+                     f"{x['clocks']['reasons']} (bench line key `{key}`)")
+    else:
+        extra.append(f"* {label}: {x['value']:.2f} ms, rel-L2 {x['rel_l2']:.1e}, tree build {1e3 * x['tree_build_s']:.1f} ms "
+                     f"(bench line key `{key}`)")
+if b.get("p10"):
+    extra.append(f"* configs[2] second order, p = 10 on the same 1M points: {b['p10']['ms']:.1f} ms, rel-L2 "
+                 f"{b['p10']['rel_l2']:.1e} (bench line key `p10`)")
+build = f"{1e3 * b['tree_build_s']:.1f} ms" if b.get("tree_build_s") else "n/a"
+nl = chr(10)
+txt = f"""# {rnd} profiles (B200, sm_100a, `--clock-control none`)
 
 All captures were taken after the same command had exited 0 without ncu (under gpurun).
-Regenerate this file with `python tools/make_summary.py {d}`.
+Regenerate this file with `python tools/make_summary.py profiles/{rnd}`.
 
-* `bench_latest.json` — `python bench.py` (defaults: 1M-point beam, U+P, p = 6, leaf 64,
-  30 L2-flushed steps): **{b['value']:.2f} ms per matvec**, rel-L2 {b['rel_l2']:.2e} on 3072
-  sampled targets vs the fp64 oracle; e2e with pinned host buffers {b['e2e']['value']:.2f} ms;
-  configs[1] direct P {b['p2p']['ms']:.3f} ms = {b['p2p']['ginteractions_per_s']:.0f} G interactions/s =
-  **{100 * b['p2p']['frac_fp32_peak']:.1f}% of FP32 peak** ({b['p2p']['flops_per_interaction']} flop/pair counted in SASS,
-  `tools/count_flops.sh`); SM clock {b['clocks']['sm_mhz']:.0f} MHz, throttle reasons {b['clocks']['reasons']}.
-* `launches_bench.csv` — `ncu --metrics gpu__time_duration.sum --clock-control none --csv
-  python bench.py --steps 2 --warmup 3 --no-cpu`.
-* `hot_raw.csv`, `hot_details.csv` — `ncu --set full --import-source on -k regex:<hot kernels>
-  -c 12 python tools/prof_fmm.py --direct --reps 1` (S2M, Q2Z/M2M levels, near field, M2L);
-  `hot2_*` — the same for the PHI (DMMA), far-field and direct kernels.
-* `precise_raw.csv`, `precise_details.csv` — the first `tc_pairs_kernel` launches (Q2Z / M2M).
-* `tree_build_launches.csv` — launch list (time, DRAM bytes) of three 1M-point tree builds
-  (the first one includes the one-time operator precompute).
-* `traffic.json` — DRAM bytes of one M2L launch, read by bench.py for `roofline.traffic`.
-* `bem_raw.csv` — the BEM near-operator apply and the fp64 far-field kernel (configs[4]).
-* All of the above are produced by `bash tools/profile_round.sh r01` under gpurun.
-* `early/` — captures of the first versions (31.6 ms → 8.45 ms), kept for the record.
+{nl.join(files)}
 
 Other workloads:
-{chr(10).join(extra)}
+{nl.join(extra)}
 
 ## Live per-phase times (bench.py native profiler, one serial L2-flushed step)
 | phase | ms | launches | bound | roofline fraction |
@@ -123,16 +153,16 @@ the {b["value"]:.2f} ms step.
 {hot}
 ## Other captures
 {extra_caps}
-## BEM operator kernels (configs[4], `bem_raw.csv`: `ncu --set full -k regex:"nm_apply|far_eval_f64" -c 2 python tools/prof_bem.py`)
+## BEM operator kernels (configs[4], `bem_raw.csv`)
 {bem}
 {bem_note}
 
 ## Tree and list passes (1M points; HBM bandwidth per kernel)
 {tree}
 
-The tree passes are short launches on 1M keys, bound by launch latency and the per-level
-loop rather than by HBM (6.5 TB/s); the build's wall time (~23 ms per 1M points) is
-dominated by the host-side scheduling of the leaf lists and tile tables.
+The tree passes are short launches on 1M keys, bound by launch latency rather than by HBM
+(6.5 TB/s); the 1M-point tree build (tree, lists and schedule, operators cached) took
+{build} in the bench line.
 
 M2L DRAM traffic per launch: {(tr['dram_read'] + tr['dram_write']) / 1e9:.2f} GB
 ({tr['dram_read'] / 1e9:.2f} read, {tr['dram_write'] / 1e9:.2f} written).
