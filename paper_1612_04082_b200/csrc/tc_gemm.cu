@@ -383,10 +383,12 @@ tc_pairs_fast_kernel(const __grid_constant__ CUtensorMap mapAb, const __grid_con
                 mbar_wait(smem_u32(&empty_b[s]), ((c / STAGES) & 1) ^ 1);
                 uint8_t* st = smem + s * STAGE_BYTES;
                 const uint32_t full = smem_u32(&full_b[s]);
+                // a second row slice entirely past the operator's M rows is neither loaded nor
+                // multiplied (p = 8: 888 rows = 3.5 tile pairs, 12% of the MMAs saved)
+                const int nmt = tl.m0 + BM < M ? MT : 1;
                 if (pi == 0 && lane == 0) {
-                    mbar_expect_tx(full, 2 * MT * OPND_BYTES);
-#pragma unroll
-                    for (int mt = 0; mt < MT; ++mt) {
+                    mbar_expect_tx(full, 2 * nmt * OPND_BYTES);
+                    for (int mt = 0; mt < nmt; ++mt) {
                         tma_load_3d(smem_u32(st + (2 * mt) * OPND_BYTES), &mapAb, kc * BK, tl.m0 + mt * BM, tl.op, full);
                         tma_load_3d(smem_u32(st + (2 * mt + 1) * OPND_BYTES), &mapAs, kc * BK, tl.m0 + mt * BM, tl.op,
                                     full);
@@ -443,6 +445,7 @@ tc_pairs_fast_kernel(const __grid_constant__ CUtensorMap mapAb, const __grid_con
                         const uint64_t off = (uint64_t)(2 * k);
 #pragma unroll
                         for (int mt = 0; mt < MT; ++mt) {
+                            if (tiles[ti].m0 + mt * BM >= M) continue;
                             const uint64_t a_b = smem_desc(st + (2 * mt) * OPND_BYTES) + off;
                             const uint64_t a_s = smem_desc(st + (2 * mt + 1) * OPND_BYTES) + off;
                             const uint32_t d = tmem + (uint32_t)((b * MT + mt) * BN);
@@ -483,6 +486,7 @@ tc_pairs_fast_kernel(const __grid_constant__ CUtensorMap mapAb, const __grid_con
                         const uint64_t off = (uint64_t)(2 * k);
 #pragma unroll
                         for (int mt = 0; mt < MT; ++mt) {
+                            if (tiles[ti].m0 + mt * BM >= M) continue;
                             const uint64_t a_b = smem_desc(st + (2 * mt) * OPND_BYTES) + off;
                             const uint64_t a_s = smem_desc(st + (2 * mt + 1) * OPND_BYTES) + off;
                             const uint32_t d = tmem + (uint32_t)((ab * MT + mt) * BN);
