@@ -564,209 +564,6 @@ tc_pairs_fast_kernel(const __grid_constant__ CUtensorMap mapAb, const __grid_con
     if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
 }
 
-// ------------------------------------------------------------------ cluster-multicast variant
-// The full-chain two-slice contraction on CTA PAIRS (thread-block clusters of 2): both CTAs
-// of a cluster take pair blocks of the SAME operator and row slices, so the operator tiles
-// (A: 64 of the 96 KB a stage moves) are loaded once per cluster -- each CTA issues half of
-// them by TMA multicast into both CTAs' shared memory -- and only the gathered B rows are per
-// CTA.  Every GEMM of this file was L2-bandwidth bound: a full-rate 3xTF32 MMA stream needs
-// ~64 B / cycle / SM of operands, the L2 supplies ~45-50; multicast brings the demand to
-// ~43 B / cycle.  A stage may be refilled only when BOTH CTAs' MMAs are done with it: each MMA
-// commit arrives on the empty barrier of both CTAs (tcgen05.commit multicast; count 2).
-namespace mc {
-constexpr int CS = 2;                                   // CTAs per cluster
-}
-
-__device__ __forceinline__ void tma_load_3d_mc(uint32_t dst, const CUtensorMap* map, int c0, int c1, int c2,
-                                               uint32_t bar, uint16_t mask) {
-    asm volatile(
-        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster "
-        "[%0], [%1, {%2, %3, %4}], [%5], %6;"
-        ::"r"(dst), "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(bar), "h"(mask)
-        : "memory");
-}
-__device__ __forceinline__ void mma_commit_mc(uint32_t bar, uint16_t mask) {
-    asm volatile(
-        "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
-        ::"r"(bar), "h"(mask)
-        : "memory");
-}
-__device__ __forceinline__ uint32_t cluster_rank() {
-    uint32_t r;
-    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
-    return r;
-}
-__device__ __forceinline__ void cluster_sync() {
-    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
-
-// tiles[2 c + r] is the work of cluster rank r in cluster tile c (same op, m0 and K range)
-__global__ void __launch_bounds__(fast::THREADS, 1)
-tc_pairs_mc_kernel(const __grid_constant__ CUtensorMap mapAb, const __grid_constant__ CUtensorMap mapAs,
-                   const float* __restrict__ Bb, const float* __restrict__ Bs, int ldb,
-                   const Tile* __restrict__ tiles, int nctiles, const int2* __restrict__ pairs, int M, int K,
-                   double* __restrict__ Y, int ldy) {
-    constexpr int MT = fast::MT, STAGES = fast::STAGES, STAGE_BYTES = fast::STAGE_BYTES, TMEM_COLS = fast::TMEM_COLS;
-    extern __shared__ __align__(1024) uint8_t smem_raw[];
-    uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-    uint64_t* bars = (uint64_t*)(smem + STAGES * STAGE_BYTES);
-    uint64_t* full_b = bars;                     // [STAGES]
-    uint64_t* empty_b = bars + STAGES;           // [STAGES]
-    uint64_t* accf_b = bars + 2 * STAGES;        // [2]
-    uint64_t* acce_b = bars + 2 * STAGES + 2;    // [2]
-    uint32_t* tmem_slot = (uint32_t*)(bars + 2 * STAGES + 4);
-
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t rank = cluster_rank();
-    const int cid = blockIdx.x / mc::CS, ncl = gridDim.x / mc::CS;
-    const uint16_t both = (uint16_t)((1u << mc::CS) - 1);
-    if (threadIdx.x == 0) {
-        for (int s = 0; s < STAGES; ++s) {
-            mbar_init(smem_u32(&full_b[s]), 1 + 32 * fast::NPROD);   // A expect_tx + cp.async arrivals
-            mbar_init(smem_u32(&empty_b[s]), mc::CS);                // both CTAs' MMA commits
-        }
-        for (int b = 0; b < 2; ++b) {
-            mbar_init(smem_u32(&accf_b[b]), 1);
-            mbar_init(smem_u32(&acce_b[b]), 4);
-        }
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    if (warp == 2) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                     "r"(TMEM_COLS));
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-    }
-    asm volatile("tcgen05.fence::before_thread_sync;");
-    cluster_sync();                              // both CTAs' barriers initialised before any multicast
-    asm volatile("tcgen05.fence::after_thread_sync;");
-    const uint32_t tmem = *tmem_slot;
-
-    if (warp == 0 || warp == 2 || warp == 3) {
-        // ---------------- producers: this CTA's half of the A tiles (multicast), its own B rows
-        const int pi = warp == 0 ? 0 : warp - 1;
-        const int piece = lane & 7, rsub = lane >> 3;
-        int c = 0;
-        for (int ci = cid; ci < nctiles; ci += ncl) {
-            const Tile tl = tiles[mc::CS * ci + rank];
-            int64_t srow[fast::NG];
-#pragma unroll
-            for (int g = 0; g < fast::NG; ++g) {
-                const int r = rsub + 4 * (pi + fast::NPROD * g);
-                srow[g] = (int64_t)__ldg(&pairs[tl.p0 + max(min(r, tl.np - 1), 0)].y) * ldb;
-            }
-            for (int kc = tl.kc0; kc < tl.kc1; ++kc, ++c) {
-                const int s = c % STAGES;
-                mbar_wait(smem_u32(&empty_b[s]), ((c / STAGES) & 1) ^ 1);
-                uint8_t* st = smem + s * STAGE_BYTES;
-                const uint32_t full = smem_u32(&full_b[s]);
-                if (pi == 0 && lane == 0) {
-                    mbar_expect_tx(full, 2 * MT * OPND_BYTES);          // all four A tiles land here
-                    // rank 0 multicasts the head tiles, rank 1 the remainder tiles
-                    const CUtensorMap* map = rank == 0 ? &mapAb : &mapAs;
-#pragma unroll
-                    for (int mt = 0; mt < MT; ++mt)
-                        tma_load_3d_mc(smem_u32(st + (2 * mt + rank) * OPND_BYTES), map, kc * BK, tl.m0 + mt * BM,
-                                       tl.op, full, both);
-                }
-                const int col = kc * BK + 4 * piece;
-                const uint32_t nb = col < ldb ? 16u : 0u;
-                const int ngrp = ((tl.np + 15) & ~15) / 4;
-                const uint32_t b0 = smem_u32(st + 2 * MT * OPND_BYTES);
-                const uint32_t b1 = b0 + OPND_BYTES;
-#pragma unroll
-                for (int g = 0; g < fast::NG; ++g) {
-                    const int grp = pi + fast::NPROD * g;
-                    if (grp < ngrp) {
-                        const int r = rsub + 4 * grp;
-                        const int64_t off = srow[g] + col;
-                        const uint32_t so = (uint32_t)(r * 128 + ((piece ^ (r & 7)) * 16));
-                        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(b0 + so),
-                                     "l"(nb ? Bb + off : Bb), "r"(nb)
-                                     : "memory");
-                        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(b1 + so),
-                                     "l"(nb ? Bs + off : Bs), "r"(nb)
-                                     : "memory");
-                    }
-                }
-                asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(full) : "memory");
-            }
-        }
-    } else if (warp == 1) {
-        // ---------------- MMA issuer; stage release goes to both CTAs
-        int c = 0, it = 0;
-        for (int ci = cid; ci < nctiles; ci += ncl, ++it) {
-            const Tile tl = tiles[mc::CS * ci + rank];
-            const int ab = it & 1;
-            const uint32_t nmma = (uint32_t)max(16, (tl.np + 15) & ~15);
-            const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((nmma >> 3) << 17) |
-                                   ((uint32_t)(BM >> 4) << 24);
-            mbar_wait(smem_u32(&acce_b[ab]), ((it >> 1) & 1) ^ 1);
-            asm volatile("tcgen05.fence::after_thread_sync;");
-            for (int kc = tl.kc0; kc < tl.kc1; ++kc, ++c) {
-                const int s = c % STAGES;
-                mbar_wait(smem_u32(&full_b[s]), (c / STAGES) & 1);
-                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                asm volatile("tcgen05.fence::after_thread_sync;");
-                if (lane == 0) {
-                    const uint32_t st = smem_u32(smem + s * STAGE_BYTES);
-                    const uint64_t bb = smem_desc(st + 2 * MT * OPND_BYTES), bs = smem_desc(st + (2 * MT + 1) * OPND_BYTES);
-                    const int ksteps = min(BK, K - kc * BK + 7) / 8;
-                    if (tl.np > 0)
-                        for (int k = 0; k < ksteps; ++k) {
-                            const uint64_t off = (uint64_t)(2 * k);
-#pragma unroll
-                            for (int mt = 0; mt < MT; ++mt) {
-                                const uint64_t a_b = smem_desc(st + (2 * mt) * OPND_BYTES) + off;
-                                const uint64_t a_s = smem_desc(st + (2 * mt + 1) * OPND_BYTES) + off;
-                                const uint32_t d = tmem + (uint32_t)((ab * MT + mt) * BN);
-                                mma_tf32(d, a_b, bb + off, idesc, kc != tl.kc0 || k != 0);
-                                mma_tf32(d, a_b, bs + off, idesc, 1);
-                                mma_tf32(d, a_s, bb + off, idesc, 1);
-                            }
-                        }
-                    mma_commit_mc(smem_u32(&empty_b[s]), both);
-                    if (kc == tl.kc1 - 1) mma_commit(smem_u32(&accf_b[ab]));
-                }
-                __syncwarp();
-            }
-        }
-    } else if (warp >= EPI_WARP0) {
-        // ---------------- epilogue: TMEM -> fp64 atomics, 32 columns at a time
-        const int wq = warp - EPI_WARP0;
-        int it = 0;
-        for (int ci = cid; ci < nctiles; ci += ncl, ++it) {
-            const Tile tl = tiles[mc::CS * ci + rank];
-            const int ab = it & 1;
-            mbar_wait(smem_u32(&accf_b[ab]), (it >> 1) & 1);
-            asm volatile("tcgen05.fence::after_thread_sync;");
-            const int2* pp = pairs + tl.p0;
-#pragma unroll
-            for (int mt = 0; mt < MT; ++mt) {
-                const int row = tl.m0 + mt * BM + 32 * wq + lane;
-#pragma unroll 1
-                for (int c0 = 0; c0 < tl.np; c0 += 32) {
-                    uint32_t v[32];
-                    tmem_ld32(tmem + ((uint32_t)(32 * wq) << 16) + (uint32_t)((ab * MT + mt) * BN + c0), v);
-                    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-                    if (row < M) {
-#pragma unroll
-                        for (int j = 0; j < 32; ++j)
-                            if (c0 + j < tl.np)
-                                atomicAdd(Y + (int64_t)__ldg(&pp[c0 + j].x) * ldy + row, (double)__uint_as_float(v[j]));
-                    }
-                }
-            }
-            asm volatile("tcgen05.fence::before_thread_sync;");
-            __syncwarp();
-            if (lane == 0) mbar_arrive(smem_u32(&acce_b[ab]));
-        }
-    }
-    asm volatile("tcgen05.fence::before_thread_sync;");
-    __syncthreads();
-    cluster_sync();                              // no CTA leaves while its peer may still signal it
-    if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
-}
-
 // ------------------------------------------------------------------ wide variant (full chain)
 // The same contraction with one 128-row operator slice x 256 pairs per tile (MMA N = 256).
 // A tf32 M128 x N x K8 MMA takes 128 N / 256 cycles and reads (128 + N) x 32 B of shared
@@ -1269,34 +1066,11 @@ int tc_fast_tile_mode() {
     // the wide (128 x 256) tiles: M2L 1.715 vs 1.632 ms alone, matvec 4.61 vs 4.46 ms
     // (profiles/r02/ab_m2l_wide.txt); EBEM_M2L_WIDE=1 selects them
     static const int m = (std::getenv("EBEM_M2L_WIDE") && std::atoi(std::getenv("EBEM_M2L_WIDE")) == 1) ? 2 : 1;
-    // cluster-multicast tiles (tc_pairs_mc_kernel): EBEM_M2L_MC=1
-    static const bool mcast = std::getenv("EBEM_M2L_MC") && std::atoi(std::getenv("EBEM_M2L_MC")) == 1;
-    if (mcast) return 3;
     return m;
 }
 
 void tc_build_tiles(OpPairs& P, int M, int K, int mode) {
     std::vector<tc::Tile> t;
-    if (mode == 3) {
-        // cluster tiles: consecutive pair blocks of one operator and row slice go to the two
-        // CTAs of a cluster (an odd last block is paired with an empty one)
-        const int nk = (K + tc::BK - 1) / tc::BK;
-        const int mstep = tc::fast::MT * tc::BM;
-        P.tile_mode = 3;
-        for (int o = 0; o < P.nops; ++o) {
-            const int a = P.op_ptr_h[o], e = P.op_ptr_h[o + 1];
-            for (int p0 = a; p0 < e; p0 += tc::mc::CS * tc::BN)
-                for (int m0 = 0; m0 < M; m0 += mstep)
-                    for (int r = 0; r < tc::mc::CS; ++r) {
-                        const int q = p0 + r * tc::BN;
-                        t.push_back({o, q < e ? q : a, q < e ? std::min(tc::BN, e - q) : 0, m0, 0, nk});
-                    }
-        }
-        P.ntiles = (int)t.size() / tc::mc::CS;
-        P.tiles.alloc(std::max<size_t>(t.size(), 1) * sizeof(tc::Tile) / sizeof(int));
-        if (!t.empty()) EB_CUDA(cudaMemcpy(P.tiles.p, t.data(), t.size() * sizeof(tc::Tile), cudaMemcpyHostToDevice));
-        return;
-    }
     const int mstep = mode == 1 ? tc::fast::MT * tc::BM : tc::BM;
     const int bn = mode == 2 ? tc::wide::BNW : tc::BN;
     const int nk = (K + tc::BK - 1) / tc::BK;
@@ -1340,34 +1114,6 @@ void tc_pairs_gemm_fast(const OpPairs& P, const CUtensorMap& Ab, const CUtensorM
         const int grid = std::min(P.ntiles, num_sms());
         tc::tc_pairs_wide_kernel<<<grid, tc::wide::THREADS, tc::wide::SMEM_BYTES, s>>>(
             Ab, As, Bb, Bs, ldb, reinterpret_cast<const tc::Tile*>(P.tiles.p), P.ntiles, P.pairs.p, M, K, Y, ldy);
-        EB_CHECK_LAUNCH();
-        return;
-    }
-    if (P.tile_mode == 3) {
-        EB_REQUIRE(!drain, "internal: cluster tiles with the drained kernel");
-        static bool mattr = false;
-        if (!mattr) {
-            EB_CUDA(cudaFuncSetAttribute(tc::tc_pairs_mc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         tc::fast::SMEM_BYTES));
-            EB_CUDA(cudaFuncSetAttribute(tc::tc_pairs_mc_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-            mattr = true;
-        }
-        const int ncl = std::min(P.ntiles, num_sms() / tc::mc::CS);
-        cudaLaunchConfig_t cfg = {};
-        cfg.gridDim = dim3(ncl * tc::mc::CS);
-        cfg.blockDim = dim3(tc::fast::THREADS);
-        cfg.dynamicSmemBytes = tc::fast::SMEM_BYTES;
-        cfg.stream = s;
-        cudaLaunchAttribute at[1];
-        at[0].id = cudaLaunchAttributeClusterDimension;
-        at[0].val.clusterDim.x = tc::mc::CS;
-        at[0].val.clusterDim.y = 1;
-        at[0].val.clusterDim.z = 1;
-        cfg.attrs = at;
-        cfg.numAttrs = 1;
-        EB_CUDA(cudaLaunchKernelEx(&cfg, tc::tc_pairs_mc_kernel, Ab, As, Bb, Bs, ldb,
-                                   reinterpret_cast<const tc::Tile*>(P.tiles.p), P.ntiles, (const int2*)P.pairs.p, M, K,
-                                   Y, ldy));
         EB_CHECK_LAUNCH();
         return;
     }

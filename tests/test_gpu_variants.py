@@ -1,7 +1,6 @@
 """Kernel variants selected by process-wide switches (read once per process, so each runs in a
-child process): the persistent M2M/L2L level-chain kernel (EBEM_ML_CHAIN=1), the
-cluster-multicast M2L (EBEM_M2L_MC=1), the wide 128 x 256 M2L tiles (EBEM_M2L_WIDE=1) and the
-packed FFMA2 near field (EBEM_NEAR_PACKED=1).  Each must meet the same bounds against the
+child process): the persistent M2M/L2L level-chain kernel (EBEM_ML_CHAIN=1), the wide
+128 x 256 M2L tiles (EBEM_M2L_WIDE=1) and the packed FFMA2 near field (EBEM_NEAR_PACKED=1).  Each must meet the same bounds against the
 fp64 oracle as the default path (the KIFMM sum of Eq. fmm_summation)."""
 import json
 import os
@@ -28,7 +27,7 @@ torch.cuda.synchronize()
 np.save({path!r}, np.stack([out.cpu().numpy(), out2.cpu().numpy()]))
 """
 
-VARIANTS = [{}, {"EBEM_ML_CHAIN": "1"}, {"EBEM_M2L_MC": "1"}, {"EBEM_M2L_WIDE": "1"}, {"EBEM_NEAR_PACKED": "1"}]
+VARIANTS = [{}, {"EBEM_ML_CHAIN": "1"}, {"EBEM_M2L_WIDE": "1"}, {"EBEM_NEAR_PACKED": "1"}]
 
 
 @pytest.fixture(scope="module")
