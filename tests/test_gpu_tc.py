@@ -8,7 +8,7 @@ import pytest
 from oracle import cdirect
 from oracle import kernels as KN
 from workloads import geometry as geo
-from tests.gpu_util import need_gpu, to_dev
+from tests.gpu_util import assert_fmm_close, need_gpu, to_dev
 
 pytestmark = pytest.mark.gpu
 
@@ -33,3 +33,8 @@ def test_tc_matches_simt(p, n):
                              nrm=d["nrm"])
     print(f"p={p}: |tc - simt| {diff:.2e}, tc err {KN.rel_l2(b, ref):.2e}, simt err {KN.rel_l2(a, ref):.2e}")
     assert diff < 1e-5
+    # and each path on its own against the fp64 oracle, at the truncation bound of its order
+    # (measured on the beam: 3.3e-3 at p = 4, 2.9e-5 at p = 6; p = 5 between)
+    bound = {4: 5e-3, 5: 1e-3, 6: 1e-4}[p]
+    assert_fmm_close(b, ref, bound, label=f"tc p={p}")
+    assert_fmm_close(a, ref, bound, label=f"simt p={p}")
