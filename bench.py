@@ -291,7 +291,7 @@ def gmres_workload(args, eb, torch, emit=True, precond=None):
             "vs_baseline": None, "dtype": "f32 FMM, f64 Krylov", "data": "synthetic",
             "config": {"workload": f"metamaterial cell, {d['verts'].shape[0]} triangles, {args.cell_voids} voids",
                        "nq": args.nq, "p": args.gmres_p, "max_pts": args.gmres_max_pts, "restart": 50, "tol": 1e-6,
-                       "precond": ["none (paper)", "block-Jacobi (right)"][precond]},
+                       "precond": ["none (paper)", "block-Jacobi 3x3 (right)", "leaf-block Jacobi (right)"][precond]},
             "converged": bool(res <= 1e-6), "iterations": it, "rel_residual": res,
             "ms_per_iteration": ms / max(it, 1), "setup_s": setup,
             "true_residual_at_restarts": [float(v) for v in true],
@@ -383,8 +383,9 @@ def main():
     ap.add_argument("--cell-level", type=int, default=5)
     ap.add_argument("--cell-voids", type=int, default=64)
     ap.add_argument("--max-iter", type=int, default=1000)
-    ap.add_argument("--precond", type=int, default=1,
-                    help="GMRES: 1 block-Jacobi right preconditioner (default), 0 the paper's plain GMRES")
+    ap.add_argument("--precond", type=int, default=2,
+                    help="GMRES: 2 leaf-block Jacobi right preconditioner (default), 1 3x3 block-Jacobi, "
+                         "0 the paper's plain GMRES")
     ap.add_argument("--no-stress", action="store_true", help="skip the configs[3] key of the matvec line")
     ap.add_argument("--no-gmres", action="store_true", help="skip the configs[4] key of the matvec line")
     ap.add_argument("--no-gmres-paper", action="store_true",
@@ -607,7 +608,7 @@ def main():
         if not args.no_stress:
             stress = stress_workload(args, eb, torch, emit=False)
         if not args.no_gmres:
-            gmres = gmres_workload(args, eb, torch, emit=False, precond=1)
+            gmres = gmres_workload(args, eb, torch, emit=False, precond=2)
         if not args.no_gmres_paper:      # plain restarted GMRES, no preconditioner
             args.max_iter = max(args.max_iter, 3000)
             gmres_paper = gmres_workload(args, eb, torch, emit=False, precond=0)

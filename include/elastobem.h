@@ -215,7 +215,12 @@ int64_t fmm_tree_export(const ebem_tree *tree, int what, void *buf, int64_t cap)
  *   precond: 0 = none (the paper's solver, l. 181, "In the future this shortcoming should be
  *   addressed with ... the appropriate preconditioner", l. 369); 1 = block-Jacobi right
  *   preconditioner with the panels' own 3x3 blocks (-U_self on Dirichlet panels,
- *   1/2 I + P_self on Neumann panels).  The solution of A x = b is the same.
+ *   1/2 I + P_self on Neumann panels); 2 = leaf-block Jacobi right preconditioner: the
+ *   diagonal blocks of A over the panels whose collocation points share an octree leaf (at
+ *   most 52 panels per block), formed in fp64 as the operator applies them and inverted
+ *   once per solve (they may take up to half of the free device memory; precond 1 is used
+ *   when they do not fit).  The solution of A x = b is the same; any other value is
+ *   EBEM_ERR_ARG.
  *   iters_out / resid_out (host, may be NULL): iterations and final relative residual.
  *   restart in [1, 63] (EBEM_ERR_ARG otherwise): the Krylov basis is (restart + 1) fp64
  *   vectors of npanels*3 on the device.

@@ -318,7 +318,8 @@ def bem_rhs(bem, bc_type, bc_val, out=None):
 
 def bem_gmres_solve(bem, bc_type, bc_val, x, restart=50, max_iter=1000, tol=1e-6, precond=0, check=True):
     """solves A x = b in place; returns (x, iterations, relative residual).
-    precond: 0 none (the paper's GMRES), 1 block-Jacobi right preconditioner."""
+    precond: 0 none (the paper's GMRES), 1 block-Jacobi (3x3 panel blocks), 2 leaf-block
+    Jacobi (the diagonal blocks of A over each octree leaf's panels) right preconditioner."""
     keep = []
     it = ctypes.c_int32(0)
     res = ctypes.c_double(0)

@@ -15,6 +15,7 @@
 // edges: "evaluated analytically", l. 179).
 // The mixed BVP moves the unknowns (p on Dirichlet panels, u on Neumann panels) to the left:
 // A x = b (Eq. num2), applied matrix-free as L(u, p) = P u - U p.
+#include <chrono>
 #include <cmath>
 
 #include <cstdio>
@@ -22,6 +23,7 @@
 #include <cstring>
 
 #include "bem_near.cuh"
+#include "bem_prec.cuh"
 #include "fmm.cuh"
 #include "p2p.cuh"
 
@@ -549,6 +551,25 @@ int bem_gmres(Bem& B, const int32_t* bc, const float* val, float* x, int m, int 
     const bool use_cm = use_nm && T.use_tc && check_matrix_enabled() &&
                         panel_op_build(T, PanelOp::S2M, B.nq, B.n, bc, B.mat, B.s2m_op, s);
     const bool use_cl = use_cm && (T.n_s2l == 0 || panel_op_build(T, PanelOp::S2L, B.nq, B.n, bc, B.mat, B.s2l_op, s));
+    // precond = 2: leaf-block Jacobi (bem_prec.cu), built after the HBM operators (they save
+    // more per byte); the 3x3 blocks when the inverses do not fit
+    LeafBlockPrec lbp;
+    const auto t_lb = std::chrono::steady_clock::now();
+    const bool use_lb = precond == 2 &&
+                        leafblock_build(T, B.n, B.nq, B.cent.p, B.qpts.p, B.qnrm.p, B.qw.p, bc, B.DU.p, B.DP.p, B.mat,
+                                        lbp, s);
+    if (precond == 2 && std::getenv("EBEM_BEM_PROFILE"))
+        std::fprintf(stderr, "[bem] leaf-block preconditioner: %s, %d blocks, %.2f GB, built in %.1f ms\n",
+                     use_lb ? "on" : "did not fit / singular (3x3 blocks)", lbp.nblocks, lbp.entries * 8e-9,
+                     std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_lb).count());
+    auto prec = [&](const double* v, double* out) {     // out = M^-1 v
+        if (use_lb) {
+            leafblock_apply(T, lbp, v, out, s);
+        } else {
+            prec_apply<<<ceil_div(B.n, 256), 256, 0, s>>>(Minv.p, v, B.n, out);
+            EB_CHECK_LAUNCH();
+        }
+    };
     struct HookGuard {
         Tree& t;
         ~HookGuard() {
@@ -583,8 +604,7 @@ int bem_gmres(Bem& B, const int32_t* bc, const float* val, float* x, int m, int 
     };
     auto pmatvec = [&](const double* v, double* out) {  // out = A M^-1 v (right preconditioning)
         if (!precond) return matvec(v, out);
-        prec_apply<<<ceil_div(B.n, 256), 256, 0, s>>>(Minv.p, v, B.n, tp.p);
-        EB_CHECK_LAUNCH();
+        prec(v, tp.p);
         matvec(tp.p, out);
     };
     int it = 0;
@@ -656,7 +676,7 @@ int bem_gmres(Bem& B, const int32_t* bc, const float* val, float* x, int m, int 
         if (precond) {     // x += M^-1 (V y)
             EB_CUDA(cudaMemsetAsync(w.p, 0, sizeof(double) * n3, s));
             axpy_basis<<<ceil_div(n3, 256), 256, 0, s>>>(V.p, n3, k, hd.p, 1.0, w.p, n3);
-            prec_apply<<<ceil_div(B.n, 256), 256, 0, s>>>(Minv.p, w.p, B.n, tp.p);
+            prec(w.p, tp.p);
             add_kernel<<<ceil_div(n3, 256), 256, 0, s>>>(tp.p, xd.p, n3);
         } else {
             axpy_basis<<<ceil_div(n3, 256), 256, 0, s>>>(V.p, n3, k, hd.p, 1.0, xd.p, n3);

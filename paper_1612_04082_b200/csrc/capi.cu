@@ -380,6 +380,7 @@ extern "C" int bem_gmres_solve(ebem_bem* bem, const int32_t* bc_type, const floa
     set_last_error("");
     EB_REQUIRE(bem && bc_type && bc_val && x, "NULL argument");
     EB_REQUIRE(restart >= 1 && restart <= 63 && max_iter >= 1 && tol > 0, "bad GMRES parameters");
+    EB_REQUIRE(precond >= 0 && precond <= 2, "precond must be 0, 1 or 2");
     EB_REQUIRE(device_args({bc_type, bc_val, x}), "bem_gmres_solve needs device pointers");
     const int rc = ebem::bem_gmres(*reinterpret_cast<Bem*>(bem), bc_type, bc_val, x, restart, max_iter, tol, iters_out,
                                    resid_out, precond, (cudaStream_t)stream);

@@ -49,10 +49,11 @@ def test_operator_and_rhs_match_dense_oracle(eb, nq):
     assert KN.rel_l2(bg, b) < 1e-5
 
 
-@pytest.mark.parametrize("precond", [0, 1])
+@pytest.mark.parametrize("precond", [0, 1, 2])
 def test_gmres_matches_dense_solve_and_patch_test(eb, precond):
-    """the paper's GMRES (precond = 0) and the block-Jacobi right-preconditioned one
-    (precond = 1, the same residual |b - A x| / |b|) against dense LU of the oracle system."""
+    """the paper's GMRES (precond = 0) and the right-preconditioned ones (precond = 1: 3x3
+    block-Jacobi, 2: leaf-block Jacobi; the same residual |b - A x| / |b|) against dense LU of
+    the oracle system."""
     verts, c, n, a, bc, val, uex, tex, V = _problem(4)
     V0, V1, V2 = (verts[:, k].astype(np.float64) for k in range(3))
     c64, n64, a64 = geo.panels(V0, V1, V2)
@@ -124,6 +125,13 @@ def test_gmres_solver_setting_of_configs4_matches_dense_oracle(eb):
     # true residual of the returned solution against the oracle's own matrix
     xs = x.cpu().numpy().reshape(-1).astype(np.float64)
     assert np.linalg.norm(b - A @ xs) / np.linalg.norm(b) < 1e-4
+    # the leaf-block Jacobi preconditioner (precond = 2): the same solution in fewer
+    # iterations (its blocks are A's own diagonal blocks over each leaf's panels)
+    x2 = torch.zeros((verts.shape[0], 3), device="cuda")
+    x2, it2, res2 = eb.bem_gmres_solve(op, bc, val, x2, restart=50, max_iter=400, tol=1e-6, precond=2)
+    err2 = KN.rel_l2(x2.cpu().numpy().reshape(-1).astype(np.float64), xref)
+    print("leaf-block Jacobi: iterations", it2, "residual", res2, "solution rel-L2 vs dense LU", err2)
+    assert res2 <= 1e-6 and err2 < 1e-4 and it2 < it
 
 
 def test_near_operator_matches_near_kernel(eb, monkeypatch):

@@ -17,6 +17,6 @@ val = torch.from_numpy(d["bc_val"]).cuda()
 op = eb.bem_create(verts, nq=16, max_pts=1536, p=8, K=d["K"], G=d["G"])
 x = torch.zeros((d["verts"].shape[0], 3), device="cuda")
 x, it, res = eb.bem_gmres_solve(op, bc, val, x, restart=50, max_iter=int(os.environ.get("IT", 3)), tol=1e-6,
-                                precond=1, check=False)
+                                precond=int(os.environ.get("PRECOND", 2)), check=False)
 torch.cuda.synchronize()
 print("ok", it, res)
