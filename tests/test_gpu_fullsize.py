@@ -86,17 +86,19 @@ def test_config3_stress_full(eb):
     assert err <= 1e-5 and worst <= 1e-4
 
 
-def test_config4_gmres_full(eb):
-    """configs[4]: the 1.93 M-triangle cell, mixed BVP, block-Jacobi GMRES(50) to 1e-6 at
-    p = 8, leaf 1536 (the bench setting): converges, and the tractions balance (net force of the solved + given
-    tractions over the closed surface ~ 0 against the applied unit load)."""
+@pytest.mark.parametrize("precond", [2, 1])
+def test_config4_gmres_full(eb, precond):
+    """configs[4]: the 1.93 M-triangle cell, mixed BVP, right-preconditioned GMRES(50) to 1e-6
+    at p = 8, leaf 1536 (the bench setting; precond 2 leaf-block Jacobi, 1 the 3x3 blocks):
+    converges, and the tractions balance (net force of the solved + given tractions over the
+    closed surface ~ 0 against the applied unit load)."""
     d = geo.metamaterial_cell(nc=160, level=5, nvoids=64)
     verts = torch.from_numpy(d["verts"]).cuda()
     bc = torch.from_numpy(d["bc_type"]).cuda()
     val = torch.from_numpy(d["bc_val"]).cuda()
     op = eb.bem_create(verts, nq=16, max_pts=1536, p=8, K=d["K"], G=d["G"])
     x = torch.zeros((d["verts"].shape[0], 3), device="cuda")
-    x, it, res = eb.bem_gmres_solve(op, bc, val, x, restart=50, max_iter=600, tol=1e-6, precond=1, check=False)
+    x, it, res = eb.bem_gmres_solve(op, bc, val, x, restart=50, max_iter=600, tol=1e-6, precond=precond, check=False)
     V = d["verts"].astype(np.float64)
     area = 0.5 * np.linalg.norm(np.cross(V[:, 1] - V[:, 0], V[:, 2] - V[:, 0]), axis=1)
     tr = np.where(d["bc_type"][:, None] == 0, x.cpu().numpy(), d["bc_val"])
@@ -104,3 +106,5 @@ def test_config4_gmres_full(eb):
     print("configs[4]: iterations", it, "residual", res, "net force", force)
     assert res <= 1e-6
     assert force < 2e-3
+    if precond == 2:
+        assert it < 150          # measured 93 (3x3 blocks: 231)
