@@ -1627,8 +1627,12 @@ void fmm_evaluate(Tree& t, int kernel, const float* f, const float* g, float* ou
 
     // downward pass (stream B forks here: started together with the upward pass it only
     // competed with the other FP32-bound kernels, measured no faster)
-    if (conc) EB_CUDA(cudaEventRecord(t.ev_fork, sa));
-    fork_b();
+    // EBEM_NEAR_AFTER_M2L=1: stream B forks after M2L (the near field beside L2L / PHI)
+    static const bool near_late = std::getenv("EBEM_NEAR_AFTER_M2L") && std::atoi(std::getenv("EBEM_NEAR_AFTER_M2L"));
+    if (!near_late) {
+        if (conc) EB_CUDA(cudaEventRecord(t.ev_fork, sa));
+        fork_b();
+    }
     if (!conc) {
         pb(PH_S2L, sa);
         s2l(sa);
@@ -1664,6 +1668,10 @@ void fmm_evaluate(Tree& t, int kernel, const float* f, const float* g, float* ou
     else if (t.use_tc) tc_pairs_gemm(t.m2l, P.mM2L_b, P.mM2L_s, t.mZb, t.mZs, me, me, t.W.p, lde, sa);
     else gemm_pairs_f32(t.m2l, P.M2L.p, me, me, lde, t.Z.p, lde, t.W.p, lde, sa);
     pe(PH_M2L, sa);
+    if (near_late) {
+        if (conc) EB_CUDA(cudaEventRecord(t.ev_fork, sa));
+        fork_b();
+    }
     if (trace) EB_CUDA(cudaEventRecord(tev[4], sa));
     if (conc) {
         EB_CUDA(cudaStreamWaitEvent(sa, t.ev_s2l, 0));
