@@ -253,7 +253,7 @@ void tc_build_chain(Chain& ch, const std::vector<const OpPairs*>& levels, const 
 // each level, [tail_row0, tail_row0 + tail_rows) after the last); Y += translations
 void tc_chain_run(const Chain& ch, const CUtensorMap& Ab, const CUtensorMap& As, const double* X, int ldx, float* Xb,
                   float* Xs, int M, int K, double* Y, int ldy, int64_t tail_row0, int64_t tail_rows, cudaStream_t s);
-int tc_fast_tile_mode();                       // 1 (two-slice tiles) unless EBEM_M2L_WIDE=1, then 2
+int tc_fast_tile_mode(int M);                  // full-chain tile shape for M operator rows: 1 two-slice, 2 wide
 int tc_fast_smem_bytes();                     // dynamic shared memory of one fast translation CTA
 int beside_translation_pad(const void* kernel);   // fmm.cu: stream-B co-residency padding
 void tc_pairs_gemm_fast(const OpPairs& P, const CUtensorMap& Ab, const CUtensorMap& As, const float* Bb,

@@ -1062,11 +1062,16 @@ template void tc_split_rows<double>(const double*, int, int64_t, int64_t, int, f
 // and Z rows in L2 across operators but re-read the operators per chunk: no faster).  Launches with fewer tiles than SMs (the coarse M2M/L2L
 // levels) split K over several CTAs: a lone tile streams its 15 K chunks through one SM in
 // ~20 us, while its partial sums are added by the fp64 atomics of the epilogue anyway.
-int tc_fast_tile_mode() {
-    // the wide (128 x 256) tiles: M2L 1.715 vs 1.632 ms alone, matvec 4.61 vs 4.46 ms
-    // (profiles/r02/ab_m2l_wide.txt); EBEM_M2L_WIDE=1 selects them
-    static const int m = (std::getenv("EBEM_M2L_WIDE") && std::atoi(std::getenv("EBEM_M2L_WIDE")) == 1) ? 2 : 1;
-    return m;
+int tc_fast_tile_mode(int M) {
+    // Tile shape of the full-chain translations by the operator's row count M = 3 n_e: the
+    // two-slice tiles (256 rows x 128 pairs: every gathered row feeds 256 outputs) unless they
+    // pad M more than the wide tiles (128 rows x 256 pairs) do.  p = 6 (456 rows): both pad to
+    // 512, two-slice (matvec 4.46 vs 4.61 ms); p = 8 (888 rows): 1024 vs 896 rows, wide (BEM
+    // operator M2L 24.6 vs 28.4 ms; configs[3] 8.76 vs 8.73 ms).  EBEM_M2L_WIDE=0 / 1 forces
+    // one of them.
+    if (const char* e = std::getenv("EBEM_M2L_WIDE")) return std::atoi(e) == 1 ? 2 : 1;
+    const int two = (M + 2 * tc::BM - 1) / (2 * tc::BM) * 2 * tc::BM, wide = (M + tc::BM - 1) / tc::BM * tc::BM;
+    return two > wide ? 2 : 1;
 }
 
 void tc_build_tiles(OpPairs& P, int M, int K, int mode) {
