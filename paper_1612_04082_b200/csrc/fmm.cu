@@ -1145,12 +1145,12 @@ void schedule_tree(Tree& t, cudaStream_t s) {
         // 0.17 ms faster, error 2.907e-5 -> 2.912e-5; at p = 8 the error grew 1.9e-6 -> 2.7e-6)
         static const int ml_fast_pmax = std::getenv("EBEM_ML_FAST") ? std::atoi(std::getenv("EBEM_ML_FAST")) : 6;
         t.ml_fast = t.tc_fast && P.p <= ml_fast_pmax;
-        // tile shapes: the full-chain kernels two-slice or wide by M (tc_fast_tile_mode), the drained
-        // M2L two-slice tiles, the one-slice precise kernel 128 x 128
+        // tile shapes: the full-chain and the drained M2L kernels two-slice or wide by M
+        // (tc_fast_tile_mode), the one-slice precise kernel 128 x 128
         const int fm = tc_fast_tile_mode(me);
         tc_build_tiles(t.q2z_up, me, mc, t.ml_fast ? fm : 0);
         tc_build_tiles(t.q2z_dn, me, mc, t.ml_fast ? fm : 0);
-        tc_build_tiles(t.m2l, me, me, t.tc_fast ? fm : (m2l_drain_fast() ? 1 : 0));
+        tc_build_tiles(t.m2l, me, me, t.tc_fast || m2l_drain_fast() ? fm : 0);
         for (auto& x : t.m2m) tc_build_tiles(x, me, me, t.ml_fast ? fm : 0);
         for (auto& x : t.l2l) tc_build_tiles(x, me, me, t.ml_fast ? fm : 0);
         // EBEM_ML_CHAIN=1: M2M and L2L chains as one persistent launch each (tc_chain_kernel).
@@ -1338,7 +1338,7 @@ void tree_m2l_fast(Tree& t, bool fast, cudaStream_t s) {
     fast = fast && t.use_tc && P.p < FAR_FP64_MIN_P;
     if (fast == t.tc_fast) return;
     t.tc_fast = fast;
-    tc_build_tiles(t.m2l, P.me, P.me, fast ? tc_fast_tile_mode(P.me) : (m2l_drain_fast() ? 1 : 0));
+    tc_build_tiles(t.m2l, P.me, P.me, fast || m2l_drain_fast() ? tc_fast_tile_mode(P.me) : 0);
     EB_CUDA(cudaStreamSynchronize(s));
 }
 

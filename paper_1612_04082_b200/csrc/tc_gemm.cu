@@ -584,7 +584,10 @@ constexpr int THREADS = 256;
 constexpr int NG = (BNW / 4 + NPROD - 1) / NPROD;       // four-row groups per producer warp
 }  // namespace wide
 
-__global__ void __launch_bounds__(wide::THREADS, 1)
+// DRAIN = true: drained groups as in tc_pairs_fast_kernel<true> (GROUP K chunks per ping-pong
+// buffer of 256 columns, eight drain warps: lane quarter x column half, fp32 register sums)
+template <bool DRAIN>
+__global__ void __launch_bounds__(DRAIN ? 384 : wide::THREADS, 1)
 tc_pairs_wide_kernel(const __grid_constant__ CUtensorMap mapAb, const __grid_constant__ CUtensorMap mapAs,
                      const float* __restrict__ Bb, const float* __restrict__ Bs, int ldb,
                      const Tile* __restrict__ tiles, int ntiles, const int2* __restrict__ pairs, int M, int K,
@@ -609,7 +612,7 @@ tc_pairs_wide_kernel(const __grid_constant__ CUtensorMap mapAb, const __grid_con
         }
         for (int b = 0; b < 2; ++b) {
             mbar_init(smem_u32(&accf_b[b]), 1);
-            mbar_init(smem_u32(&acce_b[b]), 4);
+            mbar_init(smem_u32(&acce_b[b]), DRAIN ? 8 : 4);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -669,6 +672,72 @@ tc_pairs_wide_kernel(const __grid_constant__ CUtensorMap mapAb, const __grid_con
                 asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(full) : "memory");
             }
         }
+    } else if (warp == 1 && DRAIN) {
+        // ---------------- MMA issuer, drained groups
+        int c = 0, G = 0;
+        for (int ti = blockIdx.x; ti < ntiles; ti += gridDim.x) {
+            const uint32_t nmma = (uint32_t)((tiles[ti].np + 15) & ~15);
+            const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((nmma >> 3) << 17) |
+                                   ((uint32_t)(BM >> 4) << 24);
+            const int kc0 = tiles[ti].kc0, kc1 = tiles[ti].kc1;
+            for (int kc = kc0; kc < kc1; ++kc, ++c) {
+                const int s = c % STAGES;
+                const int b = G & 1;
+                const bool gfirst = ((kc - kc0) % GROUP) == 0,
+                           glast = ((kc - kc0) % GROUP) == GROUP - 1 || kc == kc1 - 1;
+                if (gfirst) {
+                    mbar_wait(smem_u32(&acce_b[b]), ((G >> 1) & 1) ^ 1);
+                    asm volatile("tcgen05.fence::after_thread_sync;");
+                }
+                mbar_wait(smem_u32(&full_b[s]), (c / STAGES) & 1);
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                asm volatile("tcgen05.fence::after_thread_sync;");
+                if (lane == 0) {
+                    const uint32_t st = smem_u32(smem + s * STAGE_BYTES);
+                    const uint64_t a_b = smem_desc(st), a_s = smem_desc(st + A_BYTES);
+                    const uint64_t bb = smem_desc(st + 2 * A_BYTES), bs = smem_desc(st + 2 * A_BYTES + B_BYTES);
+                    const uint32_t d = tmem + (uint32_t)(b * BNW);
+                    const int ksteps = min(BK, K - kc * BK + 7) / 8;
+                    for (int k = 0; k < ksteps; ++k) {
+                        const uint64_t off = (uint64_t)(2 * k);
+                        mma_tf32(d, a_b + off, bb + off, idesc, !gfirst || k != 0);
+                        mma_tf32(d, a_b + off, bs + off, idesc, 1);
+                        mma_tf32(d, a_s + off, bb + off, idesc, 1);
+                    }
+                    mma_commit(smem_u32(&empty_b[s]));
+                    if (glast) mma_commit(smem_u32(&accf_b[b]));
+                }
+                __syncwarp();
+                if (glast) ++G;
+            }
+        }
+    } else if (warp >= EPI_WARP0 && DRAIN) {
+        // ---------------- drains: warp -> (lane quarter, column half); fp32 register sums, then atomics
+        const int wq = warp & 3, half = (warp - EPI_WARP0) >> 2;
+        int G = 0;
+        for (int ti = blockIdx.x; ti < ntiles; ti += gridDim.x) {
+            const Tile tl = tiles[ti];
+            float acc[BN];
+#pragma unroll
+            for (int j = 0; j < BN; ++j) acc[j] = 0.f;
+            const int ngroups = (tl.kc1 - tl.kc0 + GROUP - 1) / GROUP;
+            for (int g = 0; g < ngroups; ++g, ++G) {
+                const int b = G & 1;
+                mbar_wait(smem_u32(&accf_b[b]), (G >> 1) & 1);
+                asm volatile("tcgen05.fence::after_thread_sync;");
+                if (half * BN < tl.np) drain_add(tmem, wq, b * BNW + half * BN, acc);
+                asm volatile("tcgen05.fence::before_thread_sync;");
+                __syncwarp();
+                if (lane == 0) mbar_arrive(smem_u32(&acce_b[b]));
+            }
+            const int row = tl.m0 + 32 * wq + lane;
+            if (row < M) {
+                const int2* pp = pairs + tl.p0 + half * BN;
+#pragma unroll
+                for (int j = 0; j < BN; ++j)
+                    if (half * BN + j < tl.np) atomicAdd(Y + (int64_t)__ldg(&pp[j].x) * ldy + row, (double)acc[j]);
+            }
+        }
     } else if (warp == 1) {
         // ---------------- MMA issuer
         int c = 0, it = 0;
@@ -703,7 +772,7 @@ tc_pairs_wide_kernel(const __grid_constant__ CUtensorMap mapAb, const __grid_con
                 __syncwarp();
             }
         }
-    } else if (warp >= EPI_WARP0) {
+    } else if (warp >= EPI_WARP0 && warp < EPI_WARP0 + 4) {
         // ---------------- epilogue: TMEM -> fp64 atomics, 32 columns at a time
         const int wq = warp - EPI_WARP0;
         int it = 0;
@@ -1109,15 +1178,14 @@ void tc_pairs_gemm_fast(const OpPairs& P, const CUtensorMap& Ab, const CUtensorM
                         const float* Bs, int ldb, int M, int K, double* Y, int ldy, bool drain, cudaStream_t s) {
     if (P.ntiles == 0) return;
     if (P.tile_mode == 2) {
-        EB_REQUIRE(!drain, "internal: wide tiles with the drained kernel");
-        static bool wattr = false;
-        if (!wattr) {
-            EB_CUDA(cudaFuncSetAttribute(tc::tc_pairs_wide_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         tc::wide::SMEM_BYTES));
-            wattr = true;
+        static bool wattr[2] = {false, false};
+        auto wfn = drain ? tc::tc_pairs_wide_kernel<true> : tc::tc_pairs_wide_kernel<false>;
+        if (!wattr[drain]) {
+            EB_CUDA(cudaFuncSetAttribute(wfn, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::wide::SMEM_BYTES));
+            wattr[drain] = true;
         }
         const int grid = std::min(P.ntiles, num_sms());
-        tc::tc_pairs_wide_kernel<<<grid, tc::wide::THREADS, tc::wide::SMEM_BYTES, s>>>(
+        wfn<<<grid, drain ? 384 : tc::wide::THREADS, tc::wide::SMEM_BYTES, s>>>(
             Ab, As, Bb, Bs, ldb, reinterpret_cast<const tc::Tile*>(P.tiles.p), P.ntiles, P.pairs.p, M, K, Y, ldy);
         EB_CHECK_LAUNCH();
         return;
