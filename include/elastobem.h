@@ -163,6 +163,15 @@ int fmm_phase_stats(ebem_tree *tree, int kernel, ebem_phase_stat *out, int cap);
 /* number of CUDA kernel launches issued by this library since it was loaded */
 int64_t ebem_launch_count(void);
 
+/*
+ * Device memory the library keeps: released long-lived buffers of >= 1 MB (tree workspace,
+ * operators) stay cached for reuse by the next tree or solve of the same sizes, up to
+ * EBEM_CACHE_MB (environment, default 16384) MB in total; an allocation that fails returns
+ * the cache to the driver and retries.  ebem_trim_cache returns every cached block to the
+ * driver now (for a caller that needs the memory elsewhere) and reports the bytes freed.
+ */
+int64_t ebem_trim_cache(void);
+
 typedef struct ebem_tree_info {
     int64_t nsrc, ntrg, nboxes, nleaves;
     int32_t nlevels, p, max_pts, n_equiv;   /* n_equiv = 6(p-1)^2+2 surface points */

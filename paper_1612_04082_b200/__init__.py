@@ -70,6 +70,7 @@ class PhaseStat(ctypes.Structure):
 _lib.fmm_set_profiling.argtypes = [_VP, ctypes.c_int]
 _lib.fmm_phase_stats.argtypes = [_VP, ctypes.c_int, ctypes.POINTER(PhaseStat), ctypes.c_int]
 _lib.ebem_launch_count.restype = _I64
+_lib.ebem_trim_cache.restype = _I64
 
 
 class EbemError(RuntimeError):
@@ -271,6 +272,11 @@ def ebem_launch_count():
     return int(_lib.ebem_launch_count())
 
 
+def ebem_trim_cache():
+    """Return the library's cached device blocks to the driver; the bytes freed."""
+    return int(_lib.ebem_trim_cache())
+
+
 class BemOperator:
     """owning wrapper of an ebem_bem* (bem_create / bem_free): the collocation BEM operator."""
 
@@ -348,5 +354,5 @@ def bem_gmres_history(bem):
 
 __all__ = ["bem_kernel_direct", "fmm_build_tree", "fmm_matvec", "fmm_eval_stress", "fmm_tree_info",
            "fmm_tree_export", "bem_create", "bem_apply", "bem_rhs", "bem_gmres_solve", "bem_gmres_history", "BemOperator", "fmm_set_profiling", "fmm_phase_stats",
-           "ebem_launch_count", "FmmTree", "EbemError", "LIB_PATH",
+           "ebem_launch_count", "ebem_trim_cache", "FmmTree", "EbemError", "LIB_PATH",
            "KERNEL_U", "KERNEL_P", "KERNEL_UP", "KERNEL_D", "KERNEL_S", "KERNEL_DS"]

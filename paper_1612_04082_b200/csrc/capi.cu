@@ -90,12 +90,14 @@ void cache_free(void* p, size_t bytes) {
     cudaFree(p);
 }
 
-void cache_trim() {
+int64_t cache_trim() {
     BlockCache& c = block_cache();
     std::lock_guard<std::mutex> g(c.mu);
     for (auto& kv : c.free_blocks) cudaFree(kv.second);
     c.free_blocks.clear();
+    const int64_t freed = (int64_t)c.cached;
     c.cached = 0;
+    return freed;
 }
 
 int num_sms() {
@@ -307,6 +309,8 @@ extern "C" int fmm_tree_free(ebem_tree* tree) {
 }
 
 extern "C" int64_t ebem_launch_count(void) { return launch_count(); }
+
+extern "C" int64_t ebem_trim_cache(void) { return cache_trim(); }
 
 extern "C" int fmm_set_profiling(ebem_tree* tree, int on) {
     EB_API_BEGIN

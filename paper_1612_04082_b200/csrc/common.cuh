@@ -48,7 +48,7 @@ void count_launch();
 // the driver (before free-memory queries).
 void* cache_alloc(size_t bytes);
 void cache_free(void* p, size_t bytes);
-void cache_trim();
+int64_t cache_trim();        // returns the bytes handed back to the driver
 
 // Owning device allocation (the block cache above; the library's only allocator for
 // long-lived state, stream-ordered cudaMallocAsync for per-call scratch).

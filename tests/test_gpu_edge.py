@@ -8,7 +8,7 @@ from oracle import cdirect
 from oracle import kernels as KN
 from oracle import tree as OT
 from workloads import geometry as geo
-from tests.gpu_util import assert_fmm_close, csr_lists, need_gpu, torch
+from tests.gpu_util import assert_fmm_close, csr_lists, need_gpu, to_dev, torch
 
 pytestmark = pytest.mark.gpu
 
@@ -189,3 +189,23 @@ def test_empty_inputs(eb):
     assert np.asarray(eb.fmm_eval_stress(tree, eb.KERNEL_DS, f, g)).shape == (0, 6)
     with pytest.raises(eb.EbemError):
         eb.fmm_build_tree(e3, e3, trg=e3, max_pts=16, p=4)
+
+
+def test_block_cache_reuse_and_trim(eb):
+    """Released tree workspace stays cached (include/elastobem.h, ebem_trim_cache): a second
+    tree of the same problem reuses it and gives the bitwise same matvec; trimming returns the
+    cached bytes and the next build allocates afresh."""
+    import gc
+    d = geo.config2(n=20000, seed=3)
+    t = to_dev(d)
+    tree = eb.fmm_build_tree(t["src"], t["nrm"], t["w"], max_pts=64, p=6, K=d["K"], G=d["G"])
+    a = eb.fmm_matvec(tree, eb.KERNEL_UP, t["f"], t["g"]).cpu().numpy()
+    del tree
+    gc.collect()
+    torch.cuda.synchronize()
+    freed = eb.ebem_trim_cache()
+    assert freed > 0
+    assert eb.ebem_trim_cache() == 0
+    tree = eb.fmm_build_tree(t["src"], t["nrm"], t["w"], max_pts=64, p=6, K=d["K"], G=d["G"])
+    b = eb.fmm_matvec(tree, eb.KERNEL_UP, t["f"], t["g"]).cpu().numpy()
+    assert np.array_equal(a, b)
