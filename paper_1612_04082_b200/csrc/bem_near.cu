@@ -228,7 +228,10 @@ __device__ __forceinline__ float tf32_rna_nm(float x) {
 // check rows: one CTA per row set, a thread per four consecutive check points (16-B loads
 // of the [9][ncp][rows padded to 4] layout, contiguous across threads), the set's panel
 // densities staged in shared memory, fp64 accumulation, the TF32 split written to Qb / Qs
-constexpr int CK_T = 128, CK_CH = 512, CK_G = 2;   // up to CK_G x 4 x CK_T = 1024 check points
+// CK_G row groups of 4 x CK_T check points per thread, instantiated for the surface at hand
+// (p = 8: 386 points, one group: 102 -> ~70 registers and more CTAs in flight)
+constexpr int CK_T = 128, CK_CH = 512, CK_GMAX = 2;   // up to CK_GMAX x 4 x CK_T = 1024 check points
+template <int CK_G, int UNR>
 __global__ void __launch_bounds__(CK_T)
 ck_apply(int nsets, int rows, const int* __restrict__ col_first, const int* __restrict__ ncol,
          const long long* __restrict__ moff, const int* __restrict__ col_panel, const float* __restrict__ M,
@@ -258,7 +261,7 @@ ck_apply(int nsets, int rows, const int* __restrict__ col_first, const int* __re
         for (int h = 0; h < CK_G; ++h) {
             const int g = threadIdx.x + h * CK_T;          // rows 4g .. 4g+3
             if (4 * g >= r4) continue;
-#pragma unroll 2
+#pragma unroll UNR
             for (int c = 0; c < cnt; ++c) {
                 const double xv[3] = {xs[c][0], xs[c][1], xs[c][2]};
                 const float* mc = base + (int64_t)(c0 + c) * r4 + 4 * g;
@@ -548,9 +551,18 @@ void panel_op_apply(const Tree& t, const PanelOp& N, const double* x, double* ne
         nm_apply<0><<<sd.nsets, NM_T, pad, s>>>(sd.nsets, sd.box, t.tbeg.p, t.tend.p, P.nc, N.col_first.p, N.ncol.p,
                                                N.moff.p, N.col_panel.p, N.M.p, x, near, nullptr, nullptr, 0);
     } else {
-        EB_REQUIRE(P.nc <= 4 * CK_G * CK_T, "check surface too large for ck_apply");
-        ck_apply<<<sd.nsets, CK_T, 0, s>>>(sd.nsets, P.nc, N.col_first.p, N.ncol.p, N.moff.p, N.col_panel.p, N.M.p, x,
-                                           Qb, Qs, ldq);
+        EB_REQUIRE(P.nc <= 4 * CK_GMAX * CK_T, "check surface too large for ck_apply");
+        static const int unr = std::getenv("EBEM_CK_UNROLL") ? std::atoi(std::getenv("EBEM_CK_UNROLL")) : 4;
+        auto go = [&](auto fn) {
+            fn<<<sd.nsets, CK_T, 0, s>>>(sd.nsets, P.nc, N.col_first.p, N.ncol.p, N.moff.p, N.col_panel.p, N.M.p, x, Qb,
+                                         Qs, ldq);
+        };
+        if (P.nc <= 4 * CK_T) {
+            if (unr == 2) go(ck_apply<1, 2>);
+            else go(ck_apply<1, 4>);
+        } else {
+            go(ck_apply<2, 2>);
+        }
     }
     EB_CHECK_LAUNCH();
 }
