@@ -165,9 +165,10 @@ __global__ void __launch_bounds__(LB_THREADS) lb_invert(const int4* __restrict__
 // panels = 90 unknowns on configs[4]): the matrix is read and written once; 128 threads, the
 // pivot search by warp shuffles; size classes keep the shared memory (and with it the CTAs
 // per SM) proportional to the block
-template <int NLO, int NHI>
-__global__ void __launch_bounds__(128) lb_invert_smem(const int4* __restrict__ blocks, double* __restrict__ M,
-                                                      int* __restrict__ fail) {
+template <int NLO, int NHI, int NT>
+__global__ void __launch_bounds__(NT) lb_invert_smem(const int4* __restrict__ blocks, double* __restrict__ M,
+                                                     int* __restrict__ fail) {
+    constexpr int NW = NT / 32;
     extern __shared__ double sh[];
     const int4 bk = blocks[blockIdx.x];
     const int n = 3 * bk.y;
@@ -178,8 +179,8 @@ __global__ void __launch_bounds__(128) lb_invert_smem(const int4* __restrict__ b
     const int ld = n + 1;
     __shared__ double prow[NHI], pcol[NHI];
     __shared__ int piv[NHI];
-    __shared__ double wv[4];
-    __shared__ int wi[4];
+    __shared__ double wv[NW];
+    __shared__ int wi[NW];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     for (int e = threadIdx.x; e < n * n; e += blockDim.x) A[(e / n) * ld + e % n] = G[e];
     __syncthreads();
@@ -208,7 +209,7 @@ __global__ void __launch_bounds__(128) lb_invert_smem(const int4* __restrict__ b
         __syncthreads();
         int p = wi[0];
         double pv = wv[0];
-        for (int w = 1; w < 4; ++w)
+        for (int w = 1; w < NW; ++w)
             if (wv[w] > pv || (wv[w] == pv && wi[w] < p)) {
                 pv = wv[w];
                 p = wi[w];
@@ -227,7 +228,7 @@ __global__ void __launch_bounds__(128) lb_invert_smem(const int4* __restrict__ b
         for (int i = threadIdx.x; i < n; i += blockDim.x) pcol[i] = A[i * ld + k];
         __syncthreads();
         const double d = 1.0 / prow[k];
-        for (int i = warp; i < n; i += 4) {               // a warp per row
+        for (int i = warp; i < n; i += NW) {              // a warp per row
             const double f = pcol[i];
             for (int j = lane; j < n; j += 32) {
                 if (i == k) A[i * ld + j] = j == k ? d : prow[j] * d;
@@ -328,15 +329,18 @@ bool leafblock_build(const Tree& t, int64_t npanels, int nq, const float* cent, 
     DBuf<int> fail(1);
     fail.zero(s);
     {   // small blocks in shared memory (two size classes), the rest in global memory
-        auto run = [&](auto fn, int nhi) {
+        // (the large class runs one CTA per SM: more warps hide the per-step latencies)
+        auto run = [&](auto fn, int nhi, int nt) {
             const int ns = std::min(maxn, nhi);
             const size_t sm = (size_t)ns * (ns + 1) * sizeof(double);
             if (sm > 48 * 1024) EB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-            fn<<<P.nblocks, 128, sm, s>>>(P.blocks.p, P.M.p, fail.p);
+            fn<<<P.nblocks, nt, sm, s>>>(P.blocks.p, P.M.p, fail.p);
             EB_CHECK_LAUNCH();
         };
-        run(lb_invert_smem<0, 96>, 96);
-        if (maxn > 96) run(lb_invert_smem<96, LB_NSMEM>, LB_NSMEM);
+        run(lb_invert_smem<0, 96, 256>, 96, 256);
+        lap("invert<=96");
+        if (maxn > 96) run(lb_invert_smem<96, LB_NSMEM, 512>, LB_NSMEM, 512);
+        lap("invert<=156");
     }
     if (maxn > LB_NSMEM) {
         const size_t sm = (size_t)maxn * (2 * sizeof(double) + sizeof(int));
