@@ -1095,6 +1095,40 @@ void schedule_tree(Tree& t, cudaStream_t s) {
         for (int o = 0; o < t.m2l.nops; ++o) t.w_m2l_ops += t.m2l.op_ptr_h[o + 1] > t.m2l.op_ptr_h[o];
     }
     lap("  work counts");
+    // leaves in order of decreasing pair work, so that the warp-per-leaf kernels end on small
+    // leaves instead of an SM-wide tail behind the largest: the near-field kernel (and the BEM
+    // near operator's row sets) by the near sum, the far-field kernel by L2T + M2T
+    // (EBEM_EVAL_ORDER=0: Morton order for both)
+    static const bool lpt = !(std::getenv("EBEM_EVAL_ORDER") && std::atoi(std::getenv("EBEM_EVAL_ORDER")) == 0);
+    std::vector<int> fev = ev, fl2t = l2t;
+    if (lpt && !ev.empty()) {
+        std::vector<double> wn(ev.size()), wf(ev.size());
+        for (size_t i = 0; i < ev.size(); ++i) {
+            const int b = ev[i];
+            double nfar = l2t[i] >= 0 ? 1.0 : 0.0;
+            for (int e = moff[b]; e < moff[b + 1]; ++e) nfar += phiu[midx[e]] >= 0 ? 1.0 : 0.0;
+            wn[i] = (double)tsub[b] * near_ns[b];
+            wf[i] = (double)tsub[b] * P.ne * nfar;
+        }
+        auto order = [&](const std::vector<double>& w, std::vector<int>& e_out, std::vector<int>& l_out) {
+            std::vector<int> ord(ev.size());
+            for (size_t i = 0; i < ord.size(); ++i) ord[i] = (int)i;
+            std::stable_sort(ord.begin(), ord.end(), [&](int x, int y) { return w[x] > w[y]; });
+            for (size_t i = 0; i < ord.size(); ++i) {
+                e_out[i] = ev[ord[i]];
+                l_out[i] = l2t[ord[i]];
+            }
+        };
+        std::vector<int> nev(ev.size()), nl2t(ev.size());
+        order(wf, fev, fl2t);
+        order(wn, nev, nl2t);
+        ev.swap(nev);
+        l2t.swap(nl2t);
+    }
+    t.far_box.alloc(std::max<size_t>(fev.size(), 1));
+    h2d(t.far_box.p, fev.data(), fev.size(), s);
+    t.far_l2t_slot.alloc(std::max<size_t>(fl2t.size(), 1));
+    h2d(t.far_l2t_slot.p, fl2t.data(), fl2t.size(), s);
     t.n_eval = (int)ev.size();
     t.n_phid = (int)phid_box.size();
     t.n_phiu = (int)phiu_box.size();
@@ -1411,7 +1445,7 @@ static void launch_far(const Tree& t, float* out, cudaStream_t s) {
         auto go = [&](auto ffn, const auto* near, auto* o) {
             if (sm > 48 * 1024)
                 EB_CUDA(cudaFuncSetAttribute(ffn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-            ffn<<<grid, 32 * EV_WARPS, sm, s>>>(t.n_eval, t.eval_box.p, t.eval_l2t_slot.p, t.PHID.p, t.PHIU.p,
+            ffn<<<grid, 32 * EV_WARPS, sm, s>>>(t.n_eval, t.far_box.p, t.far_l2t_slot.p, t.PHID.p, t.PHIU.p,
                                                 t.phiu_slot.p, t.m2t_off.p, t.m2t_idx.p, t.tbeg.p, t.tend.p,
                                                 t.anchor.p, t.level.p, geo, P.s_e64.p, P.ne, t.trg_xyz.p, kc, cfar,
                                                 near, t.trg_perm.p, o);
@@ -1424,7 +1458,7 @@ static void launch_far(const Tree& t, float* out, cudaStream_t s) {
         const size_t sm = sizeof(float4) * 2 * P.ne * EV_WARPS;
         auto ffn = far_eval_f32_kernel<STRESS>;
         if (sm > 48 * 1024) EB_CUDA(cudaFuncSetAttribute(ffn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-        ffn<<<grid, 32 * EV_WARPS, sm, s>>>(t.n_eval, t.eval_box.p, t.eval_l2t_slot.p, t.PHIDF.p, t.PHIUF.p,
+        ffn<<<grid, 32 * EV_WARPS, sm, s>>>(t.n_eval, t.far_box.p, t.far_l2t_slot.p, t.PHIDF.p, t.PHIUF.p,
                                             t.phiu_slot.p, t.m2t_off.p, t.m2t_idx.p, t.tbeg.p, t.tend.p,
                                             t.anchor.p, t.level.p, geo, P.s_e4.p, P.ne, t.trg_xyz.p, kc,
                                             t.near_sorted.p, t.trg_perm.p, out);

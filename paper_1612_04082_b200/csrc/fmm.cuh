@@ -131,6 +131,7 @@ struct Tree {
     int n_eval = 0;                      // leaves with targets
     DBuf<int> eval_box;                  // [n_eval]
     DBuf<int> eval_l2t_slot;             // row in PHI_D (-1 if leaf level < 2)
+    DBuf<int> far_box, far_l2t_slot;     // the same leaves in the far-field kernel's order
     int n_phid = 0;                      // leaves with L2T
     DBuf<int> phid_box;                  // [n_phid] (box ids) for the fp64 phi reconstruction
     int n_phiu = 0;                      // boxes appearing in some W list (with sources)
