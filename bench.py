@@ -485,14 +485,19 @@ def main():
     phases = eb.fmm_phase_stats(tree, eb.KERNEL_UP)
     eb.fmm_set_profiling(tree, False)
     ph_out = []
-    tensor_phases = ("Q2Z_up", "M2M", "Q2Z_dn", "M2L", "L2L")   # 3xTF32 tcgen05 path
+    tensor_phases = ("Q2Z_up", "M2M", "Q2Z_dn", "M2L", "L2L")   # tcgen05 path, three products per fp32 product
     pk["tf32x3_tflops"] = pk["tf32_tflops"] / 3.0                # fp32-equivalent peak of 3xTF32
+    pk["f16x3_tflops"] = pk["bf16_tflops"] / 3.0                 # ... of 3xFP16 (fp16 dense = bf16 dense rate)
+    # operand type of the M2L (the library's default: FP16 head / remainder, EBEM_M2L_F16 = 0: TF32)
+    m2l_f16 = int(os.environ.get("EBEM_M2L_F16", "2")) >= 1
+    def tensor_peak(name):
+        return pk["f16x3_tflops"] if (name == "M2L" and m2l_f16) else pk["tf32x3_tflops"]
     for ph in phases:
         f64, f32 = ph["flops_fp64"], ph["flops"] - ph["flops_fp64"]
         sec = ph["ms"] * 1e-3
         tmem = ph["bytes"] / (pk["hbm_gbs"] * 1e9)
         if ph["name"] in tensor_phases:
-            tmin, bound = ph["flops"] / (pk["tf32x3_tflops"] * 1e12), "tensor"
+            tmin, bound = ph["flops"] / (tensor_peak(ph["name"]) * 1e12), "tensor"
         else:
             tmin, bound = f32 / (pk["fp32_tflops"] * 1e12) + f64 / (pk["fp64_tflops"] * 1e12), "alu"
         if tmem > tmin:
@@ -511,15 +516,22 @@ def main():
     sec = (dom["ms_in_situ"] or dom["ms"]) * 1e-3   # in situ: inside the timed, overlapped step
     sec_solo = dom["ms"] * 1e-3
     if dom["bound"] == "tensor":
+        tpk = tensor_peak(dom["name"])
+        f16 = dom["name"] == "M2L" and m2l_f16
         roof = {"bound": "tensor", "phase": dom["name"], "achieved": dph["flops"] / sec / 1e12,
-                "peak": pk["tf32x3_tflops"], "unit": "TFLOP/s", "frac": dph["flops"] / sec / 1e12 / pk["tf32x3_tflops"],
-                "frac_in_situ": dph["flops"] / sec / 1e12 / pk["tf32x3_tflops"],
-                "frac_solo": dph["flops"] / sec_solo / 1e12 / pk["tf32x3_tflops"],
+                "peak": tpk, "unit": "TFLOP/s", "frac": dph["flops"] / sec / 1e12 / tpk,
+                "frac_in_situ": dph["flops"] / sec / 1e12 / tpk,
+                "frac_solo": dph["flops"] / sec_solo / 1e12 / tpk,
                 "ms_in_situ": dom["ms_in_situ"], "ms_solo": dom["ms"], "traffic": None,
-                "peak_source": "measured bf16 GEMM x 1.1/2.25 (guide's nominal TF32 / bf16 dense ratio) / 3 "
-                               "(3xTF32 = fp32-accurate); achieved counts algorithmic fp32 flops 2*M*K per pair; "
+                "operands": "fp16 head/remainder (3xFP16)" if f16 else "tf32 head/remainder (3xTF32)",
+                "peak_source": ("measured bf16 GEMM (fp16 dense = bf16 dense rate) / 3 (3xFP16 = fp32-accurate)" if f16 else
+                                "measured bf16 GEMM x 1.1/2.25 (guide's nominal TF32 / bf16 dense ratio) / 3 "
+                                "(3xTF32 = fp32-accurate)") +
+                               "; achieved counts algorithmic fp32 flops 2*M*K per pair; "
                                "frac = frac_in_situ (CUDA events on the M2L stream inside the timed region), "
-                               "frac_solo = the phase run alone"}
+                               "frac_solo = the phase run alone (incl. the fp16 split of the Z rows)"}
+        if f16:   # the same time against the round-1 denominator (3xTF32), for comparison across rounds
+            roof["frac_solo_vs_tf32x3_peak"] = dph["flops"] / sec_solo / 1e12 / pk["tf32x3_tflops"]
     elif dom["bound"] == "alu":
         f64, f32 = dph["flops_fp64"], dph["flops"] - dph["flops_fp64"]
         peak = dph["flops"] / (f32 / pk["fp32_tflops"] + f64 / pk["fp64_tflops"]) if dph["flops"] else pk["fp32_tflops"]
@@ -616,7 +628,7 @@ def main():
     if rank == 0:
         line = {"metric": METRIC, "value": ms, "unit": "ms", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False, "scaling": "weak",
-                "vs_baseline": None, "dtype": "f32 (3xTF32 translations; fp64 plan, fp64 equivalent densities)",
+                "vs_baseline": None, "dtype": "f32 (3xFP16 M2L, 3xTF32 M2M/L2L/Q2Z; fp64 plan, fp64 equivalent densities)",
                 "data": "synthetic",
                 "config": {"workload": WORKLOAD, "n_points": n, "p": args.p, "max_pts": args.max_pts,
                            "kernel": "UP", "l2": "flushed between steps (256 MB write)",

@@ -693,6 +693,13 @@ near_eval_p_kernel(int n_eval, const int* __restrict__ eval_box, const int* __re
 
 // precise M2L (p >= 9, GMRES) on the two-slice fast-kernel data flow with drained groups;
 // EBEM_M2L_DRAIN=0 selects the one-slice precise kernel instead
+// EBEM_M2L_F16: 0 = M2L operands in TF32; 1 = FP16 for the full-chain M2L (p <= 8 matvec, GMRES
+// solves with tol >= 1e-6); 2 = FP16 for the drained (precise) M2L too
+static int m2l_f16_level() {
+    static const int lv = std::getenv("EBEM_M2L_F16") ? std::atoi(std::getenv("EBEM_M2L_F16")) : 2;
+    return lv;
+}
+static bool m2l_use_f16(const Tree& t) { return t.m2l_f16 && (t.tc_fast || m2l_f16_level() >= 2); }
 static bool m2l_drain_fast() {
     static const bool on = !(std::getenv("EBEM_M2L_DRAIN") && std::atoi(std::getenv("EBEM_M2L_DRAIN")) == 0);
     return on;
@@ -1184,7 +1191,17 @@ void schedule_tree(Tree& t, cudaStream_t s) {
         const int fm = tc_fast_tile_mode(me);
         tc_build_tiles(t.q2z_up, me, mc, t.ml_fast ? fm : 0);
         tc_build_tiles(t.q2z_dn, me, mc, t.ml_fast ? fm : 0);
-        tc_build_tiles(t.m2l, me, me, t.tc_fast || m2l_drain_fast() ? fm : 0);
+        // M2L operands in FP16 (3xFP16, twice the tensor rate of 3xTF32; EBEM_M2L_F16=0: TF32)
+        t.m2l_f16 = m2l_f16_level() >= 1;
+        if (t.m2l_f16) {
+            t.Zhb.alloc((size_t)std::max(1, t.n_up) * P.ldh);
+            t.Zhs.alloc((size_t)std::max(1, t.n_up) * P.ldh);
+            t.Zhinv.alloc(std::max(1, t.n_up));
+            t.Zhb.zero(s);
+            t.Zhs.zero(s);
+        }
+        tc_build_tiles(t.m2l, me, me, t.tc_fast || m2l_drain_fast() ? fm : 0,
+                       (t.tc_fast || m2l_drain_fast()) && m2l_use_f16(t) ? 64 : 32);
         for (auto& x : t.m2m) tc_build_tiles(x, me, me, t.ml_fast ? fm : 0);
         for (auto& x : t.l2l) tc_build_tiles(x, me, me, t.ml_fast ? fm : 0);
         // EBEM_ML_CHAIN=1: M2M and L2L chains as one persistent launch each (tc_chain_kernel).
@@ -1372,7 +1389,8 @@ void tree_m2l_fast(Tree& t, bool fast, cudaStream_t s) {
     fast = fast && t.use_tc && P.p < FAR_FP64_MIN_P;
     if (fast == t.tc_fast) return;
     t.tc_fast = fast;
-    tc_build_tiles(t.m2l, P.me, P.me, fast || m2l_drain_fast() ? tc_fast_tile_mode(P.me) : 0);
+    tc_build_tiles(t.m2l, P.me, P.me, fast || m2l_drain_fast() ? tc_fast_tile_mode(P.me) : 0,
+                   (fast || m2l_drain_fast()) && m2l_use_f16(t) ? 64 : 32);
     EB_CUDA(cudaStreamSynchronize(s));
 }
 
@@ -1696,7 +1714,12 @@ void fmm_evaluate(Tree& t, int kernel, const float* f, const float* g, float* ou
         if (!ps) EB_CUDA(cudaEventRecord(t.ev_m2l, sa));
     }
     pb(PH_M2L, sa);
-    if (t.use_tc && t.tc_fast) tc_pairs_gemm_fast(t.m2l, P.mM2L_b, P.mM2L_s, t.Zb.p, t.Zs.p, lde, me, me, t.W.p, lde, false, sa);
+    if (t.use_tc && m2l_use_f16(t) && (t.tc_fast || m2l_drain_fast())) {
+        // 3xFP16: row-scaled fp16 split of every Z row, then the same kernels on fp16 operands
+        tc_split_rows_h(t.Z.p, lde, 0, t.n_up, me, t.Zhb.p, t.Zhs.p, P.ldh, t.Zhinv.p, sa);
+        tc_pairs_gemm_fast(t.m2l, P.mM2L_hb, P.mM2L_hs, t.Zhb.p, t.Zhs.p, P.ldh, me, me, t.W.p, lde, !t.tc_fast, sa,
+                           true, t.Zhinv.p, P.m2l_hinv);
+    } else if (t.use_tc && t.tc_fast) tc_pairs_gemm_fast(t.m2l, P.mM2L_b, P.mM2L_s, t.Zb.p, t.Zs.p, lde, me, me, t.W.p, lde, false, sa);
     else if (t.use_tc && m2l_drain_fast())   // precise accumulation, two-slice fast-kernel data flow
         tc_pairs_gemm_fast(t.m2l, P.mM2L_b, P.mM2L_s, t.Zb.p, t.Zs.p, lde, me, me, t.W.p, lde, true, sa);
     else if (t.use_tc) tc_pairs_gemm(t.m2l, P.mM2L_b, P.mM2L_s, t.mZb, t.mZs, me, me, t.W.p, lde, sa);

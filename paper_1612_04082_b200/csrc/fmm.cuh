@@ -15,6 +15,7 @@
 // L2T and M2T.
 #pragma once
 #include <cuda.h>
+#include <cuda_fp16.h>
 
 #include <functional>
 #include <map>
@@ -48,6 +49,13 @@ struct Plan {
     // exact-TF32 head / remainder splits of the operators (3xTF32 tensor-core path)
     DBuf<float> Qu1T_b, Qu1T_s, Qd1T_b, Qd1T_s, M2M_b, M2M_s, L2L_b, L2L_s, M2L_b, M2L_s;
     CUtensorMap mQu1T_b, mQu1T_s, mQd1T_b, mQd1T_s, mM2M_b, mM2M_s, mL2L_b, mL2L_s, mM2L_b, mM2L_s;
+    // scaled FP16 head / remainder copies of the M2L operators (3xFP16 path, tc_gemm.cu): row
+    // stride ldh halves (me rounded up to 8: 16-B rows), one power-of-two scale for the set
+    // (m2l_hinv undoes it)
+    DBuf<__half> M2L_hb, M2L_hs;
+    CUtensorMap mM2L_hb, mM2L_hs;
+    int ldh = 0;
+    float m2l_hinv = 1.f;
     int off_index[343];         // (ox+3)*49+(oy+3)*7+(oz+3) -> 0..315 or -1
 };
 
@@ -65,6 +73,7 @@ struct OpPairs {
     int ntiles = 0;              // tensor-core tiles (op, first pair, #pairs, row block)
     int tile_mode = 0;           // tile shape: 0 128 rows x 128 pairs (precise), 1 256 x 128 (fast /
                                  // drained two-slice), 2 128 x 256 (wide, full-chain)
+    int tile_bke = 32;           // K elements per 128-B chunk the tiles were cut for: 32 (TF32) or 64 (FP16)
     DBuf<int> tiles;
 };
 
@@ -183,6 +192,11 @@ struct Tree {
                                          // the sum order-independent at fp32 precision (deterministic)
     DBuf<float> Qb, Qs, Qdb, Qds, Zb, Zs, Wb, Ws;   // TF32 head / remainder copies (B operands)
     CUtensorMap mQb, mQs, mQdb, mQds, mZb, mZs, mWb, mWs;
+    // 3xFP16 M2L: row-scaled fp16 head / remainder copies of the Z rows and the factors undoing
+    // each row's scale (split once per evaluation, after the upward pass)
+    DBuf<__half> Zhb, Zhs;
+    DBuf<float> Zhinv;
+    bool m2l_f16 = false;                // M2L operands in FP16 (EBEM_M2L_F16, default on)
     DBuf<double> PHID, PHIU;             // [n_phid x me], [n_phiu x me] (fp64 far field)
     DBuf<float4> PHIDF, PHIUF;           // [n_phid x ne], [n_phiu x ne] (fp32 far field, scaled)
     DBuf<float> near_sorted;             // [ntrg x 6] near field, sorted target order
@@ -247,7 +261,11 @@ void tc_split_rows(const XT* X, int ld, int64_t row0, int64_t nrows, int K, floa
 void tree_precise(Tree& t, cudaStream_t s);
 void tree_partition_sources(Tree& t, const int32_t* bc, int nq, cudaStream_t s);
 void tree_m2l_fast(Tree& t, bool fast, cudaStream_t s);
-void tc_build_tiles(OpPairs& P, int M, int K, int mode);
+void tc_build_tiles(OpPairs& P, int M, int K, int mode, int bke = 32);
+void tc_make_map_a_h(CUtensorMap* m, const __half* base, int nops, int M, int K, int ldh);
+float tc_split_ops_h(const float* X, int ld, int64_t nrows, int K, __half* Xh, __half* Xr, int ldh, cudaStream_t s);
+void tc_split_rows_h(const double* X, int ldx, int64_t row0, int64_t nrows, int K, __half* Xh, __half* Xr, int ldh,
+                     float* inv_scale, cudaStream_t s);
 void tc_build_chain(Chain& ch, const std::vector<const OpPairs*>& levels, const std::vector<int64_t>& row0,
                     const std::vector<int64_t>& nrows, int M, int K, cudaStream_t s);
 // X: fp64 state rows (ldx), split into Xb / Xs level by level ([row0, row0 + nrows) before
@@ -257,8 +275,9 @@ void tc_chain_run(const Chain& ch, const CUtensorMap& Ab, const CUtensorMap& As,
 int tc_fast_tile_mode(int M);                  // full-chain tile shape for M operator rows: 1 two-slice, 2 wide
 int tc_fast_smem_bytes();                     // dynamic shared memory of one fast translation CTA
 int beside_translation_pad(const void* kernel);   // fmm.cu: stream-B co-residency padding
-void tc_pairs_gemm_fast(const OpPairs& P, const CUtensorMap& Ab, const CUtensorMap& As, const float* Bb,
-                        const float* Bs, int ldb, int M, int K, double* Y, int ldy, bool drain, cudaStream_t s);
+void tc_pairs_gemm_fast(const OpPairs& P, const CUtensorMap& Ab, const CUtensorMap& As, const void* Bb,
+                        const void* Bs, int ldb, int M, int K, double* Y, int ldy, bool drain, cudaStream_t s,
+                        bool f16 = false, const float* bscale = nullptr, float ascale_inv = 1.f);
 void tc_pairs_gemm(const OpPairs& P, const CUtensorMap& Ab, const CUtensorMap& As, const CUtensorMap& Bb,
                    const CUtensorMap& Bs, int M, int K, double* Y, int ldy, cudaStream_t s);
 // fp64 variant with per-pair scale (r of the box, looked up from scale[t])

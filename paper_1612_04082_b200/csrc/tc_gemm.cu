@@ -15,10 +15,13 @@
 // sums into fp32 registers, then fp32 atomics into Y (coalesced along rows).
 // 3-stage smem ring of 4 x 16 KB (SWIZZLE_128B, K-major), mbarrier full/empty pipeline.
 #include <cuda.h>
+#include <cuda_fp16.h>
 
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
+#include <cmath>
 
 #include "fmm.cuh"
 
@@ -87,6 +90,27 @@ __device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t a, uint64_t b
         "setp.ne.b32 p, %4, 0;\n\t"
         "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}"
         ::"r"(tmem_d), "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void mma_f16(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}"
+        ::"r"(tmem_d), "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+// operand element type of the fast / wide kernels: TF32 (4 B, 8 per MMA) or FP16 (2 B, 16 per
+// MMA).  A K chunk is 128 B of each operand row either way, so the shared-memory layout, the
+// TMA boxes (in bytes) and the 16-B cp.async gathers are the same; an FP16 chunk carries twice
+// the K extent for the same tensor-pipe time.
+template <bool F16>
+__device__ __forceinline__ void mma_op(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+    if (F16) mma_f16(tmem_d, a, b, idesc, acc);
+    else mma_tf32(tmem_d, a, b, idesc, acc);
+}
+// instruction descriptor: D f32, A/B tf32 (format 2) or f16 (format 0), both K-major
+template <bool F16>
+__device__ __forceinline__ uint32_t make_idesc(uint32_t n, uint32_t m) {
+    return (1u << 4) | ((F16 ? 0u : 2u) << 7) | ((F16 ? 0u : 2u) << 10) | ((n >> 3) << 17) | ((m >> 4) << 24);
 }
 __device__ __forceinline__ void mma_commit(uint32_t bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
@@ -325,12 +349,41 @@ constexpr int NG = (BN / 4 + NPROD - 1) / NPROD;        // 4-row groups per prod
 // (one per TMEM lane quarter and slice) add each finished group into fp32 registers (round
 // to nearest) while the MMA fills the other buffer, so no tensor-core accumulation chain is
 // longer than GROUP chunks.
-template <bool DRAIN>
+// Epilogue of a translation tile: Y[target row][row] += v (fp64 atomic: exact, order
+// independent).  Each lane owns one TMEM lane (operator row) and walks the tile's columns
+// (pairs); the column's target row and scale are loaded once per 32 columns, one column per
+// lane (coalesced, independent loads), and broadcast by shuffles -- a uniform load per column
+// in the atomic loop left the epilogue warps on the load latency (two dependent loads per
+// column with FP16 operands).  FP16 operands are scaled by powers of two -- the operator set
+// by 1 / ascale_inv, every source row by 1 / bscale[row] (split_rows_h_kernel) -- which the
+// fp32 product undoes exactly.
+template <bool F16>
+__device__ __forceinline__ void epi_cols_load(const int2* __restrict__ pp, int c0, int np, int lane,
+                                              const float* __restrict__ bscale, float ascale_inv, int& trow,
+                                              float& sc) {
+    const int2 pr = c0 + lane < np ? __ldg(&pp[c0 + lane]) : make_int2(0, 0);
+    trow = pr.x;
+    sc = 1.f;
+    if (F16) sc = ascale_inv * __ldg(&bscale[pr.y]);
+}
+template <bool F16>
+__device__ __forceinline__ void epi_col_add(double* __restrict__ Y, int ldy, int row, bool on, int trow, float sc,
+                                            int j, float v) {
+    const int tr = __shfl_sync(0xffffffffu, trow, j);
+    if (F16) v *= __shfl_sync(0xffffffffu, sc, j);
+    if (on) atomicAdd(Y + (int64_t)tr * ldy + row, (double)v);
+}
+
+template <bool DRAIN, bool F16>
 __global__ void __launch_bounds__(DRAIN ? 384 : fast::THREADS, 1)
 tc_pairs_fast_kernel(const __grid_constant__ CUtensorMap mapAb, const __grid_constant__ CUtensorMap mapAs,
-                     const float* __restrict__ Bb, const float* __restrict__ Bs, int ldb,
+                     const void* __restrict__ Bb_, const void* __restrict__ Bs_, int ldb,
                      const Tile* __restrict__ tiles, int ntiles, const int2* __restrict__ pairs, int M, int K,
-                     double* __restrict__ Y, int ldy) {
+                     double* __restrict__ Y, int ldy, const float* __restrict__ bscale, float ascale_inv) {
+    // element size / K elements per 128-B chunk / K elements per MMA of the operand type
+    constexpr int ES = F16 ? 2 : 4, BKE = 128 / ES, KS = 32 / ES;
+    const char* Bb = reinterpret_cast<const char*>(Bb_);
+    const char* Bs = reinterpret_cast<const char*>(Bs_);
     constexpr int MT = fast::MT, STAGES = fast::STAGES, STAGE_BYTES = fast::STAGE_BYTES, TMEM_COLS = fast::TMEM_COLS;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
@@ -389,12 +442,12 @@ tc_pairs_fast_kernel(const __grid_constant__ CUtensorMap mapAb, const __grid_con
                 if (pi == 0 && lane == 0) {
                     mbar_expect_tx(full, 2 * nmt * OPND_BYTES);
                     for (int mt = 0; mt < nmt; ++mt) {
-                        tma_load_3d(smem_u32(st + (2 * mt) * OPND_BYTES), &mapAb, kc * BK, tl.m0 + mt * BM, tl.op, full);
-                        tma_load_3d(smem_u32(st + (2 * mt + 1) * OPND_BYTES), &mapAs, kc * BK, tl.m0 + mt * BM, tl.op,
+                        tma_load_3d(smem_u32(st + (2 * mt) * OPND_BYTES), &mapAb, kc * BKE, tl.m0 + mt * BM, tl.op, full);
+                        tma_load_3d(smem_u32(st + (2 * mt + 1) * OPND_BYTES), &mapAs, kc * BKE, tl.m0 + mt * BM, tl.op,
                                     full);
                     }
                 }
-                const int col = kc * BK + 4 * piece;
+                const int col = kc * BKE + (16 / ES) * piece;
                 const uint32_t nb = col < ldb ? 16u : 0u;      // zero-fill past the row
                 const int ngrp = ((tl.np + 15) & ~15) / 4;     // row groups the MMA reads (N)
                 const uint32_t b0 = smem_u32(st + 2 * MT * OPND_BYTES);
@@ -404,7 +457,7 @@ tc_pairs_fast_kernel(const __grid_constant__ CUtensorMap mapAb, const __grid_con
                     const int grp = pi + fast::NPROD * g;
                     if (grp < ngrp) {
                         const int r = rsub + 4 * grp;
-                        const int64_t off = srow[g] + col;
+                        const int64_t off = (srow[g] + col) * ES;
                         const uint32_t so = (uint32_t)(r * 128 + ((piece ^ (r & 7)) * 16));
                         asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(b0 + so),
                                      "l"(nb ? Bb + off : Bb), "r"(nb)
@@ -422,8 +475,7 @@ tc_pairs_fast_kernel(const __grid_constant__ CUtensorMap mapAb, const __grid_con
         int c = 0, G = 0;
         for (int ti = blockIdx.x; ti < ntiles; ti += gridDim.x) {
             const uint32_t nmma = (uint32_t)((tiles[ti].np + 15) & ~15);
-            const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((nmma >> 3) << 17) |
-                                   ((uint32_t)(BM >> 4) << 24);
+            const uint32_t idesc = make_idesc<F16>(nmma, BM);
             const int kc0 = tiles[ti].kc0, kc1 = tiles[ti].kc1;
             for (int kc = kc0; kc < kc1; ++kc, ++c) {
                 const int s = c % STAGES;
@@ -440,7 +492,7 @@ tc_pairs_fast_kernel(const __grid_constant__ CUtensorMap mapAb, const __grid_con
                 if (lane == 0) {
                     const uint32_t st = smem_u32(smem + s * STAGE_BYTES);
                     const uint64_t bb = smem_desc(st + 2 * MT * OPND_BYTES), bs = smem_desc(st + (2 * MT + 1) * OPND_BYTES);
-                    const int ksteps = min(BK, K - kc * BK + 7) / 8;
+                    const int ksteps = min(BKE, K - kc * BKE + KS - 1) / KS;
                     for (int k = 0; k < ksteps; ++k) {
                         const uint64_t off = (uint64_t)(2 * k);
 #pragma unroll
@@ -449,9 +501,9 @@ tc_pairs_fast_kernel(const __grid_constant__ CUtensorMap mapAb, const __grid_con
                             const uint64_t a_b = smem_desc(st + (2 * mt) * OPND_BYTES) + off;
                             const uint64_t a_s = smem_desc(st + (2 * mt + 1) * OPND_BYTES) + off;
                             const uint32_t d = tmem + (uint32_t)((b * MT + mt) * BN);
-                            mma_tf32(d, a_b, bb + off, idesc, !gfirst || k != 0);
-                            mma_tf32(d, a_b, bs + off, idesc, 1);
-                            mma_tf32(d, a_s, bb + off, idesc, 1);
+                            mma_op<F16>(d, a_b, bb + off, idesc, !gfirst || k != 0);
+                            mma_op<F16>(d, a_b, bs + off, idesc, 1);
+                            mma_op<F16>(d, a_s, bb + off, idesc, 1);
                         }
                     }
                     mma_commit(smem_u32(&empty_b[s]));
@@ -468,8 +520,7 @@ tc_pairs_fast_kernel(const __grid_constant__ CUtensorMap mapAb, const __grid_con
             const int ab = it & 1;
             // N = the tile's pairs rounded up to 16: partial tiles cost in proportion
             const uint32_t nmma = (uint32_t)((tiles[ti].np + 15) & ~15);
-            const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((nmma >> 3) << 17) |
-                                   ((uint32_t)(BM >> 4) << 24);
+            const uint32_t idesc = make_idesc<F16>(nmma, BM);
             mbar_wait(smem_u32(&acce_b[ab]), ((it >> 1) & 1) ^ 1);
             asm volatile("tcgen05.fence::after_thread_sync;");
             const int kc0 = tiles[ti].kc0, kc1 = tiles[ti].kc1;
@@ -481,7 +532,7 @@ tc_pairs_fast_kernel(const __grid_constant__ CUtensorMap mapAb, const __grid_con
                 if (lane == 0) {
                     const uint32_t st = smem_u32(smem + s * STAGE_BYTES);
                     const uint64_t bb = smem_desc(st + 2 * MT * OPND_BYTES), bs = smem_desc(st + (2 * MT + 1) * OPND_BYTES);
-                    const int ksteps = min(BK, K - kc * BK + 7) / 8;
+                    const int ksteps = min(BKE, K - kc * BKE + KS - 1) / KS;
                     for (int k = 0; k < ksteps; ++k) {
                         const uint64_t off = (uint64_t)(2 * k);
 #pragma unroll
@@ -490,9 +541,9 @@ tc_pairs_fast_kernel(const __grid_constant__ CUtensorMap mapAb, const __grid_con
                             const uint64_t a_b = smem_desc(st + (2 * mt) * OPND_BYTES) + off;
                             const uint64_t a_s = smem_desc(st + (2 * mt + 1) * OPND_BYTES) + off;
                             const uint32_t d = tmem + (uint32_t)((ab * MT + mt) * BN);
-                            mma_tf32(d, a_b, bb + off, idesc, kc != kc0 || k != 0);
-                            mma_tf32(d, a_b, bs + off, idesc, 1);
-                            mma_tf32(d, a_s, bb + off, idesc, 1);
+                            mma_op<F16>(d, a_b, bb + off, idesc, kc != kc0 || k != 0);
+                            mma_op<F16>(d, a_b, bs + off, idesc, 1);
+                            mma_op<F16>(d, a_s, bb + off, idesc, 1);
                         }
                     }
                     mma_commit(smem_u32(&empty_b[s]));
@@ -521,11 +572,16 @@ tc_pairs_fast_kernel(const __grid_constant__ CUtensorMap mapAb, const __grid_con
                 if (lane == 0) mbar_arrive(smem_u32(&acce_b[b]));
             }
             const int row = tl.m0 + mt * BM + 32 * wq + lane;
-            if (row < M) {
-                const int2* pp = pairs + tl.p0;
+            const int2* pp = pairs + tl.p0;
 #pragma unroll
-                for (int j = 0; j < BN; ++j)
-                    if (j < tl.np) atomicAdd(Y + (int64_t)__ldg(&pp[j].x) * ldy + row, (double)acc[j]);
+            for (int c0 = 0; c0 < BN; c0 += 32) {
+                if (c0 >= tl.np) break;
+                int trow;
+                float sc;
+                epi_cols_load<F16>(pp, c0, tl.np, lane, bscale, ascale_inv, trow, sc);
+#pragma unroll
+                for (int j = 0; j < 32; ++j)
+                    if (c0 + j < tl.np) epi_col_add<F16>(Y, ldy, row, row < M, trow, sc, j, acc[c0 + j]);
             }
         }
     } else if (warp >= EPI_WARP0 && warp < EPI_WARP0 + 4) {
@@ -538,20 +594,22 @@ tc_pairs_fast_kernel(const __grid_constant__ CUtensorMap mapAb, const __grid_con
             mbar_wait(smem_u32(&accf_b[ab]), (it >> 1) & 1);
             asm volatile("tcgen05.fence::after_thread_sync;");
             const int2* pp = pairs + tl.p0;
-#pragma unroll
-            for (int mt = 0; mt < MT; ++mt) {
-                const int row = tl.m0 + mt * BM + 32 * wq + lane;
 #pragma unroll 1
-                for (int c0 = 0; c0 < tl.np; c0 += 32) {
+            for (int c0 = 0; c0 < tl.np; c0 += 32) {
+                int trow;
+                float sc;
+                epi_cols_load<F16>(pp, c0, tl.np, lane, bscale, ascale_inv, trow, sc);
+#pragma unroll
+                for (int mt = 0; mt < MT; ++mt) {
+                    const int row = tl.m0 + mt * BM + 32 * wq + lane;
+                    if (tl.m0 + mt * BM >= M) continue;      // slice not multiplied (warp-uniform)
                     uint32_t v[32];
                     tmem_ld32(tmem + ((uint32_t)(32 * wq) << 16) + (uint32_t)((ab * MT + mt) * BN + c0), v);
                     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-                    if (row < M) {
 #pragma unroll
-                        for (int j = 0; j < 32; ++j)
-                            if (c0 + j < tl.np)
-                                atomicAdd(Y + (int64_t)__ldg(&pp[c0 + j].x) * ldy + row, (double)__uint_as_float(v[j]));
-                    }
+                    for (int j = 0; j < 32; ++j)
+                        if (c0 + j < tl.np)
+                            epi_col_add<F16>(Y, ldy, row, row < M, trow, sc, j, __uint_as_float(v[j]));
                 }
             }
             asm volatile("tcgen05.fence::before_thread_sync;");
@@ -586,12 +644,16 @@ constexpr int NG = (BNW / 4 + NPROD - 1) / NPROD;       // four-row groups per p
 
 // DRAIN = true: drained groups as in tc_pairs_fast_kernel<true> (GROUP K chunks per ping-pong
 // buffer of 256 columns, eight drain warps: lane quarter x column half, fp32 register sums)
-template <bool DRAIN>
+template <bool DRAIN, bool F16>
 __global__ void __launch_bounds__(DRAIN ? 384 : wide::THREADS, 1)
 tc_pairs_wide_kernel(const __grid_constant__ CUtensorMap mapAb, const __grid_constant__ CUtensorMap mapAs,
-                     const float* __restrict__ Bb, const float* __restrict__ Bs, int ldb,
+                     const void* __restrict__ Bb_, const void* __restrict__ Bs_, int ldb,
                      const Tile* __restrict__ tiles, int ntiles, const int2* __restrict__ pairs, int M, int K,
-                     double* __restrict__ Y, int ldy) {
+                     double* __restrict__ Y, int ldy, const float* __restrict__ bscale, float ascale_inv) {
+    // element size / K elements per 128-B chunk / K elements per MMA of the operand type
+    constexpr int ES = F16 ? 2 : 4, BKE = 128 / ES, KS = 32 / ES;
+    const char* Bb = reinterpret_cast<const char*>(Bb_);
+    const char* Bs = reinterpret_cast<const char*>(Bs_);
     constexpr int STAGES = wide::STAGES, STAGE_BYTES = wide::STAGE_BYTES, A_BYTES = wide::A_BYTES,
                   B_BYTES = wide::B_BYTES, TMEM_COLS = wide::TMEM_COLS, NPROD = wide::NPROD, NG = wide::NG,
                   BNW = wide::BNW;
@@ -647,10 +709,10 @@ tc_pairs_wide_kernel(const __grid_constant__ CUtensorMap mapAb, const __grid_con
                 const uint32_t full = smem_u32(&full_b[s]);
                 if (pi == 0 && lane == 0) {
                     mbar_expect_tx(full, 2 * A_BYTES);
-                    tma_load_3d(smem_u32(st), &mapAb, kc * BK, tl.m0, tl.op, full);
-                    tma_load_3d(smem_u32(st + A_BYTES), &mapAs, kc * BK, tl.m0, tl.op, full);
+                    tma_load_3d(smem_u32(st), &mapAb, kc * BKE, tl.m0, tl.op, full);
+                    tma_load_3d(smem_u32(st + A_BYTES), &mapAs, kc * BKE, tl.m0, tl.op, full);
                 }
-                const int col = kc * BK + 4 * piece;
+                const int col = kc * BKE + (16 / ES) * piece;
                 const uint32_t nb = col < ldb ? 16u : 0u;      // zero-fill past the row
                 const uint32_t b0 = smem_u32(st + 2 * A_BYTES);
                 const uint32_t b1 = b0 + B_BYTES;
@@ -659,7 +721,7 @@ tc_pairs_wide_kernel(const __grid_constant__ CUtensorMap mapAb, const __grid_con
                     const int grp = pi + NPROD * g;
                     if (grp < ngrp) {
                         const int r = rsub + 4 * grp;
-                        const int64_t off = srow[g] + col;
+                        const int64_t off = (srow[g] + col) * ES;
                         const uint32_t so = (uint32_t)(r * 128 + ((piece ^ (r & 7)) * 16));
                         asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(b0 + so),
                                      "l"(nb ? Bb + off : Bb), "r"(nb)
@@ -677,8 +739,7 @@ tc_pairs_wide_kernel(const __grid_constant__ CUtensorMap mapAb, const __grid_con
         int c = 0, G = 0;
         for (int ti = blockIdx.x; ti < ntiles; ti += gridDim.x) {
             const uint32_t nmma = (uint32_t)((tiles[ti].np + 15) & ~15);
-            const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((nmma >> 3) << 17) |
-                                   ((uint32_t)(BM >> 4) << 24);
+            const uint32_t idesc = make_idesc<F16>(nmma, BM);
             const int kc0 = tiles[ti].kc0, kc1 = tiles[ti].kc1;
             for (int kc = kc0; kc < kc1; ++kc, ++c) {
                 const int s = c % STAGES;
@@ -697,12 +758,12 @@ tc_pairs_wide_kernel(const __grid_constant__ CUtensorMap mapAb, const __grid_con
                     const uint64_t a_b = smem_desc(st), a_s = smem_desc(st + A_BYTES);
                     const uint64_t bb = smem_desc(st + 2 * A_BYTES), bs = smem_desc(st + 2 * A_BYTES + B_BYTES);
                     const uint32_t d = tmem + (uint32_t)(b * BNW);
-                    const int ksteps = min(BK, K - kc * BK + 7) / 8;
+                    const int ksteps = min(BKE, K - kc * BKE + KS - 1) / KS;
                     for (int k = 0; k < ksteps; ++k) {
                         const uint64_t off = (uint64_t)(2 * k);
-                        mma_tf32(d, a_b + off, bb + off, idesc, !gfirst || k != 0);
-                        mma_tf32(d, a_b + off, bs + off, idesc, 1);
-                        mma_tf32(d, a_s + off, bb + off, idesc, 1);
+                        mma_op<F16>(d, a_b + off, bb + off, idesc, !gfirst || k != 0);
+                        mma_op<F16>(d, a_b + off, bs + off, idesc, 1);
+                        mma_op<F16>(d, a_s + off, bb + off, idesc, 1);
                     }
                     mma_commit(smem_u32(&empty_b[s]));
                     if (glast) mma_commit(smem_u32(&accf_b[b]));
@@ -731,11 +792,17 @@ tc_pairs_wide_kernel(const __grid_constant__ CUtensorMap mapAb, const __grid_con
                 if (lane == 0) mbar_arrive(smem_u32(&acce_b[b]));
             }
             const int row = tl.m0 + 32 * wq + lane;
-            if (row < M) {
-                const int2* pp = pairs + tl.p0 + half * BN;
+            const int2* pp = pairs + tl.p0 + half * BN;
+            const int npl = tl.np - half * BN;           // this warp's columns
 #pragma unroll
-                for (int j = 0; j < BN; ++j)
-                    if (half * BN + j < tl.np) atomicAdd(Y + (int64_t)__ldg(&pp[j].x) * ldy + row, (double)acc[j]);
+            for (int c0 = 0; c0 < BN; c0 += 32) {
+                if (c0 >= npl) break;
+                int trow;
+                float sc;
+                epi_cols_load<F16>(pp, c0, npl, lane, bscale, ascale_inv, trow, sc);
+#pragma unroll
+                for (int j = 0; j < 32; ++j)
+                    if (c0 + j < npl) epi_col_add<F16>(Y, ldy, row, row < M, trow, sc, j, acc[c0 + j]);
             }
         }
     } else if (warp == 1) {
@@ -744,8 +811,7 @@ tc_pairs_wide_kernel(const __grid_constant__ CUtensorMap mapAb, const __grid_con
         for (int ti = blockIdx.x; ti < ntiles; ti += gridDim.x, ++it) {
             const int ab = it & 1;
             const uint32_t nmma = (uint32_t)((tiles[ti].np + 15) & ~15);
-            const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((nmma >> 3) << 17) |
-                                   ((uint32_t)(BM >> 4) << 24);
+            const uint32_t idesc = make_idesc<F16>(nmma, BM);
             mbar_wait(smem_u32(&acce_b[ab]), ((it >> 1) & 1) ^ 1);
             asm volatile("tcgen05.fence::after_thread_sync;");
             const int kc0 = tiles[ti].kc0, kc1 = tiles[ti].kc1;
@@ -759,12 +825,12 @@ tc_pairs_wide_kernel(const __grid_constant__ CUtensorMap mapAb, const __grid_con
                     const uint64_t a_b = smem_desc(st), a_s = smem_desc(st + A_BYTES);
                     const uint64_t bb = smem_desc(st + 2 * A_BYTES), bs = smem_desc(st + 2 * A_BYTES + B_BYTES);
                     const uint32_t d = tmem + (uint32_t)(ab * BNW);
-                    const int ksteps = min(BK, K - kc * BK + 7) / 8;
+                    const int ksteps = min(BKE, K - kc * BKE + KS - 1) / KS;
                     for (int k = 0; k < ksteps; ++k) {
                         const uint64_t off = (uint64_t)(2 * k);
-                        mma_tf32(d, a_b + off, bb + off, idesc, kc != kc0 || k != 0);
-                        mma_tf32(d, a_b + off, bs + off, idesc, 1);
-                        mma_tf32(d, a_s + off, bb + off, idesc, 1);
+                        mma_op<F16>(d, a_b + off, bb + off, idesc, kc != kc0 || k != 0);
+                        mma_op<F16>(d, a_b + off, bs + off, idesc, 1);
+                        mma_op<F16>(d, a_s + off, bb + off, idesc, 1);
                     }
                     mma_commit(smem_u32(&empty_b[s]));
                     if (kc == kc1 - 1) mma_commit(smem_u32(&accf_b[ab]));
@@ -785,15 +851,15 @@ tc_pairs_wide_kernel(const __grid_constant__ CUtensorMap mapAb, const __grid_con
             const int row = tl.m0 + 32 * wq + lane;
 #pragma unroll 1
             for (int c0 = 0; c0 < tl.np; c0 += 32) {
+                int trow;
+                float sc;
+                epi_cols_load<F16>(pp, c0, tl.np, lane, bscale, ascale_inv, trow, sc);
                 uint32_t v[32];
                 tmem_ld32(tmem + ((uint32_t)(32 * wq) << 16) + (uint32_t)(ab * BNW + c0), v);
                 asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-                if (row < M) {
 #pragma unroll
-                    for (int j = 0; j < 32; ++j)
-                        if (c0 + j < tl.np)
-                            atomicAdd(Y + (int64_t)__ldg(&pp[c0 + j].x) * ldy + row, (double)__uint_as_float(v[j]));
-                }
+                for (int j = 0; j < 32; ++j)
+                    if (c0 + j < tl.np) epi_col_add<F16>(Y, ldy, row, row < M, trow, sc, j, __uint_as_float(v[j]));
             }
             asm volatile("tcgen05.fence::before_thread_sync;");
             __syncwarp();
@@ -828,6 +894,87 @@ __global__ void split_rows_kernel(const XT* __restrict__ X, int ld, int64_t row0
     const float b = to_tf32(x);
     Xb[r * ld + c] = b;
     Xs[r * ld + c] = to_tf32(x - (XT)b);
+}
+
+// ---- FP16 head / remainder split (3xFP16 translations) ----
+// An fp16 value carries the same 11 significand bits as a TF32 one, and the tensor core
+// multiplies fp16 operands at twice the TF32 rate (kind::f16, K = 16 per MMA).  The 5-bit
+// exponent is handled by scaling with powers of two (exact): each row is scaled so that its
+// largest magnitude lies in [2^12, 2^13); head = rn_fp16(s x), remainder = rn_fp16(s x - head).
+// Entries more than 2^-15 below the row maximum have a subnormal remainder (absolute spacing
+// 2^-24, i.e. 2^-37 of the row maximum): the split keeps min(22 bits relative, 2^-37 of the
+// largest entry) -- for a dot product the same error level as the TF32 split.
+__device__ __forceinline__ float pow2_scale(float amax) {
+    // 2^(12 - floor(log2 amax)); 1 for an all-zero (or non-finite) row
+    if (!(amax > 0.f) || !isfinite(amax)) return 1.f;
+    const int e = ilogbf(amax);
+    return scalbnf(1.f, 12 - e);
+}
+
+// rows [row0, row0 + nrows) of the fp64 state X (row stride ldx) -> Xh / Xr (row stride ldh
+// halves) and the factor that undoes the row's scaling; a warp per row
+__global__ void split_rows_h_kernel(const double* __restrict__ X, int ldx, int64_t row0, int64_t nrows, int K,
+                                    __half* __restrict__ Xh, __half* __restrict__ Xr, int ldh,
+                                    float* __restrict__ inv_scale) {
+    const int lane = threadIdx.x & 31;
+    const int64_t r = row0 + ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
+    if (r >= row0 + nrows) return;
+    const double2* src = reinterpret_cast<const double2*>(X + r * ldx);
+    const int K2 = K >> 1;                       // K even (3 n_e, n_e even)
+    constexpr int NV = 16;                       // up to 1024 columns per row held in registers
+    double2 v[NV];
+    float amax = 0.f;
+#pragma unroll
+    for (int q = 0; q < NV; ++q) {
+        const int j = q * 32 + lane;
+        v[q] = j < K2 ? src[j] : make_double2(0.0, 0.0);
+        amax = fmaxf(amax, fmaxf(fabsf((float)v[q].x), fabsf((float)v[q].y)));
+    }
+    for (int j = NV * 32 + lane; j < K2; j += 32) {   // longer rows: second pass re-reads them
+        const double2 w = src[j];
+        amax = fmaxf(amax, fmaxf(fabsf((float)w.x), fabsf((float)w.y)));
+    }
+#pragma unroll
+    for (int off = 16; off; off >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, off));
+    const float sc = pow2_scale(amax);
+    if (lane == 0) inv_scale[r] = 1.f / sc;
+    __half2* dh = reinterpret_cast<__half2*>(Xh + r * ldh);
+    __half2* dr = reinterpret_cast<__half2*>(Xr + r * ldh);
+    auto put = [&](int j, double2 w) {
+        const float a = (float)(w.x * (double)sc), b = (float)(w.y * (double)sc);   // exact scaling, one rounding
+        const __half ha = __float2half_rn(a), hb = __float2half_rn(b);
+        dh[j] = __halves2half2(ha, hb);
+        dr[j] = __halves2half2(__float2half_rn(a - __half2float(ha)), __float2half_rn(b - __half2float(hb)));
+    };
+#pragma unroll
+    for (int q = 0; q < NV; ++q) {
+        const int j = q * 32 + lane;
+        if (j < K2) put(j, v[q]);
+    }
+    for (int j = NV * 32 + lane; j < K2; j += 32) put(j, src[j]);
+}
+
+// largest magnitude of a float array (bit pattern of |x| is monotone as an unsigned integer)
+__global__ void absmax_kernel(const float* __restrict__ X, int64_t n, unsigned* __restrict__ out) {
+    unsigned m = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        m = max(m, __float_as_uint(fabsf(X[i])));
+#pragma unroll
+    for (int off = 16; off; off >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, off));
+    if ((threadIdx.x & 31) == 0) atomicMax(out, m);
+}
+
+// operator rows [nrows][ld] fp32 -> scaled fp16 head / remainder [nrows][ldh] (one scale for the set)
+__global__ void split_ops_h_kernel(const float* __restrict__ X, int ld, int64_t nrows, int K, float sc,
+                                   __half* __restrict__ Xh, __half* __restrict__ Xr, int ldh) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= nrows * K) return;
+    const int64_t r = i / K;
+    const int c = (int)(i % K);
+    const float a = X[r * ld + c] * sc;
+    const __half h = __float2half_rn(a);
+    Xh[r * ldh + c] = h;
+    Xr[r * ldh + c] = __float2half_rn(a - __half2float(h));
 }
 
 // ------------------------------------------------------------------ level chain (M2M, L2L)
@@ -1118,6 +1265,43 @@ void tc_make_map_b(CUtensorMap* m, const float* base, int64_t rows, int K, int l
     EB_REQUIRE(r == CUDA_SUCCESS, "cuTensorMapEncodeTiled (B) failed: " + std::to_string((int)r));
 }
 
+// A maps of the FP16 operator copies: [nops][M][ldh] halves, box {64, 128, 1} (128-B rows)
+void tc_make_map_a_h(CUtensorMap* m, const __half* base, int nops, int M, int K, int ldh) {
+    cuuint64_t dims[3] = {(cuuint64_t)K, (cuuint64_t)M, (cuuint64_t)nops};
+    cuuint64_t strides[2] = {(cuuint64_t)ldh * 2, (cuuint64_t)M * ldh * 2};
+    cuuint32_t box[3] = {64, tc::BM, 1};
+    cuuint32_t es[3] = {1, 1, 1};
+    CUresult r = tc::encoder()(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, (void*)base, dims, strides, box, es,
+                               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    EB_REQUIRE(r == CUDA_SUCCESS, "cuTensorMapEncodeTiled (A, fp16) failed: " + std::to_string((int)r));
+}
+
+// scaled FP16 head / remainder copies of an operator set; returns the factor undoing the scale
+float tc_split_ops_h(const float* X, int ld, int64_t nrows, int K, __half* Xh, __half* Xr, int ldh, cudaStream_t s) {
+    DBuf<unsigned> m;
+    m.alloc(1);
+    m.zero(s);
+    tc::absmax_kernel<<<1024, 256, 0, s>>>(X, nrows * ld, m.p);
+    EB_CHECK_LAUNCH();
+    unsigned bits = 0;
+    EB_CUDA(cudaMemcpyAsync(&bits, m.p, sizeof(unsigned), cudaMemcpyDeviceToHost, s));
+    EB_CUDA(cudaStreamSynchronize(s));
+    float amax;
+    std::memcpy(&amax, &bits, sizeof(float));
+    const float sc = (amax > 0.f && std::isfinite(amax)) ? std::scalbn(1.f, 12 - std::ilogb(amax)) : 1.f;
+    tc::split_ops_h_kernel<<<ceil_div(nrows * K, 256), 256, 0, s>>>(X, ld, nrows, K, sc, Xh, Xr, ldh);
+    EB_CHECK_LAUNCH();
+    return 1.f / sc;
+}
+
+void tc_split_rows_h(const double* X, int ldx, int64_t row0, int64_t nrows, int K, __half* Xh, __half* Xr, int ldh,
+                     float* inv_scale, cudaStream_t s) {
+    if (nrows <= 0) return;
+    tc::split_rows_h_kernel<<<ceil_div(nrows * 32, 256), 256, 0, s>>>(X, ldx, row0, nrows, K, Xh, Xr, ldh, inv_scale);
+    EB_CHECK_LAUNCH();
+}
+
 template <class XT>
 void tc_split_rows(const XT* X, int ld, int64_t row0, int64_t nrows, int K, float* Xb, float* Xs, cudaStream_t s) {
     if (nrows <= 0) return;
@@ -1143,12 +1327,13 @@ int tc_fast_tile_mode(int M) {
     return two > wide ? 2 : 1;
 }
 
-void tc_build_tiles(OpPairs& P, int M, int K, int mode) {
+void tc_build_tiles(OpPairs& P, int M, int K, int mode, int bke) {
     std::vector<tc::Tile> t;
     const int mstep = mode == 1 ? tc::fast::MT * tc::BM : tc::BM;
     const int bn = mode == 2 ? tc::wide::BNW : tc::BN;
-    const int nk = (K + tc::BK - 1) / tc::BK;
+    const int nk = (K + bke - 1) / bke;          // K chunks of 128 B: 32 TF32 or 64 FP16 elements
     P.tile_mode = mode;
+    P.tile_bke = bke;
     // op-major; the row blocks of one pair group are consecutive (run side by side on
     // neighbouring CTAs, so the second load of the same gathered B rows hits L2)
     for (int o = 0; o < P.nops; ++o)
@@ -1174,33 +1359,43 @@ void tc_build_tiles(OpPairs& P, int M, int K, int mode) {
 
 int tc_fast_smem_bytes() { return tc::fast::SMEM_BYTES; }
 
-void tc_pairs_gemm_fast(const OpPairs& P, const CUtensorMap& Ab, const CUtensorMap& As, const float* Bb,
-                        const float* Bs, int ldb, int M, int K, double* Y, int ldy, bool drain, cudaStream_t s) {
-    if (P.ntiles == 0) return;
-    if (P.tile_mode == 2) {
-        static bool wattr[2] = {false, false};
-        auto wfn = drain ? tc::tc_pairs_wide_kernel<true> : tc::tc_pairs_wide_kernel<false>;
-        if (!wattr[drain]) {
-            EB_CUDA(cudaFuncSetAttribute(wfn, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::wide::SMEM_BYTES));
-            wattr[drain] = true;
-        }
-        const int grid = std::min(P.ntiles, num_sms());
-        wfn<<<grid, drain ? 384 : tc::wide::THREADS, tc::wide::SMEM_BYTES, s>>>(
-            Ab, As, Bb, Bs, ldb, reinterpret_cast<const tc::Tile*>(P.tiles.p), P.ntiles, P.pairs.p, M, K, Y, ldy);
-        EB_CHECK_LAUNCH();
-        return;
-    }
-    EB_REQUIRE(P.tile_mode == 1, "internal: fast kernel needs two-slice tiles");
-    static bool attr[2] = {false, false};
-    auto fn = drain ? tc::tc_pairs_fast_kernel<true> : tc::tc_pairs_fast_kernel<false>;
-    if (!attr[drain]) {
-        EB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::fast::SMEM_BYTES));
-        attr[drain] = true;
+template <class KernelT>
+static void launch_fast(KernelT fn, bool& attr, int smem, int threads, const OpPairs& P, const CUtensorMap& Ab,
+                        const CUtensorMap& As, const void* Bb, const void* Bs, int ldb, int M, int K, double* Y,
+                        int ldy, const float* bscale, float ascale_inv, cudaStream_t s) {
+    if (!attr) {
+        EB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        attr = true;
     }
     const int grid = std::min(P.ntiles, num_sms());
-    fn<<<grid, drain ? 384 : tc::fast::THREADS, tc::fast::SMEM_BYTES, s>>>(
-        Ab, As, Bb, Bs, ldb, reinterpret_cast<const tc::Tile*>(P.tiles.p), P.ntiles, P.pairs.p, M, K, Y, ldy);
+    fn<<<grid, threads, smem, s>>>(Ab, As, Bb, Bs, ldb, reinterpret_cast<const tc::Tile*>(P.tiles.p), P.ntiles,
+                                   P.pairs.p, M, K, Y, ldy, bscale, ascale_inv);
     EB_CHECK_LAUNCH();
+}
+
+// f16: Ab / As are FP16 operator maps (tc_make_map_a_h), Bb / Bs fp16 rows of ldb halves with
+// the per-row factors bscale (tc_split_rows_h) and the operator set's factor ascale_inv; the
+// tiles must have been built with 64-element chunks.  Otherwise TF32 operands in fp32 words.
+void tc_pairs_gemm_fast(const OpPairs& P, const CUtensorMap& Ab, const CUtensorMap& As, const void* Bb,
+                        const void* Bs, int ldb, int M, int K, double* Y, int ldy, bool drain, cudaStream_t s,
+                        bool f16, const float* bscale, float ascale_inv) {
+    if (P.ntiles == 0) return;
+    EB_REQUIRE(P.tile_bke == (f16 ? 64 : 32), "internal: translation tiles built for the other operand type");
+    EB_REQUIRE(P.tile_mode == 1 || P.tile_mode == 2, "internal: fast kernel needs two-slice or wide tiles");
+    static bool attr[2][2][2] = {};
+    const bool w = P.tile_mode == 2;
+    const int smem = w ? tc::wide::SMEM_BYTES : tc::fast::SMEM_BYTES;
+    const int threads = drain ? 384 : (w ? tc::wide::THREADS : tc::fast::THREADS);
+#define EB_TC_LAUNCH(KERNEL) \
+    launch_fast(KERNEL, attr[w][drain][f16], smem, threads, P, Ab, As, Bb, Bs, ldb, M, K, Y, ldy, bscale, ascale_inv, s)
+    if (w) {
+        if (drain) { if (f16) EB_TC_LAUNCH((tc::tc_pairs_wide_kernel<true, true>)); else EB_TC_LAUNCH((tc::tc_pairs_wide_kernel<true, false>)); }
+        else { if (f16) EB_TC_LAUNCH((tc::tc_pairs_wide_kernel<false, true>)); else EB_TC_LAUNCH((tc::tc_pairs_wide_kernel<false, false>)); }
+    } else {
+        if (drain) { if (f16) EB_TC_LAUNCH((tc::tc_pairs_fast_kernel<true, true>)); else EB_TC_LAUNCH((tc::tc_pairs_fast_kernel<true, false>)); }
+        else { if (f16) EB_TC_LAUNCH((tc::tc_pairs_fast_kernel<false, true>)); else EB_TC_LAUNCH((tc::tc_pairs_fast_kernel<false, false>)); }
+    }
+#undef EB_TC_LAUNCH
 }
 
 void tc_pairs_gemm(const OpPairs& P, const CUtensorMap& Ab, const CUtensorMap& As, const CUtensorMap& Bb,
