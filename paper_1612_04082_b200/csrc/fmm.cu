@@ -699,6 +699,10 @@ static int m2l_f16_level() {
     static const int lv = std::getenv("EBEM_M2L_F16") ? std::atoi(std::getenv("EBEM_M2L_F16")) : 2;
     return lv;
 }
+static bool ml_f16_on() {      // EBEM_ML_F16=0: M2M / L2L stay in TF32
+    static const bool on = !(std::getenv("EBEM_ML_F16") && std::atoi(std::getenv("EBEM_ML_F16")) == 0);
+    return on;
+}
 static bool m2l_use_f16(const Tree& t) { return t.m2l_f16 && (t.tc_fast || m2l_f16_level() >= 2); }
 static bool m2l_drain_fast() {
     static const bool on = !(std::getenv("EBEM_M2L_DRAIN") && std::atoi(std::getenv("EBEM_M2L_DRAIN")) == 0);
@@ -1202,8 +1206,24 @@ void schedule_tree(Tree& t, cudaStream_t s) {
         }
         tc_build_tiles(t.m2l, me, me, t.tc_fast || m2l_drain_fast() ? fm : 0,
                        (t.tc_fast || m2l_drain_fast()) && m2l_use_f16(t) ? 64 : 32);
-        for (auto& x : t.m2m) tc_build_tiles(x, me, me, t.ml_fast ? fm : 0);
-        for (auto& x : t.l2l) tc_build_tiles(x, me, me, t.ml_fast ? fm : 0);
+        // M2M / L2L on the fast kernel in FP16 as well: each level's rows are split (row-scaled
+        // fp16 head / remainder) as they become final, which also serves the M2L.  Not in trees
+        // deeper than 16 levels: a rounding error made at the leaves is amplified by 2 per M2M
+        // level relative to a double layer's decaying field (limitation L1), and the
+        // fp16 split (absolute precision relative to the row's largest entry) then shows where
+        // the TF32 split (relative per element) does not -- level-20 coincident cluster, GPU vs
+        // oracle KIFMM: 1.71e-3 with TF32 chains, 2.11e-3 with FP16 chains, M2L in FP16 either way.
+        static const bool chain_env = std::getenv("EBEM_ML_CHAIN") && std::atoi(std::getenv("EBEM_ML_CHAIN")) == 1;
+        t.ml_f16 = t.ml_fast && t.m2l_f16 && !chain_env && ml_f16_on() && t.nlevels <= 16;
+        if (t.ml_f16) {
+            t.Whb.alloc((size_t)std::max(1, t.n_dn) * P.ldh);
+            t.Whs.alloc((size_t)std::max(1, t.n_dn) * P.ldh);
+            t.Whinv.alloc(std::max(1, t.n_dn));
+            t.Whb.zero(s);
+            t.Whs.zero(s);
+        }
+        for (auto& x : t.m2m) tc_build_tiles(x, me, me, t.ml_fast ? fm : 0, t.ml_f16 ? 64 : 32);
+        for (auto& x : t.l2l) tc_build_tiles(x, me, me, t.ml_fast ? fm : 0, t.ml_f16 ? 64 : 32);
         // EBEM_ML_CHAIN=1: M2M and L2L chains as one persistent launch each (tc_chain_kernel).
         // Measured on the 1M beam: M2M 0.341 -> 0.317 ms, L2L 0.321 -> 0.306 ms alone, but the
         // overlapped matvec unchanged (4.41-4.44 ms either way) and the host-buffer (e2e) matvec
@@ -1665,7 +1685,11 @@ void fmm_evaluate(Tree& t, int kernel, const float* f, const float* g, float* ou
                          t.up_lstart[2], zrows(2), sa);
     } else {
     for (int l = t.nlevels - 2; l >= 2; --l) {
-        if (t.use_tc) {
+        if (t.use_tc && t.ml_f16) {
+            tc_split_rows_h(t.Z.p, lde, t.up_lstart[l + 1], zrows(l + 1), me, t.Zhb.p, t.Zhs.p, P.ldh, t.Zhinv.p, sa);
+            tc_pairs_gemm_fast(t.m2m[l], P.mM2M_hb, P.mM2M_hs, t.Zhb.p, t.Zhs.p, P.ldh, me, me, t.Z.p, lde, false, sa,
+                               true, t.Zhinv.p, P.m2m_hinv);
+        } else if (t.use_tc) {
             tc_split_rows(t.Z.p, lde, t.up_lstart[l + 1], zrows(l + 1), me, t.Zb.p, t.Zs.p, sa);
             if (t.ml_fast) tc_pairs_gemm_fast(t.m2m[l], P.mM2M_b, P.mM2M_s, t.Zb.p, t.Zs.p, lde, me, me, t.Z.p, lde, false, sa);
             else tc_pairs_gemm(t.m2m[l], P.mM2M_b, P.mM2M_s, t.mZb, t.mZs, me, me, t.Z.p, lde, sa);
@@ -1673,7 +1697,9 @@ void fmm_evaluate(Tree& t, int kernel, const float* f, const float* g, float* ou
             gemm_pairs_f32(t.m2m[l], P.M2M.p, me, me, lde, t.Z.p, lde, t.Z.p, lde, sa);
         }
     }
-    if (t.use_tc && t.nlevels > 2) tc_split_rows(t.Z.p, lde, t.up_lstart[2], zrows(2), me, t.Zb.p, t.Zs.p, sa);
+    if (t.use_tc && t.ml_f16) {       // the coarsest rows the M2L reads (or all of them in a two-level tree)
+        if (t.nlevels > 2) tc_split_rows_h(t.Z.p, lde, t.up_lstart[2], zrows(2), me, t.Zhb.p, t.Zhs.p, P.ldh, t.Zhinv.p, sa);
+    } else if (t.use_tc && t.nlevels > 2) tc_split_rows(t.Z.p, lde, t.up_lstart[2], zrows(2), me, t.Zb.p, t.Zs.p, sa);
     }
     pe(PH_M2M, sa);
 
@@ -1716,7 +1742,7 @@ void fmm_evaluate(Tree& t, int kernel, const float* f, const float* g, float* ou
     pb(PH_M2L, sa);
     if (t.use_tc && m2l_use_f16(t) && (t.tc_fast || m2l_drain_fast())) {
         // 3xFP16: row-scaled fp16 split of every Z row, then the same kernels on fp16 operands
-        tc_split_rows_h(t.Z.p, lde, 0, t.n_up, me, t.Zhb.p, t.Zhs.p, P.ldh, t.Zhinv.p, sa);
+        if (!t.ml_f16) tc_split_rows_h(t.Z.p, lde, 0, t.n_up, me, t.Zhb.p, t.Zhs.p, P.ldh, t.Zhinv.p, sa);
         tc_pairs_gemm_fast(t.m2l, P.mM2L_hb, P.mM2L_hs, t.Zhb.p, t.Zhs.p, P.ldh, me, me, t.W.p, lde, !t.tc_fast, sa,
                            true, t.Zhinv.p, P.m2l_hinv);
     } else if (t.use_tc && t.tc_fast) tc_pairs_gemm_fast(t.m2l, P.mM2L_b, P.mM2L_s, t.Zb.p, t.Zs.p, lde, me, me, t.W.p, lde, false, sa);
@@ -1741,7 +1767,11 @@ void fmm_evaluate(Tree& t, int kernel, const float* f, const float* g, float* ou
         tc_chain_run(t.l2l_chain, P.mL2L_b, P.mL2L_s, t.W.p, lde, t.Wb.p, t.Ws.p, me, me, t.W.p, lde, 0, 0, sa);
     } else {
     for (int l = 3; l < t.nlevels; ++l) {
-        if (t.use_tc) {
+        if (t.use_tc && t.ml_f16) {
+            tc_split_rows_h(t.W.p, lde, t.dn_lstart[l - 1], wrows(l - 1), me, t.Whb.p, t.Whs.p, P.ldh, t.Whinv.p, sa);
+            tc_pairs_gemm_fast(t.l2l[l], P.mL2L_hb, P.mL2L_hs, t.Whb.p, t.Whs.p, P.ldh, me, me, t.W.p, lde, false, sa,
+                               true, t.Whinv.p, P.l2l_hinv);
+        } else if (t.use_tc) {
             tc_split_rows(t.W.p, lde, t.dn_lstart[l - 1], wrows(l - 1), me, t.Wb.p, t.Ws.p, sa);
             if (t.ml_fast) tc_pairs_gemm_fast(t.l2l[l], P.mL2L_b, P.mL2L_s, t.Wb.p, t.Ws.p, lde, me, me, t.W.p, lde, false, sa);
             else tc_pairs_gemm(t.l2l[l], P.mL2L_b, P.mL2L_s, t.mWb, t.mWs, me, me, t.W.p, lde, sa);

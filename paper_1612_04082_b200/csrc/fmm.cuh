@@ -52,10 +52,10 @@ struct Plan {
     // scaled FP16 head / remainder copies of the M2L operators (3xFP16 path, tc_gemm.cu): row
     // stride ldh halves (me rounded up to 8: 16-B rows), one power-of-two scale for the set
     // (m2l_hinv undoes it)
-    DBuf<__half> M2L_hb, M2L_hs;
-    CUtensorMap mM2L_hb, mM2L_hs;
+    DBuf<__half> M2L_hb, M2L_hs, M2M_hb, M2M_hs, L2L_hb, L2L_hs;
+    CUtensorMap mM2L_hb, mM2L_hs, mM2M_hb, mM2M_hs, mL2L_hb, mL2L_hs;
     int ldh = 0;
-    float m2l_hinv = 1.f;
+    float m2l_hinv = 1.f, m2m_hinv = 1.f, l2l_hinv = 1.f;
     int off_index[343];         // (ox+3)*49+(oy+3)*7+(oz+3) -> 0..315 or -1
 };
 
@@ -194,9 +194,10 @@ struct Tree {
     CUtensorMap mQb, mQs, mQdb, mQds, mZb, mZs, mWb, mWs;
     // 3xFP16 M2L: row-scaled fp16 head / remainder copies of the Z rows and the factors undoing
     // each row's scale (split once per evaluation, after the upward pass)
-    DBuf<__half> Zhb, Zhs;
-    DBuf<float> Zhinv;
+    DBuf<__half> Zhb, Zhs, Whb, Whs;
+    DBuf<float> Zhinv, Whinv;
     bool m2l_f16 = false;                // M2L operands in FP16 (EBEM_M2L_F16, default on)
+    bool ml_f16 = false;                 // M2M / L2L on the fast kernel in FP16 too (split level by level)
     DBuf<double> PHID, PHIU;             // [n_phid x me], [n_phiu x me] (fp64 far field)
     DBuf<float4> PHIDF, PHIUF;           // [n_phid x ne], [n_phiu x ne] (fp32 far field, scaled)
     DBuf<float> near_sorted;             // [ntrg x 6] near field, sorted target order

@@ -135,13 +135,21 @@ __device__ __forceinline__ void pair_loop_packed(const float4* __restrict__ srec
     }
 }
 
+#ifndef NEAR_UNROLL1
+#define NEAR_UNROLL1 2
+#endif
+#ifndef NEAR_UNROLL2
+#define NEAR_UNROLL2 2
+#endif
 // the same for a lane group: records j = g, g + G, ... of the staged tile (stride RS float4),
 // TPT targets per thread
 template <bool SL, bool DL, bool STRESS, int TPT, int RS, bool SAFE = true>
 __device__ __forceinline__ void pair_loop_strided(const float4* __restrict__ srec, int cnt, int g, int G,
                                                   const float* x, const float* y, const float* z, const KConst& kc,
                                                   float (*acc)[STRESS ? 6 : 3]) {
-#pragma unroll 2
+    // independent pair evaluations in flight per lane = TPT x unroll
+    constexpr int UN = TPT == 1 ? NEAR_UNROLL1 : (TPT == 2 ? NEAR_UNROLL2 : 2);
+#pragma unroll UN
     for (int j = g; j < cnt; j += G) {
         const float4 p = srec[j * RS + 0];
         const float4 f = SL ? srec[j * RS + 1] : make_float4(0, 0, 0, 0);

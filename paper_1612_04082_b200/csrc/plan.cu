@@ -378,16 +378,22 @@ static std::shared_ptr<Plan> make_plan(int p, const Material& m, cudaStream_t s)
     split(P->M2M, 8, P->me, P->lde, P->M2M_b, P->M2M_s, &P->mM2M_b, &P->mM2M_s);
     split(P->L2L, 8, P->me, P->lde, P->L2L_b, P->L2L_s, &P->mL2L_b, &P->mL2L_s);
     split(P->M2L, NV_OFFSETS, P->me, P->lde, P->M2L_b, P->M2L_s, &P->mM2L_b, &P->mM2L_s);
-    // scaled FP16 copies of the M2L operators (3xFP16 translations, tc_gemm.cu)
+    // scaled FP16 copies of the M2L / M2M / L2L operators (3xFP16 translations, tc_gemm.cu)
     P->ldh = (P->me + 7) & ~7;
-    P->M2L_hb.alloc((size_t)NV_OFFSETS * P->me * P->ldh);
-    P->M2L_hs.alloc((size_t)NV_OFFSETS * P->me * P->ldh);
-    P->M2L_hb.zero(s);
-    P->M2L_hs.zero(s);
-    P->m2l_hinv = tc_split_ops_h(P->M2L.p, P->lde, (int64_t)NV_OFFSETS * P->me, P->me, P->M2L_hb.p, P->M2L_hs.p,
-                                 P->ldh, s);
-    tc_make_map_a_h(&P->mM2L_hb, P->M2L_hb.p, NV_OFFSETS, P->me, P->me, P->ldh);
-    tc_make_map_a_h(&P->mM2L_hs, P->M2L_hs.p, NV_OFFSETS, P->me, P->me, P->ldh);
+    auto split_h = [&](const DBuf<float>& X, int nops, DBuf<__half>& Xh, DBuf<__half>& Xr, CUtensorMap* mh,
+                       CUtensorMap* mr) {
+        Xh.alloc((size_t)nops * P->me * P->ldh);
+        Xr.alloc((size_t)nops * P->me * P->ldh);
+        Xh.zero(s);
+        Xr.zero(s);
+        const float inv = tc_split_ops_h(X.p, P->lde, (int64_t)nops * P->me, P->me, Xh.p, Xr.p, P->ldh, s);
+        tc_make_map_a_h(mh, Xh.p, nops, P->me, P->me, P->ldh);
+        tc_make_map_a_h(mr, Xr.p, nops, P->me, P->me, P->ldh);
+        return inv;
+    };
+    P->m2l_hinv = split_h(P->M2L, NV_OFFSETS, P->M2L_hb, P->M2L_hs, &P->mM2L_hb, &P->mM2L_hs);
+    P->m2m_hinv = split_h(P->M2M, 8, P->M2M_hb, P->M2M_hs, &P->mM2M_hb, &P->mM2M_hs);
+    P->l2l_hinv = split_h(P->L2L, 8, P->L2L_hb, P->L2L_hs, &P->mL2L_hb, &P->mL2L_hs);
     EB_CUDA(cudaStreamSynchronize(s));
     return P;
 }
