@@ -1415,11 +1415,14 @@ void tree_m2l_fast(Tree& t, bool fast, cudaStream_t s) {
 }
 
 // near field (U-list P2P) into the sorted near buffer
-// Dynamic shared memory a stream-B kernel requests so that at most two of its CTAs fit beside
-// one persistent translation CTA (tc_pairs_fast_kernel) and they fill its leftover shared
-// memory.  Measured on the 1M-point matvec (with the M2L timestamp below): 4.64 ms with three
-// near-field CTAs beside each M2L CTA (no padding), 4.45-4.48 with two, 4.60 with one — the
-// third takes issue slots the M2L producer warps need.  EBEM_NEAR_PAD=bytes overrides.
+// Dynamic shared memory a stream-B kernel requests so that a fixed number of its CTAs fit
+// beside one persistent translation CTA (tc_pairs_fast_kernel) and fill its leftover shared
+// memory.  Measured on the 1M-point matvec (with the M2L timestamp below).  With the TF32 M2L
+// (1.64 ms alone): 4.64 ms with three near-field CTAs beside each M2L CTA (no padding),
+// 4.45-4.48 with two, 4.60 with one -- the third took issue slots the M2L producer warps
+// needed.  With the FP16 M2L (1.37 ms alone) the near field is the longer of the two and three
+// CTAs are the better split: 4.04 vs 4.07 ms with two (configs[3] unchanged, 7.59 ms).
+// EBEM_NEAR_PAD=bytes overrides.
 int beside_translation_pad(const void* kernel) {
     if (const char* e = std::getenv("EBEM_NEAR_PAD")) return std::atoi(e);
     cudaFuncAttributes fa;
@@ -1429,7 +1432,8 @@ int beside_translation_pad(const void* kernel) {
     EB_CUDA(cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev));
     EB_CUDA(cudaDeviceGetAttribute(&resv, cudaDevAttrReservedSharedMemoryPerBlock, dev));
     const int free_sm = smem_sm - (tc_fast_smem_bytes() + resv);
-    const int pad = (free_sm / 2 - resv - (int)fa.sharedSizeBytes - 128) & ~127;
+    const int per_sm = 3;
+    const int pad = (free_sm / per_sm - resv - (int)fa.sharedSizeBytes - 128) & ~127;
     return pad > 0 ? pad : 0;
 }
 
