@@ -1125,13 +1125,21 @@ void schedule_tree(Tree& t, cudaStream_t s) {
             wn[i] = (double)tsub[b] * near_ns[b];
             wf[i] = (double)tsub[b] * P.ne * nfar;
         }
+        // decreasing work, ties in Morton order: one sort of packed keys (float bits of the
+        // non-negative work, complemented, then the index)
         auto order = [&](const std::vector<double>& w, std::vector<int>& e_out, std::vector<int>& l_out) {
-            std::vector<int> ord(ev.size());
-            for (size_t i = 0; i < ord.size(); ++i) ord[i] = (int)i;
-            std::stable_sort(ord.begin(), ord.end(), [&](int x, int y) { return w[x] > w[y]; });
-            for (size_t i = 0; i < ord.size(); ++i) {
-                e_out[i] = ev[ord[i]];
-                l_out[i] = l2t[ord[i]];
+            std::vector<uint64_t> key(ev.size());
+            for (size_t i = 0; i < key.size(); ++i) {
+                const float wf32 = (float)w[i];
+                uint32_t bits;
+                std::memcpy(&bits, &wf32, sizeof(bits));
+                key[i] = ((uint64_t)(~bits) << 32) | (uint32_t)i;
+            }
+            std::sort(key.begin(), key.end());
+            for (size_t i = 0; i < key.size(); ++i) {
+                const uint32_t k = (uint32_t)key[i];
+                e_out[i] = ev[k];
+                l_out[i] = l2t[k];
             }
         };
         std::vector<int> nev(ev.size()), nl2t(ev.size());

@@ -14,10 +14,11 @@ name = lambda r: r[ik].split("(")[0].replace("void ", "").replace("ebem::", "")
 starts = [i for i, r in enumerate(rs) if name(r).startswith("prepare_kernel")]
 lens = collections.Counter(b - a for a, b in zip(starts, starts[1:]) if b - a > 10)
 L = lens.most_common(1)[0][0]
-# the bench line's matvec (p = 6: full-chain M2L kernel tc_pairs_fast_kernel<0>), not the p = 10 line
+# the bench line's matvec (p = 6: full-chain M2L kernel tc_pairs_fast_kernel<0, ...>: template
+# arguments DRAIN, F16), not the p = 10 line (drained kernel, <1, ...>)
 cands = [s for s, t in zip(starts, starts[1:]) if t - s == L and
-         any("tc_pairs_fast_kernel<0>" in name(r) and "<0>" in name(r) for r in rs[s:t])]
-cands = [s for s in cands if not any("fast_kernel<1>" in name(r) for r in rs[s:s + L])] or cands
+         any("tc_pairs_fast_kernel<0" in name(r) for r in rs[s:t])]
+cands = [s for s in cands if not any("fast_kernel<1" in name(r) for r in rs[s:s + L])] or cands
 a = (cands or [s for s, t in zip(starts, starts[1:]) if t - s == L])[-1]
 agg, tot = collections.OrderedDict(), 0.0
 for r in rs[a:a + L]:
