@@ -691,8 +691,6 @@ near_eval_p_kernel(int n_eval, const int* __restrict__ eval_box, const int* __re
     }
 }
 
-// precise M2L (p >= 9, GMRES) on the two-slice fast-kernel data flow with drained groups;
-// EBEM_M2L_DRAIN=0 selects the one-slice precise kernel instead
 // EBEM_M2L_F16: 0 = M2L operands in TF32; 1 = FP16 for the full-chain M2L (p <= 8 matvec, GMRES
 // solves with tol >= 1e-6); 2 = FP16 for the drained (precise) M2L too
 static int m2l_f16_level() {
@@ -703,10 +701,26 @@ static bool ml_f16_on() {      // EBEM_ML_F16=0: M2M / L2L stay in TF32
     static const bool on = !(std::getenv("EBEM_ML_F16") && std::atoi(std::getenv("EBEM_ML_F16")) == 0);
     return on;
 }
+// EBEM_M2L_MC=cs: the full-chain two-slice M2L on clusters of cs CTAs sharing the operator tiles
+// by TMA multicast (tc_pairs_mc_kernel); 0 / 1: one CTA per tile
+static int m2l_mc_cs() {
+    static const int cs = std::getenv("EBEM_M2L_MC") ? std::atoi(std::getenv("EBEM_M2L_MC")) : 0;
+    return cs == 2 || cs == 4 ? cs : 1;
+}
 static bool m2l_use_f16(const Tree& t) { return t.m2l_f16 && (t.tc_fast || m2l_f16_level() >= 2); }
+// precise M2L (p >= 9, GMRES) on the two-slice fast-kernel data flow with drained groups;
+// EBEM_M2L_DRAIN=0 selects the one-slice precise kernel instead
 static bool m2l_drain_fast() {
     static const bool on = !(std::getenv("EBEM_M2L_DRAIN") && std::atoi(std::getenv("EBEM_M2L_DRAIN")) == 0);
     return on;
+}
+// the M2L tile table for the tree's current accumulation mode (tc_fast) and operand type
+static void build_m2l_tiles(Tree& t) {
+    const Plan& P = *t.plan;
+    const bool fastflow = t.tc_fast || m2l_drain_fast();
+    const int mode = fastflow ? tc_fast_tile_mode(P.me) : 0;
+    tc_build_tiles(t.m2l, P.me, P.me, mode, fastflow && m2l_use_f16(t) ? 64 : 32,
+                   t.tc_fast && mode == 1 ? m2l_mc_cs() : 1);
 }
 
 // ------------------------------------------------------------------ M2L pair table (device)
@@ -1216,8 +1230,7 @@ void schedule_tree(Tree& t, cudaStream_t s) {
             t.Zhb.zero(s);
             t.Zhs.zero(s);
         }
-        tc_build_tiles(t.m2l, me, me, t.tc_fast || m2l_drain_fast() ? fm : 0,
-                       (t.tc_fast || m2l_drain_fast()) && m2l_use_f16(t) ? 64 : 32);
+        build_m2l_tiles(t);
         // M2M / L2L on the fast kernel in FP16 as well: each level's rows are split (row-scaled
         // fp16 head / remainder) as they become final, which also serves the M2L.  Not in trees
         // deeper than 16 levels: a rounding error made at the leaves is amplified by 2 per M2M
@@ -1421,8 +1434,7 @@ void tree_m2l_fast(Tree& t, bool fast, cudaStream_t s) {
     fast = fast && t.use_tc && P.p < FAR_FP64_MIN_P;
     if (fast == t.tc_fast) return;
     t.tc_fast = fast;
-    tc_build_tiles(t.m2l, P.me, P.me, fast || m2l_drain_fast() ? tc_fast_tile_mode(P.me) : 0,
-                   (fast || m2l_drain_fast()) && m2l_use_f16(t) ? 64 : 32);
+    build_m2l_tiles(t);
     EB_CUDA(cudaStreamSynchronize(s));
 }
 

@@ -72,7 +72,8 @@ struct OpPairs {
     int max_per_op = 0;
     int ntiles = 0;              // tensor-core tiles (op, first pair, #pairs, row block)
     int tile_mode = 0;           // tile shape: 0 128 rows x 128 pairs (precise), 1 256 x 128 (fast /
-                                 // drained two-slice), 2 128 x 256 (wide, full-chain)
+                                 // drained two-slice), 2 128 x 256 (wide, full-chain), 3 two-slice tiles in cluster order
+    int tile_cs = 1;             // CTAs per cluster tile (tile_mode 3: tc_pairs_mc_kernel), else 1
     int tile_bke = 32;           // K elements per 128-B chunk the tiles were cut for: 32 (TF32) or 64 (FP16)
     DBuf<int> tiles;
 };
@@ -262,7 +263,7 @@ void tc_split_rows(const XT* X, int ld, int64_t row0, int64_t nrows, int K, floa
 void tree_precise(Tree& t, cudaStream_t s);
 void tree_partition_sources(Tree& t, const int32_t* bc, int nq, cudaStream_t s);
 void tree_m2l_fast(Tree& t, bool fast, cudaStream_t s);
-void tc_build_tiles(OpPairs& P, int M, int K, int mode, int bke = 32);
+void tc_build_tiles(OpPairs& P, int M, int K, int mode, int bke = 32, int cs = 1);
 void tc_make_map_a_h(CUtensorMap* m, const __half* base, int nops, int M, int K, int ldh);
 float tc_split_ops_h(const float* X, int ld, int64_t nrows, int K, __half* Xh, __half* Xr, int ldh, cudaStream_t s);
 void tc_split_rows_h(const double* X, int ldx, int64_t row0, int64_t nrows, int K, __half* Xh, __half* Xr, int ldh,

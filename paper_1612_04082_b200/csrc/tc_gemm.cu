@@ -45,6 +45,15 @@ __device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
     uint32_t done;
     do {
+#ifdef MBAR_SPIN           // measurement build: non-blocking test_wait polling instead of try_wait
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done)
+            : "r"(bar), "r"(parity)
+            : "memory");
+#else
         asm volatile(
             "{\n\t.reg .pred p;\n\t"
             "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
@@ -52,6 +61,7 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
             : "=r"(done)
             : "r"(bar), "r"(parity)
             : "memory");
+#endif
     } while (!done);
 }
 __device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
@@ -104,6 +114,9 @@ __device__ __forceinline__ void mma_f16(uint32_t tmem_d, uint64_t a, uint64_t b,
 // the K extent for the same tensor-pipe time.
 template <bool F16>
 __device__ __forceinline__ void mma_op(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+#ifdef M2L_NO_MMA          // ablation build (timing only): loads, barriers and epilogue without the MMAs
+    return;
+#endif
     if (F16) mma_f16(tmem_d, a, b, idesc, acc);
     else mma_tf32(tmem_d, a, b, idesc, acc);
 }
@@ -352,26 +365,41 @@ constexpr int NG = (BN / 4 + NPROD - 1) / NPROD;        // 4-row groups per prod
 // Epilogue of a translation tile: Y[target row][row] += v (fp64 atomic: exact, order
 // independent).  Each lane owns one TMEM lane (operator row) and walks the tile's columns
 // (pairs); the column's target row and scale are loaded once per 32 columns, one column per
-// lane (coalesced, independent loads), and broadcast by shuffles -- a uniform load per column
-// in the atomic loop left the epilogue warps on the load latency (two dependent loads per
-// column with FP16 operands).  FP16 operands are scaled by powers of two -- the operator set
-// by 1 / ascale_inv, every source row by 1 / bscale[row] (split_rows_h_kernel) -- which the
-// fp32 product undoes exactly.
+// lane (coalesced, independent loads), and broadcast by shuffles.  FP16 operands are scaled by
+// powers of two -- the operator set by 1 / ascale_inv, every source row by 1 / bscale[row]
+// (split_rows_h_kernel) -- which the fp32 product undoes exactly.
+//
+// The column code is branch-free: every lane issues its RED, lanes and columns outside the
+// tile add 0.0 to an element the tile owns anyway (a row 32 above for lanes past the
+// operator's last row, the tile's last pair for columns past np; scale 0).  With a guarded
+// `if (on) atomicAdd(...)` (also as a predicated inline-PTX RED) ptxas put a branch and a
+// convergence barrier (BSSY / BSYNC) around every column, so each column's shuffle ->
+// multiply -> convert -> RED chain (~90 cycles) ran after the previous one: the epilogue alone
+// took 1.0 ms of the 1.37 ms FP16 M2L, with or without the REDs (ablation builds M2L_NO_*,
+// DESIGN.md Sec. 6).
 template <bool F16>
 __device__ __forceinline__ void epi_cols_load(const int2* __restrict__ pp, int c0, int np, int lane,
                                               const float* __restrict__ bscale, float ascale_inv, int& trow,
                                               float& sc) {
-    const int2 pr = c0 + lane < np ? __ldg(&pp[c0 + lane]) : make_int2(0, 0);
+    const bool in = c0 + lane < np;
+    const int2 pr = __ldg(&pp[in ? c0 + lane : np - 1]);     // np >= 1 here
     trow = pr.x;
-    sc = 1.f;
-    if (F16) sc = ascale_inv * __ldg(&bscale[pr.y]);
+    sc = F16 ? ascale_inv * __ldg(&bscale[pr.y]) : 1.f;
+    if (!in) sc = 0.f;
 }
-template <bool F16>
-__device__ __forceinline__ void epi_col_add(double* __restrict__ Y, int ldy, int row, bool on, int trow, float sc,
+// rowc: the lane's row, or a valid row of the same slice for lanes past the last row (row_ok false)
+__device__ __forceinline__ void epi_col_add(double* __restrict__ Y, int ldy, int rowc, bool row_ok, int trow, float sc,
                                             int j, float v) {
     const int tr = __shfl_sync(0xffffffffu, trow, j);
-    if (F16) v *= __shfl_sync(0xffffffffu, sc, j);
-    if (on) atomicAdd(Y + (int64_t)tr * ldy + row, (double)v);
+    const float scj = __shfl_sync(0xffffffffu, sc, j);
+    v = row_ok ? v * scj : 0.f;
+#ifdef M2L_NO_ATOMICS      // ablation build (timing only): everything but the RED
+    if (v == 123456.789f)
+#endif
+#ifdef EPI_GUARD           // measurement build: the guarded (branchy) column code
+    if (row_ok && scj != 0.f)
+#endif
+    atomicAdd(Y + (int64_t)tr * ldy + rowc, (double)v);
 }
 
 template <bool DRAIN, bool F16>
@@ -440,12 +468,16 @@ tc_pairs_fast_kernel(const __grid_constant__ CUtensorMap mapAb, const __grid_con
                 // multiplied (p = 8: 888 rows = 3.5 tile pairs, 12% of the MMAs saved)
                 const int nmt = tl.m0 + BM < M ? MT : 1;
                 if (pi == 0 && lane == 0) {
+#ifdef M2L_NO_A            // ablation build (timing only): no operator tiles
+                    mbar_arrive(full);
+#else
                     mbar_expect_tx(full, 2 * nmt * OPND_BYTES);
                     for (int mt = 0; mt < nmt; ++mt) {
                         tma_load_3d(smem_u32(st + (2 * mt) * OPND_BYTES), &mapAb, kc * BKE, tl.m0 + mt * BM, tl.op, full);
                         tma_load_3d(smem_u32(st + (2 * mt + 1) * OPND_BYTES), &mapAs, kc * BKE, tl.m0 + mt * BM, tl.op,
                                     full);
                     }
+#endif
                 }
                 const int col = kc * BKE + (16 / ES) * piece;
                 const uint32_t nb = col < ldb ? 16u : 0u;      // zero-fill past the row
@@ -455,7 +487,11 @@ tc_pairs_fast_kernel(const __grid_constant__ CUtensorMap mapAb, const __grid_con
 #pragma unroll
                 for (int g = 0; g < fast::NG; ++g) {
                     const int grp = pi + fast::NPROD * g;
+#ifdef M2L_NO_B            // ablation build (timing only): no gathered rows
+                    if (false) {
+#else
                     if (grp < ngrp) {
+#endif
                         const int r = rsub + 4 * grp;
                         const int64_t off = (srow[g] + col) * ES;
                         const uint32_t so = (uint32_t)(r * 128 + ((piece ^ (r & 7)) * 16));
@@ -573,15 +609,17 @@ tc_pairs_fast_kernel(const __grid_constant__ CUtensorMap mapAb, const __grid_con
             }
             const int row = tl.m0 + mt * BM + 32 * wq + lane;
             const int2* pp = pairs + tl.p0;
+            if (row - lane < M) {                            // (warp-uniform) some of this warp's rows exist
+                const int rowc = row < M ? row : row - 32;
 #pragma unroll
-            for (int c0 = 0; c0 < BN; c0 += 32) {
-                if (c0 >= tl.np) break;
-                int trow;
-                float sc;
-                epi_cols_load<F16>(pp, c0, tl.np, lane, bscale, ascale_inv, trow, sc);
+                for (int c0 = 0; c0 < BN; c0 += 32) {
+                    if (c0 >= tl.np) break;
+                    int trow;
+                    float sc;
+                    epi_cols_load<F16>(pp, c0, tl.np, lane, bscale, ascale_inv, trow, sc);
 #pragma unroll
-                for (int j = 0; j < 32; ++j)
-                    if (c0 + j < tl.np) epi_col_add<F16>(Y, ldy, row, row < M, trow, sc, j, acc[c0 + j]);
+                    for (int j = 0; j < 32; ++j) epi_col_add(Y, ldy, rowc, row < M, trow, sc, j, acc[c0 + j]);
+                }
             }
         }
     } else if (warp >= EPI_WARP0 && warp < EPI_WARP0 + 4) {
@@ -594,22 +632,26 @@ tc_pairs_fast_kernel(const __grid_constant__ CUtensorMap mapAb, const __grid_con
             mbar_wait(smem_u32(&accf_b[ab]), (it >> 1) & 1);
             asm volatile("tcgen05.fence::after_thread_sync;");
             const int2* pp = pairs + tl.p0;
+#ifdef M2L_NO_EPI          // ablation build (timing only): accumulators released unread
+            const int np_epi = 0;
+#else
+            const int np_epi = tl.np;
+#endif
 #pragma unroll 1
-            for (int c0 = 0; c0 < tl.np; c0 += 32) {
+            for (int c0 = 0; c0 < np_epi; c0 += 32) {
                 int trow;
                 float sc;
                 epi_cols_load<F16>(pp, c0, tl.np, lane, bscale, ascale_inv, trow, sc);
 #pragma unroll
                 for (int mt = 0; mt < MT; ++mt) {
                     const int row = tl.m0 + mt * BM + 32 * wq + lane;
-                    if (tl.m0 + mt * BM >= M) continue;      // slice not multiplied (warp-uniform)
+                    if (row - lane >= M) continue;           // none of this warp's rows exist (warp-uniform)
+                    const int rowc = row < M ? row : row - 32;
                     uint32_t v[32];
                     tmem_ld32(tmem + ((uint32_t)(32 * wq) << 16) + (uint32_t)((ab * MT + mt) * BN + c0), v);
                     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-                    for (int j = 0; j < 32; ++j)
-                        if (c0 + j < tl.np)
-                            epi_col_add<F16>(Y, ldy, row, row < M, trow, sc, j, __uint_as_float(v[j]));
+                    for (int j = 0; j < 32; ++j) epi_col_add(Y, ldy, rowc, row < M, trow, sc, j, __uint_as_float(v[j]));
                 }
             }
             asm volatile("tcgen05.fence::before_thread_sync;");
@@ -619,6 +661,221 @@ tc_pairs_fast_kernel(const __grid_constant__ CUtensorMap mapAb, const __grid_con
     }
     asm volatile("tcgen05.fence::before_thread_sync;");
     __syncthreads();
+    if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
+}
+
+// ------------------------------------------------------------------ cluster-multicast variant
+// The full-chain two-slice contraction on thread-block clusters of CS = 2 or 4 CTAs: the CTAs
+// of a cluster take pair blocks of the SAME operator and row slices, so the operator tiles
+// (A: 64 of the 96 KB a stage moves) are loaded once per cluster -- each CTA issues its share
+// of the four A tiles by TMA multicast into every CTA's shared memory -- and only the gathered
+// B rows are per CTA.  With FP16 operands the MMAs of the M2L take ~0.6 ms and its operand
+// loads alone ~1.0 ms (8 GB through the L2 at p = 6; ablation builds M2L_NO_MMA /
+// M2L_NO_ATOMICS): the kernel is bound by L2 -> SM bandwidth, which multicast cuts by a third
+// (CS = 2) or a half (CS = 4).  A stage may be refilled only when EVERY CTA's MMAs are done
+// with it: each MMA commit arrives on the empty barrier of all CTAs (tcgen05.commit multicast;
+// count CS).
+__device__ __forceinline__ void tma_load_3d_mc(uint32_t dst, const CUtensorMap* map, int c0, int c1, int c2,
+                                               uint32_t bar, uint16_t mask) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster "
+        "[%0], [%1, {%2, %3, %4}], [%5], %6;"
+        ::"r"(dst), "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(bar), "h"(mask)
+        : "memory");
+}
+__device__ __forceinline__ void mma_commit_mc(uint32_t bar, uint16_t mask) {
+    asm volatile(
+        "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
+        ::"r"(bar), "h"(mask)
+        : "memory");
+}
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+// tiles[CS c + r] is the work of cluster rank r in cluster tile c (same op, m0 and K range;
+// np = 0 pads an operator's last cluster tile)
+template <bool F16, int CS>
+__global__ void __launch_bounds__(fast::THREADS, 1)
+tc_pairs_mc_kernel(const __grid_constant__ CUtensorMap mapAb, const __grid_constant__ CUtensorMap mapAs,
+                   const void* __restrict__ Bb_, const void* __restrict__ Bs_, int ldb,
+                   const Tile* __restrict__ tiles, int nctiles, const int2* __restrict__ pairs, int M, int K,
+                   double* __restrict__ Y, int ldy, const float* __restrict__ bscale, float ascale_inv) {
+    constexpr int MT = fast::MT, STAGES = fast::STAGES, STAGE_BYTES = fast::STAGE_BYTES, TMEM_COLS = fast::TMEM_COLS;
+    constexpr int ES = F16 ? 2 : 4, BKE = 128 / ES, KS = 32 / ES;
+    static_assert(CS == 2 || CS == 4, "cluster of 2 or 4");
+    const char* Bb = reinterpret_cast<const char*>(Bb_);
+    const char* Bs = reinterpret_cast<const char*>(Bs_);
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    uint64_t* bars = (uint64_t*)(smem + STAGES * STAGE_BYTES);
+    uint64_t* full_b = bars;                     // [STAGES]
+    uint64_t* empty_b = bars + STAGES;           // [STAGES]
+    uint64_t* accf_b = bars + 2 * STAGES;        // [2]
+    uint64_t* acce_b = bars + 2 * STAGES + 2;    // [2]
+    uint32_t* tmem_slot = (uint32_t*)(bars + 2 * STAGES + 4);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t rank = cluster_rank();
+    const int cid = blockIdx.x / CS, ncl = gridDim.x / CS;
+    const uint16_t all = (uint16_t)((1u << CS) - 1);
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(smem_u32(&full_b[s]), 1 + 32 * fast::NPROD);   // A expect_tx + cp.async arrivals
+            mbar_init(smem_u32(&empty_b[s]), CS);                    // every CTA's MMA commit
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(smem_u32(&accf_b[b]), 1);
+            mbar_init(smem_u32(&acce_b[b]), 4);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 2) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(TMEM_COLS));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    cluster_sync();                              // every CTA's barriers initialised before any multicast
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0 || warp == 2 || warp == 3) {
+        // ---------------- producers: this CTA's share of the A tiles (multicast), its own B rows
+        const int pi = warp == 0 ? 0 : warp - 1;
+        const int piece = lane & 7, rsub = lane >> 3;
+        int c = 0;
+        for (int ci = cid; ci < nctiles; ci += ncl) {
+            const Tile tl = tiles[CS * ci + rank];
+            int64_t srow[fast::NG];
+#pragma unroll
+            for (int g = 0; g < fast::NG; ++g) {
+                const int r = rsub + 4 * (pi + fast::NPROD * g);
+                srow[g] = (int64_t)__ldg(&pairs[tl.p0 + max(min(r, tl.np - 1), 0)].y) * ldb;
+            }
+            const int ngrp = ((tl.np + 15) & ~15) / 4;
+            for (int kc = tl.kc0; kc < tl.kc1; ++kc, ++c) {
+                const int s = c % STAGES;
+                mbar_wait(smem_u32(&empty_b[s]), ((c / STAGES) & 1) ^ 1);
+                uint8_t* st = smem + s * STAGE_BYTES;
+                const uint32_t full = smem_u32(&full_b[s]);
+                if (pi == 0 && lane == 0) {
+                    mbar_expect_tx(full, 2 * MT * OPND_BYTES);          // all four A tiles land here
+                    if (CS == 2) {   // rank 0 multicasts the head tiles, rank 1 the remainder tiles
+                        const CUtensorMap* map = rank == 0 ? &mapAb : &mapAs;
+#pragma unroll
+                        for (int mt = 0; mt < MT; ++mt)
+                            tma_load_3d_mc(smem_u32(st + (2 * mt + rank) * OPND_BYTES), map, kc * BKE, tl.m0 + mt * BM,
+                                           tl.op, full, all);
+                    } else {         // rank = 2 slice + (head 0 / remainder 1): one tile each
+                        const CUtensorMap* map = (rank & 1) == 0 ? &mapAb : &mapAs;
+                        tma_load_3d_mc(smem_u32(st + rank * OPND_BYTES), map, kc * BKE, tl.m0 + (int)(rank >> 1) * BM,
+                                       tl.op, full, all);
+                    }
+                }
+                const int col = kc * BKE + (16 / ES) * piece;
+                const uint32_t nb = col < ldb ? 16u : 0u;
+                const uint32_t b0 = smem_u32(st + 2 * MT * OPND_BYTES);
+                const uint32_t b1 = b0 + OPND_BYTES;
+#pragma unroll
+                for (int g = 0; g < fast::NG; ++g) {
+                    const int grp = pi + fast::NPROD * g;
+                    if (grp < ngrp) {
+                        const int r = rsub + 4 * grp;
+                        const int64_t off = (srow[g] + col) * ES;
+                        const uint32_t so = (uint32_t)(r * 128 + ((piece ^ (r & 7)) * 16));
+                        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(b0 + so),
+                                     "l"(nb ? Bb + off : Bb), "r"(nb)
+                                     : "memory");
+                        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(b1 + so),
+                                     "l"(nb ? Bs + off : Bs), "r"(nb)
+                                     : "memory");
+                    }
+                }
+                asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(full) : "memory");
+            }
+        }
+    } else if (warp == 1) {
+        // ---------------- MMA issuer; the stage release goes to every CTA of the cluster
+        int c = 0, it = 0;
+        for (int ci = cid; ci < nctiles; ci += ncl, ++it) {
+            const Tile tl = tiles[CS * ci + rank];
+            const int ab = it & 1;
+            const uint32_t nmma = (uint32_t)max(16, (tl.np + 15) & ~15);
+            const uint32_t idesc = make_idesc<F16>(nmma, BM);
+            mbar_wait(smem_u32(&acce_b[ab]), ((it >> 1) & 1) ^ 1);
+            asm volatile("tcgen05.fence::after_thread_sync;");
+            for (int kc = tl.kc0; kc < tl.kc1; ++kc, ++c) {
+                const int s = c % STAGES;
+                mbar_wait(smem_u32(&full_b[s]), (c / STAGES) & 1);
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                asm volatile("tcgen05.fence::after_thread_sync;");
+                if (lane == 0) {
+                    const uint32_t st = smem_u32(smem + s * STAGE_BYTES);
+                    const uint64_t bb = smem_desc(st + 2 * MT * OPND_BYTES), bs = smem_desc(st + (2 * MT + 1) * OPND_BYTES);
+                    const int ksteps = min(BKE, K - kc * BKE + KS - 1) / KS;
+                    if (tl.np > 0)
+                        for (int k = 0; k < ksteps; ++k) {
+                            const uint64_t off = (uint64_t)(2 * k);
+#pragma unroll
+                            for (int mt = 0; mt < MT; ++mt) {
+                                if (tl.m0 + mt * BM >= M) continue;
+                                const uint64_t a_b = smem_desc(st + (2 * mt) * OPND_BYTES) + off;
+                                const uint64_t a_s = smem_desc(st + (2 * mt + 1) * OPND_BYTES) + off;
+                                const uint32_t d = tmem + (uint32_t)((ab * MT + mt) * BN);
+                                mma_op<F16>(d, a_b, bb + off, idesc, kc != tl.kc0 || k != 0);
+                                mma_op<F16>(d, a_b, bs + off, idesc, 1);
+                                mma_op<F16>(d, a_s, bb + off, idesc, 1);
+                            }
+                        }
+                    mma_commit_mc(smem_u32(&empty_b[s]), all);
+                    if (kc == tl.kc1 - 1) mma_commit(smem_u32(&accf_b[ab]));
+                }
+                __syncwarp();
+            }
+        }
+    } else if (warp >= EPI_WARP0) {
+        // ---------------- epilogue: TMEM -> fp64 atomics, 32 columns at a time
+        const int wq = warp - EPI_WARP0;
+        int it = 0;
+        for (int ci = cid; ci < nctiles; ci += ncl, ++it) {
+            const Tile tl = tiles[CS * ci + rank];
+            const int ab = it & 1;
+            mbar_wait(smem_u32(&accf_b[ab]), (it >> 1) & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;");
+            const int2* pp = pairs + tl.p0;
+            const int np_epi = tl.np;
+#pragma unroll 1
+            for (int c0 = 0; c0 < np_epi; c0 += 32) {
+                int trow;
+                float sc;
+                epi_cols_load<F16>(pp, c0, tl.np, lane, bscale, ascale_inv, trow, sc);
+#pragma unroll
+                for (int mt = 0; mt < MT; ++mt) {
+                    const int row = tl.m0 + mt * BM + 32 * wq + lane;
+                    if (row - lane >= M) continue;           // none of this warp's rows exist (warp-uniform)
+                    const int rowc = row < M ? row : row - 32;
+                    uint32_t v[32];
+                    tmem_ld32(tmem + ((uint32_t)(32 * wq) << 16) + (uint32_t)((ab * MT + mt) * BN + c0), v);
+                    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) epi_col_add(Y, ldy, rowc, row < M, trow, sc, j, __uint_as_float(v[j]));
+                }
+            }
+            asm volatile("tcgen05.fence::before_thread_sync;");
+            __syncwarp();
+            if (lane == 0) mbar_arrive(smem_u32(&acce_b[ab]));
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    cluster_sync();                              // no CTA leaves while a peer may still signal it
     if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
 }
 
@@ -794,15 +1051,17 @@ tc_pairs_wide_kernel(const __grid_constant__ CUtensorMap mapAb, const __grid_con
             const int row = tl.m0 + 32 * wq + lane;
             const int2* pp = pairs + tl.p0 + half * BN;
             const int npl = tl.np - half * BN;           // this warp's columns
+            if (row - lane < M) {
+                const int rowc = row < M ? row : row - 32;
 #pragma unroll
-            for (int c0 = 0; c0 < BN; c0 += 32) {
-                if (c0 >= npl) break;
-                int trow;
-                float sc;
-                epi_cols_load<F16>(pp, c0, npl, lane, bscale, ascale_inv, trow, sc);
+                for (int c0 = 0; c0 < BN; c0 += 32) {
+                    if (c0 >= npl) break;
+                    int trow;
+                    float sc;
+                    epi_cols_load<F16>(pp, c0, npl, lane, bscale, ascale_inv, trow, sc);
 #pragma unroll
-                for (int j = 0; j < 32; ++j)
-                    if (c0 + j < npl) epi_col_add<F16>(Y, ldy, row, row < M, trow, sc, j, acc[c0 + j]);
+                    for (int j = 0; j < 32; ++j) epi_col_add(Y, ldy, rowc, row < M, trow, sc, j, acc[c0 + j]);
+                }
             }
         }
     } else if (warp == 1) {
@@ -849,8 +1108,10 @@ tc_pairs_wide_kernel(const __grid_constant__ CUtensorMap mapAb, const __grid_con
             asm volatile("tcgen05.fence::after_thread_sync;");
             const int2* pp = pairs + tl.p0;
             const int row = tl.m0 + 32 * wq + lane;
+            const int rowc = row < M ? row : row - 32;
+            const int np_epi = row - lane < M ? tl.np : 0;       // (warp-uniform) some of this warp's rows exist
 #pragma unroll 1
-            for (int c0 = 0; c0 < tl.np; c0 += 32) {
+            for (int c0 = 0; c0 < np_epi; c0 += 32) {
                 int trow;
                 float sc;
                 epi_cols_load<F16>(pp, c0, tl.np, lane, bscale, ascale_inv, trow, sc);
@@ -858,8 +1119,7 @@ tc_pairs_wide_kernel(const __grid_constant__ CUtensorMap mapAb, const __grid_con
                 tmem_ld32(tmem + ((uint32_t)(32 * wq) << 16) + (uint32_t)(ab * BNW + c0), v);
                 asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-                for (int j = 0; j < 32; ++j)
-                    if (c0 + j < tl.np) epi_col_add<F16>(Y, ldy, row, row < M, trow, sc, j, __uint_as_float(v[j]));
+                for (int j = 0; j < 32; ++j) epi_col_add(Y, ldy, rowc, row < M, trow, sc, j, __uint_as_float(v[j]));
             }
             asm volatile("tcgen05.fence::before_thread_sync;");
             __syncwarp();
@@ -1327,13 +1587,35 @@ int tc_fast_tile_mode(int M) {
     return two > wide ? 2 : 1;
 }
 
-void tc_build_tiles(OpPairs& P, int M, int K, int mode, int bke) {
+void tc_build_tiles(OpPairs& P, int M, int K, int mode, int bke, int cs) {
     std::vector<tc::Tile> t;
     const int mstep = mode == 1 ? tc::fast::MT * tc::BM : tc::BM;
     const int bn = mode == 2 ? tc::wide::BNW : tc::BN;
     const int nk = (K + bke - 1) / bke;          // K chunks of 128 B: 32 TF32 or 64 FP16 elements
     P.tile_mode = mode;
     P.tile_bke = bke;
+    P.tile_cs = 1;
+    if (mode == 1 && cs > 1) {
+        // cluster tiles (tc_pairs_mc_kernel): cs consecutive pair blocks of one operator and row
+        // slice pair go to the cs CTAs of a cluster (an operator's last cluster tile is padded
+        // with empty blocks)
+        EB_REQUIRE(cs == 2 || cs == 4, "internal: cluster size");
+        P.tile_mode = 3;
+        P.tile_cs = cs;
+        for (int o = 0; o < P.nops; ++o) {
+            const int a = P.op_ptr_h[o], e = P.op_ptr_h[o + 1];
+            for (int p0 = a; p0 < e; p0 += cs * bn)
+                for (int m0 = 0; m0 < M; m0 += mstep)
+                    for (int r = 0; r < cs; ++r) {
+                        const int q = p0 + r * bn;
+                        t.push_back({o, q < e ? q : a, q < e ? std::min(bn, e - q) : 0, m0, 0, nk});
+                    }
+        }
+        P.ntiles = (int)t.size() / cs;
+        P.tiles.alloc(std::max<size_t>(t.size(), 1) * sizeof(tc::Tile) / sizeof(int));
+        if (!t.empty()) EB_CUDA(cudaMemcpy(P.tiles.p, t.data(), t.size() * sizeof(tc::Tile), cudaMemcpyHostToDevice));
+        return;
+    }
     // op-major; the row blocks of one pair group are consecutive (run side by side on
     // neighbouring CTAs, so the second load of the same gathered B rows hits L2)
     for (int o = 0; o < P.nops; ++o)
@@ -1381,6 +1663,36 @@ void tc_pairs_gemm_fast(const OpPairs& P, const CUtensorMap& Ab, const CUtensorM
                         bool f16, const float* bscale, float ascale_inv) {
     if (P.ntiles == 0) return;
     EB_REQUIRE(P.tile_bke == (f16 ? 64 : 32), "internal: translation tiles built for the other operand type");
+    if (P.tile_mode == 3) {
+        EB_REQUIRE(!drain, "internal: cluster tiles with the drained kernel");
+        const int cs = P.tile_cs;
+        void (*fn)(const CUtensorMap, const CUtensorMap, const void*, const void*, int, const tc::Tile*, int, const int2*,
+                   int, int, double*, int, const float*, float) =
+            cs == 2 ? (f16 ? tc::tc_pairs_mc_kernel<true, 2> : tc::tc_pairs_mc_kernel<false, 2>)
+                    : (f16 ? tc::tc_pairs_mc_kernel<true, 4> : tc::tc_pairs_mc_kernel<false, 4>);
+        static bool mattr[2][2] = {};
+        if (!mattr[cs == 4][f16]) {
+            EB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::fast::SMEM_BYTES));
+            mattr[cs == 4][f16] = true;
+        }
+        const int ncl = std::min(P.ntiles, num_sms() / cs);
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(ncl * cs);
+        cfg.blockDim = dim3(tc::fast::THREADS);
+        cfg.dynamicSmemBytes = tc::fast::SMEM_BYTES;
+        cfg.stream = s;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = cs;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        EB_CUDA(cudaLaunchKernelEx(&cfg, fn, Ab, As, Bb, Bs, ldb, reinterpret_cast<const tc::Tile*>(P.tiles.p), P.ntiles,
+                                   (const int2*)P.pairs.p, M, K, Y, ldy, bscale, ascale_inv));
+        EB_CHECK_LAUNCH();
+        return;
+    }
     EB_REQUIRE(P.tile_mode == 1 || P.tile_mode == 2, "internal: fast kernel needs two-slice or wide tiles");
     static bool attr[2][2][2] = {};
     const bool w = P.tile_mode == 2;
