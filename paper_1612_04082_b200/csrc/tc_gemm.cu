@@ -173,6 +173,46 @@ __device__ __forceinline__ void drain_add(uint32_t tmem, int wq, int col, float*
     }
 }
 
+// Epilogue of a translation tile: Y[target row][row] += v (fp64 atomic: exact, order
+// independent).  Each lane owns one TMEM lane (operator row) and walks the tile's columns
+// (pairs); the column's target row and scale are loaded once per 32 columns, one column per
+// lane (coalesced, independent loads), and broadcast by shuffles.  FP16 operands are scaled by
+// powers of two -- the operator set by 1 / ascale_inv, every source row by 1 / bscale[row]
+// (split_rows_h_kernel) -- which the fp32 product undoes exactly.
+//
+// The column code is branch-free: every lane issues its RED, lanes and columns outside the
+// tile add 0.0 to an element the tile owns anyway (a row 32 above for lanes past the
+// operator's last row, the tile's last pair for columns past np; scale 0).  With a guarded
+// `if (on) atomicAdd(...)` (also as a predicated inline-PTX RED) ptxas put a branch and a
+// convergence barrier (BSSY / BSYNC) around every column, so each column's shuffle ->
+// multiply -> convert -> RED chain (~90 cycles) ran after the previous one: the epilogue alone
+// took 1.0 ms of the 1.37 ms FP16 M2L, with or without the REDs (ablation builds M2L_NO_*,
+// DESIGN.md Sec. 6).
+template <bool F16>
+__device__ __forceinline__ void epi_cols_load(const int2* __restrict__ pp, int c0, int np, int lane,
+                                              const float* __restrict__ bscale, float ascale_inv, int& trow,
+                                              float& sc) {
+    const bool in = c0 + lane < np;
+    const int2 pr = __ldg(&pp[in ? c0 + lane : np - 1]);     // np >= 1 here
+    trow = pr.x;
+    sc = F16 ? ascale_inv * __ldg(&bscale[pr.y]) : 1.f;
+    if (!in) sc = 0.f;
+}
+// rowc: the lane's row, or a valid row of the same slice for lanes past the last row (row_ok false)
+__device__ __forceinline__ void epi_col_add(double* __restrict__ Y, int ldy, int rowc, bool row_ok, int trow, float sc,
+                                            int j, float v) {
+    const int tr = __shfl_sync(0xffffffffu, trow, j);
+    const float scj = __shfl_sync(0xffffffffu, sc, j);
+    v = row_ok ? v * scj : 0.f;
+#ifdef M2L_NO_ATOMICS      // ablation build (timing only): everything but the RED
+    if (v == 123456.789f)
+#endif
+#ifdef EPI_GUARD           // measurement build: the guarded (branchy) column code
+    if (row_ok && scj != 0.f)
+#endif
+    atomicAdd(Y + (int64_t)tr * ldy + rowc, (double)v);
+}
+
 // Persistent: grid = #SMs, CTA b takes tiles b, b + grid, ... (op-major order, so the
 // concurrently running tiles share operators in L2).  The smem ring, the ping-pong main
 // accumulators and the two per-tile correction accumulators all continue across tiles,
@@ -324,11 +364,18 @@ tc_pairs_kernel(const __grid_constant__ CUtensorMap mapAb, const __grid_constant
             __syncwarp();
             if (lane == 0) mbar_arrive(smem_u32(&core_b[cb]));
             const int row = tl.m0 + 32 * wq + lane;
-            if (row < M) {
+            if (row - lane < M) {                            // (warp-uniform) some of this warp's rows exist
                 const int2* pp = pairs + tl.p0;
+                const int rowc = row < M ? row : row - 32;
 #pragma unroll
-                for (int j = 0; j < BN; ++j)
-                    if (j < tl.np) atomicAdd(Y + (int64_t)__ldg(&pp[j].x) * ldy + row, (double)acc[j]);
+                for (int c0 = 0; c0 < BN; c0 += 32) {
+                    if (c0 >= tl.np) break;
+                    int trow;
+                    float sc;
+                    epi_cols_load<false>(pp, c0, tl.np, lane, nullptr, 1.f, trow, sc);
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) epi_col_add(Y, ldy, rowc, row < M, trow, sc, j, acc[c0 + j]);
+                }
             }
         }
     }
@@ -362,46 +409,6 @@ constexpr int NG = (BN / 4 + NPROD - 1) / NPROD;        // 4-row groups per prod
 // (one per TMEM lane quarter and slice) add each finished group into fp32 registers (round
 // to nearest) while the MMA fills the other buffer, so no tensor-core accumulation chain is
 // longer than GROUP chunks.
-// Epilogue of a translation tile: Y[target row][row] += v (fp64 atomic: exact, order
-// independent).  Each lane owns one TMEM lane (operator row) and walks the tile's columns
-// (pairs); the column's target row and scale are loaded once per 32 columns, one column per
-// lane (coalesced, independent loads), and broadcast by shuffles.  FP16 operands are scaled by
-// powers of two -- the operator set by 1 / ascale_inv, every source row by 1 / bscale[row]
-// (split_rows_h_kernel) -- which the fp32 product undoes exactly.
-//
-// The column code is branch-free: every lane issues its RED, lanes and columns outside the
-// tile add 0.0 to an element the tile owns anyway (a row 32 above for lanes past the
-// operator's last row, the tile's last pair for columns past np; scale 0).  With a guarded
-// `if (on) atomicAdd(...)` (also as a predicated inline-PTX RED) ptxas put a branch and a
-// convergence barrier (BSSY / BSYNC) around every column, so each column's shuffle ->
-// multiply -> convert -> RED chain (~90 cycles) ran after the previous one: the epilogue alone
-// took 1.0 ms of the 1.37 ms FP16 M2L, with or without the REDs (ablation builds M2L_NO_*,
-// DESIGN.md Sec. 6).
-template <bool F16>
-__device__ __forceinline__ void epi_cols_load(const int2* __restrict__ pp, int c0, int np, int lane,
-                                              const float* __restrict__ bscale, float ascale_inv, int& trow,
-                                              float& sc) {
-    const bool in = c0 + lane < np;
-    const int2 pr = __ldg(&pp[in ? c0 + lane : np - 1]);     // np >= 1 here
-    trow = pr.x;
-    sc = F16 ? ascale_inv * __ldg(&bscale[pr.y]) : 1.f;
-    if (!in) sc = 0.f;
-}
-// rowc: the lane's row, or a valid row of the same slice for lanes past the last row (row_ok false)
-__device__ __forceinline__ void epi_col_add(double* __restrict__ Y, int ldy, int rowc, bool row_ok, int trow, float sc,
-                                            int j, float v) {
-    const int tr = __shfl_sync(0xffffffffu, trow, j);
-    const float scj = __shfl_sync(0xffffffffu, sc, j);
-    v = row_ok ? v * scj : 0.f;
-#ifdef M2L_NO_ATOMICS      // ablation build (timing only): everything but the RED
-    if (v == 123456.789f)
-#endif
-#ifdef EPI_GUARD           // measurement build: the guarded (branchy) column code
-    if (row_ok && scj != 0.f)
-#endif
-    atomicAdd(Y + (int64_t)tr * ldy + rowc, (double)v);
-}
-
 template <bool DRAIN, bool F16>
 __global__ void __launch_bounds__(DRAIN ? 384 : fast::THREADS, 1)
 tc_pairs_fast_kernel(const __grid_constant__ CUtensorMap mapAb, const __grid_constant__ CUtensorMap mapAs,
