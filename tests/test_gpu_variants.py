@@ -1,7 +1,8 @@
 """Kernel variants selected by process-wide switches (read once per process, so each runs in a
 child process): the persistent M2M/L2L level-chain kernel (EBEM_ML_CHAIN=1), the wide
 128 x 256 M2L tiles (EBEM_M2L_WIDE=1), the packed FFMA2 near field (EBEM_NEAR_PACKED=1) and the
-operand type of the translations (TF32 or FP16 head / remainder splits).  Each must meet the same bounds against the
+operand type of the translations (TF32 or FP16 head / remainder splits), the cluster-multicast
+M2L (EBEM_M2L_MC = 2 / 4 CTAs sharing the operator tiles).  Each must meet the same bounds against the
 fp64 oracle as the default path (the KIFMM sum of Eq. fmm_summation)."""
 import json
 import os
@@ -31,7 +32,7 @@ np.save({path!r}, np.stack([out.cpu().numpy(), out2.cpu().numpy()]))
 # EBEM_M2L_F16=0: every translation on TF32 operands; EBEM_ML_F16=0: FP16 M2L, TF32 M2M / L2L;
 # the default is FP16 operands for M2L, M2M and L2L (tc_gemm.cu, 3xFP16)
 VARIANTS = [{}, {"EBEM_ML_CHAIN": "1"}, {"EBEM_M2L_WIDE": "1"}, {"EBEM_NEAR_PACKED": "1"}, {"EBEM_M2L_F16": "0"},
-            {"EBEM_ML_F16": "0"}, {"EBEM_M2L_F16": "1"}]
+            {"EBEM_ML_F16": "0"}, {"EBEM_M2L_F16": "1"}, {"EBEM_M2L_MC": "2"}, {"EBEM_M2L_MC": "4"}]
 
 
 @pytest.fixture(scope="module")

@@ -35,6 +35,7 @@ def main():
     print("| kernel | " + " | ".join(c[1] for c in COLS) + " |")
     print("|---" * (len(COLS) + 1) + "|")
     m2l = None
+    near = None
     for r in rows[2:]:
         d, u = dict(zip(hdr, r)), dict(zip(hdr, units))
         name = d["Kernel Name"].split("(")[0].replace("void ", "")
@@ -56,8 +57,18 @@ def main():
                    "dram_read": to_base(d["dram__bytes_read.sum"], u["dram__bytes_read.sum"]),
                    "dram_write": to_base(d["dram__bytes_write.sum"], u["dram__bytes_write.sum"]),
                    "ms_under_ncu": to_base(d["gpu__time_duration.sum"], u["gpu__time_duration.sum"]) * 1e3}
+        if "near_eval_kernel" in name and near is None:      # the near field of the same matvec
+            near = {"kernel": "near_eval_kernel",
+                    "dram_read": to_base(d["dram__bytes_read.sum"], u["dram__bytes_read.sum"]),
+                    "dram_write": to_base(d["dram__bytes_write.sum"], u["dram__bytes_write.sum"]),
+                    "ms_under_ncu": dur * 1e3,
+                    "source": a.source.replace("the longest tc_pairs_fast_kernel launch", "the near_eval_kernel launch")
+                                      .replace(" (the M2L)", "")}
     if a.traffic_out and m2l:
-        json.dump({"_source": a.source, "M2L": m2l}, open(a.traffic_out, "w"), indent=1)
+        out = {"_source": a.source, "M2L": m2l}
+        if near:
+            out["NEAR"] = near
+        json.dump(out, open(a.traffic_out, "w"), indent=1)
 
 
 if __name__ == "__main__":
