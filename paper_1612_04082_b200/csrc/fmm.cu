@@ -1139,21 +1139,24 @@ void schedule_tree(Tree& t, cudaStream_t s) {
             wn[i] = (double)tsub[b] * near_ns[b];
             wf[i] = (double)tsub[b] * P.ne * nfar;
         }
-        // decreasing work, ties in Morton order: one sort of packed keys (float bits of the
-        // non-negative work, complemented, then the index)
+        // decreasing work by a counting sort on the leading 16 bits of the (non-negative) work as
+        // a float (exponent and eight mantissa bits: 0.4% classes), Morton order within a class
+        // (two std::sort calls over the ~30 k leaves took 2.5 ms of the build)
         auto order = [&](const std::vector<double>& w, std::vector<int>& e_out, std::vector<int>& l_out) {
-            std::vector<uint64_t> key(ev.size());
-            for (size_t i = 0; i < key.size(); ++i) {
+            constexpr int NB = 1 << 16;
+            std::vector<int> cls(ev.size()), start(NB + 1, 0);
+            for (size_t i = 0; i < cls.size(); ++i) {
                 const float wf32 = (float)w[i];
                 uint32_t bits;
                 std::memcpy(&bits, &wf32, sizeof(bits));
-                key[i] = ((uint64_t)(~bits) << 32) | (uint32_t)i;
+                cls[i] = NB - 1 - (int)(bits >> 15);          // sign bit 0: 16 leading bits; largest first
+                ++start[cls[i] + 1];
             }
-            std::sort(key.begin(), key.end());
-            for (size_t i = 0; i < key.size(); ++i) {
-                const uint32_t k = (uint32_t)key[i];
-                e_out[i] = ev[k];
-                l_out[i] = l2t[k];
+            for (int c = 0; c < NB; ++c) start[c + 1] += start[c];
+            for (size_t i = 0; i < cls.size(); ++i) {
+                const int pos = start[cls[i]]++;
+                e_out[pos] = ev[i];
+                l_out[pos] = l2t[i];
             }
         };
         std::vector<int> nev(ev.size()), nl2t(ev.size());
