@@ -649,7 +649,7 @@ def main():
     if rank == 0:
         line = {"metric": METRIC, "value": ms, "unit": "ms", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False, "scaling": "weak",
-                "vs_baseline": None, "dtype": "f32 (3xFP16 M2L/M2M/L2L, 3xTF32 Q2Z; fp64 plan, fp64 equivalent densities)",
+                "vs_baseline": None, "dtype": "f32 (3xFP16 tensor-core translations; fp64 plan, fp64 equivalent densities)",
                 "data": "synthetic",
                 "config": {"workload": WORKLOAD, "n_points": n, "p": args.p, "max_pts": args.max_pts,
                            "kernel": "UP", "l2": "flushed between steps (256 MB write)",

@@ -60,8 +60,10 @@ check_potential_kernel(const int* __restrict__ tbox, const int* __restrict__ sof
                        const int* __restrict__ sbeg, const int* __restrict__ send, const int* __restrict__ anchor,
                        const int* __restrict__ level, BoxGeo geo, double rad, const float* __restrict__ sc, int nc,
                        const float4* __restrict__ rec, KConst kc, float* __restrict__ Q, float* __restrict__ Qb,
-                       float* __restrict__ Qs, int ldq, const int* __restrict__ ssplit, int smode) {
+                       float* __restrict__ Qs, int ldq, const int* __restrict__ ssplit, int smode,
+                       __half* __restrict__ Qhb, __half* __restrict__ Qhs, float* __restrict__ Qhinv, int ldqh) {
     __shared__ float4 srec[CP_TILE * REC_DISP];
+    __shared__ float wmax[CP_T / 32];
     const int i = blockIdx.x;
     const int b = tbox[i];
     double cx, cy, cz, r;
@@ -112,6 +114,40 @@ check_potential_kernel(const int* __restrict__ tbox, const int* __restrict__ sof
                 pair_loop_multi<SL, DL, false, KPT, false>(srec, cnt, x, y, z, kc, acc);
             }
         }
+    }
+    if (Qhb) {
+        // FP16 operands for the Q2Z contraction (tc_gemm.cu, reading R14): the box's check
+        // potentials scaled by one power of two (largest magnitude in [2^12, 2^13)), head and
+        // remainder written as halves, the factor undoing the scale per row
+        float amax = 0.f;
+#pragma unroll
+        for (int q = 0; q < KPT; ++q)
+            if ((int)(threadIdx.x + q * blockDim.x) < nc)
+                amax = fmaxf(amax, fmaxf(fabsf(acc[q][0]), fmaxf(fabsf(acc[q][1]), fabsf(acc[q][2]))));
+#pragma unroll
+        for (int off = 16; off; off >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, off));
+        __syncthreads();                       // (srec reads done; wmax free)
+        if ((threadIdx.x & 31) == 0) wmax[threadIdx.x >> 5] = amax;
+        __syncthreads();
+        amax = 0.f;
+        for (int w = 0; w < (int)(blockDim.x + 31) / 32; ++w) amax = fmaxf(amax, wmax[w]);
+        const float scl = pow2_scale(amax);
+        if (threadIdx.x == 0) Qhinv[i] = 1.f / scl;
+#pragma unroll
+        for (int q = 0; q < KPT; ++q) {
+            const int k = threadIdx.x + q * blockDim.x;
+            if (k < nc) {
+                const int64_t o = (int64_t)i * ldqh + 3 * k;
+#pragma unroll
+                for (int c = 0; c < 3; ++c) {
+                    const float a = acc[q][c] * scl;
+                    const __half h = __float2half_rn(a);
+                    Qhb[o + c] = h;
+                    Qhs[o + c] = __float2half_rn(a - __half2float(h));
+                }
+            }
+        }
+        return;
     }
 #pragma unroll
     for (int q = 0; q < KPT; ++q) {
@@ -1222,7 +1258,19 @@ void schedule_tree(Tree& t, cudaStream_t s) {
         // tile shapes: the full-chain and the drained M2L kernels two-slice or wide by M
         // (tc_fast_tile_mode), the one-slice precise kernel 128 x 128
         const int fm = tc_fast_tile_mode(me);
-        tc_build_tiles(t.q2z_up, me, mc, t.ml_fast ? fm : 0);
+        // the upward Q2Z on FP16 operands as well (the S2M kernel writes the split; EBEM_Q2Z_F16=0: TF32)
+        static const bool q2z_h = !(std::getenv("EBEM_Q2Z_F16") && std::atoi(std::getenv("EBEM_Q2Z_F16")) == 0);
+        // (as the M2M / L2L chains, not in trees deeper than 16 levels: level-20 coincident cluster,
+        // GPU vs oracle KIFMM 2.85e-3 with the FP16 Q2Z against 1.71e-3, limitation L1)
+        t.q2z_f16 = t.ml_fast && m2l_f16_level() >= 1 && q2z_h && t.nlevels <= 16;
+        if (t.q2z_f16) {
+            t.Qhb.alloc((size_t)nq * P.ldch);
+            t.Qhs.alloc((size_t)nq * P.ldch);
+            t.Qhinv.alloc(nq);
+            t.Qhb.zero(s);
+            t.Qhs.zero(s);
+        }
+        tc_build_tiles(t.q2z_up, me, mc, t.ml_fast ? fm : 0, t.q2z_f16 ? 64 : 32);
         tc_build_tiles(t.q2z_dn, me, mc, t.ml_fast ? fm : 0);
         // M2L operands in FP16 (3xFP16, twice the tensor rate of 3xTF32; EBEM_M2L_F16=0: TF32)
         t.m2l_f16 = m2l_f16_level() >= 1;
@@ -1303,7 +1351,8 @@ void schedule_tree(Tree& t, cudaStream_t s) {
 // ------------------------------------------------------------------ evaluation
 template <bool SL, bool DL>
 static void launch_check(const Tree& t, const int* tbox, int n, const int* soff, const int* sidx, double rad,
-                         float* Q, float* Qb, float* Qs, cudaStream_t s) {
+                         float* Q, float* Qb, float* Qs, cudaStream_t s, __half* Qhb = nullptr, __half* Qhs = nullptr,
+                         float* Qhinv = nullptr) {
     if (n == 0) return;
     const Plan& P = *t.plan;
     BoxGeo geo{t.origin[0], t.origin[1], t.origin[2], t.side};
@@ -1316,7 +1365,8 @@ static void launch_check(const Tree& t, const int* tbox, int n, const int* soff,
     EB_CUDA(cudaFuncSetAttribute(check_potential_kernel<SL, DL, K>, cudaFuncAttributePreferredSharedMemoryCarveout, 100)); \
     check_potential_kernel<SL, DL, K><<<n, nthr, 0, s>>>(tbox, soff, sidx, t.sbeg.p, t.send.p, t.anchor.p,         \
                                                          t.level.p, geo, rad, P.s_c.p, P.nc, t.rec_disp.p, kc,    \
-                                                         Q, Qb, Qs, P.ldc, t.ssplit.p, t.ssplit.p ? t.split_mode : 0)
+                                                         Q, Qb, Qs, P.ldc, t.ssplit.p, t.ssplit.p ? t.split_mode : 0, \
+                                                         Qhb, Qhs, Qhinv, P.ldch)
     switch (kpt) {
         case 1: EB_CHECK_LAUNCH_KPT(1); break;
         case 2: EB_CHECK_LAUNCH_KPT(2); break;
@@ -1425,6 +1475,10 @@ void tree_precise(Tree& t, cudaStream_t s) {
         t.PHIUF.release();
         t.PHID.alloc((size_t)std::max(1, t.n_phid) * P.me);
         t.PHIU.alloc((size_t)std::max(1, t.n_phiu) * P.me);
+    }
+    if (t.q2z_f16) {      // the BEM's stored S2M operator (s2m_hook) writes the TF32 split
+        t.q2z_f16 = false;
+        tc_build_tiles(t.q2z_up, P.me, P.mc, t.ml_fast ? tc_fast_tile_mode(P.me) : 0, 32);
     }
     tree_m2l_fast(t, false, s);
     EB_CUDA(cudaStreamSynchronize(s));
@@ -1692,9 +1746,12 @@ void fmm_evaluate(Tree& t, int kernel, const float* f, const float* g, float* ou
     } else {
         float* qb = t.use_tc ? t.Qb.p : nullptr;
         float* qs = t.use_tc ? t.Qs.p : nullptr;
-        if (sl && dl) launch_check<true, true>(t, t.s2m_box.p, t.n_s2m, nullptr, nullptr, RAD_UC, t.Q.p, qb, qs, sa);
-        else if (sl) launch_check<true, false>(t, t.s2m_box.p, t.n_s2m, nullptr, nullptr, RAD_UC, t.Q.p, qb, qs, sa);
-        else launch_check<false, true>(t, t.s2m_box.p, t.n_s2m, nullptr, nullptr, RAD_UC, t.Q.p, qb, qs, sa);
+        __half* hb = t.q2z_f16 ? t.Qhb.p : nullptr;
+        __half* hs = t.q2z_f16 ? t.Qhs.p : nullptr;
+        float* hi = t.q2z_f16 ? t.Qhinv.p : nullptr;
+        if (sl && dl) launch_check<true, true>(t, t.s2m_box.p, t.n_s2m, nullptr, nullptr, RAD_UC, t.Q.p, qb, qs, sa, hb, hs, hi);
+        else if (sl) launch_check<true, false>(t, t.s2m_box.p, t.n_s2m, nullptr, nullptr, RAD_UC, t.Q.p, qb, qs, sa, hb, hs, hi);
+        else launch_check<false, true>(t, t.s2m_box.p, t.n_s2m, nullptr, nullptr, RAD_UC, t.Q.p, qb, qs, sa, hb, hs, hi);
     }
     pe(PH_S2M, sa);
     const int lde = P.lde, ldc = P.ldc;
@@ -1703,7 +1760,10 @@ void fmm_evaluate(Tree& t, int kernel, const float* f, const float* g, float* ou
     if (conc) EB_CUDA(cudaStreamWaitEvent(sa, t.ev_zz, 0));
     pb(PH_Q2Z_UP, sa);
     if (t.use_tc) {
-        if (t.ml_fast) tc_pairs_gemm_fast(t.q2z_up, P.mQu1T_b, P.mQu1T_s, t.Qb.p, t.Qs.p, ldc, me, mc, t.Z.p, lde, false, sa);
+        if (t.ml_fast && t.q2z_f16)
+            tc_pairs_gemm_fast(t.q2z_up, P.mQu1T_hb, P.mQu1T_hs, t.Qhb.p, t.Qhs.p, P.ldch, me, mc, t.Z.p, lde, false, sa, true,
+                               t.Qhinv.p, P.qu_hinv);
+        else if (t.ml_fast) tc_pairs_gemm_fast(t.q2z_up, P.mQu1T_b, P.mQu1T_s, t.Qb.p, t.Qs.p, ldc, me, mc, t.Z.p, lde, false, sa);
         else tc_pairs_gemm(t.q2z_up, P.mQu1T_b, P.mQu1T_s, t.mQb, t.mQs, me, mc, t.Z.p, lde, sa);
     } else {
         gemm_pairs_f32(t.q2z_up, P.Qu1T.p, me, mc, ldc, t.Q.p, ldc, t.Z.p, lde, sa);

@@ -27,6 +27,13 @@
 
 namespace ebem {
 
+// 2^(12 - floor(log2 amax)): the power-of-two row scale of the FP16 operand splits (tc_gemm.cu,
+// reading R14), 1 for an all-zero (or non-finite) row
+__device__ __forceinline__ float pow2_scale(float amax) {
+    if (!(amax > 0.f) || !isfinite(amax)) return 1.f;
+    return scalbnf(1.f, 12 - ilogbf(amax));
+}
+
 constexpr int MAXLEVEL = 20;
 constexpr double RAD_UE = 1.05, RAD_UC = 2.95, RAD_DE = 2.95, RAD_DC = 1.05;
 constexpr int NV_OFFSETS = 316;        // 7^3 - 3^3 M2L translation vectors
@@ -52,10 +59,10 @@ struct Plan {
     // scaled FP16 head / remainder copies of the M2L operators (3xFP16 path, tc_gemm.cu): row
     // stride ldh halves (me rounded up to 8: 16-B rows), one power-of-two scale for the set
     // (m2l_hinv undoes it)
-    DBuf<__half> M2L_hb, M2L_hs, M2M_hb, M2M_hs, L2L_hb, L2L_hs;
-    CUtensorMap mM2L_hb, mM2L_hs, mM2M_hb, mM2M_hs, mL2L_hb, mL2L_hs;
-    int ldh = 0;
-    float m2l_hinv = 1.f, m2m_hinv = 1.f, l2l_hinv = 1.f;
+    DBuf<__half> M2L_hb, M2L_hs, M2M_hb, M2M_hs, L2L_hb, L2L_hs, Qu1T_hb, Qu1T_hs;
+    CUtensorMap mM2L_hb, mM2L_hs, mM2M_hb, mM2M_hs, mL2L_hb, mL2L_hs, mQu1T_hb, mQu1T_hs;
+    int ldh = 0, ldch = 0;      // half row strides of the me- and mc-long rows
+    float m2l_hinv = 1.f, m2m_hinv = 1.f, l2l_hinv = 1.f, qu_hinv = 1.f;
     int off_index[343];         // (ox+3)*49+(oy+3)*7+(oz+3) -> 0..315 or -1
 };
 
@@ -199,6 +206,9 @@ struct Tree {
     DBuf<float> Zhinv, Whinv;
     bool m2l_f16 = false;                // M2L operands in FP16 (EBEM_M2L_F16, default on)
     bool ml_f16 = false;                 // M2M / L2L on the fast kernel in FP16 too (split level by level)
+    DBuf<__half> Qhb, Qhs;               // FP16 split of the S2M check potentials (written by the S2M kernel)
+    DBuf<float> Qhinv;
+    bool q2z_f16 = false;                // upward Q2Z on FP16 operands (not with the BEM's stored S2M operator)
     DBuf<double> PHID, PHIU;             // [n_phid x me], [n_phiu x me] (fp64 far field)
     DBuf<float4> PHIDF, PHIUF;           // [n_phid x ne], [n_phiu x ne] (fp32 far field, scaled)
     DBuf<float> near_sorted;             // [ntrg x 6] near field, sorted target order

@@ -394,6 +394,15 @@ static std::shared_ptr<Plan> make_plan(int p, const Material& m, cudaStream_t s)
     P->m2l_hinv = split_h(P->M2L, NV_OFFSETS, P->M2L_hb, P->M2L_hs, &P->mM2L_hb, &P->mM2L_hs);
     P->m2m_hinv = split_h(P->M2M, 8, P->M2M_hb, P->M2M_hs, &P->mM2M_hb, &P->mM2M_hs);
     P->l2l_hinv = split_h(P->L2L, 8, P->L2L_hb, P->L2L_hs, &P->mL2L_hb, &P->mL2L_hs);
+    // the upward check-potential rotation Q_u1^T ([me x mc], rows of mc check values)
+    P->ldch = (P->mc + 7) & ~7;
+    P->Qu1T_hb.alloc((size_t)P->me * P->ldch);
+    P->Qu1T_hs.alloc((size_t)P->me * P->ldch);
+    P->Qu1T_hb.zero(s);
+    P->Qu1T_hs.zero(s);
+    P->qu_hinv = tc_split_ops_h(P->Qu1T.p, P->ldc, P->me, P->mc, P->Qu1T_hb.p, P->Qu1T_hs.p, P->ldch, s);
+    tc_make_map_a_h(&P->mQu1T_hb, P->Qu1T_hb.p, 1, P->me, P->mc, P->ldch);
+    tc_make_map_a_h(&P->mQu1T_hs, P->Qu1T_hs.p, 1, P->me, P->mc, P->ldch);
     EB_CUDA(cudaStreamSynchronize(s));
     return P;
 }

@@ -1171,12 +1171,6 @@ __global__ void split_rows_kernel(const XT* __restrict__ X, int ld, int64_t row0
 // Entries more than 2^-15 below the row maximum have a subnormal remainder (absolute spacing
 // 2^-24, i.e. 2^-37 of the row maximum): the split keeps min(22 bits relative, 2^-37 of the
 // largest entry) -- for a dot product the same error level as the TF32 split.
-__device__ __forceinline__ float pow2_scale(float amax) {
-    // 2^(12 - floor(log2 amax)); 1 for an all-zero (or non-finite) row
-    if (!(amax > 0.f) || !isfinite(amax)) return 1.f;
-    const int e = ilogbf(amax);
-    return scalbnf(1.f, 12 - e);
-}
 
 // rows [row0, row0 + nrows) of the fp64 state X (row stride ldx) -> Xh / Xr (row stride ldh
 // halves) and the factor that undoes the row's scaling; a warp per row

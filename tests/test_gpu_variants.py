@@ -32,7 +32,8 @@ np.save({path!r}, np.stack([out.cpu().numpy(), out2.cpu().numpy()]))
 # EBEM_M2L_F16=0: every translation on TF32 operands; EBEM_ML_F16=0: FP16 M2L, TF32 M2M / L2L;
 # the default is FP16 operands for M2L, M2M and L2L (tc_gemm.cu, 3xFP16)
 VARIANTS = [{}, {"EBEM_ML_CHAIN": "1"}, {"EBEM_M2L_WIDE": "1"}, {"EBEM_NEAR_PACKED": "1"}, {"EBEM_M2L_F16": "0"},
-            {"EBEM_ML_F16": "0"}, {"EBEM_M2L_F16": "1"}, {"EBEM_M2L_MC": "2"}, {"EBEM_M2L_MC": "4"}]
+            {"EBEM_ML_F16": "0"}, {"EBEM_M2L_F16": "1"}, {"EBEM_M2L_MC": "2"}, {"EBEM_M2L_MC": "4"},
+            {"EBEM_Q2Z_F16": "0"}]
 
 
 @pytest.fixture(scope="module")
