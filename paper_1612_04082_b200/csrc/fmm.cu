@@ -1290,7 +1290,13 @@ void schedule_tree(Tree& t, cudaStream_t s) {
         // the TF32 split (relative per element) does not -- level-20 coincident cluster, GPU vs
         // oracle KIFMM: 1.71e-3 with TF32 chains, 2.11e-3 with FP16 chains, M2L in FP16 either way.
         static const bool chain_env = std::getenv("EBEM_ML_CHAIN") && std::atoi(std::getenv("EBEM_ML_CHAIN")) == 1;
-        t.ml_f16 = t.ml_fast && t.m2l_f16 && !chain_env && ml_f16_on() && t.nlevels <= 16;
+        // p = 7, 8 (fp32 far field): the chains on the same FP16 data flow with DRAINED accumulation
+        // (tc_pairs_fast / wide kernel <true, true>) instead of the one-slice precise TF32 kernel
+        // with TMA-gathered rows (EBEM_ML_DRAIN_F16=0: off; the BEM operator keeps the precise kernel)
+        static const bool drain_h = !(std::getenv("EBEM_ML_DRAIN_F16") && std::atoi(std::getenv("EBEM_ML_DRAIN_F16")) == 0);
+        t.ml_drain = t.tc_fast && !t.ml_fast && drain_h && m2l_f16_level() >= 2 && m2l_drain_fast();
+        t.ml_f16 = (t.ml_fast || t.ml_drain) && t.m2l_f16 && !chain_env && ml_f16_on() && t.nlevels <= 16;
+        t.ml_drain = t.ml_drain && t.ml_f16;
         if (t.ml_f16) {
             t.Whb.alloc((size_t)std::max(1, t.n_dn) * P.ldh);
             t.Whs.alloc((size_t)std::max(1, t.n_dn) * P.ldh);
@@ -1298,8 +1304,8 @@ void schedule_tree(Tree& t, cudaStream_t s) {
             t.Whb.zero(s);
             t.Whs.zero(s);
         }
-        for (auto& x : t.m2m) tc_build_tiles(x, me, me, t.ml_fast ? fm : 0, t.ml_f16 ? 64 : 32);
-        for (auto& x : t.l2l) tc_build_tiles(x, me, me, t.ml_fast ? fm : 0, t.ml_f16 ? 64 : 32);
+        for (auto& x : t.m2m) tc_build_tiles(x, me, me, t.ml_fast || t.ml_drain ? fm : 0, t.ml_f16 ? 64 : 32);
+        for (auto& x : t.l2l) tc_build_tiles(x, me, me, t.ml_fast || t.ml_drain ? fm : 0, t.ml_f16 ? 64 : 32);
         // EBEM_ML_CHAIN=1: M2M and L2L chains as one persistent launch each (tc_chain_kernel).
         // Measured on the 1M beam: M2M 0.341 -> 0.317 ms, L2L 0.321 -> 0.306 ms alone, but the
         // overlapped matvec unchanged (4.41-4.44 ms either way) and the host-buffer (e2e) matvec
@@ -1475,6 +1481,14 @@ void tree_precise(Tree& t, cudaStream_t s) {
         t.PHIUF.release();
         t.PHID.alloc((size_t)std::max(1, t.n_phid) * P.me);
         t.PHIU.alloc((size_t)std::max(1, t.n_phiu) * P.me);
+    }
+    // EBEM_BEM_ML_DRAIN=1: the BEM operator's chains on the drained FP16 data flow too (measurement)
+    static const bool bem_drain = std::getenv("EBEM_BEM_ML_DRAIN") && std::atoi(std::getenv("EBEM_BEM_ML_DRAIN")) == 1;
+    if (t.ml_drain && !bem_drain) {     // the operator inside GMRES keeps the one-slice precise kernel for the chains
+        t.ml_drain = false;
+        t.ml_f16 = false;
+        for (auto& x : t.m2m) tc_build_tiles(x, P.me, P.me, 0, 32);
+        for (auto& x : t.l2l) tc_build_tiles(x, P.me, P.me, 0, 32);
     }
     if (t.q2z_f16) {      // the BEM's stored S2M operator (s2m_hook) writes the TF32 split
         t.q2z_f16 = false;
@@ -1778,7 +1792,7 @@ void fmm_evaluate(Tree& t, int kernel, const float* f, const float* g, float* ou
     for (int l = t.nlevels - 2; l >= 2; --l) {
         if (t.use_tc && t.ml_f16) {
             tc_split_rows_h(t.Z.p, lde, t.up_lstart[l + 1], zrows(l + 1), me, t.Zhb.p, t.Zhs.p, P.ldh, t.Zhinv.p, sa);
-            tc_pairs_gemm_fast(t.m2m[l], P.mM2M_hb, P.mM2M_hs, t.Zhb.p, t.Zhs.p, P.ldh, me, me, t.Z.p, lde, false, sa,
+            tc_pairs_gemm_fast(t.m2m[l], P.mM2M_hb, P.mM2M_hs, t.Zhb.p, t.Zhs.p, P.ldh, me, me, t.Z.p, lde, t.ml_drain, sa,
                                true, t.Zhinv.p, P.m2m_hinv);
         } else if (t.use_tc) {
             tc_split_rows(t.Z.p, lde, t.up_lstart[l + 1], zrows(l + 1), me, t.Zb.p, t.Zs.p, sa);
@@ -1860,7 +1874,7 @@ void fmm_evaluate(Tree& t, int kernel, const float* f, const float* g, float* ou
     for (int l = 3; l < t.nlevels; ++l) {
         if (t.use_tc && t.ml_f16) {
             tc_split_rows_h(t.W.p, lde, t.dn_lstart[l - 1], wrows(l - 1), me, t.Whb.p, t.Whs.p, P.ldh, t.Whinv.p, sa);
-            tc_pairs_gemm_fast(t.l2l[l], P.mL2L_hb, P.mL2L_hs, t.Whb.p, t.Whs.p, P.ldh, me, me, t.W.p, lde, false, sa,
+            tc_pairs_gemm_fast(t.l2l[l], P.mL2L_hb, P.mL2L_hs, t.Whb.p, t.Whs.p, P.ldh, me, me, t.W.p, lde, t.ml_drain, sa,
                                true, t.Whinv.p, P.l2l_hinv);
         } else if (t.use_tc) {
             tc_split_rows(t.W.p, lde, t.dn_lstart[l - 1], wrows(l - 1), me, t.Wb.p, t.Ws.p, sa);

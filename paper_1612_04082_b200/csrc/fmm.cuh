@@ -206,6 +206,7 @@ struct Tree {
     DBuf<float> Zhinv, Whinv;
     bool m2l_f16 = false;                // M2L operands in FP16 (EBEM_M2L_F16, default on)
     bool ml_f16 = false;                 // M2M / L2L on the fast kernel in FP16 too (split level by level)
+    bool ml_drain = false;               // ... with drained accumulation (p = 7, 8; ml_fast false)
     DBuf<__half> Qhb, Qhs;               // FP16 split of the S2M check potentials (written by the S2M kernel)
     DBuf<float> Qhinv;
     bool q2z_f16 = false;                // upward Q2Z on FP16 operands (not with the BEM's stored S2M operator)
