@@ -500,8 +500,15 @@ def main():
     pk["f16x3_tflops"] = pk["bf16_tflops"] / 3.0                 # ... of 3xFP16 (fp16 dense = bf16 dense rate)
     # operand type of the M2L (the library's default: FP16 head / remainder, EBEM_M2L_F16 = 0: TF32)
     m2l_f16 = int(os.environ.get("EBEM_M2L_F16", "2")) >= 1
+    # at p <= 6 the M2M / L2L chains and the upward Q2Z run on FP16 operands too (library defaults)
+    f16_phases = {"M2L"} if m2l_f16 else set()
+    if m2l_f16 and args.p <= 6:
+        if os.environ.get("EBEM_ML_F16", "1") != "0":
+            f16_phases |= {"M2M", "L2L"}
+        if os.environ.get("EBEM_Q2Z_F16", "1") != "0":
+            f16_phases |= {"Q2Z_up"}
     def tensor_peak(name):
-        return pk["f16x3_tflops"] if (name == "M2L" and m2l_f16) else pk["tf32x3_tflops"]
+        return pk["f16x3_tflops"] if name in f16_phases else pk["tf32x3_tflops"]
     for ph in phases:
         f64, f32 = ph["flops_fp64"], ph["flops"] - ph["flops_fp64"]
         sec = ph["ms"] * 1e-3
@@ -518,6 +525,7 @@ def main():
                        "launches": ph["launches"], "bound": bound,
                        "gflop": ph["flops"] / 1e9, "gflop_fp64": f64 / 1e9, "interactions": ph["interactions"],
                        "mbytes": ph["bytes"] / 1e6, "frac": frac,
+                       "operands": ("fp16" if ph["name"] in f16_phases else "tf32") if ph["name"] in tensor_phases else None,
                        "frac_in_situ": (max(tmin, tmem) / isec) if isec > 0 else None})
     # dominant kernel: the phase with the most device time (solo; M2L at p = 6), its fraction
     # taken from its in-situ time inside the timed region (M2L and NEAR share the SMs there)
