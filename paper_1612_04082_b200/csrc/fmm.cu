@@ -1016,12 +1016,13 @@ void schedule_tree(Tree& t, cudaStream_t s) {
     // (w_direct(a): xw_direct && nsub[a] < wf n_e -- applied by leaf_lists_kernel)
     // V-list pairs of two leaves with few points: one M2L costs ~ (3 n_e)^2 tensor-core MACs
     // (x3 for 3xTF32) plus its share of the fp64 state; summing the nsrc x ntrg pairs directly
-    // is cheaper below ~kappa (3 n_e)^2 pair interactions.  kappa measured with the FP16 M2L:
-    // 1M beam, p = 6: 4.05 / 4.02 / 4.04 / 4.05 ms at kappa = 0.005 / 0.0055 / 0.006 / 0.0065;
-    // configs[3], p = 8 (the M2L is the more tensor-bound there and gained more from FP16):
-    // 7.60 / 7.26 / 7.21 / 7.38 / 7.57 ms at 0.002 / 0.003 / 0.004 / 0.005 / 0.006.
+    // is cheaper below ~kappa (3 n_e)^2 pair interactions.  kappa measured with the FP16
+    // translations and the branch-free epilogue (the cheaper the M2L, the lower the optimum):
+    // 1M beam, p = 6: 3.78 / 3.76 / 3.77 / 3.78 / 3.81 / 3.82 ms at kappa = 0.00475 / 0.005 /
+    // 0.00525 / 0.0055 / 0.006 / 0.0065; configs[3], p = 8: 6.68 / 6.53 / 6.58 / 6.66 / 6.76 ms at
+    // 0.0025 / 0.003 / 0.0035 / 0.004 / 0.0045.  (TF32 translations: 0.006 for both.)
     const double kappa = std::getenv("EBEM_V_DIRECT") ? std::atof(std::getenv("EBEM_V_DIRECT"))
-                                                      : (P.p <= 6 ? 0.006 : 0.004);
+                                                      : (P.p <= 6 ? 0.005 : 0.003);
     // (only with the fp32 far field, p <= 8: at p >= 9 the fp32 direct sums would exceed the
     // fp64 far field's error, measured 1.5e-6 vs 5.5e-7 at p = 10)
     // (v_direct(b, a): both leaves, nsub[a] tsub[b] < kappa (3 n_e)^2 -- leaf_lists_kernel and
