@@ -1,18 +1,27 @@
-// Tensor-core (tcgen05, sm_100a) operator-grouped pairs GEMM, 3xTF32:
+// Tensor-core (tcgen05, sm_100a) operator-grouped pairs GEMM with three-product operand splits:
 //     Y[t] += Mat[op] X[s]      for every pair (t, s) of every operator op
 // used for the KIFMM translations ("M2M, L2L and M2L operators ...
 // represented by matrices"): Q2Z, M2M, M2L, L2L.  Pairs are grouped by operator (for
-// M2L: by translation vector), so a CTA tile is one operator's 128-row slice times 128
-// pairs: a dense [128 x K] x [K x 128] contraction with the B operand gathered row by
-// row (TMA tile::gather4) from the state array.
+// M2L: by translation vector), so a CTA tile is operator row slices times a block of pairs:
+// a dense [rows x K] x [K x pairs] contraction with the B operand gathered row by row from
+// the state array.
 //
-// Precision: A = A_b + A_s and B = B_b + B_s with A_b = rna_tf32(A), A_s = rna_tf32(A - A_b)
-// (same for B); D += A_b B_b + A_b B_s + A_s B_b in fp32 TMEM accumulators: unbiased
-// error ~3 * 2^-22 relative per product, the fp32 level.
+// Precision: A = A_b + A_s and B = B_b + B_s with round-to-nearest heads and remainders of 11
+// significand bits (A_b = rn(A), A_s = rn(A - A_b), same for B); D += A_b B_b + A_b B_s +
+// A_s B_b in fp32 TMEM accumulators: unbiased error ~3 * 2^-22 relative per product, the fp32
+// level.  Two operand types: TF32 (kind::tf32, 8 K per MMA) and FP16 (kind::f16, 16 K per MMA,
+// twice the rate; rows scaled by powers of two so that the fp16 exponent range never shows --
+// split_rows_h_kernel, reading R14).
 //
-// CTA = 8 warps.  warp 0: TMA producer (A_b, A_s 3-D tile loads; B_b, B_s gather4),
-// warp 1 lane 0: tcgen05.mma issuer, warp 2: TMEM allocator, warps 4-7: drain TMEM partial
-// sums into fp32 registers, then fp32 atomics into Y (coalesced along rows).
+// Kernels: tc_pairs_kernel (one 128-row slice x 128 pairs, TF32, TMA gather4 rows, partial
+// sums drained every two K chunks: the precise kernel); tc_pairs_fast_kernel (two slices x 128
+// pairs) and tc_pairs_wide_kernel (one slice x 256 pairs), TF32 or FP16, rows gathered by
+// cp.async, full-K TMEM accumulation or drained groups; tc_pairs_mc_kernel (cluster multicast of
+// the operator tiles); tc_chain_kernel (a whole M2M / L2L chain in one persistent launch).
+//
+// CTA of the precise kernel = 8 warps.  warp 0: TMA producer (A_b, A_s 3-D tile loads; B_b, B_s
+// gather4), warp 1 lane 0: tcgen05.mma issuer, warp 2: TMEM allocator, warps 4-7: drain TMEM
+// partial sums into fp32 registers, then fp64 REDs into Y (coalesced along rows).
 // 3-stage smem ring of 4 x 16 KB (SWIZZLE_128B, K-major), mbarrier full/empty pipeline.
 #include <cuda.h>
 #include <cuda_fp16.h>
