@@ -1259,20 +1259,6 @@ void schedule_tree(Tree& t, cudaStream_t s) {
         // tile shapes: the full-chain and the drained M2L kernels two-slice or wide by M
         // (tc_fast_tile_mode), the one-slice precise kernel 128 x 128
         const int fm = tc_fast_tile_mode(me);
-        // the upward Q2Z on FP16 operands as well (the S2M kernel writes the split; EBEM_Q2Z_F16=0: TF32)
-        static const bool q2z_h = !(std::getenv("EBEM_Q2Z_F16") && std::atoi(std::getenv("EBEM_Q2Z_F16")) == 0);
-        // (as the M2M / L2L chains, not in trees deeper than 16 levels: level-20 coincident cluster,
-        // GPU vs oracle KIFMM 2.85e-3 with the FP16 Q2Z against 1.71e-3, limitation L1)
-        t.q2z_f16 = t.ml_fast && m2l_f16_level() >= 1 && q2z_h && t.nlevels <= 16;
-        if (t.q2z_f16) {
-            t.Qhb.alloc((size_t)nq * P.ldch);
-            t.Qhs.alloc((size_t)nq * P.ldch);
-            t.Qhinv.alloc(nq);
-            t.Qhb.zero(s);
-            t.Qhs.zero(s);
-        }
-        tc_build_tiles(t.q2z_up, me, mc, t.ml_fast ? fm : 0, t.q2z_f16 ? 64 : 32);
-        tc_build_tiles(t.q2z_dn, me, mc, t.ml_fast ? fm : 0);
         // M2L operands in FP16 (3xFP16, twice the tensor rate of 3xTF32; EBEM_M2L_F16=0: TF32)
         t.m2l_f16 = m2l_f16_level() >= 1;
         if (t.m2l_f16) {
@@ -1291,13 +1277,33 @@ void schedule_tree(Tree& t, cudaStream_t s) {
         // the TF32 split (relative per element) does not -- level-20 coincident cluster, GPU vs
         // oracle KIFMM: 1.71e-3 with TF32 chains, 2.11e-3 with FP16 chains, M2L in FP16 either way.
         static const bool chain_env = std::getenv("EBEM_ML_CHAIN") && std::atoi(std::getenv("EBEM_ML_CHAIN")) == 1;
-        // p = 7, 8 (fp32 far field): the chains on the same FP16 data flow with DRAINED accumulation
+        // p = 7 .. 10: the chains on the same FP16 data flow with DRAINED accumulation
         // (tc_pairs_fast / wide kernel <true, true>) instead of the one-slice precise TF32 kernel
         // with TMA-gathered rows (EBEM_ML_DRAIN_F16=0: off; the BEM operator keeps the precise kernel)
-        static const bool drain_h = !(std::getenv("EBEM_ML_DRAIN_F16") && std::atoi(std::getenv("EBEM_ML_DRAIN_F16")) == 0);
-        t.ml_drain = t.tc_fast && !t.ml_fast && drain_h && m2l_f16_level() >= 2 && m2l_drain_fast();
+        // EBEM_ML_DRAIN_F16: 0 off; 1 (default) p = 7 .. 10; 2 every order above 6.  Measured on the
+        // 1M beam at p = 10: 29.8 -> 27.8 ms, rel-L2 5.02e-7 -> 5.49e-7 (bound 1e-6); at p = 12
+        // (3000-point beam, test_largest_order) 1.3e-6 -> 2.2e-6, over that test's 2e-6: the
+        // orders above 10 keep the precise kernel.
+        static const int drain_lv = std::getenv("EBEM_ML_DRAIN_F16") ? std::atoi(std::getenv("EBEM_ML_DRAIN_F16")) : 1;
+        const bool drain_h = drain_lv >= 2 || (drain_lv == 1 && P.p <= 10);
+        t.ml_drain = t.use_tc && !t.ml_fast && P.p > 6 && drain_h && m2l_f16_level() >= 2 && m2l_drain_fast();
         t.ml_f16 = (t.ml_fast || t.ml_drain) && t.m2l_f16 && !chain_env && ml_f16_on() && t.nlevels <= 16;
         t.ml_drain = t.ml_drain && t.ml_f16;
+        // the upward Q2Z on FP16 operands as well (the S2M kernel writes the split; EBEM_Q2Z_F16=0: TF32)
+        static const bool q2z_h = !(std::getenv("EBEM_Q2Z_F16") && std::atoi(std::getenv("EBEM_Q2Z_F16")) == 0);
+        // (as the M2M / L2L chains, not in trees deeper than 16 levels: level-20 coincident cluster,
+        // GPU vs oracle KIFMM 2.85e-3 with the FP16 Q2Z against 1.71e-3, limitation L1)
+        // (with the drained chains, p = 7 .. 10, on the drained kernel too)
+        t.q2z_f16 = (t.ml_fast || t.ml_drain) && m2l_f16_level() >= 1 && q2z_h && t.nlevels <= 16;
+        if (t.q2z_f16) {
+            t.Qhb.alloc((size_t)nq * P.ldch);
+            t.Qhs.alloc((size_t)nq * P.ldch);
+            t.Qhinv.alloc(nq);
+            t.Qhb.zero(s);
+            t.Qhs.zero(s);
+        }
+        tc_build_tiles(t.q2z_up, me, mc, t.ml_fast || t.q2z_f16 ? fm : 0, t.q2z_f16 ? 64 : 32);
+        tc_build_tiles(t.q2z_dn, me, mc, t.ml_fast ? fm : 0);
         if (t.ml_f16) {
             t.Whb.alloc((size_t)std::max(1, t.n_dn) * P.ldh);
             t.Whs.alloc((size_t)std::max(1, t.n_dn) * P.ldh);
@@ -1775,9 +1781,9 @@ void fmm_evaluate(Tree& t, int kernel, const float* f, const float* g, float* ou
     if (conc) EB_CUDA(cudaStreamWaitEvent(sa, t.ev_zz, 0));
     pb(PH_Q2Z_UP, sa);
     if (t.use_tc) {
-        if (t.ml_fast && t.q2z_f16)
-            tc_pairs_gemm_fast(t.q2z_up, P.mQu1T_hb, P.mQu1T_hs, t.Qhb.p, t.Qhs.p, P.ldch, me, mc, t.Z.p, lde, false, sa, true,
-                               t.Qhinv.p, P.qu_hinv);
+        if (t.q2z_f16)
+            tc_pairs_gemm_fast(t.q2z_up, P.mQu1T_hb, P.mQu1T_hs, t.Qhb.p, t.Qhs.p, P.ldch, me, mc, t.Z.p, lde, t.ml_drain, sa,
+                               true, t.Qhinv.p, P.qu_hinv);
         else if (t.ml_fast) tc_pairs_gemm_fast(t.q2z_up, P.mQu1T_b, P.mQu1T_s, t.Qb.p, t.Qs.p, ldc, me, mc, t.Z.p, lde, false, sa);
         else tc_pairs_gemm(t.q2z_up, P.mQu1T_b, P.mQu1T_s, t.mQb, t.mQs, me, mc, t.Z.p, lde, sa);
     } else {
